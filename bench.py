@@ -1,0 +1,360 @@
+"""Benchmark of the LAGS-SGD sparsify -> exchange -> decode -> update hot path on B200.
+
+One *step* = one pass of the hot path over one batch of synthetic per-rank gradients with the
+ResNet-50 layer shapes (BASELINE.json configs[3]; 161 tensors, 25,557,032 fp32 elements,
+rho = 0.001 -> c = 1000, k_l = min(d, max(1, d // 1000)) as R: sparsify.py:182-184):
+
+    compress (K1 accumulate + K2 select/compact, per layer)  ->  NCCL all-gather of the fixed-size
+    sparse messages (N > 1)  ->  rank-ordered decode + SGD update of the parameters
+
+`value` = algorithmic bytes of all ranks / device time (GB/s), inputs resident in HBM.
+`e2e`   = the same metric through the reference-facing drop-in `lags_step` with HOST numpy
+          buffers (v, g, r copied in, v', r' copied out every step).
+`--impl reference` times the reference algorithm on the host cores (the numpy oracle port,
+oracle/lagsgd_oracle.py -- the reference is Python and cannot travel to the GPU box).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RHO = 0.001
+METRIC = "LAGS sparsify/decode GB/s (ResNet-50 layer shapes, rho=0.001); iter/s of the hot-path step"
+UNIT = "GB/s"
+
+
+def resnet50_dims():
+    import torchvision
+
+    return [p.numel() for p in torchvision.models.resnet50().parameters()]
+
+
+def ks_for(dims, rho=RHO):
+    c = 1.0 / rho
+    return [min(d, max(1, int(d // c))) for d in dims]
+
+
+def algorithmic_bytes(n, counts_per_rank, union, world):
+    """Per-step algorithmic bytes of all ranks (fp32): compress 12 d + 8 n_sel per rank;
+    decode reads every rank's pairs (8 B each) and reads+writes each touched weight (8 B)."""
+    sel = sum(counts_per_rank)
+    compress = world * (12 * n + 8 * sel)
+    decode = world * (8 * world * sel + 8 * union)
+    return compress, decode
+
+
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def cpu_oracle_step_rate(dims, ks, world, threads, steps=1, seed=0):
+    """Time the reference algorithm (numpy oracle port) for `steps` full steps of the workload
+    with `world` simulated workers; returns seconds per step (best of `steps`)."""
+    from oracle import lagsgd_oracle as orc
+
+    rng = np.random.default_rng(seed)
+    n = sum(dims)
+    v = rng.standard_normal(n).astype(np.float32)
+    grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
+    res = [(0.01 * rng.standard_normal(n)).astype(np.float32) for _ in range(world)]
+    best = float("inf")
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def run_reference(args, dims, ks, world, rank):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = sum(dims)
+    from oracle import lagsgd_oracle as orc
+
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal(n).astype(np.float32)
+    grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
+    res = [np.zeros(n, np.float32) for _ in range(world)]
+    for _ in range(args.warmup):
+        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
+        times.append(time.perf_counter() - t0)
+    t = sum(times)
+    sel = sum(ks)
+    comp, dec = algorithmic_bytes(n, ks, sel * world, world)
+    val = (comp + dec) * args.steps / t / 1e9
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
+        "iter_per_s": round(args.steps / t, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(dims, ks, world),
+        "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full ResNet-50-shaped lags_step with P={world} simulated workers per step "
+                                   f"(numpy oracle port of R: training.py:227-255, layers over {threads} threads)"},
+        "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def config_dict(dims, ks, world):
+    return {"workload": "resnet50-layer-shapes LAGS step: compress(161 layers) + all-gather + decode/update",
+            "model_shapes": "torchvision resnet50 parameters (161 tensors, 25,557,032 fp32 elements)",
+            "global_batch": None, "rho": RHO, "sum_k_per_rank": int(sum(ks)), "n_layers": len(dims),
+            "n_elements_per_rank": int(sum(dims)), "world": world,
+            "parallelism": f"dp{world} (sparse all-gather)",
+            "l2": "inputs larger than L2: 3 rotating 102 MB gradient buffers + 102 MB residual per rank"}
+
+
+def run_ours(args, dims, ks, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1911_08727_b200 as L
+    from paper_1911_08727_b200 import _native as N
+
+    dev = torch.device("cuda", local)
+    n = sum(dims)
+    bucket = L.Bucket(dims, ks, N.F32, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    NG = 3
+    g_bufs = [torch.randn(n, device=dev, generator=gen) for _ in range(NG)]
+    r = torch.zeros(n, device=dev)
+    v = torch.randn(n, device=dev, generator=gen)
+    msg_local = bucket.new_messages(1)
+    msgs = bucket.new_messages(world) if world > 1 else msg_local
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    alpha = 0.1
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def step(t, timed=False):
+        if timed:
+            ev[t][0].record(stream)
+        bucket.compress(g_bufs[t % NG], r, alpha, msg_local, status, stream=stream)
+        if timed:
+            ev[t][1].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(msgs, msg_local)
+        bucket.decode(msgs, world, v, stream=stream)
+
+    for t in range(args.warmup):
+        step(t)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = N.lags_kernel_launches()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    start.record(stream)
+    for t in range(args.steps):
+        step(t, timed=True)
+    stop.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = N.lags_kernel_launches() - l0
+    clk = clocks.stop()
+    ms = start.elapsed_time(stop)
+    comp_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t_ms = torch.tensor([ms, comp_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms, comp_ms = float(t_ms[0]), float(t_ms[1])
+    assert int(status.item()) == 0
+    # counts / union for the algorithmic-byte model (after the timed region)
+    counts = bucket.counts_view(msg_local).cpu().numpy().astype(np.int64)
+    sel_local = int(counts.sum())
+    union = sel_local if world == 1 else None
+    if world > 1:
+        allmsg = msgs
+        idx_all = []
+        for p in range(world):
+            m = allmsg[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes]
+            for j, (ii, _) in enumerate(bucket.unpack(m)):
+                idx_all.append(ii + int(bucket.offsets[j]))
+        union = int(np.unique(np.concatenate(idx_all)).size)
+        sel_t = torch.tensor([sel_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(sel_t)
+        sel_mean = float(sel_t.item()) / world
+    else:
+        sel_mean = sel_local
+    comp_b, dec_b = algorithmic_bytes(n, [sel_mean], union, world)
+    value = (comp_b + dec_b) * args.steps / (ms / 1e3) / 1e9
+    peak, peak_src = read_peaks()
+    comp_bytes_rank = 12 * n + 8 * sel_local
+    achieved = comp_bytes_rank / (comp_ms / 1e3) / 1e9
+
+    e2e = None
+    cpu = None
+    if rank == 0 and not args.no_e2e:
+        e2e = measure_e2e(args, dims, ks, L, dev)
+    if rank == 0 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        s = cpu_oracle_step_rate(dims, ks, 1, threads, steps=1)
+        cb, dbb = algorithmic_bytes(n, ks, sum(ks), 1)
+        cpu = {"value": round((cb + dbb) / s / 1e9, 4), "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"1 full ResNet-50-shaped lags_step, P=1 ({s:.2f} s; numpy oracle of R: training.py:227-255)"}
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "iter_per_s": round(args.steps / (ms / 1e3), 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.randn gradients, seed 1234+rank)",
+            "config": config_dict(dims, ks, world),
+            "roofline": {"kernel": "lags_compress (accum + per-layer select/compact)", "bound": "hbm",
+                         "achieved": round(achieved, 2), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "algorithmic_bytes_per_launch": int(comp_bytes_rank), "ms_per_launch": round(comp_ms, 4)},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+
+
+def measure_e2e(args, dims, ks, L, dev):
+    """Same metric through the reference-facing drop-in lags_step with host numpy buffers."""
+    import torch
+
+    n = sum(dims)
+    shape = [L.LayerShape(i + 1, d) for i, d in enumerate(dims)]
+    rng = np.random.default_rng(7)
+    v = L.LayeredVector(shape, rng.standard_normal(n).astype(np.float32))
+    gs = [L.LayeredVector(shape, rng.standard_normal(n).astype(np.float32)) for _ in range(2)]
+    res = [L.LayeredVector.zeros(shape, np.float32)]
+    counts = {i + 1: k for i, k in enumerate(ks)}
+    steps = max(3, min(args.steps, 10))
+    for t in range(2):
+        v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for t in range(steps):
+        v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res)
+    torch.cuda.synchronize(dev)
+    dt = (time.perf_counter() - t0) / steps
+    comp_b, dec_b = algorithmic_bytes(n, ks, sum(ks), 1)
+    return {"value": round((comp_b + dec_b) / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": 3 * 4 * n,
+            "d2h_bytes_per_step": 2 * 4 * n, "ms_per_step": round(dt * 1e3, 3),
+            "api": "paper_1911_08727_b200.lags_step (drop-in for R: training.py:227) on host numpy LayeredVectors",
+            "steps": steps, "world_used": 1}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    dims = resnet50_dims()
+    ks = ks_for(dims)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, dims, ks, world, rank)
+        return
+    world, rank, local = dist_setup()
+    run_ours(args, dims, ks, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

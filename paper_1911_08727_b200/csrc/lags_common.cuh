@@ -1,0 +1,69 @@
+// Shared device helpers for the LAGS-SGD B200 kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lags_b200.h"
+
+namespace lags {
+
+// |x| as an unsigned key: monotone in magnitude for finite x, 0 only for +-0.
+// Ties on equal keys are broken by lower index (R: sparsify.py:85-87).
+template <typename T> struct Key;
+template <> struct Key<float> {
+  using K = uint32_t;
+  static constexpr int BITS = 31;  // sign bit dropped
+  static constexpr int RB = 11;    // radix digit width -> 3 passes (11, 11, 9)
+  __device__ __forceinline__ static K of(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+};
+template <> struct Key<double> {
+  using K = unsigned long long;
+  static constexpr int BITS = 63;
+  static constexpr int RB = 13;  // 5 passes (13, 13, 13, 13, 11)
+  __device__ __forceinline__ static K of(double x) {
+    return static_cast<K>(__double_as_longlong(x)) & 0x7fffffffffffffffull;
+  }
+};
+
+// acc = r + alpha * g rounded twice (numpy evaluates `alpha * g` then `+`; no FMA).
+__device__ __forceinline__ float accum(float r, float g, float a) { return __fadd_rn(r, __fmul_rn(a, g)); }
+__device__ __forceinline__ double accum(double r, double g, double a) { return __dadd_rn(r, __dmul_rn(a, g)); }
+
+__device__ __forceinline__ bool nonfinite(float g) { return (__float_as_uint(g) & 0x7f800000u) == 0x7f800000u; }
+__device__ __forceinline__ bool nonfinite(double g) {
+  return (static_cast<unsigned long long>(__double_as_longlong(g)) & 0x7ff0000000000000ull) ==
+         0x7ff0000000000000ull;
+}
+
+// Block-wide exclusive scan of one uint32 per thread (NT threads, multiple of 32).
+// `warp_tot` must hold 33 uint32 of shared memory.  Returns the exclusive prefix and writes the
+// block total into *total.  Contains two __syncthreads().
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NW = NT / 32;
+    uint32_t w = lane < NW ? warp_tot[lane] : 0u;
+    uint32_t s = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NW) warp_tot[lane] = s - w;  // exclusive warp prefix
+    if (lane == 31) warp_tot[32] = s;
+  }
+  __syncthreads();
+  *total = warp_tot[32];
+  return warp_tot[warp] + x - v;
+}
+
+}  // namespace lags

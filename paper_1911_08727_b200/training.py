@@ -1,0 +1,131 @@
+"""Drop-in ``lags_step`` (R: training.py:227-255) backed by the B200 kernels.
+
+Same signature, semantics and errors as the reference: residuals are updated
+in place, a new layered vector of ``type(v)`` is returned, ``StructureError``
+on a layout mismatch and ``DivergenceError(iteration=t)`` on a non-finite
+gradient (R: training.py:170-175).  It can be monkeypatched into the
+reference's ``train()`` (R: training.py:348 looks ``lags_step`` up at call time).
+
+Host numpy buffers are copied to the device, the P simulated workers are
+compressed one after another into P sparse messages (the exchange), the
+messages are decoded in rank order, and the results are copied back.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .engine import Bucket
+from .errors import DivergenceError, StructureError
+from .layered import layout_of
+
+SCHEDULE_KINDS = ("constant", "inv-sqrt-T", "diminishing")
+
+
+@dataclass(frozen=True)
+class StepSizeSchedule:
+    """alpha_t (R: training.py:41-69); inv-sqrt-T returns np.float64 exactly like the reference."""
+
+    kind: str
+    theta: float
+
+    def __post_init__(self):
+        if self.kind not in SCHEDULE_KINDS:
+            raise ValueError(f"unknown schedule kind {self.kind!r}")
+        if self.theta <= 0:
+            raise ValueError("theta must be positive")
+
+    def alpha(self, t: int, total: int):
+        if self.kind == "constant":
+            return self.theta
+        if self.kind == "inv-sqrt-T":
+            return self.theta / np.sqrt(total)
+        return self.theta / (1.0 + t)
+
+
+def mode_for(dtype, alpha) -> int:
+    """numpy NEP 50 promotion of ``res + alpha * g`` (R: training.py:250) -> lags_dtype_t."""
+    dtype = np.dtype(dtype)
+    if dtype == np.float64:
+        return N.F64
+    if dtype == np.float32:
+        if isinstance(alpha, np.floating) and np.dtype(type(alpha)).itemsize > 4:
+            return N.F32_ACC64
+        return N.F32
+    raise TypeError(f"unsupported dtype {dtype}; the B200 path handles float32 and float64")
+
+
+_BUCKETS: dict = {}
+
+
+def _bucket_for(dims: tuple, ks: tuple, mode: int) -> Bucket:
+    key = (dims, ks, mode, torch.cuda.current_device())
+    b = _BUCKETS.get(key)
+    if b is None:
+        if len(_BUCKETS) > 32:
+            _BUCKETS.clear()
+        b = Bucket(dims, ks, mode)
+        _BUCKETS[key] = b
+    return b
+
+
+def _to_dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False)
+
+
+def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: int | None = None):
+    """Per-layer selection with error feedback on the B200; R: training.py:227-255."""
+    pairs = layout_of(v)
+    P = len(grads)
+    if P < 1 or len(residuals) != P:
+        raise ValueError("need one residual per worker and at least one worker")
+    dtype = v.data.dtype
+    mode = mode_for(dtype, alpha)
+    # R: training.py:171-175 -- worker by worker: layout, then finiteness.
+    bad_layout = next((p for p, g in enumerate(grads, start=1) if layout_of(g) != pairs), None)
+    status = torch.zeros(max(P, 1), dtype=torch.int32, device="cuda")
+    if bad_layout is not None:
+        for p in range(1, bad_layout):
+            gd = _to_dev(grads[p - 1].data)
+            N.check(N.lags_check_finite(N.F64 if gd.dtype == torch.float64 else N.F32, gd.data_ptr(), gd.numel(),
+                                        status[p - 1:p].data_ptr(), torch.cuda.current_stream().cuda_stream))
+        st = status.cpu().numpy()
+        for p in range(1, bad_layout):
+            if st[p - 1]:
+                raise DivergenceError(f"worker {p} produced a non-finite gradient", iteration=t)
+        raise StructureError(f"worker {bad_layout} gradient layout differs from params")
+    for g, r in zip(grads, residuals):
+        if g.data.dtype != dtype or r.data.dtype != dtype:
+            raise TypeError("params, gradients and residuals must share one dtype")
+        if layout_of(r) != pairs:
+            raise StructureError("residual layout differs from params")
+    dims = tuple(d for _, d in pairs)
+    ks = []
+    for lid, d in pairs:
+        k = int(counts[lid])
+        if not 1 <= k <= d:  # R: sparsify.py:82-83 (raised before any residual is touched)
+            raise ValueError(f"k={k} outside 1..{d}")
+        ks.append(k)
+    bucket = _bucket_for(dims, tuple(ks), mode)
+
+    v_d = _to_dev(v.data)
+    msgs = bucket.new_messages(P)
+    r_devs = []
+    for p in range(P):
+        g_d = _to_dev(grads[p].data)
+        r_d = _to_dev(residuals[p].data)
+        bucket.compress(g_d, r_d, alpha, msgs[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes], status[p:p + 1])
+        r_devs.append(r_d)
+    bucket.decode(msgs, P, v_d)
+    st = status.cpu().numpy()
+    for p in range(P):
+        if st[p] & N.STATUS_NONFINITE:  # residuals untouched on the host, as in the reference
+            raise DivergenceError(f"worker {p + 1} produced a non-finite gradient", iteration=t)
+    for r_d, res in zip(r_devs, residuals):
+        res.data[:] = r_d.cpu().numpy()
+    return type(v)(v.shape, v_d.cpu().numpy())
