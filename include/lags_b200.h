@@ -4,19 +4,18 @@
  * The reference (arxiv 1911.08727, /root/reference/pkg/src/lagsgd) is pure Python/numpy and has
  * no FFI; each entry point below replaces one reference function (cited as R: file:line).  The
  * Python package `paper_1911_08727_b200` binds these with ctypes and keeps the reference's Python
- * names (top_k, decompress, lags_step, ...).  See INTEGRATION.md for the binding stubs.
+ * names (top_k, decompress, lags_step, ...).  See INTEGRATION.md for binding stubs.
  *
  * Conventions
- *  - All buffer pointers are DEVICE pointers owned by the caller.  Nothing here allocates.
- *  - Every call is stream-ordered on `stream` and never synchronises the host.
+ *  - Buffer pointers are DEVICE pointers owned by the caller; the library never allocates device
+ *    memory (a bucket lives in caller-provided device memory; its handle is a small host struct).
+ *  - Every call is stream-ordered on `stream` and does not synchronise the host, except
+ *    lags_bucket_create (one-time table upload) and lags_bucket_stats (diagnostic read-back).
  *  - Return value: LAGS_OK (0) or a negative lags_status_t; lags_last_error() gives a message
  *    (thread-local).  No C++ exception crosses the ABI.
- *  - No global mutable device state: calls on distinct (stream, workspace) pairs are independent.
- *  - dtype selects storage / accumulation types (see lags_dtype_t).
- *  - A "bucket" is a contiguous run of layers inside flat per-worker buffers (the reference's
- *    LayeredVector layout, R: layered.py:46-107): layer j occupies [offset_j, offset_j + dim_j).
- *    Selected entries of layer j go to output slots [slot_j, slot_j + k_j); indices are
- *    layer-local int32, strictly ascending, values are the accumulated entries.
+ *  - A bucket is a contiguous run of layers of the flat per-worker buffers (the reference's
+ *    LayeredVector layout, R: layered.py:46-107): layer j occupies [offset_j, offset_j + dim_j),
+ *    offsets being the prefix sums of dims.  Flat buffers must be 16-byte aligned.
  */
 #ifndef LAGS_B200_H
 #define LAGS_B200_H
@@ -29,14 +28,15 @@ extern "C" {
 #endif
 
 typedef struct CUstream_st* lags_stream_t; /* == cudaStream_t */
+typedef struct lags_bucket lags_bucket_t;  /* opaque host handle */
 
 typedef enum {
   LAGS_OK = 0,
-  LAGS_ERR_INVALID_ARG = -1,   /* null pointer, bad sizes            -> ValueError      */
-  LAGS_ERR_K_OUT_OF_RANGE = -2,/* k outside 1..dim                   -> ValueError      (R: sparsify.py:82-83) */
-  LAGS_ERR_STRUCTURE = -3,     /* layer table inconsistent           -> StructureError  (R: training.py:172-173) */
-  LAGS_ERR_WORKSPACE = -4,     /* workspace too small                                    */
-  LAGS_ERR_CUDA = -5           /* CUDA launch / runtime error                            */
+  LAGS_ERR_INVALID_ARG = -1,    /* null pointer, bad sizes, misaligned buffer -> ValueError            */
+  LAGS_ERR_K_OUT_OF_RANGE = -2, /* k outside 1..dim                            -> ValueError (R: sparsify.py:82-83) */
+  LAGS_ERR_STRUCTURE = -3,      /* inconsistent layer layout                   -> StructureError (R: training.py:172-173) */
+  LAGS_ERR_WORKSPACE = -4,      /* caller memory too small                                              */
+  LAGS_ERR_CUDA = -5            /* CUDA launch / runtime error                                          */
 } lags_status_t;
 
 /* Storage / arithmetic modes (R: training.py:250 under numpy's NEP 50 promotion rules).
@@ -46,72 +46,72 @@ typedef enum {
  *                  residual stored back as float32 (R: training.py:63-64 + :250-252)        */
 typedef enum { LAGS_F32 = 0, LAGS_F64 = 1, LAGS_F32_ACC64 = 2 } lags_dtype_t;
 
-/* Status bits written (OR-ed) into the caller's device status word. */
-#define LAGS_STATUS_NONFINITE 0x1u /* some gradient entry was inf/nan -> DivergenceError (R: training.py:174-175) */
+/* Status bits OR-ed into the caller's device status word. */
+#define LAGS_STATUS_NONFINITE 0x1u /* a gradient entry was inf/nan -> DivergenceError (R: training.py:174-175) */
 
-/* One layer of a bucket.  Lives in device memory (an array of these). */
-typedef struct {
-  int64_t offset; /* first element of the layer inside the flat g / r / v buffers */
-  int64_t dim;    /* d_l >= 1                                                      */
-  int32_t k;      /* selection budget 1 <= k_l <= d_l (R: sparsify.py:182-184)     */
-  int32_t slot;   /* first output slot of the layer (prefix sum of k)              */
-} lags_layer_t;
-
-/* Per-bucket persistent selection state (device memory, one per layer, zero-initialise once).
- * Holds the predicted magnitude threshold used by the fast path; opaque to callers. */
-typedef struct {
-  uint64_t pred_key;   /* predicted threshold key (0 = no prediction yet)  */
-  uint32_t flags;      /* internal                                         */
-  uint32_t last_cands; /* candidates seen at the last call (diagnostic)    */
-} lags_layer_state_t;
+/* lags_bucket_compress flags */
+#define LAGS_COMPRESS_EXACT 0x1u /* skip the predicted-threshold fast path (dense exact selection) */
 
 int lags_abi_version(void);
 const char* lags_last_error(void);
 /* Number of kernels this library has launched in the process (diagnostic / bench evidence). */
 unsigned long long lags_kernel_launches(void);
 
-/* Bytes of workspace lags_compress needs for a bucket of `n_total` elements / `nlayers`
- * layers / `total_k` slots. */
-size_t lags_compress_workspace_bytes(int32_t dtype, int32_t nlayers, int64_t n_total, int64_t total_k);
+/* ---- bucket: the per-layer hot path ------------------------------------------------------- */
 
-/* Per-worker compress of one bucket -- replaces, per worker p and layer l, R: training.py:250-252
- * (acc = r + alpha*g; top_k(acc, k); r = acc - sent) and the finiteness check of
- * R: training.py:174 (fused; sets LAGS_STATUS_NONFINITE in *status, never clears it).
- *   g, r        flat worker buffers (dtype storage type), bucket starts at element 0
- *   idx_out     int32 [total_k]        val_out  acc type [total_k]     count_out int32 [nlayers]
- *   state       lags_layer_state_t [nlayers] or NULL (NULL = exact path every call)
- */
-int lags_compress(int32_t dtype, const lags_layer_t* layers, int32_t nlayers, int64_t n_total,
-                  int64_t total_k, const void* g, void* r, double alpha, int32_t* idx_out,
-                  void* val_out, int32_t* count_out, uint32_t* status, lags_layer_state_t* state,
-                  void* workspace, size_t workspace_bytes, lags_stream_t stream);
+/* Device bytes for a bucket of `nlayers` layers (host arrays dims[], ks[]) exchanged among up to
+ * `max_world` ranks (tables, selection state, candidate lists, decode planes). */
+size_t lags_bucket_device_bytes(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t nlayers,
+                                int32_t max_world);
+
+/* Build a bucket in `device_mem` (>= lags_bucket_device_bytes): uploads the layer/task tables and
+ * zeroes the selection state (synchronises `stream` once).  Validates 1 <= k_l <= d_l
+ * (R: sparsify.py:82-83, LAGS_ERR_K_OUT_OF_RANGE) and d_l < 2^31. */
+int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t nlayers, int32_t max_world,
+                       void* device_mem, size_t bytes, lags_stream_t stream, lags_bucket_t** out);
+void lags_bucket_destroy(lags_bucket_t* bucket);
+
+/* Byte layout of one worker's sparse message for this bucket:
+ *   counts int32[nlayers] @ off_counts | idx int32[sum k] @ off_idx | values @ off_val (float32 for
+ *   LAGS_F32, float64 otherwise); msg_bytes is a multiple of 16.  Layer j's entries occupy slots
+ *   [slot_j, slot_j + counts[j]) with slot_j = k_1 + ... + k_{j-1}; indices are layer-local,
+ *   strictly ascending. */
+int lags_bucket_message_layout(const lags_bucket_t* bucket, int64_t* off_counts, int64_t* off_idx,
+                               int64_t* off_val, int64_t* msg_bytes);
+
+/* One worker's compress of the bucket -- per layer l replaces R: training.py:250-252
+ *   acc = r + alpha*g;  chunk = top_k(acc, k_l);  r = acc - decompress(chunk)
+ * plus the finiteness check of R: training.py:174 (fused; ORs LAGS_STATUS_NONFINITE into
+ * *status, never clears it).  Writes the message (layout above) to `msg`. */
+int lags_bucket_compress(lags_bucket_t* bucket, const void* g, void* r, double alpha, void* msg, uint32_t* status,
+                         uint32_t flags, lags_stream_t stream);
+
+/* Decode + update after the exchange -- replaces R: training.py:248,253-254:
+ *   total = fp64 zeros; for p = 1..P (rank order): total[idx] += val;   v = v - total / P
+ * `msgs` holds P messages, rank p's at byte offset p * msg_stride.  mu == 0 is the reference
+ * (parity) mode and touches only selected weights; mu > 0 applies heavy-ball momentum over the
+ * whole bucket, m = mu*m + total/P, v -= m (parity unpinned: momentum is a non-goal of the
+ * reference, R: SPEC.md:366).  `momentum` may be NULL when mu == 0.  P <= max_world. */
+int lags_bucket_decode_update(lags_bucket_t* bucket, const void* msgs, int64_t msg_stride, int32_t P, void* v,
+                              void* momentum, double mu, lags_stream_t stream);
+
+/* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls} (synchronous). */
+int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 4] */, lags_stream_t stream);
+
+/* ---- single-vector operators ---------------------------------------------------------------- */
 
 /* Finiteness of x[0:n) (R: training.py:174); ORs LAGS_STATUS_NONFINITE into *status. */
 int lags_check_finite(int32_t dtype, const void* x, int64_t n, uint32_t* status, lags_stream_t stream);
 
 /* Exact magnitude top-k of one dense vector -- R: sparsify.py:71-90.  x is not modified.
  * Writes min(k, nnz) ascending int32 indices + values and the count. */
-int lags_top_k(int32_t dtype, const void* x, int64_t dim, int32_t k, int32_t* idx_out,
-               void* val_out, int32_t* count_out, void* workspace, size_t workspace_bytes,
-               lags_stream_t stream);
 size_t lags_top_k_workspace_bytes(int32_t dtype, int64_t dim);
+int lags_top_k(int32_t dtype, const void* x, int64_t dim, int32_t k, int32_t* idx_out, void* val_out,
+               int32_t* count_out, void* workspace, size_t workspace_bytes, lags_stream_t stream);
 
-/* Dense reconstruction -- R: sparsify.py:63-68.  out[0:dim] = 0; out[idx[j]] = val[j]. */
-int lags_decompress(int32_t dtype, const int32_t* idx, const void* val, const int32_t* count,
-                    int64_t dim, void* out, lags_stream_t stream);
-
-/* Decode + update of one bucket after the exchange -- replaces R: training.py:248,253-254:
- *   total = fp64 zeros; for p = 1..P (rank order): total[idx] += val;  v = v - total / P
- * Rank p's message is at byte offset p*rank_stride_bytes from idx0 / val0 / cnt0.
- * mu == 0 is the reference (parity) mode and touches only selected positions; mu > 0 adds
- * heavy-ball momentum m = mu*m + total/P; v -= m over the whole bucket (parity unpinned,
- * R: SPEC.md:366 lists momentum as a non-goal).  `momentum` may be NULL when mu == 0.
- * The decode workspace must be zero-filled before the first call; every call leaves it zeroed. */
-size_t lags_decode_workspace_bytes(int32_t dtype, int64_t n_total, int32_t P);
-int lags_decode_update(int32_t dtype, const lags_layer_t* layers, int32_t nlayers, int64_t n_total,
-                       int64_t total_k, const int32_t* idx0, const void* val0, const int32_t* cnt0,
-                       int64_t rank_stride_bytes, int32_t P, void* v, void* momentum, double mu,
-                       void* workspace, size_t workspace_bytes, lags_stream_t stream);
+/* Dense reconstruction -- R: sparsify.py:63-68.  out[0:dim] = 0; out[idx[j]] = val[j], j < *count. */
+int lags_decompress(int32_t dtype, const int32_t* idx, const void* val, const int32_t* count, int64_t dim,
+                    void* out, lags_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -5,6 +5,15 @@
 
 #include "lags_b200.h"
 
+// One layer of a bucket (device table).  Layer j occupies flat elements [offset, offset + dim)
+// and output slots [slot, slot + k).
+struct lags_layer_t {
+  int64_t offset;
+  int64_t dim;
+  int32_t k;
+  int32_t slot;
+};
+
 namespace lags {
 
 // |x| as an unsigned key: monotone in magnitude for finite x, 0 only for +-0.

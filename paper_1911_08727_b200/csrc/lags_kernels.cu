@@ -1,66 +1,39 @@
 // LAGS-SGD hot path for B200 (sm_100a): accumulate -> select -> compact -> decode/update.
 //
-// Kernels (see DESIGN.md for rooflines):
-//   K1 accum_kernel      acc = r + alpha*g (two roundings), finiteness of g, r <- acc
-//                        R: training.py:250 and :174 (fused)
-//   K2 select_kernel     per-layer exact top-k (radix select on |acc| keys, lowest-index ties)
-//                        + ordered compaction into (int32 idx, value) + zero selected residuals
-//                        R: sparsify.py:84-90, training.py:251-252
-//   K5 decode kernels    rank-ordered fp64 accumulation of the gathered sparse sets and the
-//                        SGD (optionally momentum) update  R: training.py:248,253-254
+// Kernels (DESIGN.md has the rooflines):
+//   accum_emit_kernel   (lags_fast.cuh) fp32 fused accumulate + candidate emission   R: training.py:250,174
+//   select_fast_kernel  (lags_fast.cuh) per-layer exact top-k from candidates        R: sparsify.py:84-90
+//   accum_kernel / select_dense_kernel  exact dense path (fp64, mixed, forced exact)  R: training.py:250-252
+//   decode_* kernels    rank-ordered fp64 accumulation + SGD/momentum update          R: training.py:248,253-254
 #include <cuda_runtime.h>
-#include <stdio.h>
-#include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "lags_common.cuh"
+#include "lags_fast.cuh"
 #include "lags_select.cuh"
 
 namespace lags {
 
 // ------------------------------------------------------------------------------------------
-// K1: fused accumulate over the flat bucket
+// dense accumulate (all dtypes): acc = r + alpha*g (two roundings), finiteness of g
 // ------------------------------------------------------------------------------------------
-
-// TIn: storage type of g and r.  TAcc: arithmetic type of acc.  When TIn != TAcc the
-// accumulated values go to `acc_out` (fp64 workspace) and r is rewritten by K2's epilogue.
 template <typename TIn, typename TAcc>
-__global__ void __launch_bounds__(256) accum_scalar_kernel(const TIn* __restrict__ g, TIn* __restrict__ r,
-                                                           TAcc* __restrict__ acc_out, TAcc alpha, int64_t n,
-                                                           uint32_t* status) {
+__global__ void __launch_bounds__(256) accum_kernel(const TIn* __restrict__ g, TIn* r, TAcc* acc_out, TAcc alpha,
+                                                    int64_t n, uint32_t* status) {
   bool bad = false;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const TIn gi = g[i];
     bad |= nonfinite(gi);
-    const TAcc a = accum(static_cast<TAcc>(r[i]), static_cast<TAcc>(gi), alpha);
-    acc_out[i] = a;
+    acc_out[i] = accum(static_cast<TAcc>(r[i]), static_cast<TAcc>(gi), alpha);
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
 }
 
-// fp32 fast path: 16-byte vectors, g streamed (evict-first), r read+written in place.
-__global__ void __launch_bounds__(256) accum_f32x4_kernel(const float4* __restrict__ g, float4* __restrict__ r,
-                                                          float alpha, int64_t n4, uint32_t* status) {
-  bool bad = false;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const float4 gv = __ldcs(g + i);
-    float4 rv = r[i];
-    bad |= nonfinite(gv.x) | nonfinite(gv.y) | nonfinite(gv.z) | nonfinite(gv.w);
-    rv.x = accum(rv.x, gv.x, alpha);
-    rv.y = accum(rv.y, gv.y, alpha);
-    rv.z = accum(rv.z, gv.z, alpha);
-    rv.w = accum(rv.w, gv.w, alpha);
-    r[i] = rv;
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
-}
-
-// Stand-alone finiteness check (R: training.py:174), used only to order error reports exactly
-// like the reference when a later worker also has a layout error.
 template <typename T>
 __global__ void __launch_bounds__(256) finite_kernel(const T* __restrict__ x, int64_t n, uint32_t* status) {
   bool bad = false;
@@ -70,34 +43,25 @@ __global__ void __launch_bounds__(256) finite_kernel(const T* __restrict__ x, in
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
 }
 
-// ------------------------------------------------------------------------------------------
-// K2: one CTA per layer -- exact select + ordered compaction (+ residual zeroing)
-// ------------------------------------------------------------------------------------------
-
+// One CTA per layer: exact dense top-k over acc (zeroing the selected entries of acc).
 template <typename T>
-__global__ void __launch_bounds__(SEL_NT) select_kernel(const lags_layer_t* __restrict__ layers,
-                                                        lags_layer_t single, T* acc, int32_t* idx_out,
-                                                        T* val_out, int32_t* count_out, int zero_selected) {
-  __shared__ SelectSmem<T> sm;
+__global__ void __launch_bounds__(SEL_NT) select_dense_kernel(const lags_layer_t* __restrict__ layers,
+                                                              lags_layer_t single, T* acc, int32_t* idx_out,
+                                                              T* val_out, int32_t* count_out, int zero_selected) {
+  __shared__ RadixSmem<Key<T>::RB> sm;
   const lags_layer_t L = layers ? layers[blockIdx.x] : single;
-  T* data = acc + L.offset;
-  const auto th = radix_select<T>(data, L.dim, static_cast<uint32_t>(L.k), sm);
-  const uint32_t cnt =
-      ordered_compact<T>(data, L.dim, th, idx_out + L.slot, val_out + L.slot, zero_selected != 0, sm);
+  const uint32_t cnt = exact_topk_dense<T, T>(acc + L.offset, L.dim, static_cast<uint32_t>(L.k),
+                                              idx_out + L.slot, val_out + L.slot, zero_selected != 0, sm);
   if (threadIdx.x == 0) count_out[layers ? blockIdx.x : 0] = static_cast<int32_t>(cnt);
 }
 
-// Mixed mode epilogue: r (fp32) <- fl32(acc) where acc (fp64) already has +0.0 at selected slots.
+// Mixed mode epilogue: r (fp32) <- fl32(acc) where acc (fp64) has +0.0 at the selected slots.
 __global__ void __launch_bounds__(256) store_residual_kernel(const double* __restrict__ acc, float* __restrict__ r,
                                                              int64_t n) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     r[i] = static_cast<float>(acc[i]);
 }
-
-// ------------------------------------------------------------------------------------------
-// decompress (R: sparsify.py:63-68)
-// ------------------------------------------------------------------------------------------
 
 template <typename T>
 __global__ void decompress_kernel(const int32_t* __restrict__ idx, const T* __restrict__ val,
@@ -107,44 +71,76 @@ __global__ void decompress_kernel(const int32_t* __restrict__ idx, const T* __re
 }
 
 // ------------------------------------------------------------------------------------------
-// K5: decode + update.  Phase A scatters every rank's pairs into a per-rank dense plane and
-// marks the owner bitmask; phase B lets the lowest rank holding index i sum the planes in
-// rank order (fp64, R: training.py:248,253) and apply v = v - total / P (R: :254).
-// Grid: (layer, rank); each block walks that layer's slots of that rank.
+// decode + update.  Work item e = (rank p, slot s) over all layers of the bucket.
+// P == 1: v[i] -= val (one kernel).  P > 1: phase A scatters each rank's values into its own
+// dense plane and marks a rank bitmask; phase B lets the lowest rank holding index i add the
+// planes in rank order in fp64 (R: training.py:248,253) and apply v - total / P (R: :254).
 // ------------------------------------------------------------------------------------------
+struct MsgView {
+  const char* base;
+  int64_t stride, off_cnt, off_idx, off_val;
+  __device__ __forceinline__ int32_t count(int p, int j) const {
+    return reinterpret_cast<const int32_t*>(base + p * stride + off_cnt)[j];
+  }
+  __device__ __forceinline__ int32_t idx(int p, int64_t s) const {
+    return reinterpret_cast<const int32_t*>(base + p * stride + off_idx)[s];
+  }
+  template <typename TVal>
+  __device__ __forceinline__ TVal val(int p, int64_t s) const {
+    return reinterpret_cast<const TVal*>(base + p * stride + off_val)[s];
+  }
+};
+
+template <typename TV, typename TVal>
+__global__ void __launch_bounds__(256) decode_single_kernel(const lags_layer_t* __restrict__ layers,
+                                                            const int32_t* __restrict__ slot_layer, MsgView msg,
+                                                            int64_t total_k, TV* v) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total_k; s += stride) {
+    const int j = slot_layer[s];
+    const lags_layer_t L = layers[j];
+    if (s - L.slot >= msg.count(0, j)) continue;
+    const int64_t i = L.offset + msg.idx(0, s);
+    const double total = __dadd_rn(0.0, static_cast<double>(msg.val<TVal>(0, s)));
+    v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), __ddiv_rn(total, 1.0)));
+  }
+}
 
 template <typename TVal>
 __global__ void __launch_bounds__(256) decode_scatter_kernel(const lags_layer_t* __restrict__ layers,
-                                                             const char* msg_idx, const char* msg_val,
-                                                             const char* msg_cnt, int64_t stride,
-                                                             TVal* planes, int64_t n, uint32_t* mask) {
-  const lags_layer_t L = layers[blockIdx.x];
-  const int p = blockIdx.y;
-  const int32_t* idx = reinterpret_cast<const int32_t*>(msg_idx + p * stride) + L.slot;
-  const TVal* val = reinterpret_cast<const TVal*>(msg_val + p * stride) + L.slot;
-  const int32_t cnt = reinterpret_cast<const int32_t*>(msg_cnt + p * stride)[blockIdx.x];
-  TVal* plane = planes + static_cast<int64_t>(p) * n + L.offset;
-  uint32_t* m = mask + L.offset;
-  for (int32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-    const int32_t i = idx[j];
-    plane[i] = val[j];
-    atomicOr(m + i, 1u << p);
+                                                             const int32_t* __restrict__ slot_layer, MsgView msg,
+                                                             int64_t total_k, int P, TVal* planes, int64_t n,
+                                                             uint32_t* mask) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t work = total_k * P;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < work; e += stride) {
+    const int p = static_cast<int>(e / total_k);
+    const int64_t s = e - static_cast<int64_t>(p) * total_k;
+    const int j = slot_layer[s];
+    const lags_layer_t L = layers[j];
+    if (s - L.slot >= msg.count(p, j)) continue;
+    const int64_t i = L.offset + msg.idx(p, s);
+    planes[static_cast<int64_t>(p) * n + i] = msg.val<TVal>(p, s);
+    atomicOr(mask + i, 1u << p);
   }
 }
 
 template <typename TV, typename TVal>
 __global__ void __launch_bounds__(256) decode_update_kernel(const lags_layer_t* __restrict__ layers,
-                                                            const char* msg_idx, const char* msg_cnt,
-                                                            int64_t stride, const TVal* planes, int64_t n,
-                                                            uint32_t* mask, int P, TV* v) {
-  const lags_layer_t L = layers[blockIdx.x];
-  const int p = blockIdx.y;
-  const int32_t* idx = reinterpret_cast<const int32_t*>(msg_idx + p * stride) + L.slot;
-  const int32_t cnt = reinterpret_cast<const int32_t*>(msg_cnt + p * stride)[blockIdx.x];
-  for (int32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-    const int64_t i = L.offset + idx[j];
+                                                            const int32_t* __restrict__ slot_layer, MsgView msg,
+                                                            int64_t total_k, int P, const TVal* planes, int64_t n,
+                                                            uint32_t* mask, TV* v) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t work = total_k * P;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < work; e += stride) {
+    const int p = static_cast<int>(e / total_k);
+    const int64_t s = e - static_cast<int64_t>(p) * total_k;
+    const int j = slot_layer[s];
+    const lags_layer_t L = layers[j];
+    if (s - L.slot >= msg.count(p, j)) continue;
+    const int64_t i = L.offset + msg.idx(p, s);
     const uint32_t bits = mask[i];
-    if (bits == 0 || (__ffs(bits) - 1) != p) continue;  // not the owner (or already applied)
+    if (bits == 0 || (__ffs(bits) - 1) != p) continue;  // only the lowest holding rank applies
     double total = 0.0;
     for (uint32_t b = bits; b; b &= b - 1) {
       const int q = __ffs(b) - 1;
@@ -155,10 +151,10 @@ __global__ void __launch_bounds__(256) decode_update_kernel(const lags_layer_t* 
   }
 }
 
-// Momentum variant (mu > 0, parity unpinned): dense over the bucket.
+// Momentum (mu > 0, parity unpinned): dense over the bucket after decode_scatter.
 template <typename TV, typename TVal>
-__global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes, int64_t n, uint32_t* mask,
-                                                              int P, TV* v, TV* mom, double mu) {
+__global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes, int64_t n, uint32_t* mask, int P,
+                                                              TV* v, TV* mom, double mu) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t bits = mask[i];
@@ -170,7 +166,8 @@ __global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes
       }
       mask[i] = 0u;
     }
-    const double mnew = __dadd_rn(__dmul_rn(mu, static_cast<double>(mom[i])), __ddiv_rn(total, static_cast<double>(P)));
+    const double mnew =
+        __dadd_rn(__dmul_rn(mu, static_cast<double>(mom[i])), __ddiv_rn(total, static_cast<double>(P)));
     mom[i] = static_cast<TV>(mnew);
     v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), mnew));
   }
@@ -179,24 +176,43 @@ __global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes
 }  // namespace lags
 
 // ==========================================================================================
-// C ABI
+// host side
 // ==========================================================================================
 
 using namespace lags;
 
+struct lags_bucket {
+  int32_t dtype = 0, nlayers = 0, ntasks = 0, max_world = 1, cap = 0, smem_keys = 0;
+  int64_t n_total = 0, total_k = 0;
+  int64_t off_cnt = 0, off_idx = 0, off_val = 0, msg_bytes = 0;
+  // device pointers inside the caller's memory
+  lags_layer_t* layers = nullptr;
+  int2* layer_tasks = nullptr;
+  FastState* state = nullptr;
+  Task* tasks = nullptr;
+  int32_t* slot_layer = nullptr;
+  int32_t* cand_cnt = nullptr;
+  int32_t* cand_idx = nullptr;
+  float* cand_val = nullptr;
+  int32_t* gidx = nullptr;
+  float* gval = nullptr;
+  double* acc64 = nullptr;
+  uint32_t* mask = nullptr;
+  char* planes = nullptr;
+};
+
 namespace {
 thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
 
-std::atomic<unsigned long long> g_launches{0};
-
 int cuda_check(const char* where, int launches = 1) {
   g_launches.fetch_add(static_cast<unsigned long long>(launches), std::memory_order_relaxed);
-  cudaError_t e = cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
   return LAGS_OK;
 }
@@ -216,100 +232,265 @@ int num_sms() {
 
 int stream_grid(int64_t work_items, int threads, int per_sm) {
   int64_t blocks = (work_items + threads - 1) / threads;
-  int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
+  const int64_t cap = static_cast<int64_t>(num_sms()) * per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return static_cast<int>(blocks);
 }
 
 bool valid_dtype(int32_t dtype) { return dtype == LAGS_F32 || dtype == LAGS_F64 || dtype == LAGS_F32_ACC64; }
-size_t acc_size(int32_t dtype) { return dtype == LAGS_F32 ? 4 : 8; }
+size_t val_size(int32_t dtype) { return dtype == LAGS_F32 ? 4 : 8; }
 
-template <typename TIn, typename TAcc>
-int launch_accum(const void* g, void* r, void* acc, double alpha, int64_t n, uint32_t* status, cudaStream_t s) {
-  const TAcc a = static_cast<TAcc>(alpha);  // numpy casts a Python float to the array dtype (NEP 50)
-  accum_scalar_kernel<TIn, TAcc><<<stream_grid(n, 256, 8), 256, 0, s>>>(
-      static_cast<const TIn*>(g), static_cast<TIn*>(r), static_cast<TAcc*>(acc), a, n, status);
-  return cuda_check("accum_scalar_kernel");
-}
+constexpr int SMEM_KEYS = 40960;  // candidate keys kept in shared memory by select_fast_kernel (160 KB)
 
-int launch_accum_f32(const float* g, float* r, double alpha, int64_t n, uint32_t* status, cudaStream_t s) {
-  const float a = static_cast<float>(alpha);
-  const uintptr_t ug = reinterpret_cast<uintptr_t>(g), ur = reinterpret_cast<uintptr_t>(r);
-  if (n >= 1024 && (ug % 16) == (ur % 16) && (ug % 4) == 0) {
-    const int64_t head = static_cast<int64_t>(((16 - ur % 16) % 16) / 4);
-    const int64_t n4 = (n - head) / 4;
-    const int64_t tail0 = head + n4 * 4;
-    if (head) {
-      accum_scalar_kernel<float, float><<<1, 256, 0, s>>>(g, r, r, a, head, status);
-    }
-    accum_f32x4_kernel<<<stream_grid(n4, 256, 8), 256, 0, s>>>(reinterpret_cast<const float4*>(g + head),
-                                                                reinterpret_cast<float4*>(r + head), a, n4,
-                                                                status);
-    if (tail0 < n) {
-      accum_scalar_kernel<float, float><<<1, 256, 0, s>>>(g + tail0, r + tail0, r + tail0, a, n - tail0, status);
-    }
-    return cuda_check("accum_f32x4_kernel", 1 + (head ? 1 : 0) + (tail0 < n ? 1 : 0));
+// Device memory layout shared by lags_bucket_device_bytes and lags_bucket_create.
+struct Plan {
+  int64_t n_total = 0, total_k = 0;
+  int32_t ntasks = 0, cap = 0;
+  size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, bytes = 0;
+};
+
+int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, int32_t max_world, Plan* p) {
+  if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "unknown dtype");
+  if (!dims || !ks || L <= 0) return fail(LAGS_ERR_INVALID_ARG, "empty bucket");
+  if (max_world < 1 || max_world > 32) return fail(LAGS_ERR_INVALID_ARG, "max_world must be in 1..32");
+  double max_density = 0.0;
+  for (int j = 0; j < L; ++j) {
+    if (dims[j] < 1) return fail(LAGS_ERR_STRUCTURE, "layer " + std::to_string(j + 1) + ": dim must be positive");
+    if (dims[j] > 0x7fffffffLL) return fail(LAGS_ERR_INVALID_ARG, "layer dim exceeds the int32 index range");
+    if (ks[j] < 1 || ks[j] > dims[j])
+      return fail(LAGS_ERR_K_OUT_OF_RANGE, "k=" + std::to_string(ks[j]) + " outside 1.." + std::to_string(dims[j]));
+    p->n_total += dims[j];
+    p->total_k += ks[j];
+    p->ntasks += static_cast<int32_t>((dims[j] + TASK_ELEMS - 1) / TASK_ELEMS);
+    if (dims[j] > SMALL_LAYER) max_density = std::max(max_density, static_cast<double>(ks[j]) / dims[j]);
   }
-  accum_scalar_kernel<float, float><<<stream_grid(n, 256, 8), 256, 0, s>>>(g, r, r, a, n, status);
-  return cuda_check("accum_scalar_kernel");
+  // per-task candidate capacity: 16x the expected PRED_FACTOR*k/d share, power of two in [256, TASK]
+  const double want = 16.0 * PRED_FACTOR * max_density * TASK_ELEMS;
+  int cap = 256;
+  while (cap < want && cap < TASK_ELEMS) cap <<= 1;
+  p->cap = dtype == LAGS_F32 ? cap : 0;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  const size_t nt = static_cast<size_t>(p->ntasks), cp = static_cast<size_t>(p->cap);
+  p->o_layers = take(sizeof(lags_layer_t) * L);
+  p->o_ltasks = take(sizeof(int2) * L);
+  p->o_state = take(sizeof(FastState) * L);
+  p->o_tasks = take(sizeof(Task) * nt);
+  p->o_slot = take(sizeof(int32_t) * static_cast<size_t>(p->total_k));
+  p->o_ccnt = take(sizeof(int32_t) * nt);
+  p->o_cidx = take(sizeof(int32_t) * nt * cp);
+  p->o_cval = take(sizeof(float) * nt * cp);
+  p->o_gidx = take(sizeof(int32_t) * nt * cp);
+  p->o_gval = take(sizeof(float) * nt * cp);
+  p->o_acc = take(dtype == LAGS_F32_ACC64 ? sizeof(double) * static_cast<size_t>(p->n_total) : 0);
+  p->o_mask = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total));
+  p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
+  p->bytes = o;
+  return LAGS_OK;
 }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
 
 extern "C" {
 
-int lags_abi_version(void) { return 1; }
-
+int lags_abi_version(void) { return 2; }
+const char* lags_last_error(void) { return g_last_error.c_str(); }
 unsigned long long lags_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
-const char* lags_last_error(void) { return g_last_error.c_str(); }
-
-size_t lags_compress_workspace_bytes(int32_t dtype, int32_t nlayers, int64_t n_total, int64_t total_k) {
-  (void)nlayers;
-  (void)total_k;
-  size_t b = 256;
-  if (dtype == LAGS_F32_ACC64) b += align_up(static_cast<size_t>(n_total) * 8, 256);
-  return b;
+size_t lags_bucket_device_bytes(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t nlayers,
+                                int32_t max_world) {
+  Plan p;
+  if (make_plan(dtype, dims, ks, nlayers, max_world, &p) != LAGS_OK) return 0;
+  return p.bytes + 256;  // slack for aligning the caller's pointer
 }
 
-int lags_compress(int32_t dtype, const lags_layer_t* layers, int32_t nlayers, int64_t n_total, int64_t total_k,
-                  const void* g, void* r, double alpha, int32_t* idx_out, void* val_out, int32_t* count_out,
-                  uint32_t* status, lags_layer_state_t* state, void* workspace, size_t workspace_bytes,
-                  lags_stream_t stream) {
-  (void)state;
-  if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "lags_compress: unknown dtype");
-  if (!layers || nlayers <= 0 || n_total <= 0 || !g || !r || !idx_out || !val_out || !count_out || !status)
-    return fail(LAGS_ERR_INVALID_ARG, "lags_compress: null pointer or empty bucket");
-  if (total_k <= 0) return fail(LAGS_ERR_INVALID_ARG, "lags_compress: total_k must be positive");
-  if (workspace_bytes < lags_compress_workspace_bytes(dtype, nlayers, n_total, total_k))
-    return fail(LAGS_ERR_WORKSPACE, "lags_compress: workspace too small");
+int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t nlayers, int32_t max_world,
+                       void* device_mem, size_t bytes, lags_stream_t stream, lags_bucket_t** out) {
+  if (!out || !device_mem) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_create: null pointer");
+  Plan p;
+  const int rc = make_plan(dtype, dims, ks, nlayers, max_world, &p);
+  if (rc) return rc;
+  char* base = reinterpret_cast<char*>(align_up(reinterpret_cast<uintptr_t>(device_mem), 256));
+  if (base + p.bytes > static_cast<char*>(device_mem) + bytes)
+    return fail(LAGS_ERR_WORKSPACE, "lags_bucket_create: device memory too small");
+  lags_bucket* b = new lags_bucket();
+  b->dtype = dtype;
+  b->nlayers = nlayers;
+  b->ntasks = p.ntasks;
+  b->max_world = max_world;
+  b->cap = p.cap;
+  b->n_total = p.n_total;
+  b->total_k = p.total_k;
+  b->layers = reinterpret_cast<lags_layer_t*>(base + p.o_layers);
+  b->layer_tasks = reinterpret_cast<int2*>(base + p.o_ltasks);
+  b->state = reinterpret_cast<FastState*>(base + p.o_state);
+  b->tasks = reinterpret_cast<Task*>(base + p.o_tasks);
+  b->slot_layer = reinterpret_cast<int32_t*>(base + p.o_slot);
+  b->cand_cnt = reinterpret_cast<int32_t*>(base + p.o_ccnt);
+  b->cand_idx = reinterpret_cast<int32_t*>(base + p.o_cidx);
+  b->cand_val = reinterpret_cast<float*>(base + p.o_cval);
+  b->gidx = reinterpret_cast<int32_t*>(base + p.o_gidx);
+  b->gval = reinterpret_cast<float*>(base + p.o_gval);
+  b->acc64 = reinterpret_cast<double*>(base + p.o_acc);
+  b->mask = reinterpret_cast<uint32_t*>(base + p.o_mask);
+  b->planes = base + p.o_planes;
+  b->off_cnt = 0;
+  b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
+  b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
+  b->msg_bytes = static_cast<int64_t>(align_up(b->off_val + val_size(dtype) * static_cast<size_t>(p.total_k), 16));
+  // host tables
+  std::vector<lags_layer_t> layers(nlayers);
+  std::vector<int2> ltasks(nlayers);
+  std::vector<Task> tasks;
+  std::vector<int32_t> slot_layer(static_cast<size_t>(p.total_k));
+  tasks.reserve(p.ntasks);
+  int64_t off = 0, slot = 0;
+  for (int j = 0; j < nlayers; ++j) {
+    layers[j] = lags_layer_t{off, dims[j], ks[j], static_cast<int32_t>(slot)};
+    ltasks[j].x = static_cast<int>(tasks.size());
+    for (int64_t s = 0; s < dims[j]; s += TASK_ELEMS)
+      tasks.push_back(Task{off + s, static_cast<int32_t>(std::min<int64_t>(TASK_ELEMS, dims[j] - s)), j});
+    ltasks[j].y = static_cast<int>(tasks.size());
+    for (int32_t q = 0; q < ks[j]; ++q) slot_layer[slot + q] = j;
+    off += dims[j];
+    slot += ks[j];
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  int rc;
+  const bool ok =
+      cudaMemcpyAsync(b->layers, layers.data(), sizeof(lags_layer_t) * nlayers, cudaMemcpyHostToDevice, s) ==
+          cudaSuccess &&
+      cudaMemcpyAsync(b->layer_tasks, ltasks.data(), sizeof(int2) * nlayers, cudaMemcpyHostToDevice, s) ==
+          cudaSuccess &&
+      cudaMemcpyAsync(b->tasks, tasks.data(), sizeof(Task) * tasks.size(), cudaMemcpyHostToDevice, s) == cudaSuccess &&
+      cudaMemcpyAsync(b->slot_layer, slot_layer.data(), sizeof(int32_t) * slot_layer.size(), cudaMemcpyHostToDevice,
+                      s) == cudaSuccess &&
+      cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
+      cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
+      cudaStreamSynchronize(s) == cudaSuccess;
+  if (!ok) {
+    delete b;
+    return cuda_check("lags_bucket_create upload", 0);
+  }
   if (dtype == LAGS_F32) {
-    rc = launch_accum_f32(static_cast<const float*>(g), static_cast<float*>(r), alpha, n_total, status, s);
-    if (rc) return rc;
-    select_kernel<float><<<nlayers, SEL_NT, 0, s>>>(layers, lags_layer_t{}, static_cast<float*>(r), idx_out,
-                                                    static_cast<float*>(val_out), count_out, 1);
-    return cuda_check("select_kernel<float>");
+    const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
+    if (cudaFuncSetAttribute(select_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+      delete b;
+      return cuda_check("cudaFuncSetAttribute(select_fast_kernel)", 0);
+    }
+    b->smem_keys = SMEM_KEYS;
   }
-  if (dtype == LAGS_F64) {
-    rc = launch_accum<double, double>(g, r, r, alpha, n_total, status, s);
-    if (rc) return rc;
-    select_kernel<double><<<nlayers, SEL_NT, 0, s>>>(layers, lags_layer_t{}, static_cast<double*>(r), idx_out,
-                                                     static_cast<double*>(val_out), count_out, 1);
-    return cuda_check("select_kernel<double>");
+  *out = b;
+  return LAGS_OK;
+}
+
+void lags_bucket_destroy(lags_bucket_t* bucket) { delete bucket; }
+
+int lags_bucket_message_layout(const lags_bucket_t* b, int64_t* off_counts, int64_t* off_idx, int64_t* off_val,
+                               int64_t* msg_bytes) {
+  if (!b) return fail(LAGS_ERR_INVALID_ARG, "null bucket");
+  if (off_counts) *off_counts = b->off_cnt;
+  if (off_idx) *off_idx = b->off_idx;
+  if (off_val) *off_val = b->off_val;
+  if (msg_bytes) *msg_bytes = b->msg_bytes;
+  return LAGS_OK;
+}
+
+int lags_bucket_compress(lags_bucket_t* b, const void* g, void* r, double alpha, void* msg, uint32_t* status,
+                         uint32_t flags, lags_stream_t stream) {
+  if (!b || !g || !r || !msg || !status) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
+  if (!aligned16(g) || !aligned16(r) || !aligned16(msg))
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: buffers must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  char* m = static_cast<char*>(msg);
+  int32_t* cnt = reinterpret_cast<int32_t*>(m + b->off_cnt);
+  int32_t* idx = reinterpret_cast<int32_t*>(m + b->off_idx);
+  const int64_t n = b->n_total;
+  if (b->dtype == LAGS_F32) {
+    const bool exact = (flags & LAGS_COMPRESS_EXACT) != 0;
+    const float a = static_cast<float>(alpha);  // numpy casts a Python float to float32 (NEP 50)
+    const int blocks = (b->ntasks + K1_WARPS - 1) / K1_WARPS;
+    accum_emit_kernel<<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
+                                                        static_cast<const float*>(g), static_cast<float*>(r), a, b->cap,
+                                                        b->cand_idx, b->cand_val, b->cand_cnt, status);
+    select_fast_kernel<<<b->nlayers, SEL_NT, b->smem_keys * sizeof(uint32_t), s>>>(
+        b->layers, b->layer_tasks, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval,
+        static_cast<float*>(r), idx, reinterpret_cast<float*>(m + b->off_val), cnt, b->smem_keys, exact ? 1 : 0);
+    return cuda_check("lags_bucket_compress(f32)", 2);
   }
-  // LAGS_F32_ACC64: fp64 acc in the workspace, fp32 residual written back after selection.
-  double* acc = reinterpret_cast<double*>(align_up(reinterpret_cast<uintptr_t>(workspace), 256));
-  rc = launch_accum<float, double>(g, r, acc, alpha, n_total, status, s);
-  if (rc) return rc;
-  select_kernel<double><<<nlayers, SEL_NT, 0, s>>>(layers, lags_layer_t{}, acc, idx_out,
-                                                   static_cast<double*>(val_out), count_out, 1);
-  rc = cuda_check("select_kernel<double>");
-  if (rc) return rc;
-  store_residual_kernel<<<stream_grid(n_total, 256, 8), 256, 0, s>>>(acc, static_cast<float*>(r), n_total);
-  return cuda_check("store_residual_kernel");
+  if (b->dtype == LAGS_F64) {
+    accum_kernel<double, double><<<stream_grid(n, 256, 8), 256, 0, s>>>(
+        static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(r), alpha, n, status);
+    select_dense_kernel<double><<<b->nlayers, SEL_NT, 0, s>>>(b->layers, lags_layer_t{}, static_cast<double*>(r), idx,
+                                                              reinterpret_cast<double*>(m + b->off_val), cnt, 1);
+    return cuda_check("lags_bucket_compress(f64)", 2);
+  }
+  // LAGS_F32_ACC64: fp64 acc in the bucket memory, fp32 residual rewritten after selection
+  accum_kernel<float, double><<<stream_grid(n, 256, 8), 256, 0, s>>>(
+      static_cast<const float*>(g), static_cast<float*>(r), b->acc64, alpha, n, status);
+  select_dense_kernel<double><<<b->nlayers, SEL_NT, 0, s>>>(b->layers, lags_layer_t{}, b->acc64, idx,
+                                                            reinterpret_cast<double*>(m + b->off_val), cnt, 1);
+  store_residual_kernel<<<stream_grid(n, 256, 8), 256, 0, s>>>(b->acc64, static_cast<float*>(r), n);
+  return cuda_check("lags_bucket_compress(f32/acc64)", 3);
+}
+
+}  // extern "C"
+
+namespace {
+template <typename TV, typename TVal>
+int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* momentum, double mu, cudaStream_t s) {
+  const int64_t n = b->n_total, S = b->total_k;
+  const int gwork = stream_grid(S * P, 256, 8);
+  TVal* planes = reinterpret_cast<TVal*>(b->planes);
+  if (mu != 0.0) {
+    decode_scatter_kernel<TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, P, planes, n, b->mask);
+    decode_momentum_kernel<TV, TVal><<<stream_grid(n, 256, 8), 256, 0, s>>>(
+        planes, n, b->mask, P, static_cast<TV*>(v), static_cast<TV*>(momentum), mu);
+    return cuda_check("decode(momentum)", 2);
+  }
+  if (P == 1) {
+    decode_single_kernel<TV, TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, static_cast<TV*>(v));
+    return cuda_check("decode(single)", 1);
+  }
+  decode_scatter_kernel<TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, P, planes, n, b->mask);
+  decode_update_kernel<TV, TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, P, planes, n, b->mask,
+                                                       static_cast<TV*>(v));
+  return cuda_check("decode", 2);
+}
+}  // namespace
+
+extern "C" {
+
+int lags_bucket_decode_update(lags_bucket_t* b, const void* msgs, int64_t msg_stride, int32_t P, void* v,
+                              void* momentum, double mu, lags_stream_t stream) {
+  if (!b || !msgs || !v) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: null pointer");
+  if (P < 1 || P > b->max_world)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: P outside 1..max_world");
+  if (P > 1 && msg_stride < b->msg_bytes)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: msg_stride smaller than a message");
+  if (mu != 0.0 && !momentum)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: mu != 0 needs a momentum buffer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const MsgView mv{static_cast<const char*>(msgs), msg_stride, b->off_cnt, b->off_idx, b->off_val};
+  if (b->dtype == LAGS_F32) return decode_impl<float, float>(b, mv, P, v, momentum, mu, s);
+  if (b->dtype == LAGS_F64) return decode_impl<double, double>(b, mv, P, v, momentum, mu, s);
+  return decode_impl<float, double>(b, mv, P, v, momentum, mu, s);
+}
+
+int lags_bucket_stats(const lags_bucket_t* b, uint32_t* out, lags_stream_t stream) {
+  if (!b || !out) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_stats: null pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(out, b->state, sizeof(FastState) * b->nlayers, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return cuda_check("lags_bucket_stats", 0);
+  return LAGS_OK;
 }
 
 int lags_check_finite(int32_t dtype, const void* x, int64_t n, uint32_t* status, lags_stream_t stream) {
@@ -329,101 +510,46 @@ size_t lags_top_k_workspace_bytes(int32_t dtype, int64_t dim) {
 
 int lags_top_k(int32_t dtype, const void* x, int64_t dim, int32_t k, int32_t* idx_out, void* val_out,
                int32_t* count_out, void* workspace, size_t workspace_bytes, lags_stream_t stream) {
-  if (dtype != LAGS_F32 && dtype != LAGS_F64) return fail(LAGS_ERR_INVALID_ARG, "lags_top_k: dtype must be F32 or F64");
-  if (!x || !idx_out || !val_out || !count_out || !workspace) return fail(LAGS_ERR_INVALID_ARG, "lags_top_k: null pointer");
+  if (dtype != LAGS_F32 && dtype != LAGS_F64)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_top_k: dtype must be F32 or F64");
+  if (!x || !idx_out || !val_out || !count_out || !workspace)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_top_k: null pointer");
   if (dim <= 0) return fail(LAGS_ERR_INVALID_ARG, "input must be a non-empty 1-D array");
-  if (k < 1 || k > dim) return fail(LAGS_ERR_K_OUT_OF_RANGE, "k=" + std::to_string(k) + " outside 1.." + std::to_string(dim));
-  if (dim > 0x7fffffffLL) return fail(LAGS_ERR_INVALID_ARG, "lags_top_k: dim exceeds int32 index range");
-  if (workspace_bytes < lags_top_k_workspace_bytes(dtype, dim)) return fail(LAGS_ERR_WORKSPACE, "lags_top_k: workspace too small");
+  if (k < 1 || k > dim)
+    return fail(LAGS_ERR_K_OUT_OF_RANGE, "k=" + std::to_string(k) + " outside 1.." + std::to_string(dim));
+  if (dim > 0x7fffffffLL) return fail(LAGS_ERR_INVALID_ARG, "lags_top_k: dim exceeds the int32 index range");
+  if (workspace_bytes < lags_top_k_workspace_bytes(dtype, dim))
+    return fail(LAGS_ERR_WORKSPACE, "lags_top_k: workspace too small");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t es = dtype == LAGS_F64 ? 8 : 4;
   void* copy = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 256));
   if (cudaMemcpyAsync(copy, x, static_cast<size_t>(dim) * es, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return cuda_check("lags_top_k copy", 0);
-  lags_layer_t one{0, dim, k, 0};
+  const lags_layer_t one{0, dim, k, 0};
   if (dtype == LAGS_F32)
-    select_kernel<float><<<1, SEL_NT, 0, s>>>(nullptr, one, static_cast<float*>(copy), idx_out,
-                                              static_cast<float*>(val_out), count_out, 0);
+    select_dense_kernel<float><<<1, SEL_NT, 0, s>>>(nullptr, one, static_cast<float*>(copy), idx_out,
+                                                    static_cast<float*>(val_out), count_out, 0);
   else
-    select_kernel<double><<<1, SEL_NT, 0, s>>>(nullptr, one, static_cast<double*>(copy), idx_out,
-                                               static_cast<double*>(val_out), count_out, 0);
-  return cuda_check("select_kernel(top_k)");
+    select_dense_kernel<double><<<1, SEL_NT, 0, s>>>(nullptr, one, static_cast<double*>(copy), idx_out,
+                                                     static_cast<double*>(val_out), count_out, 0);
+  return cuda_check("select_dense_kernel(top_k)");
 }
 
 int lags_decompress(int32_t dtype, const int32_t* idx, const void* val, const int32_t* count, int64_t dim, void* out,
                     lags_stream_t stream) {
-  if (dtype != LAGS_F32 && dtype != LAGS_F64) return fail(LAGS_ERR_INVALID_ARG, "lags_decompress: dtype must be F32 or F64");
+  if (dtype != LAGS_F32 && dtype != LAGS_F64)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_decompress: dtype must be F32 or F64");
   if (!idx || !val || !count || !out || dim <= 0) return fail(LAGS_ERR_INVALID_ARG, "lags_decompress: bad argument");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t es = dtype == LAGS_F64 ? 8 : 4;
-  if (cudaMemsetAsync(out, 0, static_cast<size_t>(dim) * es, s) != cudaSuccess) return cuda_check("lags_decompress memset", 0);
+  if (cudaMemsetAsync(out, 0, static_cast<size_t>(dim) * es, s) != cudaSuccess)
+    return cuda_check("lags_decompress memset", 0);
   if (dtype == LAGS_F32)
     decompress_kernel<float><<<64, 256, 0, s>>>(idx, static_cast<const float*>(val), count, static_cast<float*>(out));
   else
-    decompress_kernel<double><<<64, 256, 0, s>>>(idx, static_cast<const double*>(val), count, static_cast<double*>(out));
+    decompress_kernel<double><<<64, 256, 0, s>>>(idx, static_cast<const double*>(val), count,
+                                                 static_cast<double*>(out));
   return cuda_check("decompress_kernel");
-}
-
-size_t lags_decode_workspace_bytes(int32_t dtype, int64_t n_total, int32_t P) {
-  if (!valid_dtype(dtype) || n_total <= 0 || P <= 0) return 0;
-  return align_up(static_cast<size_t>(n_total) * 4, 256) +
-         align_up(static_cast<size_t>(n_total) * static_cast<size_t>(P) * acc_size(dtype), 256);
-}
-
-int lags_decode_update(int32_t dtype, const lags_layer_t* layers, int32_t nlayers, int64_t n_total, int64_t total_k,
-                       const int32_t* idx0, const void* val0, const int32_t* cnt0, int64_t rank_stride_bytes, int32_t P,
-                       void* v, void* momentum, double mu, void* workspace, size_t workspace_bytes,
-                       lags_stream_t stream) {
-  (void)total_k;
-  if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "lags_decode_update: unknown dtype");
-  if (!layers || nlayers <= 0 || n_total <= 0 || !idx0 || !val0 || !cnt0 || !v || !workspace)
-    return fail(LAGS_ERR_INVALID_ARG, "lags_decode_update: null pointer or empty bucket");
-  if (P < 1 || P > 32) return fail(LAGS_ERR_INVALID_ARG, "lags_decode_update: P must be in 1..32");
-  if (mu != 0.0 && !momentum) return fail(LAGS_ERR_INVALID_ARG, "lags_decode_update: mu > 0 needs a momentum buffer");
-  if (workspace_bytes < lags_decode_workspace_bytes(dtype, n_total, P))
-    return fail(LAGS_ERR_WORKSPACE, "lags_decode_update: workspace too small");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  uint32_t* mask = static_cast<uint32_t*>(workspace);
-  char* planes = static_cast<char*>(workspace) + align_up(static_cast<size_t>(n_total) * 4, 256);
-  const char* mi = reinterpret_cast<const char*>(idx0);
-  const char* mv = static_cast<const char*>(val0);
-  const char* mc = reinterpret_cast<const char*>(cnt0);
-  dim3 grid(nlayers, P);
-  if (dtype == LAGS_F32) {
-    decode_scatter_kernel<float><<<grid, 256, 0, s>>>(layers, mi, mv, mc, rank_stride_bytes,
-                                                      reinterpret_cast<float*>(planes), n_total, mask);
-    if (mu == 0.0)
-      decode_update_kernel<float, float><<<grid, 256, 0, s>>>(layers, mi, mc, rank_stride_bytes,
-                                                              reinterpret_cast<const float*>(planes), n_total,
-                                                              mask, P, static_cast<float*>(v));
-    else
-      decode_momentum_kernel<float, float><<<stream_grid(n_total, 256, 8), 256, 0, s>>>(
-          reinterpret_cast<const float*>(planes), n_total, mask, P, static_cast<float*>(v),
-          static_cast<float*>(momentum), mu);
-  } else if (dtype == LAGS_F64) {
-    decode_scatter_kernel<double><<<grid, 256, 0, s>>>(layers, mi, mv, mc, rank_stride_bytes,
-                                                       reinterpret_cast<double*>(planes), n_total, mask);
-    if (mu == 0.0)
-      decode_update_kernel<double, double><<<grid, 256, 0, s>>>(layers, mi, mc, rank_stride_bytes,
-                                                                reinterpret_cast<const double*>(planes), n_total,
-                                                                mask, P, static_cast<double*>(v));
-    else
-      decode_momentum_kernel<double, double><<<stream_grid(n_total, 256, 8), 256, 0, s>>>(
-          reinterpret_cast<const double*>(planes), n_total, mask, P, static_cast<double*>(v),
-          static_cast<double*>(momentum), mu);
-  } else {
-    decode_scatter_kernel<double><<<grid, 256, 0, s>>>(layers, mi, mv, mc, rank_stride_bytes,
-                                                       reinterpret_cast<double*>(planes), n_total, mask);
-    if (mu == 0.0)
-      decode_update_kernel<float, double><<<grid, 256, 0, s>>>(layers, mi, mc, rank_stride_bytes,
-                                                               reinterpret_cast<const double*>(planes), n_total,
-                                                               mask, P, static_cast<float*>(v));
-    else
-      decode_momentum_kernel<float, double><<<stream_grid(n_total, 256, 8), 256, 0, s>>>(
-          reinterpret_cast<const double*>(planes), n_total, mask, P, static_cast<float*>(v),
-          static_cast<float*>(momentum), mu);
-  }
-  return cuda_check("decode kernels", 2);
 }
 
 }  // extern "C"

@@ -1,9 +1,9 @@
-// Exact per-layer top-k selection + ordered compaction, one CTA per layer.
+// Exact top-k selection machinery (one CTA): radix select on magnitude keys + ordered compaction.
 //
 // Replaces R: sparsify.py:84-90 (|x|, stable argsort, drop zeros, sort indices) and the residual
-// rule of R: training.py:252 (selected residual entries become +0.0).  Selection works on the
-// magnitude key (Key<T>): the k largest keys win, ties go to the lower index, key == 0 is never
-// selected.  Output indices are produced in ascending order by an ordered block scan.
+// rule of R: training.py:252 (selected residual entries become +0.0).  The k largest keys win,
+// ties go to the lower index (= earlier position in the scanned order), key == 0 is never
+// selected.  Output indices come out ascending because the compaction is an ordered block scan.
 #pragma once
 #include "lags_common.cuh"
 
@@ -12,8 +12,8 @@ namespace lags {
 constexpr int SEL_NT = 1024;  // threads per selection CTA
 constexpr int SEL_VEC = 4;    // consecutive elements per thread per compaction chunk
 
-// Radix-select result for one layer: select key with (key & pmask) > prefix, plus the first
-// `need_eq` (in index order) with (key & pmask) == prefix.
+// Select (key & pmask) > prefix, plus the first `need_eq` (in scan order) with
+// (key & pmask) == prefix.  `full_key` is the resolved threshold (valid when pmask is full).
 template <typename K>
 struct SelectThreshold {
   K prefix;
@@ -22,29 +22,27 @@ struct SelectThreshold {
   uint32_t need_eq;
 };
 
-// Shared memory for one selection CTA.
-template <typename T>
-struct SelectSmem {
-  static constexpr int NB = 1 << Key<T>::RB;
+template <int RB>
+struct RadixSmem {
+  static constexpr int NB = 1 << RB;
   uint32_t hist[NB];
   uint32_t warp_tot[33];
-  typename Key<T>::K prefix, pmask;
-  uint32_t n_gt, rank, bin_count;
+  uint32_t above, bin_count;
   int found;
 };
 
-// Find the digit bin holding the rank-th largest (1-based) among the histogram; descending scan.
-template <typename T>
-__device__ __forceinline__ void find_bin(SelectSmem<T>& sm, uint32_t rank, uint32_t* bin, uint32_t* above,
+// Bin holding the rank-th largest (1-based) of the histogram (descending scan).  All threads.
+template <int RB>
+__device__ __forceinline__ void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint32_t* bin, uint32_t* above,
                                          uint32_t* in_bin) {
-  constexpr int NB = SelectSmem<T>::NB;
-  constexpr int PER = NB / SEL_NT;  // bins per thread (2 for fp32, 8 for fp64)
+  constexpr int NB = RadixSmem<RB>::NB;
+  constexpr int PER = NB / SEL_NT;  // 2 (fp32) or 8 (fp64) bins per thread
   const int t = threadIdx.x;
   uint32_t s = 0;
 #pragma unroll
   for (int q = 0; q < PER; ++q) s += sm.hist[NB - 1 - t * PER - q];
   uint32_t tot;
-  uint32_t ex = block_exclusive_scan<SEL_NT>(s, sm.warp_tot, &tot);
+  const uint32_t ex = block_exclusive_scan<SEL_NT>(s, sm.warp_tot, &tot);
   if (ex < rank && rank <= ex + s) {
     uint32_t c = ex;
 #pragma unroll
@@ -53,7 +51,7 @@ __device__ __forceinline__ void find_bin(SelectSmem<T>& sm, uint32_t rank, uint3
       const uint32_t h = sm.hist[b];
       if (rank <= c + h) {
         sm.bin_count = h;
-        sm.n_gt = c;  // temporarily: count strictly above bin b within the prefix
+        sm.above = c;
         sm.found = b;
         break;
       }
@@ -62,45 +60,54 @@ __device__ __forceinline__ void find_bin(SelectSmem<T>& sm, uint32_t rank, uint3
   }
   __syncthreads();
   *bin = static_cast<uint32_t>(sm.found);
-  *above = sm.n_gt;
+  *above = sm.above;
   *in_bin = sm.bin_count;
   __syncthreads();
 }
 
-// Multi-pass radix select over data[0:d) (global memory).  All threads return the same result.
-template <typename T>
-__device__ SelectThreshold<typename Key<T>::K> radix_select(const T* data, int64_t d, uint32_t k,
-                                                            SelectSmem<T>& sm) {
-  using K = typename Key<T>::K;
-  constexpr int BITS = Key<T>::BITS, RB = Key<T>::RB, NB = SelectSmem<T>::NB;
+// Multi-pass radix select over m keys produced by key_at(i).  Returns the threshold of the
+// k largest.  If pred_rank > 0, *pred_key receives the lower edge of the first-digit bin that
+// holds the pred_rank-th largest key (used to predict next call's candidate threshold).
+template <typename K, int BITS, int RB, typename KeyAt>
+__device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, RadixSmem<RB>& sm,
+                                           uint32_t pred_rank = 0, K* pred_key = nullptr) {
+  constexpr int NB = RadixSmem<RB>::NB;
   SelectThreshold<K> th;
-  if (static_cast<int64_t>(k) >= d) {  // everything nonzero is selected
+  K prefix = 0, pmask = 0;
+  uint32_t rank = k, n_gt = 0;
+  int shift = BITS - RB, width = RB;
+  bool first = true;
+  if (static_cast<int64_t>(k) >= m && pred_rank == 0) {  // everything nonzero is selected
     th.prefix = 0;
     th.pmask = ~K(0);
     th.n_gt = 0;
     th.need_eq = 0;
     return th;
   }
-  K prefix = 0, pmask = 0;
-  uint32_t rank = k, n_gt = 0;
-  int shift = BITS - RB, width = RB;
+  if (static_cast<int64_t>(rank) > m) rank = static_cast<uint32_t>(m);
   while (true) {
     for (int b = threadIdx.x; b < NB; b += SEL_NT) sm.hist[b] = 0;
     __syncthreads();
     const K dmask = (K(1) << width) - 1;
-    for (int64_t i = threadIdx.x; i < d; i += SEL_NT) {
-      const K key = Key<T>::of(data[i]);
+    for (int64_t i = threadIdx.x; i < m; i += SEL_NT) {
+      const K key = key_at(i);
       if ((key & pmask) == prefix) atomicAdd(&sm.hist[(key >> shift) & dmask], 1u);
     }
     __syncthreads();
     uint32_t b, above, in_bin;
-    find_bin<T>(sm, rank, &b, &above, &in_bin);
+    if (first && pred_rank > 0) {
+      const uint32_t pr = static_cast<int64_t>(pred_rank) < m ? pred_rank : static_cast<uint32_t>(m);
+      find_bin<RB>(sm, pr, &b, &above, &in_bin);
+      *pred_key = K(b) << shift;
+    }
+    first = false;
+    find_bin<RB>(sm, rank, &b, &above, &in_bin);
     prefix |= K(b) << shift;
     pmask |= dmask << shift;
     n_gt += above;
     rank -= above;
     if (shift == 0) break;
-    if (in_bin == rank && prefix != 0) break;  // the whole bin is taken: no need to resolve lower bits
+    if (in_bin == rank && prefix != 0) break;  // the whole bin is taken: lower bits irrelevant
     const int ns = shift > RB ? shift - RB : 0;
     width = shift - ns;
     shift = ns;
@@ -111,29 +118,37 @@ __device__ SelectThreshold<typename Key<T>::K> radix_select(const T* data, int64
   // prefix == 0 only survives to full resolution (the early exit requires prefix != 0); a zero
   // threshold means "every nonzero key": zeros are never selected (R: sparsify.py:88).
   th.need_eq = prefix == 0 ? 0u : rank;
+  if (static_cast<int64_t>(k) >= m) {  // pred-only call: select every nonzero
+    th.prefix = 0;
+    th.pmask = ~K(0);
+    th.n_gt = 0;
+    th.need_eq = 0;
+  }
   return th;
 }
 
-// Ordered compaction of data[0:d) under threshold `th`: writes ascending local indices and
-// values of the selected entries into idx_out/val_out, optionally zeroes them in `data`
-// (the residual rule), returns the count (all threads).
-template <typename T>
-__device__ uint32_t ordered_compact(T* data, int64_t d, const SelectThreshold<typename Key<T>::K>& th,
-                                    int32_t* idx_out, T* val_out, bool zero_selected, SelectSmem<T>& sm) {
-  using K = typename Key<T>::K;
+// Ordered compaction of m entries (scan order = ascending index) under threshold th.
+// load(i, &key, &val, &index) fetches entry i; emit(pos, i, index, val) writes selected entry i
+// to output position pos.  Returns the selected count (all threads).
+template <typename K, typename T, typename Load, typename Emit, int RB>
+__device__ uint32_t ordered_compact(int64_t m, const SelectThreshold<K>& th, Load load, Emit emit,
+                                    RadixSmem<RB>& sm) {
   uint32_t carry_gt = 0, carry_eq = 0;
   const int64_t chunk = static_cast<int64_t>(SEL_NT) * SEL_VEC;
-  for (int64_t base = 0; base < d; base += chunk) {
+  for (int64_t base = 0; base < m; base += chunk) {
     const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * SEL_VEC;
     T x[SEL_VEC];
+    int64_t ix[SEL_VEC];
     uint32_t gtm = 0, eqm = 0;
 #pragma unroll
     for (int v = 0; v < SEL_VEC; ++v) {
       const int64_t i = i0 + v;
-      x[v] = i < d ? data[i] : T(0);
-      const K key = Key<T>::of(x[v]);
+      K key = 0;
+      x[v] = T(0);
+      ix[v] = 0;
+      if (i < m) load(i, &key, &x[v], &ix[v]);
       const K hi = key & th.pmask;
-      if (i < d && key != 0) {
+      if (key != 0) {
         if (hi > th.prefix) gtm |= 1u << v;
         else if (hi == th.prefix) eqm |= 1u << v;
       }
@@ -147,13 +162,7 @@ __device__ uint32_t ordered_compact(T* data, int64_t d, const SelectThreshold<ty
 #pragma unroll
       for (int v = 0; v < SEL_VEC; ++v) {
         const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
-        bool take = g || (e && eq_before < th.need_eq);
-        if (take) {
-          const uint32_t pos = gt_before + min(eq_before, th.need_eq);
-          idx_out[pos] = static_cast<int32_t>(i0 + v);
-          val_out[pos] = x[v];
-          if (zero_selected) data[i0 + v] = T(0);  // acc - acc == +0.0 (R: training.py:252)
-        }
+        if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), i0 + v, ix[v], x[v]);
         gt_before += g;
         eq_before += e;
       }
@@ -163,6 +172,29 @@ __device__ uint32_t ordered_compact(T* data, int64_t d, const SelectThreshold<ty
     __syncthreads();  // warp_tot reuse by the next scan
   }
   return carry_gt + min(carry_eq, th.need_eq);
+}
+
+// Exact top-k of dense data[0:d) (global memory) by one CTA: select + ordered compaction,
+// optionally zeroing the selected entries in place.  Returns count; *pred receives the
+// predicted candidate threshold for rank pred_rank (if pred_rank > 0).
+template <typename T, typename TOut>
+__device__ uint32_t exact_topk_dense(T* data, int64_t d, uint32_t k, int32_t* idx_out, TOut* val_out,
+                                     bool zero_selected, RadixSmem<Key<T>::RB>& sm, uint32_t pred_rank = 0,
+                                     typename Key<T>::K* pred = nullptr) {
+  using K = typename Key<T>::K;
+  auto key_at = [data](int64_t i) { return Key<T>::of(data[i]); };
+  const auto th = radix_select<K, Key<T>::BITS, Key<T>::RB>(key_at, d, k, sm, pred_rank, pred);
+  auto load = [data](int64_t i, K* key, T* x, int64_t* ix) {
+    *x = data[i];
+    *key = Key<T>::of(*x);
+    *ix = i;
+  };
+  auto emit = [=](uint32_t pos, int64_t i, int64_t ix, T x) {
+    idx_out[pos] = static_cast<int32_t>(ix);
+    val_out[pos] = static_cast<TOut>(x);
+    if (zero_selected) data[i] = T(0);  // acc - acc == +0.0 (R: training.py:252)
+  };
+  return ordered_compact<K, T>(d, th, load, emit, sm);
 }
 
 }  // namespace lags

@@ -63,13 +63,13 @@ def mode_for(dtype, alpha) -> int:
 _BUCKETS: dict = {}
 
 
-def _bucket_for(dims: tuple, ks: tuple, mode: int) -> Bucket:
-    key = (dims, ks, mode, torch.cuda.current_device())
+def _bucket_for(dims: tuple, ks: tuple, mode: int, world: int) -> Bucket:
+    key = (dims, ks, mode, world, torch.cuda.current_device())
     b = _BUCKETS.get(key)
     if b is None:
-        if len(_BUCKETS) > 32:
+        if len(_BUCKETS) > 16:
             _BUCKETS.clear()
-        b = Bucket(dims, ks, mode)
+        b = Bucket(dims, ks, mode, max_world=world)
         _BUCKETS[key] = b
     return b
 
@@ -111,7 +111,7 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
         if not 1 <= k <= d:  # R: sparsify.py:82-83 (raised before any residual is touched)
             raise ValueError(f"k={k} outside 1..{d}")
         ks.append(k)
-    bucket = _bucket_for(dims, tuple(ks), mode)
+    bucket = _bucket_for(dims, tuple(ks), mode, P)
 
     v_d = _to_dev(v.data)
     msgs = bucket.new_messages(P)

@@ -16,12 +16,13 @@ HEADER = os.path.join(ROOT, "include", "lags_b200.h")
 def declared_functions():
     text = open(HEADER).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*|unsigned long long)\s+(lags_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void|size_t|const char\*|unsigned long long)\s+(lags_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_entry_points():
     names = declared_functions()
-    for must in ("lags_compress", "lags_decode_update", "lags_top_k", "lags_decompress", "lags_check_finite"):
+    for must in ("lags_bucket_compress", "lags_bucket_decode_update", "lags_bucket_create", "lags_top_k",
+                 "lags_decompress", "lags_check_finite"):
         assert must in names
 
 
@@ -32,14 +33,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     assert set(N.EXPORTS) == set(declared_functions())
-    assert N.lags_abi_version() == 1
-
-
-def test_layer_struct_layout():
-    import paper_1911_08727_b200._native as N
-
-    assert N.LAYER_DTYPE.itemsize == 24
-    assert N.LAYER_DTYPE.fields["k"][1] == 16 and N.LAYER_DTYPE.fields["slot"][1] == 20
+    assert N.lags_abi_version() == 2
 
 
 def test_argument_errors_map_to_reference_exceptions():
@@ -55,18 +49,29 @@ def test_argument_errors_map_to_reference_exceptions():
     assert rc == N.ERR_K_OUT_OF_RANGE
     with pytest.raises(ValueError, match="outside 1..10"):
         N.check(rc)
-    assert N.lags_compress(7, None, 0, 0, 0, None, None, 0.0, None, None, None, None, None, None, 0, None) \
-        == N.ERR_INVALID_ARG
-    assert N.lags_decode_update(N.F32, fake, 1, 10, 1, fake, fake, fake, 64, 33, fake, None, 0.0, fake, 1 << 30,
-                                None) == N.ERR_INVALID_ARG
+    assert N.lags_bucket_compress(None, None, None, 0.0, None, None, 0, None) == N.ERR_INVALID_ARG
+    assert N.lags_bucket_decode_update(None, fake, 64, 1, fake, None, 0.0, None) == N.ERR_INVALID_ARG
+    # bucket creation validates k before touching the device (R: sparsify.py:82-83)
+    dims = np.array([10, 5], dtype=np.int64)
+    ks = np.array([3, 6], dtype=np.int32)
+    assert N.lags_bucket_device_bytes(N.F32, dims.ctypes.data, ks.ctypes.data, 2, 1) == 0
+    h = ctypes.c_void_p()
+    rc = N.lags_bucket_create(N.F32, dims.ctypes.data, ks.ctypes.data, 2, 1, fake, 1 << 20, None, ctypes.byref(h))
+    assert rc == N.ERR_K_OUT_OF_RANGE and b"outside 1..5" in N.lags_last_error()
 
 
 def test_workspace_sizes():
     import paper_1911_08727_b200._native as N
+    from bench import resnet50_dims, ks_for
 
-    n = 25_557_032
-    assert N.lags_decode_workspace_bytes(N.F32, n, 8) >= n * 4 + 8 * n * 4
-    assert N.lags_compress_workspace_bytes(N.F32_ACC64, 161, n, 25595) >= n * 8
+    dims = resnet50_dims()
+    d = np.asarray(dims, dtype=np.int64)
+    k = np.asarray(ks_for(dims), dtype=np.int32)
+    n = int(d.sum())
+    b1 = N.lags_bucket_device_bytes(N.F32, d.ctypes.data, k.ctypes.data, len(dims), 1)
+    b8 = N.lags_bucket_device_bytes(N.F32, d.ctypes.data, k.ctypes.data, len(dims), 8)
+    assert b8 - b1 >= 7 * 4 * n - 4096  # one decode plane per extra rank
+    assert b1 < 512 * 2**20
     assert N.lags_top_k_workspace_bytes(N.F64, 1000) >= 8000
 
 

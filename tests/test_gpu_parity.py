@@ -198,6 +198,73 @@ def test_bucket_device_api_and_momentum(L):
     assert int(st.item()) == 0
 
 
+def test_fast_path_equals_exact_path(L):
+    """The predicted-threshold fast path (K1 candidate emission + K2 candidate select) must be
+    bit-identical to the dense exact path on every call: steady state, mispredictions (scale
+    drops), task-list overflow (concentrated gradients) and all-zero layers."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [20000, 64, 300000, 5000, 2359296 // 4, 70001, 1000]
+    ks = [max(1, d // 1000) for d in dims]
+    ks[1] = 64
+    fast = L.Bucket(dims, ks, N.F32)
+    exact = L.Bucket(dims, ks, N.F32)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    r_f = torch.zeros(n, device="cuda")
+    r_e = torch.zeros(n, device="cuda")
+    m_f, m_e = fast.new_messages(1), exact.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    off = np.concatenate([[0], np.cumsum(dims)])
+    for it in range(24):
+        g = torch.randn(n, device="cuda", generator=gen)
+        if it in (9, 10):
+            g *= 1e-3  # threshold collapses -> too few candidates -> dense fallback
+        if it == 14:  # one layer's mass concentrated in one task -> candidate list overflow
+            g[off[2]:off[2] + 8192] *= 1e4
+        if it == 17:
+            g[off[4]:off[5]] = 0.0
+            r_f[off[4]:off[5]] = 0.0
+            r_e[off[4]:off[5]] = 0.0
+        fast.compress(g, r_f, 0.05, m_f, st)
+        exact.compress(g, r_e, 0.05, m_e, st, exact=True)
+        assert torch.equal(m_f, m_e), f"messages differ at iteration {it}"
+        assert torch.equal(r_f.view(torch.int32), r_e.view(torch.int32)), f"residuals differ at {it}"
+    s = fast.stats()
+    big = [j for j, d in enumerate(dims) if d > 16384]
+    assert all(s[j, 3] == 24 for j in range(len(dims)))  # calls
+    assert all(s[j, 2] > 0 or j == 4 for j in big)  # candidate path active on big layers at the end
+    assert int(s[big, 1].sum()) < 8 * len(big)  # fallbacks are the exception
+    assert int(st.item()) == 0
+
+
+def test_fast_path_decode_multi_rank_equals_oracle(L):
+    """P simulated ranks through one bucket: fast compress per rank, rank-ordered decode."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [40000, 17, 123457]
+    ks = [40, 1, 123]
+    P = 5
+    b = L.Bucket(dims, ks, N.F32, max_world=P)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(8)
+    rs = [torch.zeros(n, device="cuda") for _ in range(P)]
+    v = torch.randn(n, device="cuda", generator=gen)
+    msgs = b.new_messages(P)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    v_h = v.cpu().numpy().copy()
+    r_h = [np.zeros(n, np.float32) for _ in range(P)]
+    for it in range(6):
+        gs = [torch.randn(n, device="cuda", generator=gen) for _ in range(P)]
+        for p in range(P):
+            b.compress(gs[p], rs[p], 0.1, msgs[p * b.msg_bytes:(p + 1) * b.msg_bytes], st)
+        b.decode(msgs, P, v)
+        v_h = orc.lags_step(v_h, [g.cpu().numpy() for g in gs], 0.1, dims, ks, r_h)
+        assert _same_bits(v.cpu().numpy(), v_h), it
+        for p in range(P):
+            assert _same_bits(rs[p].cpu().numpy(), r_h[p])
+
+
 def test_large_layer_properties(L):
     """Full-size layer (LSTM embedding, 15M) through the bucket API: size-independent checks
     (count == k, ascending, residual + sent == acc bitwise, selected keys dominate)."""
