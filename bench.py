@@ -76,42 +76,62 @@ class ClockSampler:
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.fh = None
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        self.fh = open(self.path, "w")
         try:
+            # python-side timestamps: one line per sample, read back with arrival times
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
+            import threading
+
+            def pump():
+                for line in self.proc.stdout:
+                    self.fh.write(f"{time.time():.4f},{line}")
+                    self.fh.flush()
+
+            self.thread = threading.Thread(target=pump, daemon=True)
+            self.thread.start()
         except Exception:
             self.proc = None
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.05)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], [], set()
+        self.thread.join(timeout=2)
+        self.fh.close()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 8:
+            if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                rows.append((float(parts[0]), float(parts[2]), float(parts[3]),
+                             {nm for nm, val in zip(names, parts[5:9]) if val.lower() == "active"}))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[4:8]):
-                if val.lower() == "active":
-                    reasons.add(nm)
         os.unlink(self.path)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        window = "timed region"
+        sel = [r for r in rows if t0 is not None and t0 - 0.03 <= r[0] <= t1 + 0.03]
+        if not sel:  # timed region shorter than the sampling period: use the soak right before it
+            window = "untimed soak immediately before the timed region (region shorter than a sample)"
+            sel = [r for r in rows if t0 is not None and r[0] <= t1 + 0.03][-5:]
+        if not sel:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        reasons = set().union(*[r[3] for r in sel])
+        return {"sm_mhz": statistics.median(r[1] for r in sel), "sm_max_mhz": max(r[2] for r in sel),
+                "reasons": sorted(reasons), "samples": len(sel), "window": window}
 
 
 def dist_setup():
@@ -161,26 +181,55 @@ def run_reference(args, dims, ks, world, rank):
     v = rng.standard_normal(n).astype(np.float32)
     grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
     res = [np.zeros(n, np.float32) for _ in range(world)]
-    for _ in range(args.warmup):
-        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
-    times = []
-    for _ in range(args.steps):
+    t0 = time.perf_counter()
+    v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)  # one full step sizes the sample
+    t_full = time.perf_counter() - t0
+    # bound the whole run to ~budget seconds: each step processes one group of layers (groups of
+    # roughly equal element count cycle over the whole model)
+    per_step = args.ref_budget / max(1, args.steps + args.warmup)
+    groups_n = max(1, int(np.ceil(t_full / per_step)))
+    groups, cur, acc, target = [], [], 0, n / groups_n
+    for j, d in enumerate(dims):
+        cur.append(j)
+        acc += d
+        if acc >= target * (len(groups) + 1) and len(groups) < groups_n - 1:
+            groups.append(cur)
+            cur = []
+    if cur:
+        groups.append(cur)
+    off = np.concatenate([[0], np.cumsum(dims)])
+    samples = []
+    for gl in groups:
+        sl = [(off[j], off[j + 1]) for j in gl]
+        gd = [dims[j] for j in gl]
+        gk = [ks[j] for j in gl]
+        cat = lambda a: np.concatenate([a[s:e] for s, e in sl])  # noqa: E731
+        samples.append((gd, gk, cat(v), [cat(g) for g in grads], [cat(r) for r in res]))
+    for i in range(args.warmup):
+        gd, gk, vv, gg, rr = samples[i % len(samples)]
+        orc.lags_step(vv, gg, 0.1, gd, gk, rr, threads=threads)
+    t, done_bytes = 0.0, 0
+    for i in range(args.steps):
+        gd, gk, vv, gg, rr = samples[(args.warmup + i) % len(samples)]
         t0 = time.perf_counter()
-        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
-        times.append(time.perf_counter() - t0)
-    t = sum(times)
-    sel = sum(ks)
-    comp, dec = algorithmic_bytes(n, ks, sel * world, world)
-    val = (comp + dec) * args.steps / t / 1e9
+        orc.lags_step(vv, gg, 0.1, gd, gk, rr, threads=threads)
+        t += time.perf_counter() - t0
+        comp, dec = algorithmic_bytes(sum(gd), gk, sum(gk) * world, world)
+        done_bytes += comp + dec
+    val = done_bytes / t / 1e9
+    cf, df = algorithmic_bytes(n, ks, sum(ks) * world, world)
+    full_bytes = cf + df
     out = {
         "impl": "reference", "metric": METRIC, "value": round(val, 4), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3),
-        "iter_per_s": round(args.steps / t, 4), "higher_is_better": True, "scaling": "weak",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * full_bytes / (val * 1e9), 3),
+        "iter_per_s": round(val * 1e9 / full_bytes, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(dims, ks, world),
         "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full ResNet-50-shaped lags_step with P={world} simulated workers per step "
-                                   f"(numpy oracle port of R: training.py:227-255, layers over {threads} threads)"},
+                         "sample": f"each step = 1 of {len(groups)} layer groups of the ResNet-50-shaped lags_step "
+                                   f"(P={world} simulated workers; full step measured {t_full:.2f} s), numpy oracle "
+                                   f"port of R: training.py:227-255, layers over {threads} threads; ms_per_step and "
+                                   f"iter_per_s are full-model equivalents"},
         "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -204,7 +253,7 @@ def run_ours(args, dims, ks, world, rank, local):
 
     dev = torch.device("cuda", local)
     n = sum(dims)
-    bucket = L.Bucket(dims, ks, N.F32, device=dev)
+    bucket = L.Bucket(dims, ks, N.F32, device=dev, max_world=world)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     NG = 3
     g_bufs = [torch.randn(n, device=dev, generator=gen) for _ in range(NG)]
@@ -227,27 +276,39 @@ def run_ours(args, dims, ks, world, rank, local):
             dist.all_gather_into_tensor(msgs, msg_local)
         bucket.decode(msgs, world, v, stream=stream)
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for t in range(args.warmup):
         step(t)
+    # keep the GPU busy (still untimed warm-up) until clocks have settled and the sampler runs
+    soak_end = time.time() + args.soak
+    t = args.warmup
+    while time.time() < soak_end:
+        for _ in range(50):
+            step(t)
+            t += 1
+        torch.cuda.synchronize(dev)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    stats0 = bucket.stats()
     l0 = N.lags_kernel_launches()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    wall0 = time.time()
     start.record(stream)
     for t in range(args.steps):
         step(t, timed=True)
     stop.record(stream)
     torch.cuda.synchronize(dev)
+    wall1 = time.time()
     if world > 1:
         dist.barrier()
     launches = N.lags_kernel_launches() - l0
-    clk = clocks.stop()
+    clk = clocks.stop(wall0, wall1)
+    stats = bucket.stats()
     ms = start.elapsed_time(stop)
     comp_ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
     t_ms = torch.tensor([ms, comp_ms], dtype=torch.float64, device=dev)
@@ -300,6 +361,10 @@ def run_ours(args, dims, ks, world, rank, local):
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "algorithmic_bytes_per_launch": int(comp_bytes_rank), "ms_per_launch": round(comp_ms, 4)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "selection": {"layers": len(dims),
+                          "dense_fallbacks_in_timed_region": int(stats[:, 1].sum() - stats0[:, 1].sum()),
+                          "candidate_path_layers": int((stats[:, 2] > 0).sum()),
+                          "candidates_per_step": int(stats[:, 2].sum())},
         }
         print(json.dumps(out), flush=True)
 
@@ -334,8 +399,10 @@ def measure_e2e(args, dims, ks, L, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds for the --impl reference run")
+    ap.add_argument("--soak", type=float, default=1.0, help="untimed busy seconds before timing (clocks)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
