@@ -1,17 +1,24 @@
 // fp32 fast path: one streaming pass over g and r that also emits index-ordered candidates above
-// a per-layer predicted threshold, then a per-layer exact select over the (few) candidates.
+// a per-layer predicted threshold, then a cooperative per-layer exact select.
 //
 // K1 (accum_emit_kernel): one warp per task (a <= TASK_ELEMS slice of one layer).  Reads g and r
 //    once (16-byte vectors), writes acc back into r, ORs the non-finite flag, and appends every
 //    entry with key(acc) >= thr[layer] to the task's candidate list in ascending index order
 //    (warp ballot + shuffle scan, no atomics).  Algorithmic traffic: 12 B/element.
-// K2 (select_fast_kernel): one CTA per layer.  If the layer's candidate set provably contains the
-//    top-k (count >= k, no task overflow) the exact top-k is taken over the candidates only
-//    (radix select in shared memory + ordered compaction), selected residual entries are zeroed
-//    by scatter, and the next threshold is predicted from the candidates.  Otherwise (first
-//    call, misprediction, overflow, small layer) it runs the dense exact path over r.
-// Both paths give bit-identical results: the candidate set contains every top-k element.
+// K2 (select_coop_kernel, cooperative launch, one CTA per SM):
+//    phase 1  CTAs take layers (largest work first).  A big layer whose candidate set provably
+//             holds its top-k (count >= k, no task overflow) is selected from the candidates
+//             alone (radix select in shared memory + ordered compaction + residual zeroing by
+//             scatter) and predicts its next threshold from them.  Small layers run the dense
+//             exact path inside the CTA.  Other big layers are queued.
+//    phase 2  all CTAs cooperate on each queued layer: a multi-CTA dense radix select over r
+//             (global histograms, grid syncs) that resolves the k-th key exactly and the
+//             PRED_FACTOR*k-th key for the next prediction, then an ordered multi-CTA compaction.
+// Every path returns exactly the reference's selection: the candidate set contains every top-k
+// element, and the dense paths scan all of r.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "lags_select.cuh"
 
 namespace lags {
@@ -21,6 +28,8 @@ constexpr int SMALL_LAYER = 16384; // layers up to this size always take the den
 constexpr int K1_WARPS = 8;        // warps per K1 CTA
 constexpr int K1_UNROLL = 4;       // float4 loads in flight per lane per operand
 constexpr int PRED_FACTOR = 2;     // predicted threshold targets PRED_FACTOR * k candidates
+constexpr int F32_PASSES = 3;      // radix passes for 31-bit keys with 11-bit digits
+constexpr int F32_BINS = 1 << Key<float>::RB;
 
 struct Task {
   int64_t start;  // flat element offset
@@ -31,8 +40,16 @@ struct Task {
 struct FastState {
   uint32_t thr;         // candidate threshold key (0 = no prediction: dense exact path)
   uint32_t fallbacks;   // dense-path executions after a prediction existed (diagnostic)
-  uint32_t last_cands;  // candidates at the last call
+  uint32_t last_cands;  // candidates at the last call (0 = dense path)
   uint32_t calls;
+};
+
+// Cross-CTA scratch of select_coop_kernel (device memory of the bucket).
+struct CoopScratch {
+  uint32_t* fb_count;   // [1] queued dense layers (reset to 0 by the kernel)
+  int32_t* fb_list;     // [nlayers]
+  uint32_t* hist;       // [nlayers][F32_PASSES][2][F32_BINS] global histograms (left zeroed)
+  uint32_t* chunk_cnt;  // [2 * grid] per-CTA (gt, eq) counts of the compaction
 };
 
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
@@ -145,7 +162,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
 }
 
-// Reduce (sum, or) over the block; all threads get the result.  Uses sm.warp_tot.
+// Block-wide sum; all threads get the result.  Uses sm.warp_tot.
 template <int RB>
 __device__ __forceinline__ uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
   uint32_t tot;
@@ -154,57 +171,33 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
   return tot;
 }
 
-__global__ void __launch_bounds__(SEL_NT) select_fast_kernel(
-    const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, FastState* state,
-    const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val,
-    int cap, int32_t* gidx, float* gval, float* r, int32_t* __restrict__ idx_out, float* __restrict__ val_out,
-    int32_t* __restrict__ count_out, int smem_keys, int force_exact) {
-  extern __shared__ uint32_t skeys[];
-  __shared__ RadixSmem<Key<float>::RB> sm;
-  const int j = blockIdx.x;
-  const lags_layer_t L = layers[j];
-  const int2 tr = layer_tasks[j];
-  const FastState st = state[j];
+struct CoopSmem {
+  RadixSmem<Key<float>::RB> sm;
+  uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
+};
+
+// Candidate path of one big layer inside one CTA.  Returns false if the candidate set cannot be
+// proven to hold the top-k (caller queues the layer for the dense path).
+__device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
+                                 const int32_t* cand_idx, const float* cand_val, int cap, int32_t* gidx,
+                                 float* gval, float* r, int32_t* idx_out, float* val_out, int32_t* count_out,
+                                 FastState* state, uint32_t* skeys, int smem_keys, CoopSmem& cs) {
+  RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
-  float* data = r + L.offset;
-  int32_t* oidx = idx_out + L.slot;
-  float* oval = val_out + L.slot;
-  const bool big = L.dim > SMALL_LAYER;
-  bool exact = force_exact || !big || st.thr == 0;
-  uint32_t m = 0;
-  if (!exact) {
-    uint32_t local = 0, over = 0;
-    for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
-      const uint32_t c = static_cast<uint32_t>(cand_cnt[t]);
-      over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
-      local += min(c, static_cast<uint32_t>(cap));
-    }
-    m = block_sum(local, sm);
-    over = block_sum(over, sm);
-    if (over || (m < k && st.thr > 1u)) exact = true;
+  uint32_t local = 0, over = 0;
+  for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
+    const uint32_t c = static_cast<uint32_t>(cand_cnt[t]);
+    over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
+    local += min(c, static_cast<uint32_t>(cap));
   }
-  uint32_t cnt;
-  if (exact) {
-    uint32_t pred = 0;
-    cnt = exact_topk_dense<float, float>(data, L.dim, k, oidx, oval, true, sm, big ? PRED_FACTOR * k : 0u, &pred);
-    if (threadIdx.x == 0) {
-      FastState ns = st;
-      ns.thr = big ? max(pred, 1u) : 0u;
-      ns.fallbacks += (st.thr != 0 && !force_exact) ? 1u : 0u;
-      ns.last_cands = 0;
-      ns.calls += 1;
-      state[j] = ns;
-    }
-  } else if (m == 0) {  // threshold <= 1 and no nonzero entry: nothing to send
-    cnt = 0;
-    if (threadIdx.x == 0) {
-      FastState ns = st;
-      ns.last_cands = 0;
-      ns.calls += 1;
-      state[j] = ns;
-    }
-  } else {
-    // gather the layer's task lists in task order (= index order) into contiguous scratch
+  const uint32_t m = block_sum(local, sm);
+  over = block_sum(over, sm);
+  if (over || (m < k && st.thr > 1u)) return false;
+  float* data = r + L.offset;
+  uint32_t cnt = 0;
+  uint32_t pred = st.thr;
+  if (m > 0) {
+    // gather the task lists in task order (= index order) into contiguous scratch
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
     const bool in_smem = m <= static_cast<uint32_t>(smem_keys);
     uint32_t carry = 0;
@@ -223,8 +216,6 @@ __global__ void __launch_bounds__(SEL_NT) select_fast_kernel(
       carry += tot;
       __syncthreads();
     }
-    __threadfence_block();
-    __syncthreads();
     const float* gv = gval + gbase;
     const int32_t* gi = gidx + gbase;
     const uint32_t* sk = skeys;
@@ -235,30 +226,207 @@ __global__ void __launch_bounds__(SEL_NT) select_fast_kernel(
       *key = Key<float>::of(*x);
       *ix = gi[i];
     };
+    int32_t* oidx = idx_out + L.slot;
+    float* oval = val_out + L.slot;
     auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
       oidx[pos] = static_cast<int32_t>(ix);
       oval[pos] = x;
       data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
     };
     cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
-    // predict the next threshold: the (PRED_FACTOR*k)-th largest key of this call's candidates
-    uint32_t pred;
+    // next threshold: the (PRED_FACTOR*k)-th largest candidate key, or an extrapolation below
+    // the current threshold from the candidate density when fewer candidates were seen
     if (m >= PRED_FACTOR * k) {
       pred = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, PRED_FACTOR * k, sm).prefix;
-    } else {
-      const uint32_t T = th.prefix;  // >= st.thr
-      const uint32_t step = max(2u * (T - min(T, st.thr)), 1u << 18);
-      pred = st.thr > step ? st.thr - step : 1u;
-    }
-    if (threadIdx.x == 0) {
-      FastState ns = st;
-      ns.thr = max(pred, 1u);
-      ns.last_cands = m;
-      ns.calls += 1;
-      state[j] = ns;
+    } else if (st.thr > 1u) {
+      const uint32_t T = max(th.prefix, st.thr);
+      const double density = (static_cast<double>(m - min(m, k)) + 1.0) / (static_cast<double>(T - st.thr) + 1.0);
+      double step = (static_cast<double>(PRED_FACTOR * k) - m) / density;
+      step = fmin(fmax(step, 64.0), 4.0 * (static_cast<double>(T - st.thr) + (1 << 16)));
+      pred = st.thr > step ? st.thr - static_cast<uint32_t>(step) : 1u;
     }
   }
-  if (threadIdx.x == 0) count_out[j] = static_cast<int32_t>(cnt);
+  if (threadIdx.x == 0) {
+    FastState ns = st;
+    ns.thr = max(pred, 1u);
+    ns.last_cands = m;
+    ns.calls += 1;
+    state[j] = ns;
+    count_out[j] = static_cast<int32_t>(cnt);
+  }
+  __syncthreads();
+  return true;
+}
+
+// Dense exact path of one big layer by all CTAs of the cooperative grid.
+__device__ void coop_dense_select(int j, int f, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
+                                  float* val_out, int32_t* count_out, FastState* state, const CoopScratch& sc,
+                                  bool force_exact, CoopSmem& cs) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  RadixSmem<Key<float>::RB>& sm = cs.sm;
+  const int64_t d = L.dim;
+  float* data = r + L.offset;
+  const uint32_t k = static_cast<uint32_t>(L.k);
+  const int G = gridDim.x, c = blockIdx.x;
+  uint32_t* H = sc.hist + static_cast<int64_t>(f) * F32_PASSES * 2 * F32_BINS;
+  uint32_t prefix[2] = {0u, 0u}, pmask[2] = {0u, 0u};
+  const int64_t pk = static_cast<int64_t>(PRED_FACTOR) * k;
+  uint32_t rank[2] = {k, static_cast<uint32_t>(pk < d ? pk : d)};
+  uint32_t n_gt0 = 0;
+  bool done[2] = {static_cast<int64_t>(k) >= d, false};
+  int shift = 31 - Key<float>::RB, width = Key<float>::RB;
+  for (int pass = 0; pass < F32_PASSES && !(done[0] && done[1]); ++pass) {
+    for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
+      sm.hist[b] = 0;
+      cs.hist2[b] = 0;
+    }
+    __syncthreads();
+    const uint32_t dmask = (1u << width) - 1u;
+    // both ranks still share their prefix (always true in pass 0): one histogram serves both
+    const bool same = !done[0] && !done[1] && prefix[0] == prefix[1] && pmask[0] == pmask[1];
+    for (int64_t i = static_cast<int64_t>(c) * SEL_NT + threadIdx.x; i < d; i += static_cast<int64_t>(G) * SEL_NT) {
+      const uint32_t key = Key<float>::of(data[i]);
+      if (!done[0] && (key & pmask[0]) == prefix[0]) atomicAdd(&sm.hist[(key >> shift) & dmask], 1u);
+      if (!same && !done[1] && (key & pmask[1]) == prefix[1]) atomicAdd(&cs.hist2[(key >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    uint32_t* Hp = H + pass * 2 * F32_BINS;
+    const uint32_t* h2 = same ? sm.hist : cs.hist2;
+    for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
+      if (sm.hist[b]) atomicAdd(Hp + b, sm.hist[b]);
+      if (h2[b]) atomicAdd(Hp + F32_BINS + b, h2[b]);
+    }
+    grid.sync();
+    for (int q = 0; q < 2; ++q) {
+      if (done[q]) continue;  // uniform across the grid
+      for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) sm.hist[b] = __ldcg(Hp + q * F32_BINS + b);
+      __syncthreads();
+      uint32_t bin, above, in_bin;
+      find_bin<Key<float>::RB>(sm, rank[q], &bin, &above, &in_bin);
+      prefix[q] |= bin << shift;
+      pmask[q] |= dmask << shift;
+      rank[q] -= above;
+      if (q == 0) n_gt0 += above;
+      if (shift == 0 || (in_bin == rank[q] && prefix[q] != 0u)) done[q] = true;
+      if (q == 1 && pass >= 1) done[1] = true;  // 22 resolved bits are plenty for a prediction
+    }
+    const int ns = shift > Key<float>::RB ? shift - Key<float>::RB : 0;
+    width = shift - ns;
+    shift = ns;
+  }
+  SelectThreshold<uint32_t> th;
+  if (static_cast<int64_t>(k) >= d) {
+    th.prefix = 0u;
+    th.pmask = 0xffffffffu;
+    th.n_gt = 0;
+    th.need_eq = 0;
+  } else {
+    th.prefix = prefix[0];
+    th.pmask = pmask[0];
+    th.n_gt = n_gt0;
+    th.need_eq = prefix[0] == 0u ? 0u : rank[0];
+  }
+  // ordered multi-CTA compaction: CTA c owns the contiguous chunk [lo, hi)
+  const int64_t per = ((d + G - 1) / G + 3) / 4 * 4;
+  const int64_t lo = min(d, static_cast<int64_t>(c) * per), hi = min(d, lo + per);
+  uint32_t lgt = 0, leq = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += SEL_NT) {
+    const uint32_t key = Key<float>::of(data[i]);
+    const uint32_t hk = key & th.pmask;
+    if (key != 0u) {
+      lgt += hk > th.prefix ? 1u : 0u;
+      leq += hk == th.prefix ? 1u : 0u;
+    }
+  }
+  lgt = block_sum(lgt, sm);
+  leq = block_sum(leq, sm);
+  if (threadIdx.x == 0) {
+    sc.chunk_cnt[2 * c] = lgt;
+    sc.chunk_cnt[2 * c + 1] = leq;
+  }
+  grid.sync();
+  uint32_t cg0 = 0, ce0 = 0;
+  for (int q = threadIdx.x; q < c; q += SEL_NT) {
+    cg0 += __ldcg(sc.chunk_cnt + 2 * q);
+    ce0 += __ldcg(sc.chunk_cnt + 2 * q + 1);
+  }
+  cg0 = block_sum(cg0, sm);
+  ce0 = block_sum(ce0, sm);
+  int32_t* oidx = idx_out + L.slot;
+  float* oval = val_out + L.slot;
+  float* chunk = data + lo;
+  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
+    *x = chunk[i];
+    *key = Key<float>::of(*x);
+    *ix = lo + i;
+  };
+  auto emit = [=](uint32_t pos, int64_t i, int64_t ix, float x) {
+    oidx[pos] = static_cast<int32_t>(ix);
+    oval[pos] = x;
+    chunk[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+  };
+  const uint32_t total = ordered_compact<uint32_t, float>(hi - lo, th, load, emit, sm, cg0, ce0);
+  if (c == G - 1 && threadIdx.x == 0) {
+    count_out[j] = static_cast<int32_t>(total);
+    FastState ns = st;
+    ns.thr = max(prefix[1], 1u);
+    ns.fallbacks += (st.thr != 0u && !force_exact) ? 1u : 0u;
+    ns.last_cands = 0;
+    ns.calls += 1;
+    state[j] = ns;
+  }
+}
+
+__global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
+    const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
+    int nlayers, FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
+    const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
+    float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc) {
+  namespace cg = cooperative_groups;
+  extern __shared__ uint32_t skeys[];
+  __shared__ CoopSmem cs;
+  cg::grid_group grid = cg::this_grid();
+  // phase 1: one CTA per layer, largest work first
+  for (int li = blockIdx.x; li < nlayers; li += gridDim.x) {
+    const int j = order[li];
+    const lags_layer_t L = layers[j];
+    const FastState st = state[j];
+    if (L.dim <= SMALL_LAYER) {
+      const uint32_t cnt = exact_topk_dense<float, float>(r + L.offset, L.dim, static_cast<uint32_t>(L.k),
+                                                          idx_out + L.slot, val_out + L.slot, true, cs.sm);
+      if (threadIdx.x == 0) {
+        count_out[j] = static_cast<int32_t>(cnt);
+        FastState ns = st;
+        ns.calls += 1;
+        state[j] = ns;
+      }
+      __syncthreads();
+      continue;
+    }
+    const bool ok = !force_exact && st.thr != 0u &&
+                    candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
+                                     idx_out, val_out, count_out, state, skeys, smem_keys, cs);
+    if (!ok && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j;
+    __syncthreads();
+  }
+  grid.sync();
+  const uint32_t nf = __ldcg(sc.fb_count);
+  if (nf == 0) return;  // uniform: every CTA read the same count after the grid sync
+  // phase 2: every queued layer by the whole grid
+  for (uint32_t f = 0; f < nf; ++f) {
+    const int j = __ldcg(sc.fb_list + f);
+    // (chunk_cnt reuse is safe: the next layer passes a grid sync before rewriting it)
+    coop_dense_select(j, static_cast<int>(f), layers[j], state[j], r, idx_out, val_out, count_out, state, sc,
+                      force_exact != 0, cs);
+  }
+  // leave the scratch clean for the next call (nobody reads the histograms after the last
+  // compaction's grid sync)
+  const int64_t hwords = static_cast<int64_t>(nf) * F32_PASSES * 2 * F32_BINS;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * SEL_NT + threadIdx.x; i < hwords;
+       i += static_cast<int64_t>(gridDim.x) * SEL_NT)
+    sc.hist[i] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sc.fb_count = 0u;
 }
 
 }  // namespace lags

@@ -199,6 +199,9 @@ struct lags_bucket {
   double* acc64 = nullptr;
   uint32_t* mask = nullptr;
   char* planes = nullptr;
+  int32_t* order = nullptr;  // layers by decreasing selection work (phase-1 schedule)
+  CoopScratch coop{};
+  int coop_grid = 0;
 };
 
 namespace {
@@ -248,8 +251,11 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_fbl = 0, o_hist = 0,
+         o_chunk = 0, bytes = 0;
 };
+
+constexpr int MAX_COOP_GRID = 1024;
 
 int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, int32_t max_world, Plan* p) {
   if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "unknown dtype");
@@ -291,6 +297,12 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_acc = take(dtype == LAGS_F32_ACC64 ? sizeof(double) * static_cast<size_t>(p->n_total) : 0);
   p->o_mask = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total));
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
+  p->o_order = take(sizeof(int32_t) * L);
+  const bool f32 = dtype == LAGS_F32;
+  p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);
+  p->o_fbl = take(f32 ? sizeof(int32_t) * L : 0);
+  p->o_hist = take(f32 ? sizeof(uint32_t) * static_cast<size_t>(L) * F32_PASSES * 2 * F32_BINS : 0);
+  p->o_chunk = take(f32 ? sizeof(uint32_t) * 2 * MAX_COOP_GRID : 0);
   p->bytes = o;
   return LAGS_OK;
 }
@@ -342,6 +354,11 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->acc64 = reinterpret_cast<double*>(base + p.o_acc);
   b->mask = reinterpret_cast<uint32_t*>(base + p.o_mask);
   b->planes = base + p.o_planes;
+  b->order = reinterpret_cast<int32_t*>(base + p.o_order);
+  b->coop.fb_count = reinterpret_cast<uint32_t*>(base + p.o_fbc);
+  b->coop.fb_list = reinterpret_cast<int32_t*>(base + p.o_fbl);
+  b->coop.hist = reinterpret_cast<uint32_t*>(base + p.o_hist);
+  b->coop.chunk_cnt = reinterpret_cast<uint32_t*>(base + p.o_chunk);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -363,6 +380,14 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     off += dims[j];
     slot += ks[j];
   }
+  // phase-1 schedule of the selection kernel: longest (estimated) work first
+  std::vector<int32_t> order(nlayers);
+  std::vector<double> cost(nlayers);
+  for (int j = 0; j < nlayers; ++j) {
+    order[j] = j;
+    cost[j] = dims[j] <= SMALL_LAYER ? 5.0 * dims[j] : 40.0 * ks[j] + 64.0 * (ltasks[j].y - ltasks[j].x);
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return cost[a] > cost[c]; });
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool ok =
       cudaMemcpyAsync(b->layers, layers.data(), sizeof(lags_layer_t) * nlayers, cudaMemcpyHostToDevice, s) ==
@@ -372,8 +397,14 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       cudaMemcpyAsync(b->tasks, tasks.data(), sizeof(Task) * tasks.size(), cudaMemcpyHostToDevice, s) == cudaSuccess &&
       cudaMemcpyAsync(b->slot_layer, slot_layer.data(), sizeof(int32_t) * slot_layer.size(), cudaMemcpyHostToDevice,
                       s) == cudaSuccess &&
+      cudaMemcpyAsync(b->order, order.data(), sizeof(int32_t) * nlayers, cudaMemcpyHostToDevice, s) ==
+          cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
+      (dtype != LAGS_F32 ||
+       (cudaMemsetAsync(b->coop.fb_count, 0, sizeof(uint32_t), s) == cudaSuccess &&
+        cudaMemsetAsync(b->coop.hist, 0, sizeof(uint32_t) * static_cast<size_t>(nlayers) * F32_PASSES * 2 * F32_BINS,
+                        s) == cudaSuccess)) &&
       cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) {
     delete b;
@@ -381,10 +412,17 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   }
   if (dtype == LAGS_F32) {
     const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
-    if (cudaFuncSetAttribute(select_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    int occ = 0;
+    if (cudaFuncSetAttribute(select_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_coop_kernel, SEL_NT, smem) != cudaSuccess) {
       delete b;
-      return cuda_check("cudaFuncSetAttribute(select_fast_kernel)", 0);
+      return cuda_check("select_coop_kernel attributes", 0);
     }
+    if (occ < 1) {
+      delete b;
+      return fail(LAGS_ERR_CUDA, "select_coop_kernel cannot be resident on an SM");
+    }
+    b->coop_grid = std::min(num_sms() * occ, MAX_COOP_GRID);
     b->smem_keys = SMEM_KEYS;
   }
   *out = b;
@@ -420,9 +458,28 @@ int lags_bucket_compress(lags_bucket_t* b, const void* g, void* r, double alpha,
     accum_emit_kernel<<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
                                                         static_cast<const float*>(g), static_cast<float*>(r), a, b->cap,
                                                         b->cand_idx, b->cand_val, b->cand_cnt, status);
-    select_fast_kernel<<<b->nlayers, SEL_NT, b->smem_keys * sizeof(uint32_t), s>>>(
-        b->layers, b->layer_tasks, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval,
-        static_cast<float*>(r), idx, reinterpret_cast<float*>(m + b->off_val), cnt, b->smem_keys, exact ? 1 : 0);
+    const lags_layer_t* layers = b->layers;
+    const int2* ltasks = b->layer_tasks;
+    const int32_t* order = b->order;
+    int nl = b->nlayers;
+    FastState* state = b->state;
+    const int32_t* ccnt = b->cand_cnt;
+    const int32_t* cidx = b->cand_idx;
+    const float* cval = b->cand_val;
+    int cap = b->cap;
+    int32_t* gidx = b->gidx;
+    float* gval = b->gval;
+    float* rr = static_cast<float*>(r);
+    float* vals = reinterpret_cast<float*>(m + b->off_val);
+    int smem_keys = b->smem_keys;
+    int fe = exact ? 1 : 0;
+    CoopScratch sc = b->coop;
+    void* args[] = {&layers, &ltasks, &order, &nl, &state, &ccnt, &cidx, &cval, &cap, &gidx, &gval,
+                    &rr, &idx, &vals, &cnt, &smem_keys, &fe, &sc};
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(select_coop_kernel), dim3(b->coop_grid),
+                                    dim3(SEL_NT), args, static_cast<size_t>(smem_keys) * sizeof(uint32_t),
+                                    s) != cudaSuccess)
+      return cuda_check("select_coop_kernel launch", 1);
     return cuda_check("lags_bucket_compress(f32)", 2);
   }
   if (b->dtype == LAGS_F64) {

@@ -130,10 +130,11 @@ __device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, 
 // Ordered compaction of m entries (scan order = ascending index) under threshold th.
 // load(i, &key, &val, &index) fetches entry i; emit(pos, i, index, val) writes selected entry i
 // to output position pos.  Returns the selected count (all threads).
+// carry_gt0 / carry_eq0: counts of gt / eq entries before entry 0 (multi-CTA compaction).
 template <typename K, typename T, typename Load, typename Emit, int RB>
 __device__ uint32_t ordered_compact(int64_t m, const SelectThreshold<K>& th, Load load, Emit emit,
-                                    RadixSmem<RB>& sm) {
-  uint32_t carry_gt = 0, carry_eq = 0;
+                                    RadixSmem<RB>& sm, uint32_t carry_gt0 = 0, uint32_t carry_eq0 = 0) {
+  uint32_t carry_gt = carry_gt0, carry_eq = carry_eq0;
   const int64_t chunk = static_cast<int64_t>(SEL_NT) * SEL_VEC;
   for (int64_t base = 0; base < m; base += chunk) {
     const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * SEL_VEC;
