@@ -196,7 +196,7 @@ __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32
   }
   __syncthreads();
   auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
-  const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, d, k, cs.sm);
+  const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, d, k, cs.sm, 0, nullptr, true);
   auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
     *x = sv[i];
     *key = Key<float>::of(*x);
@@ -262,7 +262,7 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
     const int32_t* gi = gidx + gbase;
     const uint32_t* sk = skeys;
     auto key_at = [=](int64_t i) { return in_smem ? sk[i] : Key<float>::of(gv[i]); };
-    const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, k, sm);
+    const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, k, sm, 0, nullptr, true);
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
       *x = gv[i];
       *key = Key<float>::of(*x);
@@ -279,7 +279,7 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
     // next threshold: the (PRED_FACTOR*k)-th largest candidate key, or an extrapolation below
     // the current threshold from the candidate density when fewer candidates were seen
     if (m >= PRED_FACTOR * k) {
-      pred = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, PRED_FACTOR * k, sm).prefix;
+      pred = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, PRED_FACTOR * k, sm, 0, nullptr, true).prefix;
     } else if (st.thr > 1u) {
       const uint32_t T = max(th.prefix, st.thr);
       const double density = (static_cast<double>(m - min(m, k)) + 1.0) / (static_cast<double>(T - st.thr) + 1.0);

@@ -68,10 +68,48 @@ __device__ __forceinline__ void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint3
 // Multi-pass radix select over m keys produced by key_at(i).  Returns the threshold of the
 // k largest.  If pred_rank > 0, *pred_key receives the lower edge of the first-digit bin that
 // holds the pred_rank-th largest key (used to predict next call's candidate threshold).
+// Block-wide OR of one key per thread (all threads get the result).  Uses sm.warp_tot.
+template <typename K, int RB>
+__device__ __forceinline__ K block_or(K v, RadixSmem<RB>& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(v));
+  uint32_t hi = sizeof(K) > 4 ? __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(static_cast<uint64_t>(v) >> 32)) : 0u;
+  __syncthreads();
+  if (lane == 0) {
+    sm.warp_tot[warp] = lo;
+  }
+  __syncthreads();
+  lo = 0;
+  for (int w = 0; w < SEL_NT / 32; ++w) lo |= sm.warp_tot[w];
+  __syncthreads();
+  if (sizeof(K) > 4) {
+    if (lane == 0) sm.warp_tot[warp] = hi;
+    __syncthreads();
+    hi = 0;
+    for (int w = 0; w < SEL_NT / 32; ++w) hi |= sm.warp_tot[w];
+    __syncthreads();
+  }
+  return static_cast<K>((static_cast<uint64_t>(hi) << 32) | lo);
+}
+
+// Histogram increment aggregated over the lanes of a warp that hit the same bin (candidate keys
+// crowd into a few bins; plain shared atomics would serialise).  Warp-collective.
+__device__ __forceinline__ void hist_add_warp(uint32_t* hist, uint32_t bin, bool act) {
+  const unsigned am = __ballot_sync(0xffffffffu, act);
+  if (act) {
+    const unsigned peers = __match_any_sync(am, bin);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + bin, static_cast<uint32_t>(__popc(peers)));
+  }
+}
+
+// skip_common_prefix: first OR-reduce key ^ key(0) over all m keys and start the radix passes
+// below the highest differing bit (cheap when keys live in shared memory and crowd together).
 template <typename K, int BITS, int RB, typename KeyAt>
 __device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, RadixSmem<RB>& sm,
-                                           uint32_t pred_rank = 0, K* pred_key = nullptr) {
+                                           uint32_t pred_rank = 0, K* pred_key = nullptr,
+                                           bool skip_common_prefix = false) {
   constexpr int NB = RadixSmem<RB>::NB;
+  constexpr K FULL = (K(1) << BITS) - 1;
   SelectThreshold<K> th;
   K prefix = 0, pmask = 0;
   uint32_t rank = k, n_gt = 0;
@@ -85,20 +123,42 @@ __device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, 
     return th;
   }
   if (static_cast<int64_t>(rank) > m) rank = static_cast<uint32_t>(m);
-  while (true) {
+  if (skip_common_prefix) {
+    const K key0 = key_at(0);
+    K diff = 0;
+    for (int64_t i = threadIdx.x; i < m; i += SEL_NT) diff |= key_at(i) ^ key0;
+    diff = block_or<K, RB>(diff, sm);
+    if (diff == 0) {  // all keys equal
+      pmask = FULL;
+      prefix = key0;
+      shift = 0;
+      width = 0;
+      if (pred_rank > 0 && pred_key) *pred_key = key0;
+    } else {
+      const int h = sizeof(K) > 4 ? 63 - __clzll(static_cast<long long>(diff)) : 31 - __clz(static_cast<int>(diff));
+      const K low = (K(1) << (h + 1)) - 1;
+      pmask = FULL & ~low;
+      prefix = key0 & pmask;
+      shift = h + 1 > RB ? h + 1 - RB : 0;
+      width = h + 1 - shift;
+    }
+  }
+  while (width > 0) {
     for (int b = threadIdx.x; b < NB; b += SEL_NT) sm.hist[b] = 0;
     __syncthreads();
     const K dmask = (K(1) << width) - 1;
-    for (int64_t i = threadIdx.x; i < m; i += SEL_NT) {
-      const K key = key_at(i);
-      if ((key & pmask) == prefix) atomicAdd(&sm.hist[(key >> shift) & dmask], 1u);
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = threadIdx.x - lane; i0 < m; i0 += SEL_NT) {  // warp-uniform trip count
+      const int64_t i = i0 + lane;
+      const K key = i < m ? key_at(i) : K(0);
+      hist_add_warp(sm.hist, static_cast<uint32_t>((key >> shift) & dmask), i < m && (key & pmask) == prefix);
     }
     __syncthreads();
     uint32_t b, above, in_bin;
     if (first && pred_rank > 0) {
       const uint32_t pr = static_cast<int64_t>(pred_rank) < m ? pred_rank : static_cast<uint32_t>(m);
       find_bin<RB>(sm, pr, &b, &above, &in_bin);
-      *pred_key = K(b) << shift;
+      *pred_key = prefix | (K(b) << shift);
     }
     first = false;
     find_bin<RB>(sm, rank, &b, &above, &in_bin);
