@@ -95,8 +95,10 @@ int lags_bucket_compress(lags_bucket_t* bucket, const void* g, void* r, double a
 int lags_bucket_decode_update(lags_bucket_t* bucket, const void* msgs, int64_t msg_stride, int32_t P, void* v,
                               void* momentum, double mu, lags_stream_t stream);
 
-/* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls} (synchronous). */
-int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 4] */, lags_stream_t stream);
+/* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls, last select
+ * cycles, last path (0 small dense, 1 candidates, 2 grid-wide dense), 0, 0} (synchronous). */
+#define LAGS_STATS_WORDS 8
+int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 8] */, lags_stream_t stream);
 
 /* ---- single-vector operators ---------------------------------------------------------------- */
 

@@ -42,6 +42,9 @@ struct FastState {
   uint32_t fallbacks;   // dense-path executions after a prediction existed (diagnostic)
   uint32_t last_cands;  // candidates at the last call (0 = dense path)
   uint32_t calls;
+  uint32_t cycles;      // SM cycles the layer's phase-1 work took at the last call (diagnostic)
+  uint32_t path;        // last path: 0 small dense, 1 candidates, 2 queued for the grid-wide dense path
+  uint32_t reserved[2];
 };
 
 // Cross-CTA scratch of select_coop_kernel (device memory of the bucket).
@@ -434,6 +437,8 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
     const int j = order[li];
     const lags_layer_t L = layers[j];
     const FastState st = state[j];
+    const long long t_begin = clock64();
+    uint32_t path;
     if (L.dim <= SMALL_LAYER) {
       const uint32_t cnt =
           L.dim <= smem_keys
@@ -447,14 +452,19 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
         ns.calls += 1;
         state[j] = ns;
       }
-      __syncthreads();
-      continue;
+      path = 0u;
+    } else {
+      const bool ok = !force_exact && st.thr != 0u &&
+                      candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
+                                       idx_out, val_out, count_out, state, skeys, smem_keys, cs);
+      if (!ok && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j;
+      path = ok ? 1u : 2u;
     }
-    const bool ok = !force_exact && st.thr != 0u &&
-                    candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
-                                     idx_out, val_out, count_out, state, skeys, smem_keys, cs);
-    if (!ok && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j;
     __syncthreads();
+    if (threadIdx.x == 0) {
+      state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
+      state[j].path = path;
+    }
   }
   grid.sync();
   const uint32_t nf = __ldcg(sc.fb_count);

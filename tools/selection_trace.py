@@ -51,6 +51,9 @@ def main():
             print(f"step {t + 1:4d}  compress {np.median(times[-args.every:]) * 1e3:8.1f} us (median)  "
                   f"cands {int(s[:, 2].sum()):7d} (2k={2 * sum(ks[j] for j in big)})  fallbacks {int(s[:, 1].sum()):5d}  "
                   f"worst m/k {[(round(float(x), 1), dims[j]) for x, j in ratio[:4]]}", flush=True)
+            slow = np.argsort(-s[:, 4].astype(np.int64))[:6]
+            print("   slowest layers (kcycles, path, dim, k, m):",
+                  [(int(s[j, 4]) // 1000, int(s[j, 5]), dims[j], ks[j], int(s[j, 2])) for j in slow], flush=True)
 
 
 if __name__ == "__main__":
