@@ -213,12 +213,87 @@ __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32
   return ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
 }
 
+// Two ranks in one set of radix passes over m keys (shared memory): the exact threshold of the
+// k largest (select form) and a lower bound of the k2-th largest key (the next prediction).
+// Passes start below the common prefix of all keys (candidates crowd just above the threshold).
+template <typename KeyAt>
+__device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t k2, CoopSmem& cs,
+                                  SelectThreshold<uint32_t>* th_out, uint32_t* key2_out) {
+  constexpr int RB = Key<float>::RB;
+  constexpr uint32_t FULL = 0x7fffffffu;
+  RadixSmem<RB>& sm = cs.sm;
+  const uint32_t key0 = key_at(0);
+  uint32_t diff = 0;
+  for (int64_t i = threadIdx.x; i < m; i += SEL_NT) diff |= key_at(i) ^ key0;
+  diff = block_or<uint32_t, RB>(diff, sm);
+  uint32_t prefix[2], pmask[2];
+  uint32_t rank[2] = {static_cast<int64_t>(k) < m ? k : static_cast<uint32_t>(m),
+                      static_cast<int64_t>(k2) < m ? k2 : static_cast<uint32_t>(m)};
+  uint32_t n_gt0 = 0;
+  bool done[2] = {false, false};
+  int shift = 0, width = 0;
+  if (diff == 0) {
+    prefix[0] = prefix[1] = key0;
+    pmask[0] = pmask[1] = FULL;
+  } else {
+    const int h = 31 - __clz(static_cast<int>(diff));
+    const uint32_t pm = FULL & ~((1u << (h + 1)) - 1u);
+    prefix[0] = prefix[1] = key0 & pm;
+    pmask[0] = pmask[1] = pm;
+    shift = h + 1 > RB ? h + 1 - RB : 0;
+    width = h + 1 - shift;
+  }
+  while (width > 0 && !(done[0] && done[1])) {
+    const bool same = !done[0] && !done[1] && prefix[0] == prefix[1] && pmask[0] == pmask[1];
+    for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
+      sm.hist[b] = 0;
+      cs.hist2[b] = 0;
+    }
+    __syncthreads();
+    const uint32_t dmask = (1u << width) - 1u;
+    for (int64_t i = threadIdx.x; i < m; i += SEL_NT) {
+      const uint32_t key = key_at(i);
+      const uint32_t bin = (key >> shift) & dmask;
+      if (!done[0] && (key & pmask[0]) == prefix[0]) atomicAdd(&sm.hist[bin], 1u);
+      if (!same && !done[1] && (key & pmask[1]) == prefix[1]) atomicAdd(&cs.hist2[bin], 1u);
+    }
+    __syncthreads();
+    for (int q = 0; q < 2; ++q) {
+      if (done[q]) continue;
+      uint32_t bin, above, in_bin;
+      find_bin<RB>(sm, rank[q], &bin, &above, &in_bin, (q == 0 || same) ? sm.hist : cs.hist2);
+      prefix[q] |= bin << shift;
+      pmask[q] |= dmask << shift;
+      rank[q] -= above;
+      if (q == 0) n_gt0 += above;
+      if (shift == 0 || (in_bin == rank[q] && prefix[q] != 0u)) done[q] = true;
+    }
+    const int ns = shift > RB ? shift - RB : 0;
+    width = shift - ns;
+    shift = ns;
+  }
+  if (static_cast<int64_t>(k) >= m) {  // every nonzero candidate is selected
+    th_out->prefix = 0u;
+    th_out->pmask = 0xffffffffu;
+    th_out->n_gt = 0;
+    th_out->need_eq = 0;
+  } else {
+    th_out->prefix = prefix[0];
+    th_out->pmask = pmask[0];
+    th_out->n_gt = n_gt0;
+    th_out->need_eq = prefix[0] == 0u ? 0u : rank[0];
+  }
+  *key2_out = prefix[1];
+}
+
 // Candidate path of one big layer inside one CTA.  Returns false if the candidate set cannot be
-// proven to hold the top-k (caller queues the layer for the dense path).
+// proven to hold the top-k (the caller queues the layer for the grid-wide dense path).
+// Candidates are gathered once into shared memory (value + index, ascending index order) when
+// they fit (2*m words <= smem_words), else into the bucket's global scratch.
 __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
-                                 const int32_t* cand_idx, const float* cand_val, int cap, int32_t* gidx,
-                                 float* gval, float* r, int32_t* idx_out, float* val_out, int32_t* count_out,
-                                 FastState* state, uint32_t* skeys, int smem_keys, CoopSmem& cs) {
+                                 const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
+                                 int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
+                                 int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, CoopSmem& cs) {
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
   uint32_t local = 0, over = 0;
@@ -234,42 +309,42 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
   uint32_t cnt = 0;
   uint32_t pred = st.thr;
   if (m > 0) {
-    // gather the task lists in task order (= index order) into contiguous scratch
+    const bool in_smem = 2u * m <= static_cast<uint32_t>(smem_words);
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
-    const bool in_smem = m <= static_cast<uint32_t>(smem_keys);
+    float* sv = in_smem ? reinterpret_cast<float*>(dyn) : gval + gbase;
+    int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + m : gidx + gbase;
+    // gather: positions by a block scan over task counts, then one thread per entry (the owning
+    // task is found by binary search over the positions), every load independent
     uint32_t carry = 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
-      const int t = t0 + threadIdx.x;
-      const uint32_t c = t < tr.y ? static_cast<uint32_t>(cand_cnt[t]) : 0u;
+      const int nt = min(SEL_NT, tr.y - t0);
+      const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(cand_cnt[t0 + threadIdx.x]) : 0u;
       uint32_t tot;
-      const uint32_t pos = carry + block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
+      const uint32_t pos = block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
       cs.tpos[threadIdx.x] = pos;
-      cs.tcnt[threadIdx.x] = c;
       __syncthreads();
-      // one warp per task: coalesced copy of its list
-      for (int tt = warp; tt < SEL_NT && t0 + tt < tr.y; tt += SEL_NT / 32) {
-        const uint32_t tc = cs.tcnt[tt], tp = cs.tpos[tt];
-        const int64_t src0 = static_cast<int64_t>(t0 + tt) * cap;
-        for (uint32_t q = lane; q < tc; q += 32) {
-          const float x = cand_val[src0 + q];
-          gidx[gbase + tp + q] = cand_idx[src0 + q];
-          gval[gbase + tp + q] = x;
-          if (in_smem) skeys[tp + q] = Key<float>::of(x);
+      for (uint32_t e = threadIdx.x; e < tot; e += SEL_NT) {
+        int lo = 0, hi = nt - 1;  // last task whose start position <= e
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (cs.tpos[mid] <= e) lo = mid;
+          else hi = mid - 1;
         }
+        const int64_t src = static_cast<int64_t>(t0 + lo) * cap + (e - cs.tpos[lo]);
+        sv[carry + e] = __ldcg(cand_val + src);
+        si[carry + e] = __ldcg(cand_idx + src);
       }
       carry += tot;
       __syncthreads();
     }
-    const float* gv = gval + gbase;
-    const int32_t* gi = gidx + gbase;
-    const uint32_t* sk = skeys;
-    auto key_at = [=](int64_t i) { return in_smem ? sk[i] : Key<float>::of(gv[i]); };
-    const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, k, sm, 0, nullptr, true);
+    auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
+    SelectThreshold<uint32_t> th;
+    uint32_t key2;
+    radix_select_dual(key_at, m, k, PRED_FACTOR * k, cs, &th, &key2);
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
-      *x = gv[i];
+      *x = sv[i];
       *key = Key<float>::of(*x);
-      *ix = gi[i];
+      *ix = si[i];
     };
     int32_t* oidx = idx_out + L.slot;
     float* oval = val_out + L.slot;
@@ -279,10 +354,10 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
       data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
     };
     cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
-    // next threshold: the (PRED_FACTOR*k)-th largest candidate key, or an extrapolation below
-    // the current threshold from the candidate density when fewer candidates were seen
+    // next threshold: the (PRED_FACTOR*k)-th largest candidate key, or, when fewer candidates were
+    // seen, an extrapolation below the current threshold from the observed candidate density
     if (m >= PRED_FACTOR * k) {
-      pred = radix_select<uint32_t, 31, Key<float>::RB>(key_at, m, PRED_FACTOR * k, sm, 0, nullptr, true).prefix;
+      pred = key2;
     } else if (st.thr > 1u) {
       const uint32_t T = max(th.prefix, st.thr);
       const double density = (static_cast<double>(m - min(m, k)) + 1.0) / (static_cast<double>(T - st.thr) + 1.0);

@@ -32,15 +32,17 @@ struct RadixSmem {
 };
 
 // Bin holding the rank-th largest (1-based) of the histogram (descending scan).  All threads.
+// `hist` (shared, NB bins) defaults to sm.hist.
 template <int RB>
 __device__ __forceinline__ void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint32_t* bin, uint32_t* above,
-                                         uint32_t* in_bin) {
+                                         uint32_t* in_bin, const uint32_t* hist = nullptr) {
   constexpr int NB = RadixSmem<RB>::NB;
   constexpr int PER = NB / SEL_NT;  // 2 (fp32) or 8 (fp64) bins per thread
+  const uint32_t* H = hist ? hist : sm.hist;
   const int t = threadIdx.x;
   uint32_t s = 0;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) s += sm.hist[NB - 1 - t * PER - q];
+  for (int q = 0; q < PER; ++q) s += H[NB - 1 - t * PER - q];
   uint32_t tot;
   const uint32_t ex = block_exclusive_scan<SEL_NT>(s, sm.warp_tot, &tot);
   if (ex < rank && rank <= ex + s) {
@@ -48,7 +50,7 @@ __device__ __forceinline__ void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint3
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
       const int b = NB - 1 - t * PER - q;
-      const uint32_t h = sm.hist[b];
+      const uint32_t h = H[b];
       if (rank <= c + h) {
         sm.bin_count = h;
         sm.above = c;
@@ -148,10 +150,10 @@ __device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, 
     __syncthreads();
     const K dmask = (K(1) << width) - 1;
     const int lane = threadIdx.x & 31;
-    for (int64_t i0 = threadIdx.x - lane; i0 < m; i0 += SEL_NT) {  // warp-uniform trip count
-      const int64_t i = i0 + lane;
-      const K key = i < m ? key_at(i) : K(0);
-      hist_add_warp(sm.hist, static_cast<uint32_t>((key >> shift) & dmask), i < m && (key & pmask) == prefix);
+    (void)lane;
+    for (int64_t i = threadIdx.x; i < m; i += SEL_NT) {
+      const K key = key_at(i);
+      if ((key & pmask) == prefix) atomicAdd(&sm.hist[(key >> shift) & dmask], 1u);
     }
     __syncthreads();
     uint32_t b, above, in_bin;
