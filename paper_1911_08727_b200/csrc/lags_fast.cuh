@@ -44,8 +44,25 @@ struct FastState {
   uint32_t calls;
   uint32_t cycles;      // SM cycles the layer's phase-1 work took at the last call (diagnostic)
   uint32_t path;        // last path: 0 small dense, 1 candidates, 2 queued for the grid-wide dense path
-  uint32_t reserved[2];
+  uint32_t pf256;       // adaptive prediction rank factor x256 (0 = PRED_FACTOR)
+  uint32_t reserved;
 };
+
+constexpr float PRED_TARGET = 2.0f;  // wanted candidates per selected entry (m / k)
+
+__device__ __forceinline__ float pred_factor(const FastState& st) {
+  return st.pf256 ? st.pf256 / 256.0f : static_cast<float>(PRED_FACTOR);
+}
+
+// Rank whose key becomes the next threshold: pf * k (at least k + 1).
+__device__ __forceinline__ uint32_t pred_rank(const FastState& st, uint32_t k) {
+  const float r = pred_factor(st) * static_cast<float>(k);
+  return max(k + 1u, static_cast<uint32_t>(fminf(r, 4.0e9f)));
+}
+
+__device__ __forceinline__ uint32_t pf_encode(float pf) {
+  return static_cast<uint32_t>(fminf(fmaxf(pf, 1.25f), 8.0f) * 256.0f);
+}
 
 // Cross-CTA scratch of select_coop_kernel (device memory of the bucket).
 struct CoopScratch {
@@ -286,14 +303,16 @@ __device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t 
   *key2_out = prefix[1];
 }
 
-// Candidate path of one big layer inside one CTA.  Returns false if the candidate set cannot be
-// proven to hold the top-k (the caller queues the layer for the grid-wide dense path).
-// Candidates are gathered once into shared memory (value + index, ascending index order) when
-// they fit (2*m words <= smem_words), else into the bucket's global scratch.
-__device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
-                                 const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
-                                 int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
-                                 int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, CoopSmem& cs) {
+// Candidate path of one big layer inside one CTA.  Returns 0 on success, or why the candidate set
+// cannot be proven to hold the top-k (FB_TOO_FEW / FB_OVERFLOW); the caller then queues the layer
+// for the grid-wide dense path.  Candidates are gathered once into shared memory (value + index,
+// ascending index order) when they fit (2*m words <= smem_words), else into global scratch.
+constexpr int FB_TOO_FEW = 1, FB_OVERFLOW = 2;
+
+__device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
+                                const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
+                                int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
+                                int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, CoopSmem& cs) {
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
   uint32_t local = 0, over = 0;
@@ -304,10 +323,12 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
   }
   const uint32_t m = block_sum(local, sm);
   over = block_sum(over, sm);
-  if (over || (m < k && st.thr > 1u)) return false;
+  if (over) return FB_OVERFLOW;
+  if (m < k && st.thr > 1u) return FB_TOO_FEW;
   float* data = r + L.offset;
   uint32_t cnt = 0;
   uint32_t pred = st.thr;
+  const uint32_t k2 = pred_rank(st, k);
   if (m > 0) {
     const bool in_smem = 2u * m <= static_cast<uint32_t>(smem_words);
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
@@ -340,7 +361,7 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
     auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
     SelectThreshold<uint32_t> th;
     uint32_t key2;
-    radix_select_dual(key_at, m, k, PRED_FACTOR * k, cs, &th, &key2);
+    radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
       *x = sv[i];
       *key = Key<float>::of(*x);
@@ -354,14 +375,14 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
       data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
     };
     cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
-    // next threshold: the (PRED_FACTOR*k)-th largest candidate key, or, when fewer candidates were
-    // seen, an extrapolation below the current threshold from the observed candidate density
-    if (m >= PRED_FACTOR * k) {
+    // next threshold: the k2-th largest candidate key, or, when fewer candidates were seen, an
+    // extrapolation below the current threshold from the observed candidate density
+    if (m >= k2) {
       pred = key2;
     } else if (st.thr > 1u) {
       const uint32_t T = max(th.prefix, st.thr);
       const double density = (static_cast<double>(m - min(m, k)) + 1.0) / (static_cast<double>(T - st.thr) + 1.0);
-      double step = (static_cast<double>(PRED_FACTOR * k) - m) / density;
+      double step = (static_cast<double>(k2) - m) / density;
       step = fmin(fmax(step, 64.0), 4.0 * (static_cast<double>(T - st.thr) + (1 << 16)));
       pred = st.thr > step ? st.thr - static_cast<uint32_t>(step) : 1u;
     }
@@ -371,17 +392,24 @@ __device__ bool candidate_select(int j, const lags_layer_t& L, int2 tr, FastStat
     ns.thr = max(pred, 1u);
     ns.last_cands = m;
     ns.calls += 1;
+    // feedback on the rank factor: the threshold set last call (rank pf*k) produced m candidates
+    // now; steer the next one toward PRED_TARGET * k (geometric mean of old and corrected factor)
+    if (m > 0) {
+      const float pf = pred_factor(st);
+      const float corrected = pf * PRED_TARGET * static_cast<float>(k) / static_cast<float>(m);
+      ns.pf256 = pf_encode(sqrtf(pf * fmaxf(corrected, 0.25f)));
+    }
     state[j] = ns;
     count_out[j] = static_cast<int32_t>(cnt);
   }
   __syncthreads();
-  return true;
+  return 0;
 }
 
 // Dense exact path of one big layer by all CTAs of the cooperative grid.
 __device__ void coop_dense_select(int j, int f, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
                                   float* val_out, int32_t* count_out, FastState* state, const CoopScratch& sc,
-                                  bool force_exact, CoopSmem& cs) {
+                                  bool force_exact, int why, CoopSmem& cs) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   RadixSmem<Key<float>::RB>& sm = cs.sm;
@@ -391,8 +419,10 @@ __device__ void coop_dense_select(int j, int f, const lags_layer_t& L, FastState
   const int G = gridDim.x, c = blockIdx.x;
   uint32_t* H = sc.hist + static_cast<int64_t>(f) * F32_PASSES * 2 * F32_BINS;
   uint32_t prefix[2] = {0u, 0u}, pmask[2] = {0u, 0u};
-  const int64_t pk = static_cast<int64_t>(PRED_FACTOR) * k;
-  uint32_t rank[2] = {k, static_cast<uint32_t>(pk < d ? pk : d)};
+  // a failed prediction widens the candidate margin (too few) or narrows it (task overflow)
+  const float pf_next = why == FB_OVERFLOW ? 0.5f * pred_factor(st) : 2.0f * pred_factor(st);
+  const int64_t pk = static_cast<int64_t>(pf_next * static_cast<float>(k));
+  uint32_t rank[2] = {k, static_cast<uint32_t>(pk < d ? (pk > k ? pk : k + 1) : d)};
   uint32_t n_gt0 = 0;
   bool done[2] = {static_cast<int64_t>(k) >= d, false};
   int shift = 31 - Key<float>::RB, width = Key<float>::RB;
@@ -494,6 +524,7 @@ __device__ void coop_dense_select(int j, int f, const lags_layer_t& L, FastState
     ns.fallbacks += (st.thr != 0u && !force_exact) ? 1u : 0u;
     ns.last_cands = 0;
     ns.calls += 1;
+    if (st.thr != 0u && !force_exact) ns.pf256 = pf_encode(pf_next);
     state[j] = ns;
   }
 }
@@ -529,11 +560,12 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
       }
       path = 0u;
     } else {
-      const bool ok = !force_exact && st.thr != 0u &&
-                      candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
-                                       idx_out, val_out, count_out, state, skeys, smem_keys, cs);
-      if (!ok && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j;
-      path = ok ? 1u : 2u;
+      const int why = (force_exact || st.thr == 0u)
+                          ? FB_TOO_FEW
+                          : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx,
+                                             gval, r, idx_out, val_out, count_out, state, skeys, smem_keys, cs);
+      if (why && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j | (why << 24);
+      path = why ? 2u : 1u;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -546,10 +578,11 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
   if (nf == 0) return;  // uniform: every CTA read the same count after the grid sync
   // phase 2: every queued layer by the whole grid
   for (uint32_t f = 0; f < nf; ++f) {
-    const int j = __ldcg(sc.fb_list + f);
+    const int entry = __ldcg(sc.fb_list + f);
+    const int j = entry & 0xffffff;
     // (chunk_cnt reuse is safe: the next layer passes a grid sync before rewriting it)
     coop_dense_select(j, static_cast<int>(f), layers[j], state[j], r, idx_out, val_out, count_out, state, sc,
-                      force_exact != 0, cs);
+                      force_exact != 0, entry >> 24, cs);
   }
   // leave the scratch clean for the next call (nobody reads the histograms after the last
   // compaction's grid sync)
