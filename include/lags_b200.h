@@ -50,7 +50,8 @@ typedef enum { LAGS_F32 = 0, LAGS_F64 = 1, LAGS_F32_ACC64 = 2 } lags_dtype_t;
 #define LAGS_STATUS_NONFINITE 0x1u /* a gradient entry was inf/nan -> DivergenceError (R: training.py:174-175) */
 
 /* lags_bucket_compress flags */
-#define LAGS_COMPRESS_EXACT 0x1u /* skip the predicted-threshold fast path (dense exact selection) */
+#define LAGS_COMPRESS_EXACT 0x1u     /* skip the predicted-threshold fast path (dense exact selection) */
+#define LAGS_COMPRESS_ZERO_GRAD 0x2u /* clear g after reading it (fused zero_grad of the optimizer)   */
 
 int lags_abi_version(void);
 const char* lags_last_error(void);
@@ -82,8 +83,9 @@ int lags_bucket_message_layout(const lags_bucket_t* bucket, int64_t* off_counts,
 /* One worker's compress of the bucket -- per layer l replaces R: training.py:250-252
  *   acc = r + alpha*g;  chunk = top_k(acc, k_l);  r = acc - decompress(chunk)
  * plus the finiteness check of R: training.py:174 (fused; ORs LAGS_STATUS_NONFINITE into
- * *status, never clears it).  Writes the message (layout above) to `msg`. */
-int lags_bucket_compress(lags_bucket_t* bucket, const void* g, void* r, double alpha, void* msg, uint32_t* status,
+ * *status, never clears it).  Writes the message (layout above) to `msg`.  g is read-only unless
+ * LAGS_COMPRESS_ZERO_GRAD is set. */
+int lags_bucket_compress(lags_bucket_t* bucket, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, lags_stream_t stream);
 
 /* Decode + update after the exchange -- replaces R: training.py:248,253-254:

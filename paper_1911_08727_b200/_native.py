@@ -16,6 +16,7 @@ _LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblagsb20
 F32, F64, F32_ACC64 = 0, 1, 2
 STATUS_NONFINITE = 0x1
 COMPRESS_EXACT = 0x1
+COMPRESS_ZERO_GRAD = 0x2
 OK, ERR_INVALID_ARG, ERR_K_OUT_OF_RANGE, ERR_STRUCTURE, ERR_WORKSPACE, ERR_CUDA = 0, -1, -2, -3, -4, -5
 
 if not os.path.exists(_LIB_PATH):

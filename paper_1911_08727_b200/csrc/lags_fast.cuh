@@ -101,9 +101,12 @@ __device__ __forceinline__ void emit_candidates(uint32_t bits, const float* vals
   cnt += __shfl_sync(0xffffffffu, inc, 31);
 }
 
+// ZERO_G: also clear the gradient after reading it (the optimizer's zero_grad fused into the pass;
+// +4 B/element of writes instead of a separate memset pass).
+template <bool ZERO_G>
 __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
-    const FastState* __restrict__ state, const float* __restrict__ g, float* __restrict__ r, float alpha, int cap,
+    const FastState* __restrict__ state, float* __restrict__ g, float* __restrict__ r, float alpha, int cap,
     int32_t* __restrict__ cand_idx, float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
     uint32_t* status) {
   const int lane = threadIdx.x & 31;
@@ -125,6 +128,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     float a = 0.f;
     if (lane < h) {
       const float gi = g[s + lane];
+      if (ZERO_G) g[s + lane] = 0.0f;
       bad |= nonfinite(gi);
       a = accum(r[s + lane], gi, alpha);
       r[s + lane] = a;
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
   }
   const int64_t vb = s + h;
   const int64_t n4 = (e - vb) >> 2;
-  const float4* g4 = reinterpret_cast<const float4*>(g + vb);
+  float4* g4 = reinterpret_cast<float4*>(g + vb);
   float4* r4 = reinterpret_cast<float4*>(r + vb);
   for (int64_t q0 = 0; q0 < n4; q0 += 32 * K1_UNROLL) {
     float4 gv[K1_UNROLL], rv[K1_UNROLL];
@@ -144,6 +148,13 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
       if (q < n4) {
         gv[u] = __ldcs(g4 + q);
         rv[u] = r4[q];
+      }
+    }
+    if (ZERO_G) {
+#pragma unroll
+      for (int u = 0; u < K1_UNROLL; ++u) {
+        const int64_t q = q0 + u * 32 + lane;
+        if (q < n4) __stcs(g4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
       }
     }
 #pragma unroll
@@ -171,6 +182,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     float a = 0.f;
     if (t0 + lane < e) {
       const float gi = g[t0 + lane];
+      if (ZERO_G) g[t0 + lane] = 0.0f;
       bad |= nonfinite(gi);
       a = accum(r[t0 + lane], gi, alpha);
       r[t0 + lane] = a;

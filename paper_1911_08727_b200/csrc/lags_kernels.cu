@@ -441,7 +441,7 @@ int lags_bucket_message_layout(const lags_bucket_t* b, int64_t* off_counts, int6
   return LAGS_OK;
 }
 
-int lags_bucket_compress(lags_bucket_t* b, const void* g, void* r, double alpha, void* msg, uint32_t* status,
+int lags_bucket_compress(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, lags_stream_t stream) {
   if (!b || !g || !r || !msg || !status) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
   if (!aligned16(g) || !aligned16(r) || !aligned16(msg))
@@ -455,9 +455,14 @@ int lags_bucket_compress(lags_bucket_t* b, const void* g, void* r, double alpha,
     const bool exact = (flags & LAGS_COMPRESS_EXACT) != 0;
     const float a = static_cast<float>(alpha);  // numpy casts a Python float to float32 (NEP 50)
     const int blocks = (b->ntasks + K1_WARPS - 1) / K1_WARPS;
-    accum_emit_kernel<<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
-                                                        static_cast<const float*>(g), static_cast<float*>(r), a, b->cap,
-                                                        b->cand_idx, b->cand_val, b->cand_cnt, status);
+    if (flags & LAGS_COMPRESS_ZERO_GRAD)
+      accum_emit_kernel<true><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
+                                                               static_cast<float*>(g), static_cast<float*>(r), a,
+                                                               b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status);
+    else
+      accum_emit_kernel<false><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
+                                                                static_cast<float*>(g), static_cast<float*>(r), a,
+                                                                b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status);
     const lags_layer_t* layers = b->layers;
     const int2* ltasks = b->layer_tasks;
     const int32_t* order = b->order;
@@ -487,6 +492,8 @@ int lags_bucket_compress(lags_bucket_t* b, const void* g, void* r, double alpha,
         static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(r), alpha, n, status);
     select_dense_kernel<double><<<b->nlayers, SEL_NT, 0, s>>>(b->layers, lags_layer_t{}, static_cast<double*>(r), idx,
                                                               reinterpret_cast<double*>(m + b->off_val), cnt, 1);
+    if ((flags & LAGS_COMPRESS_ZERO_GRAD) && cudaMemsetAsync(const_cast<void*>(g), 0, sizeof(double) * n, s) != cudaSuccess)
+      return cuda_check("zero grad", 2);
     return cuda_check("lags_bucket_compress(f64)", 2);
   }
   // LAGS_F32_ACC64: fp64 acc in the bucket memory, fp32 residual rewritten after selection
@@ -495,6 +502,8 @@ int lags_bucket_compress(lags_bucket_t* b, const void* g, void* r, double alpha,
   select_dense_kernel<double><<<b->nlayers, SEL_NT, 0, s>>>(b->layers, lags_layer_t{}, b->acc64, idx,
                                                             reinterpret_cast<double*>(m + b->off_val), cnt, 1);
   store_residual_kernel<<<stream_grid(n, 256, 8), 256, 0, s>>>(b->acc64, static_cast<float*>(r), n);
+  if ((flags & LAGS_COMPRESS_ZERO_GRAD) && cudaMemsetAsync(const_cast<void*>(g), 0, sizeof(float) * n, s) != cudaSuccess)
+    return cuda_check("zero grad", 3);
   return cuda_check("lags_bucket_compress(f32/acc64)", 3);
 }
 

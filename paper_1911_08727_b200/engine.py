@@ -102,16 +102,17 @@ class Bucket:
 
     # -- kernels -----------------------------------------------------------------------------
     def compress(self, g: torch.Tensor, r: torch.Tensor, alpha: float, msg: torch.Tensor,
-                 status: torch.Tensor, stream=None, exact: bool = False) -> None:
-        """acc = r + alpha*g; per-layer top-k; r <- acc with selected entries +0.0; msg <- pairs."""
+                 status: torch.Tensor, stream=None, exact: bool = False, zero_grad: bool = False) -> None:
+        """acc = r + alpha*g; per-layer top-k; r <- acc with selected entries +0.0; msg <- pairs.
+        ``zero_grad`` clears g in the same pass (the optimizer's fused zero_grad)."""
         sd = storage_dtype(self.mode)
         if g.dtype != sd or r.dtype != sd:
             raise TypeError(f"bucket mode {self.mode} expects {sd} buffers")
         if g.numel() < self.n_total or r.numel() < self.n_total or msg.numel() < self.msg_bytes:
             raise ValueError("buffer smaller than the bucket")
+        flags = (N.COMPRESS_EXACT if exact else 0) | (N.COMPRESS_ZERO_GRAD if zero_grad else 0)
         N.check(N.lags_bucket_compress(self._h, g.data_ptr(), r.data_ptr(), float(alpha), msg.data_ptr(),
-                                       status.data_ptr(), N.COMPRESS_EXACT if exact else 0, stream_handle(stream)),
-                "lags_bucket_compress")
+                                       status.data_ptr(), flags, stream_handle(stream)), "lags_bucket_compress")
 
     def decode(self, msgs: torch.Tensor, P: int, v: torch.Tensor, momentum: torch.Tensor | None = None,
                mu: float = 0.0, stream=None, msg_stride: int | None = None) -> None:

@@ -1,0 +1,260 @@
+"""LagsSGD: layer-wise adaptive gradient sparsification as a torch optimizer on real ranks.
+
+The reference simulates P workers in one process (R: training.py:227-255) and only *models*
+the overlap of communication with backprop (R: perf.py:173-195).  Here every rank is a GPU:
+
+* parameters, gradients and the error-feedback residual live in flat per-rank buffers with the
+  reference's layer layout (R: layered.py:46-107); ``p.data`` / ``p.grad`` are views into them;
+* layers are grouped into fusion buckets in backprop order with the reference's flush rule
+  (R: sparsify.py:209-238), using the fixed k_l-slot message of each layer as the chunk size;
+* a ``post_accumulate_grad`` hook marks a parameter ready; when a bucket is complete it is launched
+  on a side stream: compress (residual add + per-layer exact top-k + residual zeroing + fused
+  zero_grad) -> all-gather of the fixed-size sparse messages (NCCL over NVLink) -> rank-ordered
+  fp64 decode + SGD (or momentum) update of the bucket's weights.  Buckets launch strictly in
+  release order on every rank ("one serial network channel in release order", R: perf.py:188-193),
+  so layer l's exchange overlaps the backprop of layers < l;
+* ``step()`` launches buckets whose hooks never fired, then makes the compute stream wait for the
+  side stream (the next forward trails the last arrival, R: perf.py:194).
+
+Numerics per layer and rank are exactly ``lags_step``'s (fp32 storage, lr absorbed into the
+residual as in R: training.py:250): selection bit-exact, aggregation in fp64 in rank order.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Iterable, Sequence
+
+import torch
+import torch.distributed as dist
+
+from .errors import DivergenceError
+from .sparsify import CompressionPolicy
+
+CHUNK_HEADER_BYTES = 8  # R: sparsify.py:23 (accounting header of a chunk)
+INDEX_BYTES = 4
+
+
+def selection_counts(dims: Sequence[int], ratios: Sequence[float]) -> list[int]:
+    """k_l = min(d, max(1, floor(d / c_l))) -- R: sparsify.py:182-184."""
+    return [min(d, max(1, int(d // c))) for d, c in zip(dims, ratios)]
+
+
+def plan_buckets(dims: Sequence[int], ks: Sequence[int], capacity_bytes: int, value_width: int = 4):
+    """Fusion buckets in backprop order (layer L first), by the reference's rule
+    (R: sparsify.py:209-238): chunks accumulate until their accounted bytes reach the capacity or
+    the first layer has been produced; chunks are never split or reordered.  A chunk that alone
+    reaches the capacity travels alone (the reference's fusion_flush rejects it; a runtime must
+    still ship it).  Chunk bytes = 8 + k_l * (4 + value_width) with the fixed k_l-slot message.
+    Returns inclusive 0-based layer ranges (lo, hi) in release order."""
+    if capacity_bytes <= 0:
+        raise ValueError("capacity_bytes must be positive")
+    out, pending, total = [], [], 0
+    for l in range(len(dims) - 1, -1, -1):
+        size = CHUNK_HEADER_BYTES + ks[l] * (INDEX_BYTES + value_width)
+        if size >= capacity_bytes:
+            if pending:
+                out.append((min(pending), max(pending)))
+                pending, total = [], 0
+            out.append((l, l))
+            continue
+        pending.append(l)
+        total += size
+        if total >= capacity_bytes or l == 0:
+            out.append((min(pending), max(pending)))
+            pending, total = [], 0
+    return out
+
+
+@dataclass
+class _BucketRT:
+    lo: int
+    hi: int
+    offset: int
+    numel: int
+    engine: object
+    msg_local: torch.Tensor
+    msg_all: torch.Tensor | None
+
+
+class LagsSGD(torch.optim.Optimizer):
+    """Sparsified data-parallel SGD with per-layer density rho_l and error feedback.
+
+    Args:
+        params: parameters in layer order (layer ids 1..L, backprop visits L..1).
+        lr: step size alpha (absorbed into the residual: acc = r + lr * g).
+        rho: uniform density (c = 1/rho), or ``policy`` (a CompressionPolicy over layer ids 1..L).
+        momentum: heavy-ball factor applied to the decoded update (0 = the reference's plain SGD).
+        process_group: torch.distributed group (default: WORLD if initialised, else single rank).
+        bucket_cap_bytes: fusion capacity of the reference's flush rule.
+        engine_factory: builds a bucket engine (default: the CUDA ``Bucket``); tests inject stubs.
+        check_every: read the non-finite flag back every this many steps (DivergenceError).
+    """
+
+    def __init__(self, params: Iterable[torch.nn.Parameter], lr: float, rho: float | None = None,
+                 policy: CompressionPolicy | None = None, momentum: float = 0.0, process_group=None,
+                 bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1):
+        params = [p for p in params]
+        if not params:
+            raise ValueError("no parameters")
+        if (rho is None) == (policy is None):
+            raise ValueError("give exactly one of rho or policy")
+        super().__init__(params, dict(lr=lr, momentum=momentum))
+        self.params = params
+        self.device = params[0].device
+        self.dims = [p.numel() for p in params]
+        L = len(params)
+        if policy is None:
+            policy = CompressionPolicy({i + 1: 1.0 / rho for i in range(L)}, 1.0 / rho)
+        self.policy = policy
+        self.ratios = [policy.ratio_for(i + 1) for i in range(L)]
+        self.ks = selection_counts(self.dims, self.ratios)
+        self.group = process_group
+        self.world = dist.get_world_size(process_group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(process_group) if self.world > 1 else 0
+        self.check_every = max(1, int(check_every))
+        self.mu = float(momentum)
+        # flat per-rank buffers with the reference's layer layout; params and grads become views
+        n = sum(self.dims)
+        self.offsets = [0]
+        for d in self.dims[:-1]:
+            self.offsets.append(self.offsets[-1] + d)
+        with torch.no_grad():
+            self.flat_param = torch.empty(n, dtype=torch.float32, device=self.device)
+            self.flat_grad = torch.zeros(n, dtype=torch.float32, device=self.device)
+            self.residual = torch.zeros(n, dtype=torch.float32, device=self.device)
+            self.momentum_buf = torch.zeros(n, dtype=torch.float32, device=self.device) if self.mu else None
+            for p, off, d in zip(params, self.offsets, self.dims):
+                if p.dtype != torch.float32:
+                    raise TypeError("LagsSGD keeps fp32 parameters")
+                self.flat_param[off:off + d].copy_(p.detach().reshape(-1))
+                p.data = self.flat_param[off:off + d].view_as(p)
+                p.grad = self.flat_grad[off:off + d].view_as(p)
+        if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
+            dist.broadcast(self.flat_param, src=0, group=process_group)
+        if engine_factory is None:
+            from . import _native as N
+            from .engine import Bucket
+
+            def engine_factory(dims, ks, world, device):
+                return Bucket(dims, ks, N.F32, device=device, max_world=world)
+
+        self.buckets: list[_BucketRT] = []
+        self._bucket_of_param = {}
+        for lo, hi in plan_buckets(self.dims, self.ks, bucket_cap_bytes):
+            eng = engine_factory(self.dims[lo:hi + 1], self.ks[lo:hi + 1], self.world, self.device)
+            msg_local = eng.new_messages(1)
+            msg_all = eng.new_messages(self.world) if self.world > 1 else None
+            b = _BucketRT(lo, hi, self.offsets[lo], sum(self.dims[lo:hi + 1]), eng, msg_local, msg_all)
+            for l in range(lo, hi + 1):
+                self._bucket_of_param[id(params[l])] = len(self.buckets)
+            self.buckets.append(b)
+        self._size = [b.hi - b.lo + 1 for b in self.buckets]
+        self._pending = list(self._size)
+        self._next = 0  # next bucket to launch (release order)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
+        self._steps = 0
+        self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in params]
+        self.timing = None  # optional per-bucket CUDA events (see enable_timing)
+
+    # -- scheduling -------------------------------------------------------------------------
+    def _on_grad(self, p: torch.Tensor) -> None:
+        b = self._bucket_of_param.get(id(p))
+        if b is None:
+            return
+        self._pending[b] -= 1
+        # launch every complete bucket in release order (identical collective order on all ranks)
+        while self._next < len(self.buckets) and self._pending[self._next] <= 0:
+            self._launch(self._next)
+            self._next += 1
+
+    def _launch(self, i: int) -> None:
+        b = self.buckets[i]
+        lr = self.param_groups[0]["lr"]
+        g = self.flat_grad[b.offset:b.offset + b.numel]
+        r = self.residual[b.offset:b.offset + b.numel]
+        v = self.flat_param[b.offset:b.offset + b.numel]
+        m = self.momentum_buf[b.offset:b.offset + b.numel] if self.momentum_buf is not None else None
+        if self.side is None:
+            self._run_bucket(i, b, g, r, v, m, lr, None)
+            return
+        cur = torch.cuda.current_stream(self.device)
+        self.side.wait_stream(cur)  # the bucket's gradients are complete on the compute stream
+        with torch.cuda.stream(self.side):
+            self._run_bucket(i, b, g, r, v, m, lr, self.side)
+
+    def _run_bucket(self, i, b, g, r, v, m, lr, stream):
+        t = self.timing[i] if self.timing is not None else None
+        if t is not None:
+            t[0].record(stream)
+        b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=True)
+        if t is not None:
+            t[1].record(stream)
+        if self.world > 1:
+            dist.all_gather_into_tensor(b.msg_all, b.msg_local, group=self.group)
+            msgs = b.msg_all
+        else:
+            msgs = b.msg_local
+        if t is not None:
+            t[2].record(stream)
+        b.engine.decode(msgs, self.world, v, momentum=m, mu=self.mu, stream=stream)
+        if t is not None:
+            t[3].record(stream)
+
+    def enable_timing(self, on: bool = True) -> None:
+        """Record CUDA events around each bucket's compress / exchange / decode."""
+        if on and self.device.type == "cuda":
+            self.timing = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in self.buckets]
+        else:
+            self.timing = None
+
+    def bucket_times_ms(self):
+        """[(compress, exchange, decode)] per bucket of the last step (synchronises)."""
+        if self.timing is None:
+            return None
+        torch.cuda.synchronize(self.device)
+        return [(a.elapsed_time(b), b.elapsed_time(c), c.elapsed_time(d)) for a, b, c, d in self.timing]
+
+    # -- optimizer API ----------------------------------------------------------------------
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = None
+        if closure is not None:
+            with torch.enable_grad():
+                loss = closure()
+        while self._next < len(self.buckets):  # hooks that never fired (unused params, no backward)
+            self._launch(self._next)
+            self._next += 1
+        if self.side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._pending = list(self._size)
+        self._next = 0
+        self._steps += 1
+        if self._steps % self.check_every == 0 and int(self.status.item()):
+            raise DivergenceError("a worker produced a non-finite gradient", iteration=self._steps)
+        return loss
+
+    def zero_grad(self, set_to_none: bool = False):
+        """Gradients are cleared by the compress pass itself; the views must stay in place."""
+        return None
+
+    def state_dict(self):
+        sd = super().state_dict()
+        sd["lags"] = {"residual": self.residual.clone(), "momentum": None if self.momentum_buf is None
+                      else self.momentum_buf.clone(), "steps": self._steps, "ks": list(self.ks)}
+        return sd
+
+    def load_state_dict(self, state_dict):
+        lags = state_dict.pop("lags", None)
+        super().load_state_dict(state_dict)
+        if lags is not None:
+            self.residual.copy_(lags["residual"])
+            if self.momentum_buf is not None and lags["momentum"] is not None:
+                self.momentum_buf.copy_(lags["momentum"])
+            self._steps = int(lags["steps"])
+
+    def remove_hooks(self):
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
