@@ -280,14 +280,19 @@ def run_ours(args, dims, ks, world, rank, local):
     clocks.start()
     for t in range(args.warmup):
         step(t)
-    # keep the GPU busy (still untimed warm-up) until clocks have settled and the sampler runs
-    soak_end = time.time() + args.soak
-    t = args.warmup
-    while time.time() < soak_end:
-        for _ in range(50):
-            step(t)
-            t += 1
-        torch.cuda.synchronize(dev)
+    # keep the GPU busy (still untimed warm-up) until clocks have settled and the sampler runs;
+    # the step count is agreed across ranks (every rank must issue the same collectives)
+    torch.cuda.synchronize(dev)
+    t0 = time.time()
+    for t in range(10):
+        step(t)
+    torch.cuda.synchronize(dev)
+    per_step = max((time.time() - t0) / 10, 1e-6)
+    n_soak = torch.tensor([int(args.soak / per_step)], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(n_soak, op=dist.ReduceOp.MAX)
+    for t in range(int(n_soak.item())):
+        step(t)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -341,6 +346,11 @@ def run_ours(args, dims, ks, world, rank, local):
 
     e2e = None
     cpu = None
+    train = None
+    if not args.no_train:  # all ranks (collectives inside)
+        del g_bufs
+        torch.cuda.empty_cache()
+        train = measure_train(args, world, rank, local, dev)
     if rank == 0 and not args.no_e2e:
         e2e = measure_e2e(args, dims, ks, L, dev)
     if rank == 0 and not args.no_cpu:
@@ -361,12 +371,95 @@ def run_ours(args, dims, ks, world, rank, local):
                          "frac": round(achieved / peak, 4), "traffic": None,
                          "algorithmic_bytes_per_launch": int(comp_bytes_rank), "ms_per_launch": round(comp_ms, 4)},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
+            "resnet50_train": train,
             "selection": {"layers": len(dims),
                           "dense_fallbacks_in_timed_region": int(stats[:, 1].sum() - stats0[:, 1].sum()),
                           "candidate_path_layers": int((stats[:, 2] > 0).sum()),
                           "candidates_per_step": int(stats[:, 2].sum())},
         }
         print(json.dumps(out), flush=True)
+
+
+def measure_train(args, world, rank, local, dev):
+    """ResNet-50 (config 4) training iterations/s, batch 64/GPU, bf16 autocast, synthetic data:
+    LagsSGD (hook-driven sparse exchange) vs dense S-SGD (torch DDP, NCCL all-reduce, 25 MB
+    buckets), plus LagsSGD with the exchange replaced by a local no-op for the hidden fraction."""
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    from paper_1911_08727_b200.optim import LagsSGD
+    from paper_1911_08727_b200.workloads import resnet50, synthetic_images
+
+    torch.backends.cudnn.benchmark = True
+    x, y = synthetic_images(64, 224, 1000, dev, seed=rank)
+
+    def run(kind):
+        torch.manual_seed(0)
+        model = resnet50().to(dev)
+        if kind == "dense":
+            net = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local], bucket_cap_mb=25) \
+                if world > 1 else model
+            opt = torch.optim.SGD(model.parameters(), lr=0.1)
+        else:
+            net = model
+            opt = LagsSGD(model.parameters(), lr=0.1, rho=RHO, bucket_cap_bytes=args.bucket_cap,
+                          exchange=(kind == "lags"))
+
+        def it():
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                loss = F.cross_entropy(net(x), y)
+            loss.backward()
+            opt.step()
+            if kind == "dense":
+                opt.zero_grad(set_to_none=True)
+
+        for _ in range(args.train_warmup):
+            it()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.train_steps):
+            it()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = torch.tensor([e0.elapsed_time(e1) / args.train_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        comm = None
+        if kind == "lags":
+            opt.enable_timing(True)
+            it()
+            times = opt.bucket_times_ms()
+            comm = torch.tensor([sum(t[1] for t in times), sum(t[0] for t in times), sum(t[2] for t in times)],
+                                device=dev)
+            if world > 1:
+                dist.all_reduce(comm, op=dist.ReduceOp.MAX)
+            comm = [float(c) for c in comm]
+            nb = len(opt.buckets)
+            opt.remove_hooks()
+        else:
+            nb = None
+        del opt, net, model
+        torch.cuda.empty_cache()
+        return float(ms), comm, nb
+
+    lags_ms, comm, nb = run("lags")
+    nx_ms, _, _ = run("lags_noexchange")
+    dense_ms, _, _ = run("dense")
+    out = {"model": "resnet50 (torchvision, random init)", "batch_per_gpu": 64, "amp": "bf16 autocast, fp32 weights",
+           "rho": RHO, "buckets": nb, "bucket_cap_bytes": args.bucket_cap, "steps": args.train_steps,
+           "lags_iter_per_s": round(1e3 / lags_ms, 3), "lags_ms_per_iter": round(lags_ms, 3),
+           "dense_ddp_iter_per_s": round(1e3 / dense_ms, 3), "dense_ms_per_iter": round(dense_ms, 3),
+           "lags_no_exchange_ms_per_iter": round(nx_ms, 3),
+           "sum_compress_ms": round(comm[1], 3), "sum_exchange_ms": round(comm[0], 3),
+           "sum_decode_ms": round(comm[2], 3)}
+    if world > 1 and comm[0] > 0:
+        exposed = max(0.0, lags_ms - nx_ms)
+        out["exchange_hidden_fraction"] = round(max(0.0, min(1.0, 1.0 - exposed / comm[0])), 4)
+    return out
 
 
 def measure_e2e(args, dims, ks, L, dev):
@@ -406,6 +499,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the ResNet-50 training-iteration measurement")
+    ap.add_argument("--train-steps", type=int, default=20)
+    ap.add_argument("--train-warmup", type=int, default=8)
+    ap.add_argument("--bucket-cap", type=int, default=1 << 16, help="fusion capacity (bytes) for LagsSGD")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     dims = resnet50_dims()

@@ -93,7 +93,8 @@ class LagsSGD(torch.optim.Optimizer):
 
     def __init__(self, params: Iterable[torch.nn.Parameter], lr: float, rho: float | None = None,
                  policy: CompressionPolicy | None = None, momentum: float = 0.0, process_group=None,
-                 bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1):
+                 bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1,
+                 exchange: bool = True):
         params = [p for p in params]
         if not params:
             raise ValueError("no parameters")
@@ -114,6 +115,9 @@ class LagsSGD(torch.optim.Optimizer):
         self.rank = dist.get_rank(process_group) if self.world > 1 else 0
         self.check_every = max(1, int(check_every))
         self.mu = float(momentum)
+        # exchange=False replaces the all-gather by a local no-op (decode of the own message only):
+        # a measurement mode for the exposed-communication time, not a training mode
+        self.exchange = bool(exchange)
         # flat per-rank buffers with the reference's layer layout; params and grads become views
         n = sum(self.dims)
         self.offsets = [0]
@@ -191,14 +195,14 @@ class LagsSGD(torch.optim.Optimizer):
         b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=True)
         if t is not None:
             t[1].record(stream)
-        if self.world > 1:
+        if self.world > 1 and self.exchange:
             dist.all_gather_into_tensor(b.msg_all, b.msg_local, group=self.group)
-            msgs = b.msg_all
+            msgs, P = b.msg_all, self.world
         else:
-            msgs = b.msg_local
+            msgs, P = b.msg_local, 1
         if t is not None:
             t[2].record(stream)
-        b.engine.decode(msgs, self.world, v, momentum=m, mu=self.mu, stream=stream)
+        b.engine.decode(msgs, P, v, momentum=m, mu=self.mu, stream=stream)
         if t is not None:
             t[3].record(stream)
 
