@@ -1,24 +1,20 @@
 // fp32 fast path: one streaming pass over g and r that also emits index-ordered candidates above
-// a per-layer predicted threshold, then a cooperative per-layer exact select.
+// a per-layer predicted threshold, then a per-layer exact select over the candidates.
 //
 // K1 (accum_emit_kernel): one warp per task (a <= TASK_ELEMS slice of one layer).  Reads g and r
 //    once (16-byte vectors), writes acc back into r, ORs the non-finite flag, and appends every
 //    entry with key(acc) >= thr[layer] to the task's candidate list in ascending index order
 //    (warp ballot + shuffle scan, no atomics).  Algorithmic traffic: 12 B/element.
-// K2 (select_coop_kernel, cooperative launch, one CTA per SM):
-//    phase 1  CTAs take layers (largest work first).  A big layer whose candidate set provably
-//             holds its top-k (count >= k, no task overflow) is selected from the candidates
-//             alone (radix select in shared memory + ordered compaction + residual zeroing by
-//             scatter) and predicts its next threshold from them.  Small layers run the dense
-//             exact path inside the CTA.  Other big layers are queued.
-//    phase 2  all CTAs cooperate on each queued layer: a multi-CTA dense radix select over r
-//             (global histograms, grid syncs) that resolves the k-th key exactly and the
-//             PRED_FACTOR*k-th key for the next prediction, then an ordered multi-CTA compaction.
+// K2a (select_phase1_kernel, one CTA per layer, largest work first): a big layer whose candidate
+//    set provably holds its top-k (count >= k, no task overflow) is selected from the candidates
+//    alone (dual-rank radix select in shared memory, ordered compaction, residual zeroing by
+//    scatter) and predicts its next threshold; small layers run the dense exact path staged in
+//    shared memory; other big layers are queued.
+// K2b (select_fallback_kernel): one CTA per queued layer runs the dense exact path over r.
 // Every path returns exactly the reference's selection: the candidate set contains every top-k
-// element, and the dense paths scan all of r.
+// element, and the dense paths scan all of r.  All launches are ordinary (not cooperative), so
+// the selection can share the GPU with backprop kernels on other streams.
 #pragma once
-#include <cooperative_groups.h>
-
 #include "lags_select.cuh"
 
 namespace lags {
@@ -64,12 +60,10 @@ __device__ __forceinline__ uint32_t pf_encode(float pf) {
   return static_cast<uint32_t>(fminf(fmaxf(pf, 1.25f), 8.0f) * 256.0f);
 }
 
-// Cross-CTA scratch of select_coop_kernel (device memory of the bucket).
+// Queue of layers for the dense fallback (device memory of the bucket).
 struct CoopScratch {
-  uint32_t* fb_count;   // [1] queued dense layers (reset to 0 by the kernel)
-  int32_t* fb_list;     // [nlayers]
-  uint32_t* hist;       // [nlayers][F32_PASSES][2][F32_BINS] global histograms (left zeroed)
-  uint32_t* chunk_cnt;  // [2 * grid] per-CTA (gt, eq) counts of the compaction
+  uint32_t* fb_count;  // [1] queued layers (reset by the next call's accum_emit_kernel)
+  int32_t* fb_list;    // [nlayers] layer | reason << 24
 };
 
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
@@ -108,9 +102,10 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
     const FastState* __restrict__ state, float* __restrict__ g, float* __restrict__ r, float alpha, int cap,
     int32_t* __restrict__ cand_idx, float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
-    uint32_t* status) {
+    uint32_t* status, uint32_t* fb_count) {
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
+  if (wid == 0 && lane == 0) *fb_count = 0u;  // the previous call's fallback kernel has completed
   if (wid >= ntasks) return;
   const Task T = tasks[wid];
   const int64_t loff = layers[T.layer].offset;
@@ -245,16 +240,20 @@ __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32
 // Two ranks in one set of radix passes over m keys (shared memory): the exact threshold of the
 // k largest (select form) and a lower bound of the k2-th largest key (the next prediction).
 // Passes start below the common prefix of all keys (candidates crowd just above the threshold).
+// skip_prefix = false (dense data in global memory) starts at the top bit without the OR pass.
 template <typename KeyAt>
 __device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t k2, CoopSmem& cs,
-                                  SelectThreshold<uint32_t>* th_out, uint32_t* key2_out) {
+                                  SelectThreshold<uint32_t>* th_out, uint32_t* key2_out, bool skip_prefix = true) {
   constexpr int RB = Key<float>::RB;
   constexpr uint32_t FULL = 0x7fffffffu;
   RadixSmem<RB>& sm = cs.sm;
-  const uint32_t key0 = key_at(0);
-  uint32_t diff = 0;
-  for (int64_t i = threadIdx.x; i < m; i += SEL_NT) diff |= key_at(i) ^ key0;
-  diff = block_or<uint32_t, RB>(diff, sm);
+  const uint32_t key0 = skip_prefix ? key_at(0) : 0u;
+  uint32_t diff = FULL;
+  if (skip_prefix) {
+    diff = 0;
+    for (int64_t i = threadIdx.x; i < m; i += SEL_NT) diff |= key_at(i) ^ key0;
+    diff = block_or<uint32_t, RB>(diff, sm);
+  }
   uint32_t prefix[2], pmask[2];
   uint32_t rank[2] = {static_cast<int64_t>(k) < m ? k : static_cast<uint32_t>(m),
                       static_cast<int64_t>(k2) < m ? k2 : static_cast<uint32_t>(m)};
@@ -418,191 +417,110 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
   return 0;
 }
 
-// Dense exact path of one big layer by all CTAs of the cooperative grid.
-__device__ void coop_dense_select(int j, int f, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
-                                  float* val_out, int32_t* count_out, FastState* state, const CoopScratch& sc,
-                                  bool force_exact, int why, CoopSmem& cs) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  RadixSmem<Key<float>::RB>& sm = cs.sm;
-  const int64_t d = L.dim;
+// Dense exact path of one big layer inside one CTA (first call of a layer, failed prediction or
+// forced exact mode): radix select of the k-th key and, in the same passes, of the next
+// prediction rank over r, then an ordered compaction that zeroes the selected residuals.
+__device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
+                                      float* val_out, int32_t* count_out, FastState* state, bool force_exact,
+                                      int why, CoopSmem& cs) {
   float* data = r + L.offset;
+  const int64_t d = L.dim;
   const uint32_t k = static_cast<uint32_t>(L.k);
-  const int G = gridDim.x, c = blockIdx.x;
-  uint32_t* H = sc.hist + static_cast<int64_t>(f) * F32_PASSES * 2 * F32_BINS;
-  uint32_t prefix[2] = {0u, 0u}, pmask[2] = {0u, 0u};
   // a failed prediction widens the candidate margin (too few) or narrows it (task overflow)
-  const float pf_next = why == FB_OVERFLOW ? 0.5f * pred_factor(st) : 2.0f * pred_factor(st);
-  const int64_t pk = static_cast<int64_t>(pf_next * static_cast<float>(k));
-  uint32_t rank[2] = {k, static_cast<uint32_t>(pk < d ? (pk > k ? pk : k + 1) : d)};
-  uint32_t n_gt0 = 0;
-  bool done[2] = {static_cast<int64_t>(k) >= d, false};
-  int shift = 31 - Key<float>::RB, width = Key<float>::RB;
-  for (int pass = 0; pass < F32_PASSES && !(done[0] && done[1]); ++pass) {
-    for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
-      sm.hist[b] = 0;
-      cs.hist2[b] = 0;
-    }
-    __syncthreads();
-    const uint32_t dmask = (1u << width) - 1u;
-    // both ranks still share their prefix (always true in pass 0): one histogram serves both
-    const bool same = !done[0] && !done[1] && prefix[0] == prefix[1] && pmask[0] == pmask[1];
-    for (int64_t i = static_cast<int64_t>(c) * SEL_NT + threadIdx.x; i < d; i += static_cast<int64_t>(G) * SEL_NT) {
-      const uint32_t key = Key<float>::of(data[i]);
-      if (!done[0] && (key & pmask[0]) == prefix[0]) atomicAdd(&sm.hist[(key >> shift) & dmask], 1u);
-      if (!same && !done[1] && (key & pmask[1]) == prefix[1]) atomicAdd(&cs.hist2[(key >> shift) & dmask], 1u);
-    }
-    __syncthreads();
-    uint32_t* Hp = H + pass * 2 * F32_BINS;
-    const uint32_t* h2 = same ? sm.hist : cs.hist2;
-    for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
-      if (sm.hist[b]) atomicAdd(Hp + b, sm.hist[b]);
-      if (h2[b]) atomicAdd(Hp + F32_BINS + b, h2[b]);
-    }
-    grid.sync();
-    for (int q = 0; q < 2; ++q) {
-      if (done[q]) continue;  // uniform across the grid
-      for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) sm.hist[b] = __ldcg(Hp + q * F32_BINS + b);
-      __syncthreads();
-      uint32_t bin, above, in_bin;
-      find_bin<Key<float>::RB>(sm, rank[q], &bin, &above, &in_bin);
-      prefix[q] |= bin << shift;
-      pmask[q] |= dmask << shift;
-      rank[q] -= above;
-      if (q == 0) n_gt0 += above;
-      if (shift == 0 || (in_bin == rank[q] && prefix[q] != 0u)) done[q] = true;
-      if (q == 1 && pass >= 1) done[1] = true;  // 22 resolved bits are plenty for a prediction
-    }
-    const int ns = shift > Key<float>::RB ? shift - Key<float>::RB : 0;
-    width = shift - ns;
-    shift = ns;
-  }
+  const bool predicted = st.thr != 0u && !force_exact;
+  const float pf_next = !predicted ? pred_factor(st)
+                                   : (why == FB_OVERFLOW ? 0.5f * pred_factor(st) : 2.0f * pred_factor(st));
+  const int64_t pk = static_cast<int64_t>(fmaxf(pf_next, 1.0f) * static_cast<float>(k));
+  const uint32_t k2 = static_cast<uint32_t>(pk < d ? (pk > k ? pk : k + 1) : d);
+  auto key_at = [=](int64_t i) { return Key<float>::of(__ldcg(data + i)); };
   SelectThreshold<uint32_t> th;
-  if (static_cast<int64_t>(k) >= d) {
-    th.prefix = 0u;
-    th.pmask = 0xffffffffu;
-    th.n_gt = 0;
-    th.need_eq = 0;
-  } else {
-    th.prefix = prefix[0];
-    th.pmask = pmask[0];
-    th.n_gt = n_gt0;
-    th.need_eq = prefix[0] == 0u ? 0u : rank[0];
-  }
-  // ordered multi-CTA compaction: CTA c owns the contiguous chunk [lo, hi)
-  const int64_t per = ((d + G - 1) / G + 3) / 4 * 4;
-  const int64_t lo = min(d, static_cast<int64_t>(c) * per), hi = min(d, lo + per);
-  uint32_t lgt = 0, leq = 0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += SEL_NT) {
-    const uint32_t key = Key<float>::of(data[i]);
-    const uint32_t hk = key & th.pmask;
-    if (key != 0u) {
-      lgt += hk > th.prefix ? 1u : 0u;
-      leq += hk == th.prefix ? 1u : 0u;
-    }
-  }
-  lgt = block_sum(lgt, sm);
-  leq = block_sum(leq, sm);
-  if (threadIdx.x == 0) {
-    sc.chunk_cnt[2 * c] = lgt;
-    sc.chunk_cnt[2 * c + 1] = leq;
-  }
-  grid.sync();
-  uint32_t cg0 = 0, ce0 = 0;
-  for (int q = threadIdx.x; q < c; q += SEL_NT) {
-    cg0 += __ldcg(sc.chunk_cnt + 2 * q);
-    ce0 += __ldcg(sc.chunk_cnt + 2 * q + 1);
-  }
-  cg0 = block_sum(cg0, sm);
-  ce0 = block_sum(ce0, sm);
+  uint32_t key2;
+  radix_select_dual(key_at, d, k, k2, cs, &th, &key2, false);
+  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
+    *x = __ldcg(data + i);
+    *key = Key<float>::of(*x);
+    *ix = i;
+  };
   int32_t* oidx = idx_out + L.slot;
   float* oval = val_out + L.slot;
-  float* chunk = data + lo;
-  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
-    *x = chunk[i];
-    *key = Key<float>::of(*x);
-    *ix = lo + i;
-  };
-  auto emit = [=](uint32_t pos, int64_t i, int64_t ix, float x) {
-    oidx[pos] = static_cast<int32_t>(ix);
+  auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
+    oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
-    chunk[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
   };
-  const uint32_t total = ordered_compact<uint32_t, float>(hi - lo, th, load, emit, sm, cg0, ce0);
-  if (c == G - 1 && threadIdx.x == 0) {
-    count_out[j] = static_cast<int32_t>(total);
+  const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
+  if (threadIdx.x == 0) {
+    count_out[j] = static_cast<int32_t>(cnt);
     FastState ns = st;
-    ns.thr = max(prefix[1], 1u);
-    ns.fallbacks += (st.thr != 0u && !force_exact) ? 1u : 0u;
+    ns.thr = max(key2, 1u);
+    ns.fallbacks += predicted ? 1u : 0u;
     ns.last_cands = 0;
     ns.calls += 1;
-    if (st.thr != 0u && !force_exact) ns.pf256 = pf_encode(pf_next);
+    ns.pf256 = pf_encode(pf_next);
     state[j] = ns;
   }
 }
 
-__global__ void __launch_bounds__(SEL_NT, 1) select_coop_kernel(
+// Phase 1: one CTA per layer (largest selection work first).  Big layers take the candidate path
+// when it provably holds the top-k; otherwise they are queued for select_fallback_kernel.  Small
+// layers run the dense exact path staged in shared memory.  An ordinary launch (not cooperative),
+// so the selection overlaps backprop kernels running on other streams.
+__global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
-    int nlayers, FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
+    FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
     const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
     float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc) {
-  namespace cg = cooperative_groups;
   extern __shared__ uint32_t skeys[];
   __shared__ CoopSmem cs;
-  cg::grid_group grid = cg::this_grid();
-  // phase 1: one CTA per layer, largest work first
-  for (int li = blockIdx.x; li < nlayers; li += gridDim.x) {
-    const int j = order[li];
-    const lags_layer_t L = layers[j];
-    const FastState st = state[j];
-    const long long t_begin = clock64();
-    uint32_t path;
-    if (L.dim <= SMALL_LAYER) {
-      const uint32_t cnt =
-          L.dim <= smem_keys
-              ? small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
-                                   val_out + L.slot, reinterpret_cast<float*>(skeys), cs)
-              : exact_topk_dense<float, float>(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
-                                               val_out + L.slot, true, cs.sm);
-      if (threadIdx.x == 0) {
-        count_out[j] = static_cast<int32_t>(cnt);
-        FastState ns = st;
-        ns.calls += 1;
-        state[j] = ns;
-      }
-      path = 0u;
-    } else {
-      const int why = (force_exact || st.thr == 0u)
-                          ? FB_TOO_FEW
-                          : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx,
-                                             gval, r, idx_out, val_out, count_out, state, skeys, smem_keys, cs);
-      if (why && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j | (why << 24);
-      path = why ? 2u : 1u;
-    }
-    __syncthreads();
+  const int j = order[blockIdx.x];
+  const lags_layer_t L = layers[j];
+  const FastState st = state[j];
+  const long long t_begin = clock64();
+  uint32_t path;
+  if (L.dim <= SMALL_LAYER) {
+    const uint32_t cnt =
+        L.dim <= smem_keys
+            ? small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot, val_out + L.slot,
+                                 reinterpret_cast<float*>(skeys), cs)
+            : exact_topk_dense<float, float>(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
+                                             val_out + L.slot, true, cs.sm);
     if (threadIdx.x == 0) {
-      state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
-      state[j].path = path;
+      count_out[j] = static_cast<int32_t>(cnt);
+      FastState ns = st;
+      ns.calls += 1;
+      state[j] = ns;
     }
+    path = 0u;
+  } else {
+    const int why = (force_exact || st.thr == 0u)
+                        ? FB_TOO_FEW
+                        : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval,
+                                           r, idx_out, val_out, count_out, state, skeys, smem_keys, cs);
+    if (why && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j | (why << 24);
+    path = why ? 2u : 1u;
   }
-  grid.sync();
-  const uint32_t nf = __ldcg(sc.fb_count);
-  if (nf == 0) return;  // uniform: every CTA read the same count after the grid sync
-  // phase 2: every queued layer by the whole grid
-  for (uint32_t f = 0; f < nf; ++f) {
-    const int entry = __ldcg(sc.fb_list + f);
-    const int j = entry & 0xffffff;
-    // (chunk_cnt reuse is safe: the next layer passes a grid sync before rewriting it)
-    coop_dense_select(j, static_cast<int>(f), layers[j], state[j], r, idx_out, val_out, count_out, state, sc,
-                      force_exact != 0, entry >> 24, cs);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
+    state[j].path = path;
   }
-  // leave the scratch clean for the next call (nobody reads the histograms after the last
-  // compaction's grid sync)
-  const int64_t hwords = static_cast<int64_t>(nf) * F32_PASSES * 2 * F32_BINS;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * SEL_NT + threadIdx.x; i < hwords;
-       i += static_cast<int64_t>(gridDim.x) * SEL_NT)
-    sc.hist[i] = 0u;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *sc.fb_count = 0u;
+}
+
+// Phase 2: one CTA per queued layer (CTAs beyond the queue exit at once).  fb_count is reset by
+// the next call's accum_emit_kernel.
+__global__ void __launch_bounds__(SEL_NT, 1) select_fallback_kernel(const lags_layer_t* __restrict__ layers,
+                                                                    FastState* state, float* r, int32_t* idx_out,
+                                                                    float* val_out, int32_t* count_out,
+                                                                    int force_exact, CoopScratch sc) {
+  __shared__ CoopSmem cs;
+  if (blockIdx.x >= __ldcg(sc.fb_count)) return;
+  const int entry = __ldcg(sc.fb_list + blockIdx.x);
+  const int j = entry & 0xffffff;
+  const long long t_begin = clock64();
+  dense_fallback_select(j, layers[j], state[j], r, idx_out, val_out, count_out, state, force_exact != 0, entry >> 24,
+                        cs);
+  __syncthreads();
+  if (threadIdx.x == 0) state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
 }
 
 }  // namespace lags

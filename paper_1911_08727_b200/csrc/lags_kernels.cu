@@ -201,7 +201,7 @@ struct lags_bucket {
   char* planes = nullptr;
   int32_t* order = nullptr;  // layers by decreasing selection work (phase-1 schedule)
   CoopScratch coop{};
-  int coop_grid = 0;
+  int n_big = 1;  // layers that can be queued for the dense fallback (its grid size)
 };
 
 namespace {
@@ -251,11 +251,8 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_fbl = 0, o_hist = 0,
-         o_chunk = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_fbl = 0, bytes = 0;
 };
-
-constexpr int MAX_COOP_GRID = 1024;
 
 int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, int32_t max_world, Plan* p) {
   if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "unknown dtype");
@@ -301,8 +298,6 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   const bool f32 = dtype == LAGS_F32;
   p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);
   p->o_fbl = take(f32 ? sizeof(int32_t) * L : 0);
-  p->o_hist = take(f32 ? sizeof(uint32_t) * static_cast<size_t>(L) * F32_PASSES * 2 * F32_BINS : 0);
-  p->o_chunk = take(f32 ? sizeof(uint32_t) * 2 * MAX_COOP_GRID : 0);
   p->bytes = o;
   return LAGS_OK;
 }
@@ -357,8 +352,6 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->order = reinterpret_cast<int32_t*>(base + p.o_order);
   b->coop.fb_count = reinterpret_cast<uint32_t*>(base + p.o_fbc);
   b->coop.fb_list = reinterpret_cast<int32_t*>(base + p.o_fbl);
-  b->coop.hist = reinterpret_cast<uint32_t*>(base + p.o_hist);
-  b->coop.chunk_cnt = reinterpret_cast<uint32_t*>(base + p.o_chunk);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -401,10 +394,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
-      (dtype != LAGS_F32 ||
-       (cudaMemsetAsync(b->coop.fb_count, 0, sizeof(uint32_t), s) == cudaSuccess &&
-        cudaMemsetAsync(b->coop.hist, 0, sizeof(uint32_t) * static_cast<size_t>(nlayers) * F32_PASSES * 2 * F32_BINS,
-                        s) == cudaSuccess)) &&
+      (dtype != LAGS_F32 || cudaMemsetAsync(b->coop.fb_count, 0, sizeof(uint32_t), s) == cudaSuccess) &&
       cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) {
     delete b;
@@ -412,18 +402,15 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   }
   if (dtype == LAGS_F32) {
     const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
-    int occ = 0;
-    if (cudaFuncSetAttribute(select_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, select_coop_kernel, SEL_NT, smem) != cudaSuccess) {
+    if (cudaFuncSetAttribute(select_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+        cudaSuccess) {
       delete b;
-      return cuda_check("select_coop_kernel attributes", 0);
+      return cuda_check("select_phase1_kernel attributes", 0);
     }
-    if (occ < 1) {
-      delete b;
-      return fail(LAGS_ERR_CUDA, "select_coop_kernel cannot be resident on an SM");
-    }
-    b->coop_grid = std::min(num_sms() * occ, MAX_COOP_GRID);
     b->smem_keys = SMEM_KEYS;
+    b->n_big = 0;
+    for (int j = 0; j < nlayers; ++j) b->n_big += dims[j] > SMALL_LAYER ? 1 : 0;
+    if (b->n_big == 0) b->n_big = 1;
   }
   *out = b;
   return LAGS_OK;
@@ -455,37 +442,22 @@ int lags_bucket_compress(lags_bucket_t* b, void* g, void* r, double alpha, void*
     const bool exact = (flags & LAGS_COMPRESS_EXACT) != 0;
     const float a = static_cast<float>(alpha);  // numpy casts a Python float to float32 (NEP 50)
     const int blocks = (b->ntasks + K1_WARPS - 1) / K1_WARPS;
-    if (flags & LAGS_COMPRESS_ZERO_GRAD)
-      accum_emit_kernel<true><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
-                                                               static_cast<float*>(g), static_cast<float*>(r), a,
-                                                               b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status);
-    else
-      accum_emit_kernel<false><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
-                                                                static_cast<float*>(g), static_cast<float*>(r), a,
-                                                                b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status);
-    const lags_layer_t* layers = b->layers;
-    const int2* ltasks = b->layer_tasks;
-    const int32_t* order = b->order;
-    int nl = b->nlayers;
-    FastState* state = b->state;
-    const int32_t* ccnt = b->cand_cnt;
-    const int32_t* cidx = b->cand_idx;
-    const float* cval = b->cand_val;
-    int cap = b->cap;
-    int32_t* gidx = b->gidx;
-    float* gval = b->gval;
     float* rr = static_cast<float*>(r);
     float* vals = reinterpret_cast<float*>(m + b->off_val);
-    int smem_keys = b->smem_keys;
-    int fe = exact ? 1 : 0;
-    CoopScratch sc = b->coop;
-    void* args[] = {&layers, &ltasks, &order, &nl, &state, &ccnt, &cidx, &cval, &cap, &gidx, &gval,
-                    &rr, &idx, &vals, &cnt, &smem_keys, &fe, &sc};
-    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(select_coop_kernel), dim3(b->coop_grid),
-                                    dim3(SEL_NT), args, static_cast<size_t>(smem_keys) * sizeof(uint32_t),
-                                    s) != cudaSuccess)
-      return cuda_check("select_coop_kernel launch", 1);
-    return cuda_check("lags_bucket_compress(f32)", 2);
+    if (flags & LAGS_COMPRESS_ZERO_GRAD)
+      accum_emit_kernel<true><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
+                                                               static_cast<float*>(g), rr, a, b->cap, b->cand_idx,
+                                                               b->cand_val, b->cand_cnt, status, b->coop.fb_count);
+    else
+      accum_emit_kernel<false><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
+                                                                static_cast<float*>(g), rr, a, b->cap, b->cand_idx,
+                                                                b->cand_val, b->cand_cnt, status, b->coop.fb_count);
+    select_phase1_kernel<<<b->nlayers, SEL_NT, static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), s>>>(
+        b->layers, b->layer_tasks, b->order, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
+        b->gval, rr, idx, vals, cnt, b->smem_keys, exact ? 1 : 0, b->coop);
+    select_fallback_kernel<<<b->n_big, SEL_NT, 0, s>>>(b->layers, b->state, rr, idx, vals, cnt, exact ? 1 : 0,
+                                                       b->coop);
+    return cuda_check("lags_bucket_compress(f32)", 3);
   }
   if (b->dtype == LAGS_F64) {
     accum_kernel<double, double><<<stream_grid(n, 256, 8), 256, 0, s>>>(
