@@ -158,6 +158,9 @@ class LagsSGD(torch.optim.Optimizer):
         self._next = 0  # next bucket to launch (release order)
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
+        self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=self.device.type == "cuda")
+        self._status_event = None
+        self._status_step = 0
         self._steps = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in params]
         self.timing = None  # optional per-bucket CUDA events (see enable_timing)
@@ -235,9 +238,31 @@ class LagsSGD(torch.optim.Optimizer):
         self._pending = list(self._size)
         self._next = 0
         self._steps += 1
-        if self._steps % self.check_every == 0 and int(self.status.item()):
-            raise DivergenceError("a worker produced a non-finite gradient", iteration=self._steps)
+        self._poll_status()
         return loss
+
+    def _poll_status(self) -> None:
+        """Non-finite gradients (R: training.py:174-175) without stalling the host: the device flag
+        is copied to pinned memory behind the step and inspected at a later step() once the copy
+        has landed (so DivergenceError may surface a step late); check_divergence() waits."""
+        if self.device.type != "cuda":
+            if int(self.status.item()):
+                raise DivergenceError("a worker produced a non-finite gradient", iteration=self._steps)
+            return
+        if self._status_event is not None and self._status_event.query():
+            if int(self._status_host.item()):
+                raise DivergenceError("a worker produced a non-finite gradient", iteration=self._status_step)
+            self._status_event = None
+        if self._status_event is None and self._steps % self.check_every == 0:
+            self._status_host.copy_(self.status, non_blocking=True)
+            self._status_event = torch.cuda.Event()
+            self._status_event.record(torch.cuda.current_stream(self.device))
+            self._status_step = self._steps
+
+    def check_divergence(self) -> None:
+        """Synchronous check of the non-finite flag (raises DivergenceError)."""
+        if int(self.status.item()):
+            raise DivergenceError("a worker produced a non-finite gradient", iteration=self._steps)
 
     def zero_grad(self, set_to_none: bool = False):
         """Gradients are cleared by the compress pass itself; the views must stay in place."""

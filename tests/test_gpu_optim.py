@@ -67,5 +67,12 @@ def test_lagssgd_divergence(L):
     opt = LagsSGD(model.parameters(), lr=0.05, rho=0.01)
     out = model(torch.randn(4, 256, device="cuda")).sum() * float("nan")
     out.backward()
+    opt.step()  # the flag is read back asynchronously ...
     with pytest.raises(L.DivergenceError):
-        opt.step()
+        opt.check_divergence()  # ... or synchronously on demand
+    torch.cuda.synchronize()
+    with pytest.raises(L.DivergenceError):
+        for _ in range(3):  # ... and surfaces at a later step() once the copy has landed
+            model(torch.randn(4, 256, device="cuda")).sum().backward()
+            opt.step()
+            torch.cuda.synchronize()
