@@ -13,6 +13,7 @@ messages are decoded in rank order, and the results are copied back.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -78,6 +79,68 @@ def _to_dev(a: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False)
 
 
+class HostPinner:
+    """DMA-friendly host buffers for the drop-in's numpy arguments.
+
+    Arrays seen a second time (residuals updated in place, reused gradient buffers) are
+    page-locked in place with cudaHostRegister (bounded LRU, the array is kept alive while
+    registered); first-seen arrays go through pinned staging; results are returned in pinned
+    memory so passing them back next step is a direct DMA.
+    """
+
+    def __init__(self, max_bytes: int = 16 << 30, max_entries: int = 64):
+        self.max_bytes, self.max_entries = max_bytes, max_entries
+        self.registered: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
+        self.seen: "OrderedDict[tuple, bool]" = OrderedDict()
+        self.bytes = 0
+
+    def pinned(self, arr: np.ndarray) -> bool:
+        if not arr.flags.c_contiguous or arr.nbytes == 0:
+            return False
+        key = (arr.ctypes.data, arr.nbytes)
+        if key in self.registered:
+            self.registered.move_to_end(key)
+            return True
+        t = torch.from_numpy(arr)
+        if t.is_pinned():
+            return True
+        if key not in self.seen:
+            self.seen[key] = True
+            if len(self.seen) > 4 * self.max_entries:
+                self.seen.popitem(last=False)
+            return False
+        while self.registered and (self.bytes + arr.nbytes > self.max_bytes or len(self.registered) >= self.max_entries):
+            (ptr, nb), _ = self.registered.popitem(last=False)
+            torch._C._cudart.cudaHostUnregister(ptr)
+            self.bytes -= nb
+        if int(torch._C._cudart.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)) != 0:
+            return False
+        self.registered[key] = arr
+        self.bytes += arr.nbytes
+        return True
+
+    def h2d(self, arr: np.ndarray, device) -> torch.Tensor:
+        arr = np.ascontiguousarray(arr)
+        t = torch.from_numpy(arr)
+        if not self.pinned(arr):
+            st = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            st.copy_(t)
+            t = st
+        return t.to(device, non_blocking=True)
+
+    def d2h_into(self, arr: np.ndarray, src: torch.Tensor):
+        """Copy src into the numpy array; returns a finisher to call after synchronising."""
+        if self.pinned(arr):
+            torch.from_numpy(arr).copy_(src, non_blocking=True)
+            return lambda: None
+        st = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        st.copy_(src, non_blocking=True)
+        return lambda: np.copyto(arr, st.numpy())
+
+
+_PINNER = HostPinner()
+
+
 def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: int | None = None):
     """Per-layer selection with error feedback on the B200; R: training.py:227-255."""
     pairs = layout_of(v)
@@ -113,19 +176,25 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
         ks.append(k)
     bucket = _bucket_for(dims, tuple(ks), mode, P)
 
-    v_d = _to_dev(v.data)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pin = _PINNER
+    v_d = pin.h2d(v.data, dev)
     msgs = bucket.new_messages(P)
     r_devs = []
     for p in range(P):
-        g_d = _to_dev(grads[p].data)
-        r_d = _to_dev(residuals[p].data)
+        g_d = pin.h2d(grads[p].data, dev)
+        r_d = pin.h2d(residuals[p].data, dev)
         bucket.compress(g_d, r_d, alpha, msgs[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes], status[p:p + 1])
         r_devs.append(r_d)
     bucket.decode(msgs, P, v_d)
-    st = status.cpu().numpy()
+    out = torch.empty(v_d.shape, dtype=v_d.dtype, pin_memory=True)
+    out.copy_(v_d, non_blocking=True)
+    st = status.cpu().numpy()  # synchronises: inputs copied, compress + decode done
     for p in range(P):
         if st[p] & N.STATUS_NONFINITE:  # residuals untouched on the host, as in the reference
             raise DivergenceError(f"worker {p + 1} produced a non-finite gradient", iteration=t)
-    for r_d, res in zip(r_devs, residuals):
-        res.data[:] = r_d.cpu().numpy()
-    return type(v)(v.shape, v_d.cpu().numpy())
+    finish = [pin.d2h_into(res.data, r_d) for r_d, res in zip(r_devs, residuals)]
+    torch.cuda.current_stream(dev).synchronize()
+    for f in finish:
+        f()
+    return type(v)(v.shape, out.numpy())
