@@ -340,7 +340,9 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
   uint32_t cnt = 0;
   uint32_t pred = st.thr;
   const uint32_t k2 = pred_rank(st, k);
+  uint32_t phases = 0;  // diagnostic: gather / select / compact cycles (units of 64, 11 bits each)
   if (m > 0) {
+    const long long c0 = clock64();
     const bool in_smem = 2u * m <= static_cast<uint32_t>(smem_words);
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
     float* sv = in_smem ? reinterpret_cast<float*>(dyn) : gval + gbase;
@@ -372,7 +374,9 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
     SelectThreshold<uint32_t> th;
     uint32_t key2;
+    const long long c1 = clock64();
     radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+    const long long c2 = clock64();
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
       *x = sv[i];
       *key = Key<float>::of(*x);
@@ -386,6 +390,9 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
     };
     cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
+    const long long c3 = clock64();
+    auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
+    phases = q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22);
     // next threshold: the k2-th largest candidate key, or, when fewer candidates were seen, an
     // extrapolation below the current threshold from the observed candidate density
     if (m >= k2) {
@@ -403,6 +410,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     ns.thr = max(pred, 1u);
     ns.last_cands = m;
     ns.calls += 1;
+    ns.reserved = phases;
     // feedback on the rank factor: the threshold set last call (rank pf*k) produced m candidates
     // now; steer the next one toward PRED_TARGET * k (geometric mean of old and corrected factor)
     if (m > 0) {

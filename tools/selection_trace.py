@@ -54,6 +54,9 @@ def main():
             slow = np.argsort(-s[:, 4].astype(np.int64))[:6]
             print("   slowest layers (kcycles, path, dim, k, m):",
                   [(int(s[j, 4]) // 1000, int(s[j, 5]), dims[j], ks[j], int(s[j, 2])) for j in slow], flush=True)
+            ph = lambda w: (int(w) & 2047, (int(w) >> 11) & 2047, (int(w) >> 22) & 2047)  # noqa: E731
+            print("   candidate-path phases x64 cycles (gather, select, compact):",
+                  [ph(s[j, 7]) for j in slow], flush=True)
 
 
 if __name__ == "__main__":
