@@ -22,7 +22,8 @@ template <typename T> struct Key;
 template <> struct Key<float> {
   using K = uint32_t;
   static constexpr int BITS = 31;  // sign bit dropped
-  static constexpr int RB = 11;    // radix digit width -> 3 passes (11, 11, 9)
+  static constexpr int RB = 12;    // radix digit width -> <= 3 passes (12, 12, 7); crowded
+                                   // candidate keys (common prefix skipped) usually need 2
   __device__ __forceinline__ static K of(float x) { return __float_as_uint(x) & 0x7fffffffu; }
 };
 template <> struct Key<double> {

@@ -357,16 +357,42 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       const uint32_t pos = block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
       cs.tpos[threadIdx.x] = pos;
       __syncthreads();
-      for (uint32_t e = threadIdx.x; e < tot; e += SEL_NT) {
-        int lo = 0, hi = nt - 1;  // last task whose start position <= e
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (cs.tpos[mid] <= e) lo = mid;
-          else hi = mid - 1;
+      // batches of GATHER_ILP entries per thread: all source addresses first, then all loads in
+      // flight together, then the stores (the destination may alias global scratch)
+      constexpr int GATHER_ILP = 8;
+      for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
+        int64_t src[GATHER_ILP];
+#pragma unroll
+        for (int u = 0; u < GATHER_ILP; ++u) {
+          const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
+          src[u] = -1;
+          if (e < tot) {
+            int lo = 0, hi = nt - 1;  // last task whose start position <= e
+            while (lo < hi) {
+              const int mid = (lo + hi + 1) >> 1;
+              if (cs.tpos[mid] <= e) lo = mid;
+              else hi = mid - 1;
+            }
+            src[u] = static_cast<int64_t>(t0 + lo) * cap + (e - cs.tpos[lo]);
+          }
         }
-        const int64_t src = static_cast<int64_t>(t0 + lo) * cap + (e - cs.tpos[lo]);
-        sv[carry + e] = __ldcg(cand_val + src);
-        si[carry + e] = __ldcg(cand_idx + src);
+        float xv[GATHER_ILP];
+        int32_t xi[GATHER_ILP];
+#pragma unroll
+        for (int u = 0; u < GATHER_ILP; ++u) {
+          if (src[u] >= 0) {
+            xv[u] = __ldcg(cand_val + src[u]);
+            xi[u] = __ldcg(cand_idx + src[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < GATHER_ILP; ++u) {
+          if (src[u] >= 0) {
+            const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
+            sv[carry + e] = xv[u];
+            si[carry + e] = xi[u];
+          }
+        }
       }
       carry += tot;
       __syncthreads();
