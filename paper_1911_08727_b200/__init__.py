@@ -12,10 +12,10 @@ from .engine import Bucket
 from .errors import DivergenceError, StructureError
 from .layered import LayeredVector, LayerShape, concat
 from .sparsify import CompressionPolicy, SparseChunk, decompress, top_k, top_k_device
-from .training import StepSizeSchedule, lags_step
+from .training import StepSizeSchedule, lags_step, slgs_step
 
 __all__ = [
     "Bucket", "CompressionPolicy", "DivergenceError", "LayeredVector", "LayerShape", "SparseChunk",
-    "StepSizeSchedule", "StructureError", "concat", "decompress", "lags_step", "top_k", "top_k_device",
+    "StepSizeSchedule", "StructureError", "concat", "decompress", "lags_step", "slgs_step", "top_k", "top_k_device",
 ]
 __version__ = "0.1.0"

@@ -143,19 +143,9 @@ class LagsSGD(torch.optim.Optimizer):
             def engine_factory(dims, ks, world, device):
                 return Bucket(dims, ks, N.F32, device=device, max_world=world)
 
-        self.buckets: list[_BucketRT] = []
-        self._bucket_of_param = {}
-        for lo, hi in plan_buckets(self.dims, self.ks, bucket_cap_bytes):
-            eng = engine_factory(self.dims[lo:hi + 1], self.ks[lo:hi + 1], self.world, self.device)
-            msg_local = eng.new_messages(1)
-            msg_all = eng.new_messages(self.world) if self.world > 1 else None
-            b = _BucketRT(lo, hi, self.offsets[lo], sum(self.dims[lo:hi + 1]), eng, msg_local, msg_all)
-            for l in range(lo, hi + 1):
-                self._bucket_of_param[id(params[l])] = len(self.buckets)
-            self.buckets.append(b)
-        self._size = [b.hi - b.lo + 1 for b in self.buckets]
-        self._pending = list(self._size)
-        self._next = 0  # next bucket to launch (release order)
+        self.engine_factory = engine_factory
+        self.bucket_cap_bytes = int(bucket_cap_bytes)
+        self._build_buckets()
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=self.device.type == "cuda")
@@ -163,13 +153,93 @@ class LagsSGD(torch.optim.Optimizer):
         self._status_step = 0
         self._steps = 0
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in params]
+        self._layer_of_param = {id(p): l for l, p in enumerate(params)}
         self.timing = None  # optional per-bucket CUDA events (see enable_timing)
+        self._hook_events = None  # optional per-layer CUDA events at gradient readiness
+
+    def _build_buckets(self) -> None:
+        """(Re)plan fusion buckets for the current ks; residual and momentum state are kept."""
+        self.buckets: list[_BucketRT] = []
+        self._bucket_of_param = {}
+        for lo, hi in plan_buckets(self.dims, self.ks, self.bucket_cap_bytes):
+            eng = self.engine_factory(self.dims[lo:hi + 1], self.ks[lo:hi + 1], self.world, self.device)
+            msg_local = eng.new_messages(1)
+            msg_all = eng.new_messages(self.world) if self.world > 1 else None
+            b = _BucketRT(lo, hi, self.offsets[lo], sum(self.dims[lo:hi + 1]), eng, msg_local, msg_all)
+            for l in range(lo, hi + 1):
+                self._bucket_of_param[id(self.params[l])] = len(self.buckets)
+            self.buckets.append(b)
+        self._size = [b.hi - b.lo + 1 for b in self.buckets]
+        self._pending = list(self._size)
+        self._next = 0  # next bucket to launch (release order)
+        if getattr(self, "timing", None) is not None:
+            self.enable_timing(True)
+
+    def set_policy(self, policy: CompressionPolicy) -> None:
+        """New per-layer ratios (e.g. from perf.select_ratios): recompute k_l, re-plan buckets.
+        Call between steps.  The error-feedback residual carries over unchanged."""
+        self.policy = policy
+        self.ratios = [policy.ratio_for(i + 1) for i in range(len(self.params))]
+        self.ks = selection_counts(self.dims, self.ratios)
+        self._build_buckets()
+
+    def adapt(self, network, ratio_cap: float = 1000.0, ratio_grid=None) -> CompressionPolicy:
+        """Adaptive rho_l (R: perf.py:231-260) from this rank's device timings of the last step
+        (enable_layer_timing + enable_timing before it): each layer gets the smallest grid ratio
+        whose exchange + compress hides behind the next layer's backprop.  Rank 0's choice is
+        broadcast so every rank plans identical buckets and messages."""
+        from . import perf
+
+        grid = perf.DEFAULT_RATIO_GRID if ratio_grid is None else ratio_grid
+        pol = perf.select_ratios(self.dims, self.layer_backward_times(), self.layer_spar_times(), network,
+                                 self.world, ratio_cap, grid)
+        ratios = torch.tensor([pol.ratio_for(i + 1) for i in range(len(self.params))], dtype=torch.float64,
+                              device=self.device)
+        if self.world > 1:
+            dist.broadcast(ratios, src=0, group=self.group)
+        pol = CompressionPolicy({i + 1: float(c) for i, c in enumerate(ratios.tolist())}, ratio_cap)
+        self.set_policy(pol)
+        return pol
+
+    # -- measurement for the adaptive selector ------------------------------------------------
+    def enable_layer_timing(self, on: bool = True) -> None:
+        """Record a CUDA event on the compute stream when each layer's gradient is ready."""
+        self._hook_events = ([torch.cuda.Event(enable_timing=True) for _ in self.params]
+                             if on and self.device.type == "cuda" else None)
+
+    def layer_backward_times(self, floor_s: float = 1e-6) -> list[float]:
+        """Seconds of backprop attributed to each layer at the last step (layer ids 1..L order):
+        the gap between consecutive gradient-ready events in backprop order (the first layer of
+        backprop gets the next gap).  Synchronises."""
+        ev = self._hook_events
+        if ev is None:
+            raise RuntimeError("enable_layer_timing() first")
+        torch.cuda.synchronize(self.device)
+        L = len(ev)
+        t = [0.0] * L
+        for l in range(L - 1, 0, -1):  # backprop order L..1
+            t[l - 1] = max(ev[l].elapsed_time(ev[l - 1]) / 1e3, floor_s)
+        t[L - 1] = t[L - 2] if L > 1 else floor_s
+        return t
+
+    def layer_spar_times(self) -> list[float]:
+        """Compress time of each bucket (last step) spread over its layers by size.  Synchronises."""
+        times = self.bucket_times_ms()
+        if times is None:
+            raise RuntimeError("enable_timing() first")
+        out = [0.0] * len(self.params)
+        for b, (comp, _, _) in zip(self.buckets, times):
+            for l in range(b.lo, b.hi + 1):
+                out[l] = comp / 1e3 * self.dims[l] / b.numel
+        return out
 
     # -- scheduling -------------------------------------------------------------------------
     def _on_grad(self, p: torch.Tensor) -> None:
         b = self._bucket_of_param.get(id(p))
         if b is None:
             return
+        if self._hook_events is not None:
+            self._hook_events[self._layer_of_param[id(p)]].record(torch.cuda.current_stream(self.device))
         self._pending[b] -= 1
         # launch every complete bucket in release order (identical collective order on all ranks)
         while self._next < len(self.buckets) and self._pending[self._next] <= 0:

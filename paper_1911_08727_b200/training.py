@@ -141,6 +141,31 @@ class HostPinner:
 _PINNER = HostPinner()
 
 
+def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: int | None = None):
+    """Single-layer (whole stacked vector) selection with error feedback -- R: training.py:203-224.
+
+    The same kernels with one "layer" spanning the flat vector: R: training.py:216-217 checks k
+    against the full dimension, selection and aggregation are then lags_step's with L = 1.
+    """
+    from .layered import LayerShape
+
+    dim = int(v.data.shape[0])
+    if not 1 <= global_k <= dim:
+        raise ValueError(f"global_k={global_k} outside 1..{dim}")
+
+    class _Flat:  # the stacked vector seen as one layer (views, no copies)
+        def __init__(self, data):
+            self.shape = (LayerShape(1, dim),)
+            self.data = data
+
+    for p, g in enumerate(grads, start=1):  # layout check against the real layer split first
+        if layout_of(g) != layout_of(v):
+            return lags_step(v, grads, alpha, {ls.layer_id: 1 for ls in v.shape}, residuals, t)
+    flat_res = [_Flat(r.data) for r in residuals]
+    out = lags_step(_Flat(v.data), [_Flat(g.data) for g in grads], alpha, {1: int(global_k)}, flat_res, t)
+    return type(v)(v.shape, out.data)
+
+
 def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: int | None = None):
     """Per-layer selection with error feedback on the B200; R: training.py:227-255."""
     pairs = layout_of(v)

@@ -12,6 +12,7 @@ Fixtures:
   topk_cases.npz         top_k(x, k) -> (indices, values)          R: sparsify.py:71-90
   lags_step_cases.npz    lags_step(v, grads, alpha, counts, res)   R: training.py:227-255
   config1_trajectory.npz train() config 1 with lags_step recorded  R: training.py:261-384
+  slgs_cases.npz         slgs_step(v, grads, alpha, global_k, res) R: training.py:203-224
   perf_cases.json        select_ratios / comm_time / schedules     R: perf.py:59-260
   wire_cases.json        encode_chunk / fusion_flush               R: sparsify.py:209-310
 """
@@ -152,6 +153,28 @@ def make_lags_step():
     return len(cases)
 
 
+def make_slgs():
+    """slgs_step(v, grads, alpha, global_k, residuals) cases -- R: training.py:203-224."""
+    rng = np.random.default_rng(9)
+    out = {}
+    specs = [([300, 17, 2048], 2, np.float64, 0.2, 40), ([5000, 3], 3, np.float32, 0.05, 50),
+             ([64, 64], 1, np.float64, 1.0, 128)]
+    for i, (dims, P, dtype, alpha, gk) in enumerate(specs):
+        shape = [LayerShape(j + 1, d) for j, d in enumerate(dims)]
+        n = sum(dims)
+        v = LayeredVector(shape, _dist(rng, "normal", n, dtype))
+        grads = [LayeredVector(shape, _dist(rng, "heavy", n, dtype)) for _ in range(P)]
+        r_in = [(0.01 * _dist(rng, "normal", n, dtype)).astype(dtype) for _ in range(P)]
+        res = [LayeredVector(shape, r.copy()) for r in r_in]
+        new_v = ref_training.slgs_step(v, grads, alpha, gk, res)
+        out.update({f"dims{i}": np.array(dims), f"k{i}": np.array(gk), f"alpha{i}": np.array(alpha),
+                    f"v{i}": v.data, f"g{i}": np.stack([g.data for g in grads]), f"r_in{i}": np.stack(r_in),
+                    f"r_out{i}": np.stack([r.data for r in res]), f"v_out{i}": new_v.data})
+    out["n"] = np.array(len(specs))
+    np.savez_compressed(os.path.join(HERE, "slgs_cases.npz"), **out)
+    return len(specs)
+
+
 def _digest(*arrays):
     h = hashlib.sha256()
     for a in arrays:
@@ -263,6 +286,7 @@ if __name__ == "__main__":
     print("topk cases", make_topk())
     print("lags_step cases", make_lags_step())
     print("config1 iterations", make_config1())
+    print("slgs cases", make_slgs())
     make_perf()
     make_wire()
     print("reference version", lagsgd.__version__)

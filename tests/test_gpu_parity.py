@@ -291,3 +291,18 @@ def test_large_layer_properties(L):
     mask[idx] = False
     assert _same_bits(r_h[mask], acc_h[mask])
     assert np.abs(val).min() >= np.abs(acc_h[mask]).max()
+
+
+def test_slgs_step_golden(L):
+    """SLGS arm (R: training.py:203-224): whole-vector selection with the same kernels."""
+    from conftest import load_npz
+
+    z = load_npz("slgs_cases.npz")
+    for i in range(int(z["n"])):
+        dims = [int(d) for d in z[f"dims{i}"]]
+        res = [_lv(L, dims, r.copy()) for r in z[f"r_in{i}"]]
+        out = L.slgs_step(_lv(L, dims, z[f"v{i}"]), [_lv(L, dims, g) for g in z[f"g{i}"]], float(z[f"alpha{i}"]),
+                          int(z[f"k{i}"]), res)
+        assert _same_bits(out.data, z[f"v_out{i}"])
+        for a, b in zip(res, z[f"r_out{i}"]):
+            assert _same_bits(a.data, b)

@@ -141,3 +141,15 @@ def test_wire_golden():
             continue
         assert c["error"] is None
         assert bool(got) == (c["result"] is not None)
+
+
+def test_slgs_golden():
+    from conftest import load_npz
+
+    z = load_npz("slgs_cases.npz")
+    for i in range(int(z["n"])):
+        res = [r.copy() for r in z[f"r_in{i}"]]
+        out = orc.slgs_step(z[f"v{i}"], list(z[f"g{i}"]), float(z[f"alpha{i}"]), int(z[f"k{i}"]), res)
+        assert _bits(out).tobytes() == _bits(z[f"v_out{i}"]).tobytes()
+        for a, b in zip(res, z[f"r_out{i}"]):
+            assert _bits(a).tobytes() == _bits(b).tobytes()
