@@ -107,12 +107,14 @@ def fit_network(message_bytes: Sequence[float], seconds: Sequence[float], worker
     """Least-squares alpha-beta fit of measured exchange times: t = m(P) * (a + b * bytes)."""
     x = np.asarray(message_bytes, dtype=np.float64)
     y = np.asarray(seconds, dtype=np.float64) / max(ring_multiplier(workers), 1.0)
-    A = np.stack([np.ones_like(x), x], axis=1)
-    (a, b), *_ = np.linalg.lstsq(A, y, rcond=None)
+    w = 1.0 / np.maximum(y, 1e-12)  # relative error: latency- and bandwidth-bound sizes count alike
+    A = np.stack([np.ones_like(x), x], axis=1) * w[:, None]
+    (a, b), *_ = np.linalg.lstsq(A, y * w, rcond=None)
     return NetworkModel(max(float(a), 0.0), max(float(b), 0.0))
 
 
-def measure_allgather(group=None, device=None, sizes=(256, 4096, 65536, 1 << 20), reps: int = 20):
+def measure_allgather(group=None, device=None, sizes=(256, 4096, 65536, 1 << 20, 1 << 23, 1 << 26),
+                      reps: int = 10):
     """Device-timed NCCL all-gather of uint8 messages (CUDA events, max over ranks).
     Returns (bytes per rank, seconds)."""
     import torch

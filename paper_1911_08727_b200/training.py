@@ -154,15 +154,16 @@ def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: 
         raise ValueError(f"global_k={global_k} outside 1..{dim}")
 
     class _Flat:  # the stacked vector seen as one layer (views, no copies)
-        def __init__(self, data):
-            self.shape = (LayerShape(1, dim),)
+        def __init__(self, shape, data):
+            self.shape = shape
             self.data = data
 
+    one = (LayerShape(1, dim),)
     for p, g in enumerate(grads, start=1):  # layout check against the real layer split first
         if layout_of(g) != layout_of(v):
             return lags_step(v, grads, alpha, {ls.layer_id: 1 for ls in v.shape}, residuals, t)
-    flat_res = [_Flat(r.data) for r in residuals]
-    out = lags_step(_Flat(v.data), [_Flat(g.data) for g in grads], alpha, {1: int(global_k)}, flat_res, t)
+    flat_res = [_Flat(one, r.data) for r in residuals]
+    out = lags_step(_Flat(one, v.data), [_Flat(one, g.data) for g in grads], alpha, {1: int(global_k)}, flat_res, t)
     return type(v)(v.shape, out.data)
 
 
