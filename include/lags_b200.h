@@ -93,9 +93,13 @@ int lags_bucket_compress(lags_bucket_t* bucket, void* g, void* r, double alpha, 
  * `msgs` holds P messages, rank p's at byte offset p * msg_stride.  mu == 0 is the reference
  * (parity) mode and touches only selected weights; mu > 0 applies heavy-ball momentum over the
  * whole bucket, m = mu*m + total/P, v -= m (parity unpinned: momentum is a non-goal of the
- * reference, R: SPEC.md:366).  `momentum` may be NULL when mu == 0.  P <= max_world. */
+ * reference, R: SPEC.md:366).  `momentum` may be NULL when mu == 0.  P <= max_world.
+ * flags: LAGS_DECODE_V64 -- v (and momentum) are float64 whatever the bucket dtype, v = fl64(v -
+ * total/P) without rounding to the storage type (the reference's slgs_step returns its float32
+ * parameters promoted to float64, R: training.py:224). */
+#define LAGS_DECODE_V64 0x1u
 int lags_bucket_decode_update(lags_bucket_t* bucket, const void* msgs, int64_t msg_stride, int32_t P, void* v,
-                              void* momentum, double mu, lags_stream_t stream);
+                              void* momentum, double mu, uint32_t flags, lags_stream_t stream);
 
 /* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls, last select
  * cycles, last path (0 small dense, 1 candidates, 2 grid-wide dense), 0, 0} (synchronous). */

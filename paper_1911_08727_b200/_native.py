@@ -47,7 +47,9 @@ lags_bucket_create = _fn("lags_bucket_create", C.c_int, _i32, _vp, _vp, _i32, _i
 lags_bucket_destroy = _fn("lags_bucket_destroy", None, _vp)
 lags_bucket_message_layout = _fn("lags_bucket_message_layout", C.c_int, _vp, _i64p, _i64p, _i64p, _i64p)
 lags_bucket_compress = _fn("lags_bucket_compress", C.c_int, _vp, _vp, _vp, _dbl, _vp, _vp, _u32, _vp)
-lags_bucket_decode_update = _fn("lags_bucket_decode_update", C.c_int, _vp, _vp, _i64, _i32, _vp, _vp, _dbl, _vp)
+lags_bucket_decode_update = _fn("lags_bucket_decode_update", C.c_int, _vp, _vp, _i64, _i32, _vp, _vp, _dbl, _u32,
+                                _vp)
+DECODE_V64 = 0x1
 lags_bucket_stats = _fn("lags_bucket_stats", C.c_int, _vp, _vp, _vp)
 lags_check_finite = _fn("lags_check_finite", C.c_int, _i32, _vp, _i64, _vp, _vp)
 lags_top_k_workspace_bytes = _fn("lags_top_k_workspace_bytes", _sz, _i32, _i64)

@@ -507,7 +507,7 @@ int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* m
 extern "C" {
 
 int lags_bucket_decode_update(lags_bucket_t* b, const void* msgs, int64_t msg_stride, int32_t P, void* v,
-                              void* momentum, double mu, lags_stream_t stream) {
+                              void* momentum, double mu, uint32_t flags, lags_stream_t stream) {
   if (!b || !msgs || !v) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: null pointer");
   if (P < 1 || P > b->max_world)
     return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: P outside 1..max_world");
@@ -517,6 +517,10 @@ int lags_bucket_decode_update(lags_bucket_t* b, const void* msgs, int64_t msg_st
     return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_decode_update: mu != 0 needs a momentum buffer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const MsgView mv{static_cast<const char*>(msgs), msg_stride, b->off_cnt, b->off_idx, b->off_val};
+  if (flags & LAGS_DECODE_V64) {
+    if (b->dtype == LAGS_F32) return decode_impl<double, float>(b, mv, P, v, momentum, mu, s);
+    return decode_impl<double, double>(b, mv, P, v, momentum, mu, s);
+  }
   if (b->dtype == LAGS_F32) return decode_impl<float, float>(b, mv, P, v, momentum, mu, s);
   if (b->dtype == LAGS_F64) return decode_impl<double, double>(b, mv, P, v, momentum, mu, s);
   return decode_impl<float, double>(b, mv, P, v, momentum, mu, s);

@@ -116,15 +116,18 @@ class Bucket:
 
     def decode(self, msgs: torch.Tensor, P: int, v: torch.Tensor, momentum: torch.Tensor | None = None,
                mu: float = 0.0, stream=None, msg_stride: int | None = None) -> None:
-        """Rank-ordered fp64 decode of P messages and v <- v - total/P (or heavy-ball momentum)."""
+        """Rank-ordered fp64 decode of P messages and v <- v - total/P (or heavy-ball momentum).
+        A float64 ``v`` with a float32 bucket keeps the unrounded fp64 result (LAGS_DECODE_V64)."""
         stride = self.msg_bytes if msg_stride is None else int(msg_stride)
         if msgs.numel() < (P - 1) * stride + self.msg_bytes:
             raise ValueError("message buffer smaller than P messages")
-        if v.dtype != storage_dtype(self.mode) or v.numel() < self.n_total:
+        v64 = v.dtype == torch.float64 and storage_dtype(self.mode) != torch.float64
+        if (v.dtype != storage_dtype(self.mode) and not v64) or v.numel() < self.n_total:
             raise ValueError("parameter buffer does not match the bucket")
         N.check(N.lags_bucket_decode_update(self._h, msgs.data_ptr(), stride, int(P), v.data_ptr(),
                                             momentum.data_ptr() if momentum is not None else None, float(mu),
-                                            stream_handle(stream)), "lags_bucket_decode_update")
+                                            N.DECODE_V64 if v64 else 0, stream_handle(stream)),
+                "lags_bucket_decode_update")
 
     # -- host helpers (tests / diagnostics) ----------------------------------------------------
     def stats(self, stream=None) -> np.ndarray:

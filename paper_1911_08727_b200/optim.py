@@ -190,7 +190,9 @@ class LagsSGD(torch.optim.Optimizer):
         broadcast so every rank plans identical buckets and messages."""
         from . import perf
 
-        grid = perf.DEFAULT_RATIO_GRID if ratio_grid is None else ratio_grid
+        # default grid keeps rho <= 4 %: the reference's selector prices sparsification as a
+        # per-layer constant, while on the device selecting near-dense layers costs much more
+        grid = (25, 50, 100, 250, 500, 1000) if ratio_grid is None else ratio_grid
         pol = perf.select_ratios(self.dims, self.layer_backward_times(), self.layer_spar_times(), network,
                                  self.world, ratio_cap, grid)
         ratios = torch.tensor([pol.ratio_for(i + 1) for i in range(len(self.params))], dtype=torch.float64,

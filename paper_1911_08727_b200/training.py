@@ -163,12 +163,17 @@ def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: 
         if layout_of(g) != layout_of(v):
             return lags_step(v, grads, alpha, {ls.layer_id: 1 for ls in v.shape}, residuals, t)
     flat_res = [_Flat(one, r.data) for r in residuals]
-    out = lags_step(_Flat(one, v.data), [_Flat(one, g.data) for g in grads], alpha, {1: int(global_k)}, flat_res, t)
+    out = lags_step(_Flat(one, v.data), [_Flat(one, g.data) for g in grads], alpha, {1: int(global_k)}, flat_res, t,
+                    _promote_v=True)
     return type(v)(v.shape, out.data)
 
 
-def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: int | None = None):
-    """Per-layer selection with error feedback on the B200; R: training.py:227-255."""
+def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: int | None = None, *,
+              _promote_v: bool = False):
+    """Per-layer selection with error feedback on the B200; R: training.py:227-255.
+
+    (_promote_v: return float32 parameters as the unrounded float64 ``v - total / P``, which is
+    what the reference's slgs_step does, R: training.py:224.)"""
     pairs = layout_of(v)
     P = len(grads)
     if P < 1 or len(residuals) != P:
@@ -205,6 +210,8 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
     dev = torch.device("cuda", torch.cuda.current_device())
     pin = _PINNER
     v_d = pin.h2d(v.data, dev)
+    if _promote_v and v_d.dtype == torch.float32:
+        v_d = v_d.double()
     msgs = bucket.new_messages(P)
     r_devs = []
     for p in range(P):

@@ -50,7 +50,7 @@ def test_argument_errors_map_to_reference_exceptions():
     with pytest.raises(ValueError, match="outside 1..10"):
         N.check(rc)
     assert N.lags_bucket_compress(None, None, None, 0.0, None, None, 0, None) == N.ERR_INVALID_ARG
-    assert N.lags_bucket_decode_update(None, fake, 64, 1, fake, None, 0.0, None) == N.ERR_INVALID_ARG
+    assert N.lags_bucket_decode_update(None, fake, 64, 1, fake, None, 0.0, 0, None) == N.ERR_INVALID_ARG
     # bucket creation validates k before touching the device (R: sparsify.py:82-83)
     dims = np.array([10, 5], dtype=np.int64)
     ks = np.array([3, 6], dtype=np.int32)
