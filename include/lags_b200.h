@@ -88,6 +88,12 @@ int lags_bucket_message_layout(const lags_bucket_t* bucket, int64_t* off_counts,
 int lags_bucket_compress(lags_bucket_t* bucket, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, lags_stream_t stream);
 
+/* Single-rank step (P = 1, no exchange): lags_bucket_compress plus the update v = v - total / 1
+ * fused into the selection epilogue (no separate decode pass).  The message is still written.
+ * Equivalent to lags_bucket_compress followed by lags_bucket_decode_update(..., P = 1, ...). */
+int lags_bucket_step_local(lags_bucket_t* bucket, void* g, void* r, double alpha, void* v, void* msg,
+                           uint32_t* status, uint32_t flags, lags_stream_t stream);
+
 /* Decode + update after the exchange -- replaces R: training.py:248,253-254:
  *   total = fp64 zeros; for p = 1..P (rank order): total[idx] += val;   v = v - total / P
  * `msgs` holds P messages, rank p's at byte offset p * msg_stride.  mu == 0 is the reference

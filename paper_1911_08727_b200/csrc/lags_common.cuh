@@ -39,6 +39,10 @@ template <> struct Key<double> {
 __device__ __forceinline__ float accum(float r, float g, float a) { return __fadd_rn(r, __fmul_rn(a, g)); }
 __device__ __forceinline__ double accum(double r, double g, double a) { return __dadd_rn(r, __dmul_rn(a, g)); }
 
+// Programmatic dependent launch (sm_90+): wait until the preceding kernel on the stream has
+// completed and its memory is visible.  A no-op for kernels launched without the attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ bool nonfinite(float g) { return (__float_as_uint(g) & 0x7f800000u) == 0x7f800000u; }
 __device__ __forceinline__ bool nonfinite(double g) {
   return (static_cast<unsigned long long>(__double_as_longlong(g)) & 0x7ff0000000000000ull) ==

@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     uint32_t* status, uint32_t* fb_count) {
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
+  griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
   if (wid == 0 && lane == 0) *fb_count = 0u;  // the previous call's fallback kernel has completed
   if (wid >= ntasks) return;
   const Task T = tasks[wid];
@@ -205,10 +206,17 @@ struct CoopSmem {
   uint32_t tcnt[SEL_NT];
 };
 
+// P = 1 update fused into the selection epilogue (no exchange, no separate decode): exactly the
+// decode of R: training.py:248,253-254 with one worker, v = fl32(fl64(v) - (0.0 + x) / 1).
+__device__ __forceinline__ void single_rank_update(float* v, float x) {
+  const double total = __dadd_rn(0.0, static_cast<double>(x));
+  *v = static_cast<float>(__dsub_rn(static_cast<double>(*v), __ddiv_rn(total, 1.0)));
+}
+
 // Dense exact top-k of a small layer staged once in shared memory (`sv`, >= d floats): every
 // radix pass and the compaction then read shared memory instead of L2.
 __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32_t* oidx, float* oval, float* sv,
-                                       CoopSmem& cs) {
+                                       CoopSmem& cs, float* vl) {
   const bool vec = ((reinterpret_cast<uintptr_t>(data) & 15u) == 0u);
   if (vec) {
     const float4* d4 = reinterpret_cast<const float4*>(data);
@@ -233,6 +241,7 @@ __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32
     oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
     data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    if (vl) single_rank_update(vl + i, x);
   };
   return ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
 }
@@ -323,7 +332,8 @@ constexpr int FB_TOO_FEW = 1, FB_OVERFLOW = 2;
 __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
                                 const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
                                 int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
-                                int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, CoopSmem& cs) {
+                                int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, CoopSmem& cs,
+                                float* vupd) {
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
   uint32_t local = 0, over = 0;
@@ -410,10 +420,12 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     };
     int32_t* oidx = idx_out + L.slot;
     float* oval = val_out + L.slot;
+    float* vl = vupd ? vupd + L.offset : nullptr;
     auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
       oidx[pos] = static_cast<int32_t>(ix);
       oval[pos] = x;
       data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+      if (vl) single_rank_update(vl + ix, x);
     };
     cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
     const long long c3 = clock64();
@@ -456,7 +468,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
 // prediction rank over r, then an ordered compaction that zeroes the selected residuals.
 __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
                                       float* val_out, int32_t* count_out, FastState* state, bool force_exact,
-                                      int why, CoopSmem& cs) {
+                                      int why, CoopSmem& cs, float* vupd) {
   float* data = r + L.offset;
   const int64_t d = L.dim;
   const uint32_t k = static_cast<uint32_t>(L.k);
@@ -477,10 +489,12 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
   };
   int32_t* oidx = idx_out + L.slot;
   float* oval = val_out + L.slot;
+  float* vl = vupd ? vupd + L.offset : nullptr;
   auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
     oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
     data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    if (vl) single_rank_update(vl + i, x);
   };
   const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
   if (threadIdx.x == 0) {
@@ -503,21 +517,19 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
     FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
     const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
-    float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc) {
+    float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc, float* vupd) {
   extern __shared__ uint32_t skeys[];
   __shared__ CoopSmem cs;
+  griddep_wait();  // programmatic dependent launch: K1's results are visible after this
   const int j = order[blockIdx.x];
   const lags_layer_t L = layers[j];
   const FastState st = state[j];
   const long long t_begin = clock64();
   uint32_t path;
-  if (L.dim <= SMALL_LAYER) {
-    const uint32_t cnt =
-        L.dim <= smem_keys
-            ? small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot, val_out + L.slot,
-                                 reinterpret_cast<float*>(skeys), cs)
-            : exact_topk_dense<float, float>(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
-                                             val_out + L.slot, true, cs.sm);
+  if (L.dim <= SMALL_LAYER) {  // SMALL_LAYER <= shared-memory staging capacity
+    const uint32_t cnt = small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
+                                            val_out + L.slot, reinterpret_cast<float*>(skeys), cs,
+                                            vupd ? vupd + L.offset : nullptr);
     if (threadIdx.x == 0) {
       count_out[j] = static_cast<int32_t>(cnt);
       FastState ns = st;
@@ -529,7 +541,7 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     const int why = (force_exact || st.thr == 0u)
                         ? FB_TOO_FEW
                         : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval,
-                                           r, idx_out, val_out, count_out, state, skeys, smem_keys, cs);
+                                           r, idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
     if (why && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j | (why << 24);
     path = why ? 2u : 1u;
   }
@@ -545,14 +557,15 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
 __global__ void __launch_bounds__(SEL_NT, 1) select_fallback_kernel(const lags_layer_t* __restrict__ layers,
                                                                     FastState* state, float* r, int32_t* idx_out,
                                                                     float* val_out, int32_t* count_out,
-                                                                    int force_exact, CoopScratch sc) {
+                                                                    int force_exact, CoopScratch sc, float* vupd) {
   __shared__ CoopSmem cs;
+  griddep_wait();
   if (blockIdx.x >= __ldcg(sc.fb_count)) return;
   const int entry = __ldcg(sc.fb_list + blockIdx.x);
   const int j = entry & 0xffffff;
   const long long t_begin = clock64();
   dense_fallback_select(j, layers[j], state[j], r, idx_out, val_out, count_out, state, force_exact != 0, entry >> 24,
-                        cs);
+                        cs, vupd);
   __syncthreads();
   if (threadIdx.x == 0) state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
 }

@@ -25,6 +25,7 @@ template <typename TIn, typename TAcc>
 __global__ void __launch_bounds__(256) accum_kernel(const TIn* __restrict__ g, TIn* r, TAcc* acc_out, TAcc alpha,
                                                     int64_t n, uint32_t* status) {
   bool bad = false;
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const TIn gi = g[i];
@@ -37,6 +38,7 @@ __global__ void __launch_bounds__(256) accum_kernel(const TIn* __restrict__ g, T
 template <typename T>
 __global__ void __launch_bounds__(256) finite_kernel(const T* __restrict__ x, int64_t n, uint32_t* status) {
   bool bad = false;
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     bad |= nonfinite(x[i]);
@@ -58,6 +60,7 @@ __global__ void __launch_bounds__(SEL_NT) select_dense_kernel(const lags_layer_t
 // Mixed mode epilogue: r (fp32) <- fl32(acc) where acc (fp64) has +0.0 at the selected slots.
 __global__ void __launch_bounds__(256) store_residual_kernel(const double* __restrict__ acc, float* __restrict__ r,
                                                              int64_t n) {
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
     r[i] = static_cast<float>(acc[i]);
@@ -95,6 +98,7 @@ template <typename TV, typename TVal>
 __global__ void __launch_bounds__(256) decode_single_kernel(const lags_layer_t* __restrict__ layers,
                                                             const int32_t* __restrict__ slot_layer, MsgView msg,
                                                             int64_t total_k, TV* v) {
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total_k; s += stride) {
     const int j = slot_layer[s];
@@ -111,6 +115,7 @@ __global__ void __launch_bounds__(256) decode_scatter_kernel(const lags_layer_t*
                                                              const int32_t* __restrict__ slot_layer, MsgView msg,
                                                              int64_t total_k, int P, TVal* planes, int64_t n,
                                                              uint32_t* mask) {
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t work = total_k * P;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < work; e += stride) {
@@ -130,6 +135,7 @@ __global__ void __launch_bounds__(256) decode_update_kernel(const lags_layer_t* 
                                                             const int32_t* __restrict__ slot_layer, MsgView msg,
                                                             int64_t total_k, int P, const TVal* planes, int64_t n,
                                                             uint32_t* mask, TV* v) {
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t work = total_k * P;
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < work; e += stride) {
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(256) decode_update_kernel(const lags_layer_t* 
 template <typename TV, typename TVal>
 __global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes, int64_t n, uint32_t* mask, int P,
                                                               TV* v, TV* mom, double mu) {
+  griddep_wait();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
     const uint32_t bits = mask[i];
@@ -304,6 +311,23 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
+// previous kernel on the stream drains; it calls griddep_wait() before touching its inputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace
 
 extern "C" {
@@ -428,8 +452,10 @@ int lags_bucket_message_layout(const lags_bucket_t* b, int64_t* off_counts, int6
   return LAGS_OK;
 }
 
-int lags_bucket_compress(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
-                         uint32_t flags, lags_stream_t stream) {
+// compress of one worker; v_update (nullable, LAGS_F32 only) fuses the P = 1 update into the
+// selection epilogue (lags_bucket_step_local).
+static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
+                         uint32_t flags, void* v_update, lags_stream_t stream) {
   if (!b || !g || !r || !msg || !status) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
   if (!aligned16(g) || !aligned16(r) || !aligned16(msg))
     return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: buffers must be 16-byte aligned");
@@ -443,22 +469,30 @@ int lags_bucket_compress(lags_bucket_t* b, void* g, void* r, double alpha, void*
     const float a = static_cast<float>(alpha);  // numpy casts a Python float to float32 (NEP 50)
     const int blocks = (b->ntasks + K1_WARPS - 1) / K1_WARPS;
     float* rr = static_cast<float*>(r);
+    float* gg = static_cast<float*>(g);
     float* vals = reinterpret_cast<float*>(m + b->off_val);
+    float* vu = static_cast<float*>(v_update);
+    const int fe = exact ? 1 : 0;
+    cudaError_t e;
     if (flags & LAGS_COMPRESS_ZERO_GRAD)
-      accum_emit_kernel<true><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
-                                                               static_cast<float*>(g), rr, a, b->cap, b->cand_idx,
-                                                               b->cand_val, b->cand_cnt, status, b->coop.fb_count);
+      e = launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, b->ntasks, b->layers,
+                     b->state, gg, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status, b->coop.fb_count);
     else
-      accum_emit_kernel<false><<<blocks, K1_WARPS * 32, 0, s>>>(b->tasks, b->ntasks, b->layers, b->state,
-                                                                static_cast<float*>(g), rr, a, b->cap, b->cand_idx,
-                                                                b->cand_val, b->cand_cnt, status, b->coop.fb_count);
-    select_phase1_kernel<<<b->nlayers, SEL_NT, static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), s>>>(
-        b->layers, b->layer_tasks, b->order, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
-        b->gval, rr, idx, vals, cnt, b->smem_keys, exact ? 1 : 0, b->coop);
-    select_fallback_kernel<<<b->n_big, SEL_NT, 0, s>>>(b->layers, b->state, rr, idx, vals, cnt, exact ? 1 : 0,
-                                                       b->coop);
+      e = launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, b->ntasks,
+                     b->layers, b->state, gg, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status,
+                     b->coop.fb_count);
+    if (e == cudaSuccess)
+      e = launch_pdl(select_phase1_kernel, dim3(b->nlayers), dim3(SEL_NT),
+                     static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), s, b->layers, b->layer_tasks, b->order,
+                     b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt,
+                     b->smem_keys, fe, b->coop, vu);
+    if (e == cudaSuccess)
+      e = launch_pdl(select_fallback_kernel, dim3(b->n_big), dim3(SEL_NT), 0, s, b->layers, b->state, rr, idx, vals,
+                     cnt, fe, b->coop, vu);
+    if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
     return cuda_check("lags_bucket_compress(f32)", 3);
   }
+  if (v_update) return fail(LAGS_ERR_INVALID_ARG, "fused single-rank update needs an LAGS_F32 bucket");
   if (b->dtype == LAGS_F64) {
     accum_kernel<double, double><<<stream_grid(n, 256, 8), 256, 0, s>>>(
         static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(r), alpha, n, status);
@@ -493,13 +527,19 @@ int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* m
         planes, n, b->mask, P, static_cast<TV*>(v), static_cast<TV*>(momentum), mu);
     return cuda_check("decode(momentum)", 2);
   }
+  cudaError_t e;
   if (P == 1) {
-    decode_single_kernel<TV, TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, static_cast<TV*>(v));
+    e = launch_pdl(decode_single_kernel<TV, TVal>, dim3(gwork), dim3(256), 0, s, b->layers, b->slot_layer, mv, S,
+                   static_cast<TV*>(v));
+    if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     return cuda_check("decode(single)", 1);
   }
-  decode_scatter_kernel<TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, P, planes, n, b->mask);
-  decode_update_kernel<TV, TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, P, planes, n, b->mask,
-                                                       static_cast<TV*>(v));
+  e = launch_pdl(decode_scatter_kernel<TVal>, dim3(gwork), dim3(256), 0, s, b->layers, b->slot_layer, mv, S, P,
+                 planes, n, b->mask);
+  if (e == cudaSuccess)
+    e = launch_pdl(decode_update_kernel<TV, TVal>, dim3(gwork), dim3(256), 0, s, b->layers, b->slot_layer, mv, S, P,
+                   static_cast<const TVal*>(planes), n, b->mask, static_cast<TV*>(v));
+  if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
   return cuda_check("decode", 2);
 }
 }  // namespace
@@ -524,6 +564,22 @@ int lags_bucket_decode_update(lags_bucket_t* b, const void* msgs, int64_t msg_st
   if (b->dtype == LAGS_F32) return decode_impl<float, float>(b, mv, P, v, momentum, mu, s);
   if (b->dtype == LAGS_F64) return decode_impl<double, double>(b, mv, P, v, momentum, mu, s);
   return decode_impl<float, double>(b, mv, P, v, momentum, mu, s);
+}
+
+int lags_bucket_compress(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
+                         uint32_t flags, lags_stream_t stream) {
+  return compress_impl(b, g, r, alpha, msg, status, flags, nullptr, stream);
+}
+
+int lags_bucket_step_local(lags_bucket_t* b, void* g, void* r, double alpha, void* v, void* msg, uint32_t* status,
+                           uint32_t flags, lags_stream_t stream) {
+  if (!v || !b) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_step_local: null pointer");
+  if (b->dtype != LAGS_F32) {  // parity modes: compress, then the ordinary P = 1 decode
+    const int rc = lags_bucket_compress(b, g, r, alpha, msg, status, flags, stream);
+    if (rc != LAGS_OK) return rc;
+    return lags_bucket_decode_update(b, msg, b->msg_bytes, 1, v, nullptr, 0.0, 0, stream);
+  }
+  return compress_impl(b, g, r, alpha, msg, status, flags, v, stream);
 }
 
 int lags_bucket_stats(const lags_bucket_t* b, uint32_t* out, lags_stream_t stream) {

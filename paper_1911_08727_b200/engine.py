@@ -114,6 +114,19 @@ class Bucket:
         N.check(N.lags_bucket_compress(self._h, g.data_ptr(), r.data_ptr(), float(alpha), msg.data_ptr(),
                                        status.data_ptr(), flags, stream_handle(stream)), "lags_bucket_compress")
 
+    def step_local(self, g: torch.Tensor, r: torch.Tensor, alpha: float, v: torch.Tensor, msg: torch.Tensor,
+                   status: torch.Tensor, stream=None, exact: bool = False, zero_grad: bool = False) -> None:
+        """Single rank (P = 1): compress with v <- v - sent fused into the selection epilogue."""
+        sd = storage_dtype(self.mode)
+        if g.dtype != sd or r.dtype != sd or v.dtype != sd:
+            raise TypeError(f"bucket mode {self.mode} expects {sd} buffers")
+        if min(g.numel(), r.numel(), v.numel()) < self.n_total or msg.numel() < self.msg_bytes:
+            raise ValueError("buffer smaller than the bucket")
+        flags = (N.COMPRESS_EXACT if exact else 0) | (N.COMPRESS_ZERO_GRAD if zero_grad else 0)
+        N.check(N.lags_bucket_step_local(self._h, g.data_ptr(), r.data_ptr(), float(alpha), v.data_ptr(),
+                                         msg.data_ptr(), status.data_ptr(), flags, stream_handle(stream)),
+                "lags_bucket_step_local")
+
     def decode(self, msgs: torch.Tensor, P: int, v: torch.Tensor, momentum: torch.Tensor | None = None,
                mu: float = 0.0, stream=None, msg_stride: int | None = None) -> None:
         """Rank-ordered fp64 decode of P messages and v <- v - total/P (or heavy-ball momentum).

@@ -267,6 +267,14 @@ class LagsSGD(torch.optim.Optimizer):
         t = self.timing[i] if self.timing is not None else None
         if t is not None:
             t[0].record(stream)
+        local = self.world == 1 or not self.exchange
+        if local and m is None and hasattr(b.engine, "step_local"):  # P = 1: update fused into selection
+            b.engine.step_local(g, r, lr, v, b.msg_local, self.status, stream=stream, zero_grad=True)
+            if t is not None:
+                t[1].record(stream)
+                t[2].record(stream)
+                t[3].record(stream)
+            return
         b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=True)
         if t is not None:
             t[1].record(stream)

@@ -214,12 +214,18 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
         v_d = v_d.double()
     msgs = bucket.new_messages(P)
     r_devs = []
+    fused = P == 1 and mode == N.F32 and v_d.dtype == torch.float32
     for p in range(P):
         g_d = pin.h2d(grads[p].data, dev)
         r_d = pin.h2d(residuals[p].data, dev)
-        bucket.compress(g_d, r_d, alpha, msgs[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes], status[p:p + 1])
+        msg_p = msgs[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes]
+        if fused:  # one worker: the update is fused into the selection epilogue
+            bucket.step_local(g_d, r_d, alpha, v_d, msg_p, status[p:p + 1])
+        else:
+            bucket.compress(g_d, r_d, alpha, msg_p, status[p:p + 1])
         r_devs.append(r_d)
-    bucket.decode(msgs, P, v_d)
+    if not fused:
+        bucket.decode(msgs, P, v_d)
     out = torch.empty(v_d.shape, dtype=v_d.dtype, pin_memory=True)
     out.copy_(v_d, non_blocking=True)
     st = status.cpu().numpy()  # synchronises: inputs copied, compress + decode done

@@ -266,6 +266,31 @@ def test_fast_path_decode_multi_rank_equals_oracle(L):
             assert _same_bits(rs[p].cpu().numpy(), r_h[p])
 
 
+def test_step_local_equals_compress_plus_decode(L):
+    """P = 1 fused update (lags_bucket_step_local) == compress + decode, over the dense first
+    call, the candidate path and a forced misprediction."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [300000, 64, 16000, 70001, 9]
+    ks = [300, 64, 16, 70, 1]
+    a, b = L.Bucket(dims, ks, N.F32), L.Bucket(dims, ks, N.F32)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    ra, rb = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    va = torch.randn(n, device="cuda", generator=gen)
+    vb = va.clone()
+    ma, mb = a.new_messages(1), b.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for it in range(8):
+        g = torch.randn(n, device="cuda", generator=gen) * (1e-3 if it == 5 else 1.0)
+        a.step_local(g, ra, 0.1, va, ma, st)
+        b.compress(g, rb, 0.1, mb, st)
+        b.decode(mb, 1, vb)
+        assert torch.equal(ma, mb), it
+        assert torch.equal(ra.view(torch.int32), rb.view(torch.int32)), it
+        assert torch.equal(va.view(torch.int32), vb.view(torch.int32)), it
+
+
 def test_large_layer_properties(L):
     """Full-size layer (LSTM embedding, 15M) through the bucket API: size-independent checks
     (count == k, ascending, residual + sent == acc bitwise, selected keys dominate)."""
