@@ -479,7 +479,7 @@ def measure_e2e(args, dims, ks, L, dev):
     res = [L.LayeredVector.zeros(shape, np.float32)]
     counts = {i + 1: k for i, k in enumerate(ks)}
     steps = max(3, min(args.steps, 10))
-    for t in range(2):
+    for t in range(5):  # past the one-time page-locking of the reused host buffers
         v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res)
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
