@@ -206,9 +206,25 @@ struct lags_bucket {
   double* acc64 = nullptr;
   uint32_t* mask = nullptr;
   char* planes = nullptr;
-  int32_t* order = nullptr;  // layers by decreasing selection work (phase-1 schedule)
-  CoopScratch coop{};
-  int n_big = 1;  // layers that can be queued for the dense fallback (its grid size)
+  int32_t* order = nullptr;  // layers by decreasing selection work, group by group (phase-1 schedule)
+  // fp32 pipeline groups: the selection of group 0 (the layers with the heaviest selection work)
+  // runs on `side` while K1 streams group 1 (see compress_impl)
+  struct Group {
+    int task_base = 0, ntasks = 0;    // contiguous range of the task table
+    int order_base = 0, nlayers = 0;  // contiguous range of `order`
+    int n_big = 1;                    // fallback grid (layers that can be queued)
+    CoopScratch q{};                  // fallback queue of the group
+  };
+  int ngroups = 1;
+  Group grp[2];
+  CoopScratch coop{};  // storage of both groups' fallback queues
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~lags_bucket() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
+  }
 };
 
 namespace {
@@ -303,10 +319,40 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
   p->o_order = take(sizeof(int32_t) * L);
   const bool f32 = dtype == LAGS_F32;
-  p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);
-  p->o_fbl = take(f32 ? sizeof(int32_t) * L : 0);
+  p->o_fbc = take(f32 ? 2 * sizeof(uint32_t) : 0);     // one fallback queue per pipeline group
+  p->o_fbl = take(f32 ? 2 * sizeof(int32_t) * L : 0);
   p->bytes = o;
   return LAGS_OK;
+}
+
+// Split the layers into (at most) two pipeline groups so the selection of group 0 overlaps the
+// streaming of group 1: T = K1(G0) + max(K2(G0), K1(G1)) + K2(G1), with K1 ~ bytes and K2 ~ the
+// slowest layer's selection (one CTA per layer).  Returns group ids per layer (0/1).
+std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
+  auto k1 = [](double elems) { return elems > 0 ? 3e-6 + 1.8e-12 * elems : 0.0; };  // ~12 B/elem at ~6.5 TB/s
+  auto k2 = [&](int j) {
+    return dims[j] <= SMALL_LAYER ? 2e-6 + 4e-10 * static_cast<double>(dims[j]) : 4e-6 + 6e-9 * ks[j];
+  };
+  std::vector<int> by_cost(L);
+  for (int j = 0; j < L; ++j) by_cost[j] = j;
+  std::stable_sort(by_cost.begin(), by_cost.end(), [&](int a, int c) { return k2(a) > k2(c); });
+  double total = 0;
+  for (int j = 0; j < L; ++j) total += static_cast<double>(dims[j]);
+  const double single = k1(total) + k2(by_cost[0]) + 3e-6;
+  double best = single, e0 = 0;
+  int best_s = 0;
+  for (int s = 1; s < L; ++s) {  // group 0 = the s layers with the heaviest selection
+    e0 += static_cast<double>(dims[by_cost[s - 1]]);
+    const double t = k1(e0) + std::max(k2(by_cost[0]) + 3e-6, k1(total - e0)) + k2(by_cost[s]) + 3e-6;
+    if (t < best) {
+      best = t;
+      best_s = s;
+    }
+  }
+  std::vector<int> gid(L, 0);
+  if (best_s > 0 && best < 0.97 * single)
+    for (int s = best_s; s < L; ++s) gid[by_cost[s]] = 1;
+  return gid;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -380,31 +426,54 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
   b->msg_bytes = static_cast<int64_t>(align_up(b->off_val + val_size(dtype) * static_cast<size_t>(p.total_k), 16));
-  // host tables
+  // host tables.  fp32 buckets are split into two pipeline groups; the task table holds group 0's
+  // tasks first so each group's tasks (and candidate lists) are one contiguous range.
+  const std::vector<int> gid = dtype == LAGS_F32 ? plan_groups(dims, ks, nlayers) : std::vector<int>(nlayers, 0);
   std::vector<lags_layer_t> layers(nlayers);
   std::vector<int2> ltasks(nlayers);
   std::vector<Task> tasks;
   std::vector<int32_t> slot_layer(static_cast<size_t>(p.total_k));
+  std::vector<int64_t> offs(nlayers);
   tasks.reserve(p.ntasks);
   int64_t off = 0, slot = 0;
   for (int j = 0; j < nlayers; ++j) {
     layers[j] = lags_layer_t{off, dims[j], ks[j], static_cast<int32_t>(slot)};
-    ltasks[j].x = static_cast<int>(tasks.size());
-    for (int64_t s = 0; s < dims[j]; s += TASK_ELEMS)
-      tasks.push_back(Task{off + s, static_cast<int32_t>(std::min<int64_t>(TASK_ELEMS, dims[j] - s)), j});
-    ltasks[j].y = static_cast<int>(tasks.size());
+    offs[j] = off;
     for (int32_t q = 0; q < ks[j]; ++q) slot_layer[slot + q] = j;
     off += dims[j];
     slot += ks[j];
   }
-  // phase-1 schedule of the selection kernel: longest (estimated) work first
-  std::vector<int32_t> order(nlayers);
-  std::vector<double> cost(nlayers);
-  for (int j = 0; j < nlayers; ++j) {
-    order[j] = j;
-    cost[j] = dims[j] <= SMALL_LAYER ? 5.0 * dims[j] : 40.0 * ks[j] + 64.0 * (ltasks[j].y - ltasks[j].x);
+  for (int g = 0; g < 2; ++g) {
+    b->grp[g].task_base = static_cast<int>(tasks.size());
+    for (int j = 0; j < nlayers; ++j) {
+      if (gid[j] != g) continue;
+      ltasks[j].x = static_cast<int>(tasks.size());
+      for (int64_t s = 0; s < dims[j]; s += TASK_ELEMS)
+        tasks.push_back(Task{offs[j] + s, static_cast<int32_t>(std::min<int64_t>(TASK_ELEMS, dims[j] - s)), j});
+      ltasks[j].y = static_cast<int>(tasks.size());
+    }
+    b->grp[g].ntasks = static_cast<int>(tasks.size()) - b->grp[g].task_base;
   }
-  std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return cost[a] > cost[c]; });
+  // phase-1 schedule of the selection kernel: longest (estimated) work first, group by group
+  std::vector<int32_t> order;
+  std::vector<double> cost(nlayers);
+  for (int j = 0; j < nlayers; ++j)
+    cost[j] = dims[j] <= SMALL_LAYER ? 5.0 * dims[j] : 40.0 * ks[j] + 64.0 * (ltasks[j].y - ltasks[j].x);
+  for (int g = 0; g < 2; ++g) {
+    b->grp[g].order_base = static_cast<int>(order.size());
+    std::vector<int32_t> og;
+    int nbig = 0;
+    for (int j = 0; j < nlayers; ++j)
+      if (gid[j] == g) {
+        og.push_back(j);
+        nbig += dims[j] > SMALL_LAYER ? 1 : 0;
+      }
+    std::stable_sort(og.begin(), og.end(), [&](int a, int c) { return cost[a] > cost[c]; });
+    order.insert(order.end(), og.begin(), og.end());
+    b->grp[g].nlayers = static_cast<int>(og.size());
+    b->grp[g].n_big = std::max(nbig, 1);
+  }
+  b->ngroups = b->grp[1].nlayers > 0 ? 2 : 1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool ok =
       cudaMemcpyAsync(b->layers, layers.data(), sizeof(lags_layer_t) * nlayers, cudaMemcpyHostToDevice, s) ==
@@ -418,11 +487,15 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
-      (dtype != LAGS_F32 || cudaMemsetAsync(b->coop.fb_count, 0, sizeof(uint32_t), s) == cudaSuccess) &&
+      (dtype != LAGS_F32 || cudaMemsetAsync(b->coop.fb_count, 0, 2 * sizeof(uint32_t), s) == cudaSuccess) &&
       cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) {
     delete b;
     return cuda_check("lags_bucket_create upload", 0);
+  }
+  for (int g = 0; g < 2; ++g) {
+    b->grp[g].q.fb_count = b->coop.fb_count + g;
+    b->grp[g].q.fb_list = b->coop.fb_list + static_cast<size_t>(g) * nlayers;
   }
   if (dtype == LAGS_F32) {
     const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
@@ -432,9 +505,13 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       return cuda_check("select_phase1_kernel attributes", 0);
     }
     b->smem_keys = SMEM_KEYS;
-    b->n_big = 0;
-    for (int j = 0; j < nlayers; ++j) b->n_big += dims[j] > SMALL_LAYER ? 1 : 0;
-    if (b->n_big == 0) b->n_big = 1;
+    if (b->ngroups == 2 &&
+        (cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+      delete b;
+      return cuda_check("pipeline stream/events", 0);
+    }
   }
   *out = b;
   return LAGS_OK;
@@ -467,30 +544,56 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
   if (b->dtype == LAGS_F32) {
     const bool exact = (flags & LAGS_COMPRESS_EXACT) != 0;
     const float a = static_cast<float>(alpha);  // numpy casts a Python float to float32 (NEP 50)
-    const int blocks = (b->ntasks + K1_WARPS - 1) / K1_WARPS;
     float* rr = static_cast<float*>(r);
     float* gg = static_cast<float*>(g);
     float* vals = reinterpret_cast<float*>(m + b->off_val);
     float* vu = static_cast<float*>(v_update);
     const int fe = exact ? 1 : 0;
+    const bool zg = (flags & LAGS_COMPRESS_ZERO_GRAD) != 0;
+    // K1 over one group's task range (candidate lists indexed by global task id)
+    auto k1 = [&](const lags_bucket::Group& G, cudaStream_t st) -> cudaError_t {
+      if (G.ntasks == 0) return cudaSuccess;
+      const int blocks = (G.ntasks + K1_WARPS - 1) / K1_WARPS;
+      const int64_t cb = static_cast<int64_t>(G.task_base) * b->cap;
+      if (zg)
+        return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
+                          G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
+                          b->cand_cnt + G.task_base, status, G.q.fb_count);
+      return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
+                        G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
+                        b->cand_cnt + G.task_base, status, G.q.fb_count);
+    };
+    // K2a + K2b over one group's layers
+    auto k2 = [&](const lags_bucket::Group& G, cudaStream_t st) -> cudaError_t {
+      if (G.nlayers == 0) return cudaSuccess;
+      cudaError_t e = launch_pdl(select_phase1_kernel, dim3(G.nlayers), dim3(SEL_NT),
+                                 static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), st, b->layers, b->layer_tasks,
+                                 b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap,
+                                 b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu);
+      if (e == cudaSuccess)
+        e = launch_pdl(select_fallback_kernel, dim3(G.n_big), dim3(SEL_NT), 0, st, b->layers, b->state, rr, idx, vals,
+                       cnt, fe, G.q, vu);
+      return e;
+    };
     cudaError_t e;
-    if (flags & LAGS_COMPRESS_ZERO_GRAD)
-      e = launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, b->ntasks, b->layers,
-                     b->state, gg, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status, b->coop.fb_count);
-    else
-      e = launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, b->ntasks,
-                     b->layers, b->state, gg, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status,
-                     b->coop.fb_count);
-    if (e == cudaSuccess)
-      e = launch_pdl(select_phase1_kernel, dim3(b->nlayers), dim3(SEL_NT),
-                     static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), s, b->layers, b->layer_tasks, b->order,
-                     b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt,
-                     b->smem_keys, fe, b->coop, vu);
-    if (e == cudaSuccess)
-      e = launch_pdl(select_fallback_kernel, dim3(b->n_big), dim3(SEL_NT), 0, s, b->layers, b->state, rr, idx, vals,
-                     cnt, fe, b->coop, vu);
+    int launches = 3;
+    if (b->ngroups == 1) {
+      e = k1(b->grp[0], s);
+      if (e == cudaSuccess) e = k2(b->grp[0], s);
+    } else {
+      // pipeline: select group 0 on the side stream while K1 streams group 1
+      e = k1(b->grp[0], s);
+      if (e == cudaSuccess) e = cudaEventRecord(b->ev_fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(b->side, b->ev_fork, 0);
+      if (e == cudaSuccess) e = k2(b->grp[0], b->side);
+      if (e == cudaSuccess) e = cudaEventRecord(b->ev_join, b->side);
+      if (e == cudaSuccess) e = k1(b->grp[1], s);
+      if (e == cudaSuccess) e = k2(b->grp[1], s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, b->ev_join, 0);
+      launches = 6;
+    }
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
-    return cuda_check("lags_bucket_compress(f32)", 3);
+    return cuda_check("lags_bucket_compress(f32)", launches);
   }
   if (v_update) return fail(LAGS_ERR_INVALID_ARG, "fused single-rank update needs an LAGS_F32 bucket");
   if (b->dtype == LAGS_F64) {
