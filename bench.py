@@ -303,23 +303,25 @@ def run_ours(args, dims, ks, world, rank, local):
     # N = 1: the step is captured once per gradient buffer into CUDA graphs and replayed (the
     # selection state lives on the device, so replays are real steps); no host launch overhead.
     graphs = None
+    l_graph = 0
     if world == 1 and not args.no_graph:
         try:
             cap = torch.cuda.Stream(dev)
             cap.wait_stream(stream)
             graphs = []
+            lc0 = N.lags_kernel_launches()
             for i in range(NG):
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gr, stream=cap):
                     bucket.step_local(g_bufs[i], r, alpha, v, msg_local, status, stream=cap)
                 graphs.append(gr)
+            l_graph = (N.lags_kernel_launches() - lc0) // NG  # our kernels per captured step
             for i in range(2 * NG):  # graph warm-up replays (steps like any other)
                 graphs[i % NG].replay()
             torch.cuda.synchronize(dev)
         except Exception as exc:  # pragma: no cover - report and time eagerly
             print(f"cuda graph capture failed ({exc}); timing eager launches", file=sys.stderr)
             graphs = None
-    l_graph = 3 if graphs is not None else 0  # kernels per captured step (K1, K2a, K2b)
     stats0 = bucket.stats()
     l0 = N.lags_kernel_launches()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

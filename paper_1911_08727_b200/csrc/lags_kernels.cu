@@ -350,7 +350,9 @@ std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
     }
   }
   std::vector<int> gid(L, 0);
-  if (best_s > 0 && best < 0.97 * single)
+  // Measured on B200 (ResNet-50 shapes): the 1024-thread / ~200 KB selection CTAs cannot share an
+  // SM with K1's CTAs, so a modest modelled gain does not materialise; split only for large ones.
+  if (best_s > 0 && best < 0.8 * single)
     for (int s = best_s; s < L; ++s) gid[by_cost[s]] = 1;
   return gid;
 }
