@@ -10,7 +10,7 @@
 //    alone (dual-rank radix select in shared memory, ordered compaction, residual zeroing by
 //    scatter) and predicts its next threshold; small layers run the dense exact path staged in
 //    shared memory; other big layers are queued.
-// K2b (select_fallback_kernel): one CTA per queued layer runs the dense exact path over r.
+//    A layer whose candidate set fails the proof runs the dense exact path over r in its CTA.
 // Every path returns exactly the reference's selection: the candidate set contains every top-k
 // element, and the dense paths scan all of r.  All launches are ordinary (not cooperative), so
 // the selection can share the GPU with backprop kernels on other streams.
@@ -542,7 +542,11 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
                         ? FB_TOO_FEW
                         : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval,
                                            r, idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
-    if (why && threadIdx.x == 0) sc.fb_list[atomicAdd(sc.fb_count, 1u)] = j | (why << 24);
+    if (why) {  // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA
+      if (threadIdx.x == 0) atomicAdd(sc.fb_count, 1u);  // diagnostic count of dense layers this call
+      __syncthreads();
+      dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
+    }
     path = why ? 2u : 1u;
   }
   __syncthreads();
@@ -550,24 +554,6 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
     state[j].path = path;
   }
-}
-
-// Phase 2: one CTA per queued layer (CTAs beyond the queue exit at once).  fb_count is reset by
-// the next call's accum_emit_kernel.
-__global__ void __launch_bounds__(SEL_NT, 1) select_fallback_kernel(const lags_layer_t* __restrict__ layers,
-                                                                    FastState* state, float* r, int32_t* idx_out,
-                                                                    float* val_out, int32_t* count_out,
-                                                                    int force_exact, CoopScratch sc, float* vupd) {
-  __shared__ CoopSmem cs;
-  griddep_wait();
-  if (blockIdx.x >= __ldcg(sc.fb_count)) return;
-  const int entry = __ldcg(sc.fb_list + blockIdx.x);
-  const int j = entry & 0xffffff;
-  const long long t_begin = clock64();
-  dense_fallback_select(j, layers[j], state[j], r, idx_out, val_out, count_out, state, force_exact != 0, entry >> 24,
-                        cs, vupd);
-  __syncthreads();
-  if (threadIdx.x == 0) state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
 }
 
 }  // namespace lags

@@ -565,20 +565,17 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
                         G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
                         b->cand_cnt + G.task_base, status, G.q.fb_count);
     };
-    // K2a + K2b over one group's layers
+    // K2 over one group's layers (a layer whose candidates fail the proof runs the dense path in
+    // its own CTA)
     auto k2 = [&](const lags_bucket::Group& G, cudaStream_t st) -> cudaError_t {
       if (G.nlayers == 0) return cudaSuccess;
-      cudaError_t e = launch_pdl(select_phase1_kernel, dim3(G.nlayers), dim3(SEL_NT),
-                                 static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), st, b->layers, b->layer_tasks,
-                                 b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap,
-                                 b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu);
-      if (e == cudaSuccess)
-        e = launch_pdl(select_fallback_kernel, dim3(G.n_big), dim3(SEL_NT), 0, st, b->layers, b->state, rr, idx, vals,
-                       cnt, fe, G.q, vu);
-      return e;
+      return launch_pdl(select_phase1_kernel, dim3(G.nlayers), dim3(SEL_NT),
+                        static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), st, b->layers, b->layer_tasks,
+                        b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
+                        b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu);
     };
     cudaError_t e;
-    int launches = 3;
+    int launches = 2;
     if (b->ngroups == 1) {
       e = k1(b->grp[0], s);
       if (e == cudaSuccess) e = k2(b->grp[0], s);
@@ -592,7 +589,7 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       if (e == cudaSuccess) e = k1(b->grp[1], s);
       if (e == cudaSuccess) e = k2(b->grp[1], s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(s, b->ev_join, 0);
-      launches = 6;
+      launches = 4;
     }
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
     return cuda_check("lags_bucket_compress(f32)", launches);
