@@ -1,0 +1,78 @@
+"""Kernel timeline of the bench step (CUPTI activity records via torch.profiler; no nsys here).
+
+Prints, for the last steps, each kernel's start offset, duration and the idle gap before it, for
+eager launches and for CUDA-graph replay.  Diagnostic only.
+"""
+
+import json
+import os
+import sys
+import tempfile
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1911_08727_b200 as L  # noqa: E402
+from paper_1911_08727_b200 import _native as N  # noqa: E402
+from bench import ks_for, resnet50_dims  # noqa: E402
+
+
+def kernels_from_trace(path):
+    ev = json.load(open(path))["traceEvents"]
+    ks = [e for e in ev if e.get("cat") == "kernel"]
+    ks.sort(key=lambda e: e["ts"])
+    return [(e["ts"], e["dur"], e["name"]) for e in ks]
+
+
+def show(title, ks, last=12):
+    print(f"--- {title}")
+    ks = ks[-last:]
+    t0 = ks[0][0]
+    prev_end = None
+    for ts, dur, name in ks:
+        gap = 0.0 if prev_end is None else ts - prev_end
+        print(f"  +{ts - t0:9.1f} us  dur {dur:7.1f}  gap {gap:6.1f}  {name[:60]}")
+        prev_end = ts + dur
+
+
+def main():
+    dims = resnet50_dims()
+    ks = ks_for(dims)
+    n = sum(dims)
+    b = L.Bucket(dims, ks, N.F32)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    gs = [torch.randn(n, device="cuda", generator=gen) for _ in range(3)]
+    r = torch.zeros(n, device="cuda")
+    v = torch.randn(n, device="cuda", generator=gen)
+    msg = b.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for t in range(400):
+        b.step_local(gs[t % 3], r, 0.1, v, msg, st)
+    torch.cuda.synchronize()
+    tmp = tempfile.mkdtemp()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        for t in range(12):
+            b.step_local(gs[t % 3], r, 0.1, v, msg, st)
+        torch.cuda.synchronize()
+    prof.export_chrome_trace(os.path.join(tmp, "eager.json"))
+    show("eager", kernels_from_trace(os.path.join(tmp, "eager.json")))
+    cap = torch.cuda.Stream()
+    graphs = []
+    for i in range(3):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cap):
+            b.step_local(gs[i], r, 0.1, v, msg, st, stream=cap)
+        graphs.append(gr)
+    for t in range(30):
+        graphs[t % 3].replay()
+    torch.cuda.synchronize()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        for t in range(12):
+            graphs[t % 3].replay()
+        torch.cuda.synchronize()
+    prof.export_chrome_trace(os.path.join(tmp, "graph.json"))
+    show("graph replay", kernels_from_trace(os.path.join(tmp, "graph.json")))
+
+
+if __name__ == "__main__":
+    main()
