@@ -108,9 +108,10 @@ int lags_bucket_decode_update(lags_bucket_t* bucket, const void* msgs, int64_t m
                               void* momentum, double mu, uint32_t flags, lags_stream_t stream);
 
 /* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls, last select
- * cycles, last path (0 small dense, 1 candidates, 2 grid-wide dense), 0, 0} (synchronous). */
-#define LAGS_STATS_WORDS 8
-int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 8] */, lags_stream_t stream);
+ * cycles, last path (0 small dense, 1 candidates, 2 dense after a failed prediction), phase
+ * cycles, select start / end / CTA launch (%globaltimer ns, low 32 bits), 0} (synchronous). */
+#define LAGS_STATS_WORDS 12
+int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 12] */, lags_stream_t stream);
 
 /* ---- single-vector operators ---------------------------------------------------------------- */
 

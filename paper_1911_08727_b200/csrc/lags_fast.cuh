@@ -41,8 +41,18 @@ struct FastState {
   uint32_t cycles;      // SM cycles the layer's phase-1 work took at the last call (diagnostic)
   uint32_t path;        // last path: 0 small dense, 1 candidates, 2 queued for the grid-wide dense path
   uint32_t pf256;       // adaptive prediction rank factor x256 (0 = PRED_FACTOR)
-  uint32_t reserved;
+  uint32_t reserved;    // candidate-path phase cycles (diagnostic)
+  uint32_t t_start;     // %globaltimer (ns, low 32 bits) when the layer's CTA started / ended its
+  uint32_t t_end;       //   selection work at the last call (diagnostic timeline)
+  uint32_t t_launch;    // %globaltimer when the CTA entered the kernel (before griddepcontrol.wait)
+  uint32_t pad;
 };
+
+__device__ __forceinline__ uint32_t globaltimer_lo() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return static_cast<uint32_t>(t);
+}
 
 constexpr float PRED_TARGET = 2.0f;  // wanted candidates per selected entry (m / k)
 
@@ -520,7 +530,9 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc, float* vupd) {
   extern __shared__ uint32_t skeys[];
   __shared__ CoopSmem cs;
+  const uint32_t t_launch = globaltimer_lo();
   griddep_wait();  // programmatic dependent launch: K1's results are visible after this
+  const uint32_t t_start = globaltimer_lo();
   const int j = order[blockIdx.x];
   const lags_layer_t L = layers[j];
   const FastState st = state[j];
@@ -553,6 +565,9 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
   if (threadIdx.x == 0) {
     state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
     state[j].path = path;
+    state[j].t_start = t_start;
+    state[j].t_end = globaltimer_lo();
+    state[j].t_launch = t_launch;
   }
 }
 

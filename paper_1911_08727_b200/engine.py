@@ -144,8 +144,9 @@ class Bucket:
 
     # -- host helpers (tests / diagnostics) ----------------------------------------------------
     def stats(self, stream=None) -> np.ndarray:
-        """Per-layer [threshold key, fallbacks, last candidates, calls, cycles, path, 0, 0] (synchronous)."""
-        out = np.zeros((self.nlayers, 8), dtype=np.uint32)
+        """Per-layer [threshold key, fallbacks, last candidates, calls, cycles, path, phase cycles,
+        t_start, t_end, t_launch (globaltimer ns, low 32 bits), 0] (synchronous)."""
+        out = np.zeros((self.nlayers, 12), dtype=np.uint32)
         N.check(N.lags_bucket_stats(self._h, out.ctypes.data, stream_handle(stream)))
         return out
 

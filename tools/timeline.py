@@ -9,6 +9,7 @@ import os
 import sys
 import tempfile
 
+import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -72,6 +73,18 @@ def main():
         torch.cuda.synchronize()
     prof.export_chrome_trace(os.path.join(tmp, "graph.json"))
     show("graph replay", kernels_from_trace(os.path.join(tmp, "graph.json")))
+    # per-layer CTA spans inside the last selection kernel (globaltimer, ns)
+    s = b.stats().astype(np.int64)
+    t0 = int(s[:, 9].min())
+    rows = sorted(range(len(dims)), key=lambda j: -(s[j, 8] - s[j, 7]))
+    print("--- selection CTAs (us from first CTA launch): launch, start, end, kcycles, path, dim, k, m")
+    for j in rows[:8]:
+        print(f"  {(s[j, 9] - t0) / 1e3:7.2f} {(s[j, 7] - t0) / 1e3:7.2f} {(s[j, 8] - t0) / 1e3:7.2f}"
+              f" {s[j, 4] // 1000:4d} {s[j, 5]} {dims[j]:8d} {ks[j]:5d} {s[j, 2]:6d}")
+    last = sorted(range(len(dims)), key=lambda j: -s[j, 8])[:5]
+    print("  latest-ending layers:", [(dims[j], round((s[j, 8] - t0) / 1e3, 2)) for j in last])
+    print("  latest-starting layers:", [(dims[j], round((s[j, 7] - t0) / 1e3, 2))
+                                       for j in sorted(range(len(dims)), key=lambda j: -s[j, 7])[:5]])
 
 
 if __name__ == "__main__":
