@@ -75,16 +75,22 @@ def main():
     show("graph replay", kernels_from_trace(os.path.join(tmp, "graph.json")))
     # per-layer CTA spans inside the last selection kernel (globaltimer, ns)
     s = b.stats().astype(np.int64)
-    t0 = int(s[:, 9].min())
-    rows = sorted(range(len(dims)), key=lambda j: -(s[j, 8] - s[j, 7]))
-    print("--- selection CTAs (us from first CTA launch): launch, start, end, kcycles, path, dim, k, m")
+    ref = int(s[0, 10])
+    rel = lambda x: ((int(x) - ref + 2**31) % 2**32 - 2**31) / 1e3  # noqa: E731  (us, wrap-safe)
+    launch = [rel(s[j, 10]) for j in range(len(dims))]
+    base = min(launch)
+    start = [rel(s[j, 8]) - base for j in range(len(dims))]
+    end = [rel(s[j, 9]) - base for j in range(len(dims))]
+    launch = [x - base for x in launch]
+    rows = sorted(range(len(dims)), key=lambda j: -(end[j] - start[j]))
+    print("--- selection CTAs (us from the first CTA launch): launch, start, end, kcycles, path, dim, k, m")
     for j in rows[:8]:
-        print(f"  {(s[j, 9] - t0) / 1e3:7.2f} {(s[j, 7] - t0) / 1e3:7.2f} {(s[j, 8] - t0) / 1e3:7.2f}"
-              f" {s[j, 4] // 1000:4d} {s[j, 5]} {dims[j]:8d} {ks[j]:5d} {s[j, 2]:6d}")
-    last = sorted(range(len(dims)), key=lambda j: -s[j, 8])[:5]
-    print("  latest-ending layers:", [(dims[j], round((s[j, 8] - t0) / 1e3, 2)) for j in last])
-    print("  latest-starting layers:", [(dims[j], round((s[j, 7] - t0) / 1e3, 2))
-                                       for j in sorted(range(len(dims)), key=lambda j: -s[j, 7])[:5]])
+        print(f"  {launch[j]:7.2f} {start[j]:7.2f} {end[j]:7.2f} {s[j, 4] // 1000:4d} {s[j, 5]} {dims[j]:8d}"
+              f" {ks[j]:5d} {s[j, 2]:6d}")
+    print("  latest-ending:", [(dims[j], round(end[j], 2)) for j in sorted(range(len(dims)), key=lambda j: -end[j])[:6]])
+    print("  latest-launched:", [(dims[j], round(launch[j], 2))
+                                 for j in sorted(range(len(dims)), key=lambda j: -launch[j])[:6]])
+    print("  start after griddep wait: min %.2f max %.2f" % (min(start), max(start)))
 
 
 if __name__ == "__main__":
