@@ -91,6 +91,8 @@ def main():
     print("  latest-launched:", [(dims[j], round(launch[j], 2))
                                  for j in sorted(range(len(dims)), key=lambda j: -launch[j])[:6]])
     print("  start after griddep wait: min %.2f max %.2f" % (min(start), max(start)))
+    ph = lambda w: (int(w) & 2047, (int(w) >> 11) & 2047, (int(w) >> 22) & 2047)  # noqa: E731
+    print("  phases x64 cycles (gather, select, compact) of the slowest:", [ph(s[j, 7]) for j in rows[:6]])
 
 
 if __name__ == "__main__":
