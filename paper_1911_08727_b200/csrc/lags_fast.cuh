@@ -218,9 +218,32 @@ struct CoopSmem {
 
 // P = 1 update fused into the selection epilogue (no exchange, no separate decode): exactly the
 // decode of R: training.py:248,253-254 with one worker, v = fl32(fl64(v) - (0.0 + x) / 1).
-__device__ __forceinline__ void single_rank_update(float* v, float x) {
+__device__ __forceinline__ float single_rank_update(float v, float x) {
   const double total = __dadd_rn(0.0, static_cast<double>(x));
-  *v = static_cast<float>(__dsub_rn(static_cast<double>(*v), __ddiv_rn(total, 1.0)));
+  return static_cast<float>(__dsub_rn(static_cast<double>(v), __ddiv_rn(total, 1.0)));
+}
+
+// Post-pass over a layer's selected (idx, val) just written by the compaction: batches of
+// independent weight loads in flight per thread (the weights are HBM-resident and scattered).
+__device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32_t* oidx, const float* oval,
+                                                          uint32_t cnt) {
+  __syncthreads();  // the block's compaction writes are visible
+  constexpr int B = 4;
+  for (uint32_t q0 = 0; q0 < cnt; q0 += SEL_NT * B) {
+    int32_t ix[B];
+    float x[B], w[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const uint32_t q = q0 + u * SEL_NT + threadIdx.x;
+      ix[u] = q < cnt ? oidx[q] : -1;
+      x[u] = q < cnt ? oval[q] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) w[u] = ix[u] >= 0 ? vl[ix[u]] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (ix[u] >= 0) vl[ix[u]] = single_rank_update(w[u], x[u]);
+  }
 }
 
 // Dense exact top-k of a small layer staged once in shared memory (`sv`, >= d floats): every
@@ -251,9 +274,10 @@ __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32
     oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
     data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
-    if (vl) single_rank_update(vl + i, x);
   };
-  return ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
+  const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
+  if (vl) apply_single_rank_updates(vl, oidx, oval, cnt);
+  return cnt;
 }
 
 // Two ranks in one set of radix passes over m keys (shared memory): the exact threshold of the
@@ -435,9 +459,9 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       oidx[pos] = static_cast<int32_t>(ix);
       oval[pos] = x;
       data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
-      if (vl) single_rank_update(vl + ix, x);
     };
     cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
+    if (vl) apply_single_rank_updates(vl, oidx, oval, cnt);
     const long long c3 = clock64();
     auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
     phases = q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22);
@@ -504,9 +528,9 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
     oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
     data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
-    if (vl) single_rank_update(vl + i, x);
   };
   const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
+  if (vl) apply_single_rank_updates(vl, oidx, oval, cnt);
   if (threadIdx.x == 0) {
     count_out[j] = static_cast<int32_t>(cnt);
     FastState ns = st;
