@@ -31,7 +31,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 RHO = 0.001
-METRIC = "LAGS sparsify/decode GB/s (ResNet-50 layer shapes, rho=0.001); iter/s of the hot-path step"
+# DRAM bytes of one K1 launch from the committed ncu --set full capture (profiles/r1_ncu_full_raw.csv:
+# dram__bytes_read.sum 204.59 MB + dram__bytes_write.sum 50.82 MB; ncu flushes caches per replay)
+K1_DRAM_TRAFFIC = 255_408_384
+METRIC ="LAGS sparsify/decode GB/s (ResNet-50 layer shapes, rho=0.001); iter/s of the hot-path step"
 UNIT = "GB/s"
 
 
@@ -353,6 +356,21 @@ def run_ours(args, dims, ks, world, rank, local):
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms, comp_ms = float(t_ms[0]), float(t_ms[1])
     assert int(status.item()) == 0
+    # dominant kernel (K1, the streaming pass) timed live: the library records these events
+    # around K1 inside every compress call (eager steps after the timed region, all ranks)
+    probes = []
+    for t in range(min(args.steps, 50)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        bucket.set_probe_events(e0, e1)
+        step(t)
+        probes.append((e0, e1))
+    bucket.set_probe_events(None, None)
+    torch.cuda.synchronize(dev)
+    k1_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in probes) / len(probes)], dtype=torch.float64,
+                         device=dev)
+    if world > 1:
+        dist.all_reduce(k1_ms, op=dist.ReduceOp.MAX)
+    k1_ms = float(k1_ms)
     # counts / union for the algorithmic-byte model (after the timed region)
     counts = bucket.counts_view(msg_local).cpu().numpy().astype(np.int64)
     sel_local = int(counts.sum())
@@ -398,11 +416,16 @@ def run_ours(args, dims, ks, world, rank, local):
             "iter_per_s": round(args.steps / (ms / 1e3), 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.randn gradients, seed 1234+rank)",
             "config": config_dict(dims, ks, world),
-            "roofline": {"kernel": "compress = K1 accum_emit + K2 select/compact (+fused P=1 update at N=1)",
-                         "bound": "hbm",
-                         "achieved": round(achieved, 2), "peak": peak, "peak_source": peak_src, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
-                         "algorithmic_bytes_per_launch": int(comp_bytes_rank), "ms_per_launch": round(comp_ms, 4)},
+            "roofline": {"kernel": "K1 accum_emit_kernel (dominant: acc = r + a*g, r <- acc, candidate emission)",
+                         "bound": "hbm", "achieved": round(12 * n / (k1_ms / 1e3) / 1e9, 2), "peak": peak,
+                         "peak_source": peak_src, "unit": "GB/s",
+                         "frac": round(12 * n / (k1_ms / 1e3) / 1e9 / peak, 4), "traffic": K1_DRAM_TRAFFIC,
+                         "traffic_source": "profiles/r1_ncu_full_raw.csv dram__bytes_read.sum + dram__bytes_write.sum",
+                         "algorithmic_bytes_per_launch": int(12 * n), "ms_per_launch": round(k1_ms, 4),
+                         "compress": {"what": "K1 + K2 select/compact (+fused P=1 update at N=1)",
+                                      "achieved": round(achieved, 2), "frac": round(achieved / peak, 4),
+                                      "algorithmic_bytes_per_call": int(comp_bytes_rank),
+                                      "ms_per_call": round(comp_ms, 4)}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
             "launch_mode": "cuda graph replay (one captured step per gradient buffer)" if graphs is not None
             else "eager (ctypes -> cudaLaunchKernelEx with programmatic dependent launch)",

@@ -107,6 +107,10 @@ int lags_bucket_step_local(lags_bucket_t* bucket, void* g, void* r, double alpha
 int lags_bucket_decode_update(lags_bucket_t* bucket, const void* msgs, int64_t msg_stride, int32_t P, void* v,
                               void* momentum, double mu, uint32_t flags, lags_stream_t stream);
 
+/* Diagnostics: when set (non-NULL cudaEvent_t handles), every fp32 compress records `before` and
+ * `after` around its streaming kernel (K1) so callers can time the dominant kernel live. */
+int lags_bucket_set_probe_events(lags_bucket_t* bucket, void* before, void* after);
+
 /* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls, last select
  * cycles, last path (0 small dense, 1 candidates, 2 dense after a failed prediction), phase
  * cycles, select start / end / CTA launch (%globaltimer ns, low 32 bits), 0} (synchronous). */

@@ -220,6 +220,7 @@ struct lags_bucket {
   CoopScratch coop{};  // storage of both groups' fallback queues
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t probe_before = nullptr, probe_after = nullptr;  // caller-owned, optional
   ~lags_bucket() {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
@@ -574,10 +575,12 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
                         b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
                         b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu);
     };
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     int launches = 2;
     if (b->ngroups == 1) {
-      e = k1(b->grp[0], s);
+      if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
+      if (e == cudaSuccess) e = k1(b->grp[0], s);
+      if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
       if (e == cudaSuccess) e = k2(b->grp[0], s);
     } else {
       // pipeline: select group 0 on the side stream while K1 streams group 1
@@ -682,6 +685,13 @@ int lags_bucket_step_local(lags_bucket_t* b, void* g, void* r, double alpha, voi
     return lags_bucket_decode_update(b, msg, b->msg_bytes, 1, v, nullptr, 0.0, 0, stream);
   }
   return compress_impl(b, g, r, alpha, msg, status, flags, v, stream);
+}
+
+int lags_bucket_set_probe_events(lags_bucket_t* b, void* before, void* after) {
+  if (!b) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_set_probe_events: null bucket");
+  b->probe_before = static_cast<cudaEvent_t>(before);
+  b->probe_after = static_cast<cudaEvent_t>(after);
+  return LAGS_OK;
 }
 
 int lags_bucket_stats(const lags_bucket_t* b, uint32_t* out, lags_stream_t stream) {

@@ -143,6 +143,13 @@ class Bucket:
                 "lags_bucket_decode_update")
 
     # -- host helpers (tests / diagnostics) ----------------------------------------------------
+    def set_probe_events(self, before, after) -> None:
+        """Record these torch.cuda.Events around the streaming kernel K1 of every fp32 compress
+        (None, None to stop)."""
+        self._probes = (before, after)  # keep them alive while the library holds the handles
+        N.check(N.lags_bucket_set_probe_events(self._h, before.cuda_event if before is not None else None,
+                                               after.cuda_event if after is not None else None))
+
     def stats(self, stream=None) -> np.ndarray:
         """Per-layer [threshold key, fallbacks, last candidates, calls, cycles, path, phase cycles,
         t_start, t_end, t_launch (globaltimer ns, low 32 bits), 0] (synchronous)."""
