@@ -361,6 +361,8 @@ def run_ours(args, dims, ks, world, rank, local):
     probes = []
     for t in range(min(args.steps, 50)):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)  # torch creates CUDA events lazily; the library re-records them around K1
+        e1.record(stream)
         bucket.set_probe_events(e0, e1)
         step(t)
         probes.append((e0, e1))
