@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblagsb200.so")
 SOURCES = ["lags_kernels.cu"]
-HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh"]
+HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh", "lags_cluster.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

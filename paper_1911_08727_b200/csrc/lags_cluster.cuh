@@ -1,0 +1,237 @@
+// Selection of the largest layers by a thread-block cluster (CLUSTER CTAs, distributed shared
+// memory).  One CTA per layer made the handful of ~2 M-element ResNet-50 layers the critical path
+// of the selection (gather + compaction of ~2k candidates in one CTA); here the CTAs of a cluster
+// each own a contiguous quarter of the layer's K1 task lists (= a contiguous index range):
+//   1. candidate counts are exchanged over DSMEM (cluster.sync) -> the exactness proof, prefixes;
+//   2. every CTA gathers its candidates (value, index) into its own shared memory and pushes the
+//      keys into rank 0's shared memory at its prefix offset (remote DSMEM stores);
+//   3. rank 0 runs the dual-rank radix select (k-th key + next prediction) on all keys;
+//   4. the threshold is read back over DSMEM, per-CTA (gt, eq) counts are exchanged, and every CTA
+//      compacts its own range in order with the carried counts (global output positions), zeroes
+//      the selected residuals and applies the optional fused P = 1 update.
+// Results are identical to the single-CTA candidate path (same keys, same order, same rule).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "lags_fast.cuh"
+
+namespace lags {
+
+constexpr int CLUSTER = 4;             // CTAs per cluster layer
+constexpr int CLUSTER_MIN_K = 512;     // layers with at least this k (and > SMALL_LAYER) use clusters
+
+struct ClusterShared {
+  uint32_t m, over;          // this CTA's candidate count / overflow
+  uint32_t gt, eq;           // this CTA's compaction counts
+  uint32_t prefix, pmask, n_gt, need_eq, key2;  // rank 0: the threshold
+};
+
+__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(SEL_NT, 1) select_cluster_kernel(
+    const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ big,
+    FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
+    const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
+    float* val_out, int32_t* count_out, int smem_words, int force_exact, float* vupd) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ uint32_t dyn[];
+  __shared__ CoopSmem cs;
+  __shared__ ClusterShared csh;
+  const uint32_t t_launch = globaltimer_lo();
+  griddep_wait();
+  const uint32_t t_start = globaltimer_lo();
+  const long long t_begin = clock64();
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int j = big[blockIdx.x / CLUSTER];
+  const lags_layer_t L = layers[j];
+  const int2 tr = layer_tasks[j];
+  const FastState st = state[j];
+  const uint32_t k = static_cast<uint32_t>(L.k);
+  const int T = tr.y - tr.x;
+  const int t_lo = tr.x + static_cast<int>((static_cast<int64_t>(T) * rank) / CLUSTER);
+  const int t_hi = tr.x + static_cast<int>((static_cast<int64_t>(T) * (rank + 1)) / CLUSTER);
+  // 1. counts
+  uint32_t local = 0, over = 0;
+  for (int t = t_lo + threadIdx.x; t < t_hi; t += SEL_NT) {
+    const uint32_t c = static_cast<uint32_t>(cand_cnt[t]);
+    over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
+    local += min(c, static_cast<uint32_t>(cap));
+  }
+  local = block_sum(local, cs.sm);
+  over = block_sum(over, cs.sm);
+  if (threadIdx.x == 0) {
+    csh.m = local;
+    csh.over = over;
+  }
+  cluster.sync();
+  uint32_t m = 0, pre = 0, m_max = 0, over_any = 0;
+  for (int q = 0; q < CLUSTER; ++q) {
+    const ClusterShared* o = cluster.map_shared_rank(&csh, q);
+    const uint32_t mq = o->m;
+    if (q < rank) pre += mq;
+    m += mq;
+    m_max = max(m_max, mq);
+    over_any |= o->over;
+  }
+  cluster.sync();  // every CTA has read the counts
+  const bool fits = static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
+  int why = 0;
+  if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
+  else if (over_any) why = FB_OVERFLOW;
+  else if (m < k && st.thr > 1u) why = FB_TOO_FEW;
+  if (why || !fits || m == 0) {  // uniform across the cluster; rank 0 finishes the layer alone
+    if (rank == 0) {
+      if (why) {
+        dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
+      } else {  // too many candidates for the cluster's shared memory, or none: one-CTA path
+        candidate_select(j, L, tr, st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out, val_out, count_out,
+                         state, dyn, smem_words, cs, vupd);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
+        state[j].path = why ? 2u : 1u;
+        state[j].t_start = t_start;
+        state[j].t_end = globaltimer_lo();
+        state[j].t_launch = t_launch;
+      }
+    }
+    return;
+  }
+  // 2. gather: own (value, index) at [m, m + mr) / [m + mr, m + 2 mr) of dyn; keys -> rank 0's dyn
+  const long long c0 = clock64();
+  const uint32_t mr = local;
+  float* sv = reinterpret_cast<float*>(dyn + m);
+  int32_t* si = reinterpret_cast<int32_t*>(dyn + m + mr);
+  uint32_t* keys0 = cluster.map_shared_rank(dyn, 0);
+  uint32_t carry = 0;
+  for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
+    const int nt = min(SEL_NT, t_hi - t0);
+    const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(cand_cnt[t0 + threadIdx.x]) : 0u;
+    uint32_t tot;
+    const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
+    cs.tpos[threadIdx.x] = pos;
+    __syncthreads();
+    constexpr int GATHER_ILP = 8;
+    for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
+      int64_t src[GATHER_ILP];
+#pragma unroll
+      for (int u = 0; u < GATHER_ILP; ++u) {
+        const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
+        src[u] = -1;
+        if (e < tot) {
+          int lo = 0, hi = nt - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cs.tpos[mid] <= e) lo = mid;
+            else hi = mid - 1;
+          }
+          src[u] = static_cast<int64_t>(t0 + lo) * cap + (e - cs.tpos[lo]);
+        }
+      }
+      float xv[GATHER_ILP];
+      int32_t xi[GATHER_ILP];
+#pragma unroll
+      for (int u = 0; u < GATHER_ILP; ++u) {
+        if (src[u] >= 0) {
+          xv[u] = __ldcg(cand_val + src[u]);
+          xi[u] = __ldcg(cand_idx + src[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GATHER_ILP; ++u) {
+        if (src[u] >= 0) {
+          const uint32_t e = carry + e0 + u * SEL_NT + threadIdx.x;
+          sv[e] = xv[u];
+          si[e] = xi[u];
+          keys0[pre + e] = Key<float>::of(xv[u]);
+        }
+      }
+    }
+    carry += tot;
+    __syncthreads();
+  }
+  cluster.sync();  // all keys are in rank 0
+  const long long c1 = clock64();
+  // 3. rank 0 selects
+  const uint32_t k2 = pred_rank(st, k);
+  if (rank == 0) {
+    const uint32_t* keys = dyn;
+    auto key_at = [=](int64_t i) { return keys[i]; };
+    SelectThreshold<uint32_t> th;
+    uint32_t key2;
+    radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+    if (threadIdx.x == 0) {
+      csh.prefix = th.prefix;
+      csh.pmask = th.pmask;
+      csh.n_gt = th.n_gt;
+      csh.need_eq = th.need_eq;
+      csh.key2 = key2;
+    }
+  }
+  cluster.sync();
+  const long long c2 = clock64();
+  SelectThreshold<uint32_t> th;
+  {
+    const ClusterShared* o = cluster.map_shared_rank(&csh, 0);
+    th.prefix = o->prefix;
+    th.pmask = o->pmask;
+    th.n_gt = o->n_gt;
+    th.need_eq = o->need_eq;
+  }
+  const uint32_t key2 = cluster.map_shared_rank(&csh, 0)->key2;
+  // 4. ordered compaction of the own range with the carried counts of the lower ranks
+  uint32_t lgt = 0, leq = 0;
+  for (uint32_t i = threadIdx.x; i < mr; i += SEL_NT) {
+    const uint32_t key = Key<float>::of(sv[i]);
+    const uint32_t hk = key & th.pmask;
+    if (key != 0u) {
+      lgt += hk > th.prefix ? 1u : 0u;
+      leq += hk == th.prefix ? 1u : 0u;
+    }
+  }
+  lgt = block_sum(lgt, cs.sm);
+  leq = block_sum(leq, cs.sm);
+  if (threadIdx.x == 0) {
+    csh.gt = lgt;
+    csh.eq = leq;
+  }
+  cluster.sync();
+  uint32_t cg0 = 0, ce0 = 0;
+  for (int q = 0; q < rank; ++q) {
+    const ClusterShared* o = cluster.map_shared_rank(&csh, q);
+    cg0 += o->gt;
+    ce0 += o->eq;
+  }
+  float* data = r + L.offset;
+  int32_t* oidx = idx_out + L.slot;
+  float* oval = val_out + L.slot;
+  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
+    *x = sv[i];
+    *key = Key<float>::of(*x);
+    *ix = si[i];
+  };
+  auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
+    oidx[pos] = static_cast<int32_t>(ix);
+    oval[pos] = x;
+    data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+  };
+  const uint32_t first = cg0 + min(ce0, th.need_eq);
+  const uint32_t end = ordered_compact<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0);
+  if (vupd) apply_single_rank_updates(vupd + L.offset, oidx + first, oval + first, end - first);
+  const long long c3 = clock64();
+  if (rank == CLUSTER - 1 && threadIdx.x == 0) count_out[j] = static_cast<int32_t>(end);
+  if (rank == 0 && threadIdx.x == 0) {
+    auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
+    FastState ns = candidate_state(st, next_threshold(st, m, k, k2, th.prefix, key2), m, k,
+                                   q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22));
+    ns.cycles = static_cast<uint32_t>(clock64() - t_begin);
+    ns.path = 3u;
+    ns.t_start = t_start;
+    ns.t_end = globaltimer_lo();
+    ns.t_launch = t_launch;
+    state[j] = ns;
+  }
+  cluster.sync();  // no CTA leaves while others may still read its shared memory
+}
+
+}  // namespace lags

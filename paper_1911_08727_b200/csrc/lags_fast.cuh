@@ -357,6 +357,37 @@ __device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t 
   *key2_out = prefix[1];
 }
 
+// Next candidate threshold: the k2-th largest candidate key, or, when fewer candidates were seen,
+// an extrapolation below the current threshold from the observed candidate density.
+__device__ __forceinline__ uint32_t next_threshold(const FastState& st, uint32_t m, uint32_t k, uint32_t k2,
+                                                   uint32_t th_prefix, uint32_t key2) {
+  if (m >= k2) return key2;
+  if (st.thr <= 1u) return st.thr;
+  const uint32_t T = max(th_prefix, st.thr);
+  const double density = (static_cast<double>(m - min(m, k)) + 1.0) / (static_cast<double>(T - st.thr) + 1.0);
+  double step = (static_cast<double>(k2) - m) / density;
+  step = fmin(fmax(step, 64.0), 4.0 * (static_cast<double>(T - st.thr) + (1 << 16)));
+  return st.thr > step ? st.thr - static_cast<uint32_t>(step) : 1u;
+}
+
+// State after a candidate-path selection; the rank factor gets feedback: the threshold set last
+// call (rank pf*k) produced m candidates now, steer the next toward PRED_TARGET * k (geometric
+// mean of the old and the corrected factor).
+__device__ __forceinline__ FastState candidate_state(const FastState& st, uint32_t pred, uint32_t m, uint32_t k,
+                                                     uint32_t phases) {
+  FastState ns = st;
+  ns.thr = max(pred, 1u);
+  ns.last_cands = m;
+  ns.calls += 1;
+  ns.reserved = phases;
+  if (m > 0) {
+    const float pf = pred_factor(st);
+    const float corrected = pf * PRED_TARGET * static_cast<float>(k) / static_cast<float>(m);
+    ns.pf256 = pf_encode(sqrtf(pf * fmaxf(corrected, 0.25f)));
+  }
+  return ns;
+}
+
 // Candidate path of one big layer inside one CTA.  Returns 0 on success, or why the candidate set
 // cannot be proven to hold the top-k (FB_TOO_FEW / FB_OVERFLOW); the caller then queues the layer
 // for the grid-wide dense path.  Candidates are gathered once into shared memory (value + index,
@@ -465,32 +496,10 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     const long long c3 = clock64();
     auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
     phases = q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22);
-    // next threshold: the k2-th largest candidate key, or, when fewer candidates were seen, an
-    // extrapolation below the current threshold from the observed candidate density
-    if (m >= k2) {
-      pred = key2;
-    } else if (st.thr > 1u) {
-      const uint32_t T = max(th.prefix, st.thr);
-      const double density = (static_cast<double>(m - min(m, k)) + 1.0) / (static_cast<double>(T - st.thr) + 1.0);
-      double step = (static_cast<double>(k2) - m) / density;
-      step = fmin(fmax(step, 64.0), 4.0 * (static_cast<double>(T - st.thr) + (1 << 16)));
-      pred = st.thr > step ? st.thr - static_cast<uint32_t>(step) : 1u;
-    }
+    pred = next_threshold(st, m, k, k2, th.prefix, key2);
   }
   if (threadIdx.x == 0) {
-    FastState ns = st;
-    ns.thr = max(pred, 1u);
-    ns.last_cands = m;
-    ns.calls += 1;
-    ns.reserved = phases;
-    // feedback on the rank factor: the threshold set last call (rank pf*k) produced m candidates
-    // now; steer the next one toward PRED_TARGET * k (geometric mean of old and corrected factor)
-    if (m > 0) {
-      const float pf = pred_factor(st);
-      const float corrected = pf * PRED_TARGET * static_cast<float>(k) / static_cast<float>(m);
-      ns.pf256 = pf_encode(sqrtf(pf * fmaxf(corrected, 0.25f)));
-    }
-    state[j] = ns;
+    state[j] = candidate_state(st, pred, m, k, phases);
     count_out[j] = static_cast<int32_t>(cnt);
   }
   __syncthreads();

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "lags_common.cuh"
+#include "lags_cluster.cuh"
 #include "lags_fast.cuh"
 #include "lags_select.cuh"
 
@@ -326,35 +327,12 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   return LAGS_OK;
 }
 
-// Split the layers into (at most) two pipeline groups so the selection of group 0 overlaps the
-// streaming of group 1: T = K1(G0) + max(K2(G0), K1(G1)) + K2(G1), with K1 ~ bytes and K2 ~ the
-// slowest layer's selection (one CTA per layer).  Returns group ids per layer (0/1).
+// Selection groups of an fp32 bucket: 0 = one CTA per layer (select_phase1_kernel), 1 = the
+// largest layers, one thread-block cluster per layer (select_cluster_kernel, run concurrently on
+// the bucket's side stream).
 std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
-  auto k1 = [](double elems) { return elems > 0 ? 3e-6 + 1.8e-12 * elems : 0.0; };  // ~12 B/elem at ~6.5 TB/s
-  auto k2 = [&](int j) {
-    return dims[j] <= SMALL_LAYER ? 2e-6 + 4e-10 * static_cast<double>(dims[j]) : 4e-6 + 6e-9 * ks[j];
-  };
-  std::vector<int> by_cost(L);
-  for (int j = 0; j < L; ++j) by_cost[j] = j;
-  std::stable_sort(by_cost.begin(), by_cost.end(), [&](int a, int c) { return k2(a) > k2(c); });
-  double total = 0;
-  for (int j = 0; j < L; ++j) total += static_cast<double>(dims[j]);
-  const double single = k1(total) + k2(by_cost[0]) + 3e-6;
-  double best = single, e0 = 0;
-  int best_s = 0;
-  for (int s = 1; s < L; ++s) {  // group 0 = the s layers with the heaviest selection
-    e0 += static_cast<double>(dims[by_cost[s - 1]]);
-    const double t = k1(e0) + std::max(k2(by_cost[0]) + 3e-6, k1(total - e0)) + k2(by_cost[s]) + 3e-6;
-    if (t < best) {
-      best = t;
-      best_s = s;
-    }
-  }
   std::vector<int> gid(L, 0);
-  // Measured on B200 (ResNet-50 shapes): the 1024-thread / ~200 KB selection CTAs cannot share an
-  // SM with K1's CTAs, so a modest modelled gain does not materialise; split only for large ones.
-  if (best_s > 0 && best < 0.8 * single)
-    for (int s = best_s; s < L; ++s) gid[by_cost[s]] = 1;
+  for (int j = 0; j < L; ++j) gid[j] = (dims[j] > SMALL_LAYER && ks[j] >= CLUSTER_MIN_K) ? 1 : 0;
   return gid;
 }
 
@@ -503,9 +481,11 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   if (dtype == LAGS_F32) {
     const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
     if (cudaFuncSetAttribute(select_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess) {
+            cudaSuccess ||
+        cudaFuncSetAttribute(select_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess) {
       delete b;
-      return cuda_check("select_phase1_kernel attributes", 0);
+      return cuda_check("select kernel attributes", 0);
     }
     b->smem_keys = SMEM_KEYS;
     if (b->ngroups == 2 &&
@@ -577,23 +557,30 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     };
     cudaError_t e = cudaSuccess;
     int launches = 2;
-    if (b->ngroups == 1) {
-      if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
-      if (e == cudaSuccess) e = k1(b->grp[0], s);
-      if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
-      if (e == cudaSuccess) e = k2(b->grp[0], s);
-    } else {
-      // pipeline: select group 0 on the side stream while K1 streams group 1
-      e = k1(b->grp[0], s);
+    lags_bucket::Group all = b->grp[0];  // K1 streams every task (group 0's then group 1's)
+    all.task_base = 0;
+    all.ntasks = b->grp[0].ntasks + b->grp[1].ntasks;
+    if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
+    if (e == cudaSuccess) e = k1(all, s);
+    if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
+    if (b->ngroups == 2) {
+      // the largest layers: one 4-CTA cluster each, on the side stream, concurrently with the
+      // one-CTA-per-layer selection of the others
       if (e == cudaSuccess) e = cudaEventRecord(b->ev_fork, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(b->side, b->ev_fork, 0);
-      if (e == cudaSuccess) e = k2(b->grp[0], b->side);
+      if (e == cudaSuccess) {
+        const lags_bucket::Group& G = b->grp[1];
+        select_cluster_kernel<<<G.nlayers * CLUSTER, SEL_NT, static_cast<size_t>(b->smem_keys) * sizeof(uint32_t),
+                                b->side>>>(b->layers, b->layer_tasks, b->order + G.order_base, b->state, b->cand_cnt,
+                                           b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt,
+                                           b->smem_keys, fe, vu);
+        e = cudaGetLastError();
+      }
       if (e == cudaSuccess) e = cudaEventRecord(b->ev_join, b->side);
-      if (e == cudaSuccess) e = k1(b->grp[1], s);
-      if (e == cudaSuccess) e = k2(b->grp[1], s);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, b->ev_join, 0);
-      launches = 4;
+      launches = 3;
     }
+    if (e == cudaSuccess) e = k2(b->grp[0], s);
+    if (b->ngroups == 2 && e == cudaSuccess) e = cudaStreamWaitEvent(s, b->ev_join, 0);
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
     return cuda_check("lags_bucket_compress(f32)", launches);
   }

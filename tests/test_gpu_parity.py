@@ -271,8 +271,8 @@ def test_step_local_equals_compress_plus_decode(L):
     call, the candidate path and a forced misprediction."""
     from paper_1911_08727_b200 import _native as N
 
-    dims = [300000, 64, 16000, 70001, 9]
-    ks = [300, 64, 16, 70, 1]
+    dims = [300000, 64, 1000003, 16000, 70001, 9]  # 1000003 / k=1000 -> thread-block-cluster path
+    ks = [300, 64, 1000, 16, 70, 1]
     a, b = L.Bucket(dims, ks, N.F32), L.Bucket(dims, ks, N.F32)
     n = sum(dims)
     gen = torch.Generator(device="cuda").manual_seed(21)
