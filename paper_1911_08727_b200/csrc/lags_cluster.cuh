@@ -37,7 +37,8 @@ __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(SEL_NT, 1) sel
   __shared__ CoopSmem cs;
   __shared__ ClusterShared csh;
   const uint32_t t_launch = globaltimer_lo();
-  griddep_wait();
+  griddep_wait();                // K1 has completed and its writes are visible
+  griddep_launch_dependents();   // the per-layer selection kernel may start alongside
   const uint32_t t_start = globaltimer_lo();
   const long long t_begin = clock64();
   const int rank = static_cast<int>(cluster.block_rank());

@@ -42,6 +42,10 @@ __device__ __forceinline__ double accum(double r, double g, double a) { return _
 // Programmatic dependent launch (sm_90+): wait until the preceding kernel on the stream has
 // completed and its memory is visible.  A no-op for kernels launched without the attribute.
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Allow the next kernel on the stream (launched with PDL) to be scheduled now.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ bool nonfinite(float g) { return (__float_as_uint(g) & 0x7f800000u) == 0x7f800000u; }
 __device__ __forceinline__ bool nonfinite(double g) {

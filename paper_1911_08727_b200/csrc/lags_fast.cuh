@@ -560,11 +560,16 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
     FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
     const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
-    float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc, float* vupd) {
+    float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc, float* vupd,
+    int after_cluster) {
   extern __shared__ uint32_t skeys[];
   __shared__ CoopSmem cs;
   const uint32_t t_launch = globaltimer_lo();
-  griddep_wait();  // programmatic dependent launch: K1's results are visible after this
+  // programmatic dependent launch.  Directly after K1: wait for it here.  After the cluster
+  // kernel (which waited on K1 before triggering this launch): K1's writes are already visible;
+  // wait on the cluster kernel only at the end, so the next kernel on the stream (waiting on this
+  // one) is also ordered after the cluster kernel.
+  if (!after_cluster) griddep_wait();
   const uint32_t t_start = globaltimer_lo();
   const int j = order[blockIdx.x];
   const lags_layer_t L = layers[j];
@@ -602,6 +607,7 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     state[j].t_end = globaltimer_lo();
     state[j].t_launch = t_launch;
   }
+  if (after_cluster) griddep_wait();
 }
 
 }  // namespace lags

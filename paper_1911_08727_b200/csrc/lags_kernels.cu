@@ -553,7 +553,7 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       return launch_pdl(select_phase1_kernel, dim3(G.nlayers), dim3(SEL_NT),
                         static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), st, b->layers, b->layer_tasks,
                         b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
-                        b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu);
+                        b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu, b->ngroups == 2 ? 1 : 0);
     };
     cudaError_t e = cudaSuccess;
     int launches = 2;
@@ -563,24 +563,17 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
     if (e == cudaSuccess) e = k1(all, s);
     if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
-    if (b->ngroups == 2) {
-      // the largest layers: one 4-CTA cluster each, on the side stream, concurrently with the
-      // one-CTA-per-layer selection of the others
-      if (e == cudaSuccess) e = cudaEventRecord(b->ev_fork, s);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(b->side, b->ev_fork, 0);
-      if (e == cudaSuccess) {
-        const lags_bucket::Group& G = b->grp[1];
-        select_cluster_kernel<<<G.nlayers * CLUSTER, SEL_NT, static_cast<size_t>(b->smem_keys) * sizeof(uint32_t),
-                                b->side>>>(b->layers, b->layer_tasks, b->order + G.order_base, b->state, b->cand_cnt,
-                                           b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt,
-                                           b->smem_keys, fe, vu);
-        e = cudaGetLastError();
-      }
-      if (e == cudaSuccess) e = cudaEventRecord(b->ev_join, b->side);
+    if (b->ngroups == 2 && e == cudaSuccess) {
+      // the largest layers: one 4-CTA cluster each; it waits on K1, then triggers the launch of
+      // the per-layer selection of the other layers, which runs alongside (PDL, same stream)
+      const lags_bucket::Group& G = b->grp[1];
+      e = launch_pdl(select_cluster_kernel, dim3(G.nlayers * CLUSTER), dim3(SEL_NT),
+                     static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), s, b->layers, b->layer_tasks,
+                     b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
+                     b->gval, rr, idx, vals, cnt, b->smem_keys, fe, vu);
       launches = 3;
     }
     if (e == cudaSuccess) e = k2(b->grp[0], s);
-    if (b->ngroups == 2 && e == cudaSuccess) e = cudaStreamWaitEvent(s, b->ev_join, 0);
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
     return cuda_check("lags_bucket_compress(f32)", launches);
   }
