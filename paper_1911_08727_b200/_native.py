@@ -11,7 +11,10 @@ import os
 
 from .errors import StructureError
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liblagsb200.so")
+# LAGS_B200_LIB: an alternative build of the same library (kernel variants under study); the
+# default is the in-tree build
+_LIB_PATH = os.environ.get("LAGS_B200_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "liblagsb200.so")
 
 F32, F64, F32_ACC64 = 0, 1, 2
 STATUS_NONFINITE = 0x1

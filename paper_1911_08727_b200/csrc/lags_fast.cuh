@@ -70,10 +70,11 @@ __device__ __forceinline__ uint32_t pf_encode(float pf) {
   return static_cast<uint32_t>(fminf(fmaxf(pf, 1.25f), 8.0f) * 256.0f);
 }
 
-// Queue of layers for the dense fallback (device memory of the bucket).
+// Per-call counters of the selection kernel (device memory of the bucket, two words, both reset
+// by the next call's accum_emit_kernel).
 struct CoopScratch {
-  uint32_t* fb_count;  // [1] queued layers (reset by the next call's accum_emit_kernel)
-  int32_t* fb_list;    // [nlayers] layer | reason << 24
+  uint32_t* fb_count;  // layers that took the dense exact path this call (diagnostic)
+  uint32_t* work;      // next position of the LPT layer list to hand out (persistent CTAs)
 };
 
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
@@ -116,7 +117,10 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
   griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
-  if (wid == 0 && lane == 0) *fb_count = 0u;  // the previous call's fallback kernel has completed
+  if (wid == 0 && lane == 0) {  // the previous call's selection kernel has completed
+    fb_count[0] = 0u;
+    fb_count[1] = 0u;
+  }
   if (wid >= ntasks) return;
   const Task T = tasks[wid];
   const int64_t loff = layers[T.layer].offset;
@@ -552,60 +556,69 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
   }
 }
 
-// Phase 1: one CTA per layer (largest selection work first).  Big layers take the candidate path
-// when it provably holds the top-k; otherwise they are queued for select_fallback_kernel.  Small
-// layers run the dense exact path staged in shared memory.  An ordinary launch (not cooperative),
-// so the selection overlaps backprop kernels running on other streams.
+// Per-layer selection: persistent CTAs walk the layer list (largest estimated selection work
+// first); the first layer of a CTA is its block index, the following ones are handed out by an
+// atomic counter, so a grid no larger than the free SMs runs the list in one wave, balanced
+// dynamically (longest-processing-time first).  Big layers take the candidate path when it
+// provably holds the top-k, otherwise the dense exact path in the same CTA; small layers run the
+// dense exact path staged in shared memory.  An ordinary launch (not cooperative), so the
+// selection overlaps backprop kernels running on other streams.
 __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
-    FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
+    int nl, FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
     const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
     float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc, float* vupd,
     int after_cluster) {
   extern __shared__ uint32_t skeys[];
   __shared__ CoopSmem cs;
+  __shared__ int next_pos;
   const uint32_t t_launch = globaltimer_lo();
   // programmatic dependent launch.  Directly after K1: wait for it here.  After the cluster
   // kernel (which waited on K1 before triggering this launch): K1's writes are already visible;
   // wait on the cluster kernel only at the end, so the next kernel on the stream (waiting on this
   // one) is also ordered after the cluster kernel.
   if (!after_cluster) griddep_wait();
-  const uint32_t t_start = globaltimer_lo();
-  const int j = order[blockIdx.x];
-  const lags_layer_t L = layers[j];
-  const FastState st = state[j];
-  const long long t_begin = clock64();
-  uint32_t path;
-  if (L.dim <= SMALL_LAYER) {  // SMALL_LAYER <= shared-memory staging capacity
-    const uint32_t cnt = small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
-                                            val_out + L.slot, reinterpret_cast<float*>(skeys), cs,
-                                            vupd ? vupd + L.offset : nullptr);
+  for (int pos = blockIdx.x; pos < nl;) {
+    const uint32_t t_start = globaltimer_lo();
+    const int j = order[pos];
+    const lags_layer_t L = layers[j];
+    const FastState st = state[j];
+    const long long t_begin = clock64();
+    if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + static_cast<int>(gridDim.x);
+    uint32_t path;
+    if (L.dim <= SMALL_LAYER) {  // SMALL_LAYER <= shared-memory staging capacity
+      const uint32_t cnt = small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
+                                              val_out + L.slot, reinterpret_cast<float*>(skeys), cs,
+                                              vupd ? vupd + L.offset : nullptr);
+      if (threadIdx.x == 0) {
+        count_out[j] = static_cast<int32_t>(cnt);
+        FastState ns = st;
+        ns.calls += 1;
+        state[j] = ns;
+      }
+      path = 0u;
+    } else {
+      const int why = (force_exact || st.thr == 0u)
+                          ? FB_TOO_FEW
+                          : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval,
+                                             r, idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
+      if (why) {  // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA
+        if (threadIdx.x == 0) atomicAdd(sc.fb_count, 1u);  // diagnostic count of dense layers this call
+        __syncthreads();
+        dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
+      }
+      path = why ? 2u : 1u;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      count_out[j] = static_cast<int32_t>(cnt);
-      FastState ns = st;
-      ns.calls += 1;
-      state[j] = ns;
+      state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
+      state[j].path = path;
+      state[j].t_start = t_start;
+      state[j].t_end = globaltimer_lo();
+      state[j].t_launch = t_launch;
     }
-    path = 0u;
-  } else {
-    const int why = (force_exact || st.thr == 0u)
-                        ? FB_TOO_FEW
-                        : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval,
-                                           r, idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
-    if (why) {  // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA
-      if (threadIdx.x == 0) atomicAdd(sc.fb_count, 1u);  // diagnostic count of dense layers this call
-      __syncthreads();
-      dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
-    }
-    path = why ? 2u : 1u;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
-    state[j].path = path;
-    state[j].t_start = t_start;
-    state[j].t_end = globaltimer_lo();
-    state[j].t_launch = t_launch;
+    pos = next_pos;
+    __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
   }
   if (after_cluster) griddep_wait();
 }

@@ -213,12 +213,10 @@ struct lags_bucket {
   struct Group {
     int task_base = 0, ntasks = 0;    // contiguous range of the task table
     int order_base = 0, nlayers = 0;  // contiguous range of `order`
-    int n_big = 1;                    // fallback grid (layers that can be queued)
-    CoopScratch q{};                  // fallback queue of the group
   };
   int ngroups = 1;
   Group grp[2];
-  CoopScratch coop{};  // storage of both groups' fallback queues
+  CoopScratch coop{};  // per-call selection counters
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t probe_before = nullptr, probe_after = nullptr;  // caller-owned, optional
@@ -276,7 +274,7 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_fbl = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, bytes = 0;
 };
 
 int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, int32_t max_world, Plan* p) {
@@ -321,8 +319,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
   p->o_order = take(sizeof(int32_t) * L);
   const bool f32 = dtype == LAGS_F32;
-  p->o_fbc = take(f32 ? 2 * sizeof(uint32_t) : 0);     // one fallback queue per pipeline group
-  p->o_fbl = take(f32 ? 2 * sizeof(int32_t) * L : 0);
+  p->o_fbc = take(f32 ? 2 * sizeof(uint32_t) : 0);  // selection counters (CoopScratch)
   p->bytes = o;
   return LAGS_OK;
 }
@@ -402,7 +399,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->planes = base + p.o_planes;
   b->order = reinterpret_cast<int32_t*>(base + p.o_order);
   b->coop.fb_count = reinterpret_cast<uint32_t*>(base + p.o_fbc);
-  b->coop.fb_list = reinterpret_cast<int32_t*>(base + p.o_fbl);
+  b->coop.work = b->coop.fb_count + 1;
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -443,16 +440,11 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   for (int g = 0; g < 2; ++g) {
     b->grp[g].order_base = static_cast<int>(order.size());
     std::vector<int32_t> og;
-    int nbig = 0;
     for (int j = 0; j < nlayers; ++j)
-      if (gid[j] == g) {
-        og.push_back(j);
-        nbig += dims[j] > SMALL_LAYER ? 1 : 0;
-      }
+      if (gid[j] == g) og.push_back(j);
     std::stable_sort(og.begin(), og.end(), [&](int a, int c) { return cost[a] > cost[c]; });
     order.insert(order.end(), og.begin(), og.end());
     b->grp[g].nlayers = static_cast<int>(og.size());
-    b->grp[g].n_big = std::max(nbig, 1);
   }
   b->ngroups = b->grp[1].nlayers > 0 ? 2 : 1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -473,10 +465,6 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   if (!ok) {
     delete b;
     return cuda_check("lags_bucket_create upload", 0);
-  }
-  for (int g = 0; g < 2; ++g) {
-    b->grp[g].q.fb_count = b->coop.fb_count + g;
-    b->grp[g].q.fb_list = b->coop.fb_list + static_cast<size_t>(g) * nlayers;
   }
   if (dtype == LAGS_F32) {
     const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
@@ -541,19 +529,22 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       if (zg)
         return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                           G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
-                          b->cand_cnt + G.task_base, status, G.q.fb_count);
+                          b->cand_cnt + G.task_base, status, b->coop.fb_count);
       return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                         G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
-                        b->cand_cnt + G.task_base, status, G.q.fb_count);
+                        b->cand_cnt + G.task_base, status, b->coop.fb_count);
     };
     // K2 over one group's layers (a layer whose candidates fail the proof runs the dense path in
     // its own CTA)
     auto k2 = [&](const lags_bucket::Group& G, cudaStream_t st) -> cudaError_t {
       if (G.nlayers == 0) return cudaSuccess;
-      return launch_pdl(select_phase1_kernel, dim3(G.nlayers), dim3(SEL_NT),
+      // persistent CTAs: one wave on the SMs the cluster kernel leaves free (1 CTA per SM)
+      const int busy = b->ngroups == 2 ? b->grp[1].nlayers * CLUSTER : 0;
+      const int grid = std::min(G.nlayers, std::max(num_sms() - busy, num_sms() / 2));
+      return launch_pdl(select_phase1_kernel, dim3(grid), dim3(SEL_NT),
                         static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), st, b->layers, b->layer_tasks,
-                        b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
-                        b->gval, rr, idx, vals, cnt, b->smem_keys, fe, G.q, vu, b->ngroups == 2 ? 1 : 0);
+                        b->order + G.order_base, G.nlayers, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap,
+                        b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->coop, vu, b->ngroups == 2 ? 1 : 0);
     };
     cudaError_t e = cudaSuccess;
     int launches = 2;

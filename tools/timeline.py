@@ -93,6 +93,16 @@ def main():
     print("  start after griddep wait: min %.2f max %.2f" % (min(start), max(start)))
     ph = lambda w: (int(w) & 2047, (int(w) >> 11) & 2047, (int(w) >> 22) & 2047)  # noqa: E731
     print("  phases x64 cycles (gather, select, compact) of the slowest:", [ph(s[j, 7]) for j in rows[:6]])
+    names = {0: "small-dense", 1: "candidate", 2: "dense-fallback", 3: "cluster"}
+    for p in sorted(set(int(x) for x in s[:, 5])):
+        js = [j for j in range(len(dims)) if s[j, 5] == p]
+        du = np.array([end[j] - start[j] for j in js])
+        big = max(js, key=lambda j: dims[j])
+        print(f"  path {names.get(p, p)}: {len(js)} layers, us per layer median {np.median(du):.2f} max {du.max():.2f}"
+              f" sum {du.sum():.1f}; largest dim {dims[big]} took {end[big] - start[big]:.2f}")
+        if p in (1, 3):
+            print("    phases of the 4 largest:",
+                  [(dims[j], ph(s[j, 7])) for j in sorted(js, key=lambda j: -dims[j])[:4]])
 
 
 if __name__ == "__main__":
