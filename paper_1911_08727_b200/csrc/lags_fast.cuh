@@ -19,10 +19,16 @@
 
 namespace lags {
 
-constexpr int TASK_ELEMS = 8192;   // elements per K1 task (one warp)
+#ifndef LAGS_TASK_ELEMS
+#define LAGS_TASK_ELEMS 8192
+#endif
+#ifndef LAGS_K1_UNROLL
+#define LAGS_K1_UNROLL 4
+#endif
+constexpr int TASK_ELEMS = LAGS_TASK_ELEMS;  // elements per streaming task (one warp)
 constexpr int SMALL_LAYER = 16384; // layers up to this size always take the dense exact path
 constexpr int K1_WARPS = 8;        // warps per K1 CTA
-constexpr int K1_UNROLL = 4;       // float4 loads in flight per lane per operand
+constexpr int K1_UNROLL = LAGS_K1_UNROLL;        // float4 loads in flight per lane per operand (K1)
 constexpr int PRED_FACTOR = 3;     // predicted threshold targets PRED_FACTOR * k candidates
 constexpr int F32_PASSES = 3;      // radix passes for 31-bit keys with 11-bit digits
 constexpr int F32_BINS = 1 << Key<float>::RB;
@@ -70,11 +76,10 @@ __device__ __forceinline__ uint32_t pf_encode(float pf) {
   return static_cast<uint32_t>(fminf(fmaxf(pf, 1.25f), 8.0f) * 256.0f);
 }
 
-// Per-call counters of the selection kernel (device memory of the bucket, two words, both reset
-// by the next call's accum_emit_kernel).
+// Per-call counter of the selection kernel (device memory of the bucket, reset by the next
+// call's accum_emit_kernel): next position of the LPT layer list to hand out (persistent CTAs).
 struct CoopScratch {
-  uint32_t* fb_count;  // layers that took the dense exact path this call (diagnostic)
-  uint32_t* work;      // next position of the LPT layer list to hand out (persistent CTAs)
+  uint32_t* work;
 };
 
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
@@ -87,9 +92,10 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
 }
 
 // Append this lane's candidate bits (ascending element order within the lane, lanes in index
-// order) to the task list.  Warp-collective.
-__device__ __forceinline__ void emit_candidates(uint32_t bits, const float* vals, int64_t local0, int lane,
-                                                uint32_t& cnt, int32_t* cidx, float* cval, int cap) {
+// order) to the task list.  Warp-collective.  The lane's (up to 4) values come by value: a
+// dynamically indexed array would live in local memory.
+__device__ __forceinline__ void emit_candidates(uint32_t bits, float4 vals, int64_t local0, int lane, uint32_t& cnt,
+                                                int32_t* cidx, float* cval, int cap) {
   if (__ballot_sync(0xffffffffu, bits != 0) == 0u) return;
   const uint32_t c = __popc(bits);
   const uint32_t inc = warp_inclusive_scan(c, lane);
@@ -98,7 +104,7 @@ __device__ __forceinline__ void emit_candidates(uint32_t bits, const float* vals
     const int b = __ffs(bits) - 1;
     if (pos < static_cast<uint32_t>(cap)) {
       cidx[pos] = static_cast<int32_t>(local0 + b);
-      cval[pos] = vals[b];
+      cval[pos] = b == 0 ? vals.x : b == 1 ? vals.y : b == 2 ? vals.z : vals.w;
     }
     ++pos;
     bits &= bits - 1;
@@ -106,28 +112,22 @@ __device__ __forceinline__ void emit_candidates(uint32_t bits, const float* vals
   cnt += __shfl_sync(0xffffffffu, inc, 31);
 }
 
+// One task of the streaming pass, by one warp (warp-collective): acc = r + alpha * g written back
+// into r, the non-finite flag, and the task's candidate list (entries with key(acc) >= thr[layer],
+// ascending index order) with its count in cand_cnt[tid].
 // ZERO_G: also clear the gradient after reading it (the optimizer's zero_grad fused into the pass;
 // +4 B/element of writes instead of a separate memset pass).
-template <bool ZERO_G>
-__global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
-    const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
-    const FastState* __restrict__ state, float* __restrict__ g, float* __restrict__ r, float alpha, int cap,
-    int32_t* __restrict__ cand_idx, float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
-    uint32_t* status, uint32_t* fb_count) {
-  const int lane = threadIdx.x & 31;
-  const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
-  griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
-  if (wid == 0 && lane == 0) {  // the previous call's selection kernel has completed
-    fb_count[0] = 0u;
-    fb_count[1] = 0u;
-  }
-  if (wid >= ntasks) return;
-  const Task T = tasks[wid];
+template <bool ZERO_G, int UNROLL>
+__device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, const lags_layer_t* __restrict__ layers,
+                                            const FastState* state, float* __restrict__ g, float* __restrict__ r,
+                                            float alpha, int cap, int32_t* __restrict__ cand_idx,
+                                            float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
+                                            uint32_t* status) {
   const int64_t loff = layers[T.layer].offset;
   const uint32_t thr0 = state[T.layer].thr;
   const uint32_t thr = thr0 ? thr0 : 0xffffffffu;
-  int32_t* cidx = cand_idx + static_cast<int64_t>(wid) * cap;
-  float* cval = cand_val + static_cast<int64_t>(wid) * cap;
+  int32_t* cidx = cand_idx + static_cast<int64_t>(tid) * cap;
+  float* cval = cand_val + static_cast<int64_t>(tid) * cap;
   uint32_t cnt = 0;
   bool bad = false;
   const int64_t s = T.start, e = T.start + T.len;
@@ -144,16 +144,16 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
       r[s + lane] = a;
       bits = (Key<float>::of(a) >= thr) ? 1u : 0u;
     }
-    emit_candidates(bits, &a, s + lane - loff, lane, cnt, cidx, cval, cap);
+    emit_candidates(bits, make_float4(a, a, a, a), s + lane - loff, lane, cnt, cidx, cval, cap);
   }
   const int64_t vb = s + h;
   const int64_t n4 = (e - vb) >> 2;
   float4* g4 = reinterpret_cast<float4*>(g + vb);
   float4* r4 = reinterpret_cast<float4*>(r + vb);
-  for (int64_t q0 = 0; q0 < n4; q0 += 32 * K1_UNROLL) {
-    float4 gv[K1_UNROLL], rv[K1_UNROLL];
+  for (int64_t q0 = 0; q0 < n4; q0 += 32 * UNROLL) {
+    float4 gv[UNROLL], rv[UNROLL];
 #pragma unroll
-    for (int u = 0; u < K1_UNROLL; ++u) {
+    for (int u = 0; u < UNROLL; ++u) {
       const int64_t q = q0 + u * 32 + lane;
       if (q < n4) {
         gv[u] = __ldcs(g4 + q);
@@ -162,25 +162,25 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     }
     if (ZERO_G) {
 #pragma unroll
-      for (int u = 0; u < K1_UNROLL; ++u) {
+      for (int u = 0; u < UNROLL; ++u) {
         const int64_t q = q0 + u * 32 + lane;
         if (q < n4) __stcs(g4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
       }
     }
 #pragma unroll
-    for (int u = 0; u < K1_UNROLL; ++u) {
+    for (int u = 0; u < UNROLL; ++u) {
       const int64_t q = q0 + u * 32 + lane;
       uint32_t bits = 0;
-      float a[4] = {0.f, 0.f, 0.f, 0.f};
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
       if (q < n4) {
         bad |= nonfinite(gv[u].x) | nonfinite(gv[u].y) | nonfinite(gv[u].z) | nonfinite(gv[u].w);
-        a[0] = accum(rv[u].x, gv[u].x, alpha);
-        a[1] = accum(rv[u].y, gv[u].y, alpha);
-        a[2] = accum(rv[u].z, gv[u].z, alpha);
-        a[3] = accum(rv[u].w, gv[u].w, alpha);
-        r4[q] = make_float4(a[0], a[1], a[2], a[3]);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) bits |= (Key<float>::of(a[c]) >= thr ? 1u : 0u) << c;
+        a.x = accum(rv[u].x, gv[u].x, alpha);
+        a.y = accum(rv[u].y, gv[u].y, alpha);
+        a.z = accum(rv[u].z, gv[u].z, alpha);
+        a.w = accum(rv[u].w, gv[u].w, alpha);
+        r4[q] = a;
+        bits = (Key<float>::of(a.x) >= thr ? 1u : 0u) | (Key<float>::of(a.y) >= thr ? 2u : 0u) |
+               (Key<float>::of(a.z) >= thr ? 4u : 0u) | (Key<float>::of(a.w) >= thr ? 8u : 0u);
       }
       if (q0 + u * 32 < n4) emit_candidates(bits, a, vb + 4 * q - loff, lane, cnt, cidx, cval, cap);
     }
@@ -198,10 +198,25 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
       r[t0 + lane] = a;
       bits = (Key<float>::of(a) >= thr) ? 1u : 0u;
     }
-    if (t0 < e) emit_candidates(bits, &a, t0 + lane - loff, lane, cnt, cidx, cval, cap);
+    if (t0 < e) emit_candidates(bits, make_float4(a, a, a, a), t0 + lane - loff, lane, cnt, cidx, cval, cap);
   }
-  if (lane == 0) cand_cnt[wid] = static_cast<int32_t>(cnt);
+  if (lane == 0) cand_cnt[tid] = static_cast<int32_t>(cnt);
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
+}
+
+// K1: one warp per task.
+template <bool ZERO_G>
+__global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
+    const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
+    const FastState* __restrict__ state, float* __restrict__ g, float* __restrict__ r, float alpha, int cap,
+    int32_t* __restrict__ cand_idx, float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
+    uint32_t* status, uint32_t* work) {
+  const int lane = threadIdx.x & 31;
+  const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
+  griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
+  if (wid == 0 && lane == 0) *work = 0u;  // the previous call's selection kernel has completed
+  if (wid >= ntasks) return;
+  stream_task<ZERO_G, K1_UNROLL>(tasks[wid], wid, lane, layers, state, g, r, alpha, cap, cand_idx, cand_val, cand_cnt, status);
 }
 
 // Block-wide sum; all threads get the result.  Uses sm.warp_tot.
@@ -261,7 +276,7 @@ __device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32
     const int64_t n4 = d >> 2;
 #pragma unroll 4
     for (int64_t i = threadIdx.x; i < n4; i += SEL_NT) s4[i] = __ldcg(d4 + i);
-    for (int64_t i = 4 * n4 + threadIdx.x; i < d; i += SEL_NT) sv[i] = data[i];
+    for (int64_t i = 4 * n4 + threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
   } else {
 #pragma unroll 4
     for (int64_t i = threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
@@ -407,7 +422,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
   const uint32_t k = static_cast<uint32_t>(L.k);
   uint32_t local = 0, over = 0;
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
-    const uint32_t c = static_cast<uint32_t>(cand_cnt[t]);
+    const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
     local += min(c, static_cast<uint32_t>(cap));
   }
@@ -431,7 +446,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     uint32_t carry = 0;
     for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
       const int nt = min(SEL_NT, tr.y - t0);
-      const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(cand_cnt[t0 + threadIdx.x]) : 0u;
+      const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)) : 0u;
       uint32_t tot;
       const uint32_t pos = block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
       cs.tpos[threadIdx.x] = pos;
@@ -556,12 +571,51 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
   }
 }
 
+// Selection of layer j by the whole CTA (all paths), with its diagnostic timeline entry.
+__device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks,
+                             FastState* state, const int32_t* cand_cnt, const int32_t* cand_idx, const float* cand_val,
+                             int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
+                             int32_t* count_out, uint32_t* skeys, int smem_keys, int force_exact, CoopSmem& cs,
+                             float* vupd, uint32_t t_launch) {
+  const uint32_t t_start = globaltimer_lo();
+  const lags_layer_t L = layers[j];
+  const FastState st = state[j];
+  const long long t_begin = clock64();
+  uint32_t path;
+  if (L.dim <= SMALL_LAYER) {  // SMALL_LAYER <= shared-memory staging capacity
+    const uint32_t cnt = small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
+                                            val_out + L.slot, reinterpret_cast<float*>(skeys), cs,
+                                            vupd ? vupd + L.offset : nullptr);
+    if (threadIdx.x == 0) {
+      count_out[j] = static_cast<int32_t>(cnt);
+      FastState ns = st;
+      ns.calls += 1;
+      state[j] = ns;
+    }
+    path = 0u;
+  } else {
+    const int why = (force_exact || st.thr == 0u)
+                        ? FB_TOO_FEW
+                        : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
+                                           idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
+    // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA
+    if (why) dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
+    path = why ? 2u : 1u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
+    state[j].path = path;
+    state[j].t_start = t_start;
+    state[j].t_end = globaltimer_lo();
+    state[j].t_launch = t_launch;
+  }
+}
+
 // Per-layer selection: persistent CTAs walk the layer list (largest estimated selection work
 // first); the first layer of a CTA is its block index, the following ones are handed out by an
 // atomic counter, so a grid no larger than the free SMs runs the list in one wave, balanced
-// dynamically (longest-processing-time first).  Big layers take the candidate path when it
-// provably holds the top-k, otherwise the dense exact path in the same CTA; small layers run the
-// dense exact path staged in shared memory.  An ordinary launch (not cooperative), so the
+// dynamically (longest-processing-time first).  An ordinary launch (not cooperative), so the
 // selection overlaps backprop kernels running on other streams.
 __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
     const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
@@ -579,44 +633,9 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
   // one) is also ordered after the cluster kernel.
   if (!after_cluster) griddep_wait();
   for (int pos = blockIdx.x; pos < nl;) {
-    const uint32_t t_start = globaltimer_lo();
-    const int j = order[pos];
-    const lags_layer_t L = layers[j];
-    const FastState st = state[j];
-    const long long t_begin = clock64();
     if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + static_cast<int>(gridDim.x);
-    uint32_t path;
-    if (L.dim <= SMALL_LAYER) {  // SMALL_LAYER <= shared-memory staging capacity
-      const uint32_t cnt = small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
-                                              val_out + L.slot, reinterpret_cast<float*>(skeys), cs,
-                                              vupd ? vupd + L.offset : nullptr);
-      if (threadIdx.x == 0) {
-        count_out[j] = static_cast<int32_t>(cnt);
-        FastState ns = st;
-        ns.calls += 1;
-        state[j] = ns;
-      }
-      path = 0u;
-    } else {
-      const int why = (force_exact || st.thr == 0u)
-                          ? FB_TOO_FEW
-                          : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval,
-                                             r, idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
-      if (why) {  // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA
-        if (threadIdx.x == 0) atomicAdd(sc.fb_count, 1u);  // diagnostic count of dense layers this call
-        __syncthreads();
-        dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
-      }
-      path = why ? 2u : 1u;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
-      state[j].path = path;
-      state[j].t_start = t_start;
-      state[j].t_end = globaltimer_lo();
-      state[j].t_launch = t_launch;
-    }
+    select_layer(order[pos], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out,
+                 val_out, count_out, skeys, smem_keys, force_exact, cs, vupd, t_launch);
     pos = next_pos;
     __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
   }

@@ -1,8 +1,9 @@
 // LAGS-SGD hot path for B200 (sm_100a): accumulate -> select -> compact -> decode/update.
 //
 // Kernels (DESIGN.md has the rooflines):
-//   accum_emit_kernel   (lags_fast.cuh) fp32 fused accumulate + candidate emission   R: training.py:250,174
-//   select_fast_kernel  (lags_fast.cuh) per-layer exact top-k from candidates        R: sparsify.py:84-90
+//   accum_emit_kernel     (lags_fast.cuh) fp32 accumulate + candidate emission (K1)  R: training.py:250,174
+//   select_cluster_kernel (lags_cluster.cuh) largest layers: 4-CTA cluster select    R: sparsify.py:84-90
+//   select_phase1_kernel  (lags_fast.cuh) other layers: persistent per-layer select   R: sparsify.py:84-90
 //   accum_kernel / select_dense_kernel  exact dense path (fp64, mixed, forced exact)  R: training.py:250-252
 //   decode_* kernels    rank-ordered fp64 accumulation + SGD/momentum update          R: training.py:248,253-254
 #include <cuda_runtime.h>
@@ -216,15 +217,8 @@ struct lags_bucket {
   };
   int ngroups = 1;
   Group grp[2];
-  CoopScratch coop{};  // per-call selection counters
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  CoopScratch coop{};  // per-call selection counter (two-kernel path)
   cudaEvent_t probe_before = nullptr, probe_after = nullptr;  // caller-owned, optional
-  ~lags_bucket() {
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (side) cudaStreamDestroy(side);
-  }
 };
 
 namespace {
@@ -319,7 +313,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
   p->o_order = take(sizeof(int32_t) * L);
   const bool f32 = dtype == LAGS_F32;
-  p->o_fbc = take(f32 ? 2 * sizeof(uint32_t) : 0);  // selection counters (CoopScratch)
+  p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (CoopScratch)
   p->bytes = o;
   return LAGS_OK;
 }
@@ -398,8 +392,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->mask = reinterpret_cast<uint32_t*>(base + p.o_mask);
   b->planes = base + p.o_planes;
   b->order = reinterpret_cast<int32_t*>(base + p.o_order);
-  b->coop.fb_count = reinterpret_cast<uint32_t*>(base + p.o_fbc);
-  b->coop.work = b->coop.fb_count + 1;
+  b->coop.work = reinterpret_cast<uint32_t*>(base + p.o_fbc);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -460,7 +453,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
-      (dtype != LAGS_F32 || cudaMemsetAsync(b->coop.fb_count, 0, 2 * sizeof(uint32_t), s) == cudaSuccess) &&
+      (dtype != LAGS_F32 || cudaMemsetAsync(b->coop.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
       cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) {
     delete b;
@@ -476,13 +469,6 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       return cuda_check("select kernel attributes", 0);
     }
     b->smem_keys = SMEM_KEYS;
-    if (b->ngroups == 2 &&
-        (cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking) != cudaSuccess ||
-         cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-         cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
-      delete b;
-      return cuda_check("pipeline stream/events", 0);
-    }
   }
   *out = b;
   return LAGS_OK;
@@ -529,10 +515,10 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       if (zg)
         return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                           G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
-                          b->cand_cnt + G.task_base, status, b->coop.fb_count);
+                          b->cand_cnt + G.task_base, status, b->coop.work);
       return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                         G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
-                        b->cand_cnt + G.task_base, status, b->coop.fb_count);
+                        b->cand_cnt + G.task_base, status, b->coop.work);
     };
     // K2 over one group's layers (a layer whose candidates fail the proof runs the dense path in
     // its own CTA)
