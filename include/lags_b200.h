@@ -132,6 +132,42 @@ int lags_top_k(int32_t dtype, const void* x, int64_t dim, int32_t k, int32_t* id
 int lags_decompress(int32_t dtype, const int32_t* idx, const void* val, const int32_t* count, int64_t dim,
                     void* out, lags_stream_t stream);
 
+/* ---- sparse wire format -- R: sparsify.py:260-310 --------------------------------------------
+ *   chunk   = u32 layer_id, u32 dim, u32 count, count x (u32 index, f64 value)   little-endian, packed
+ *   message = u32 chunk count, then the chunks back to back
+ * A chunk table names the chunks to encode / receives the decoded ones: device arrays layer_ids,
+ * dims, counts and first (the chunk's first entry in idx / val).  A bucket message
+ * (lags_bucket_message_layout) is a chunk table whose first[j] is layer j's slot offset.
+ * Errors are reported in *error (device u64): ~0 = none, else (chunk << 8) | LAGS_WIRE_ERR_*,
+ * the first failing chunk in stream order (the reference raises at the first bad chunk). */
+#define LAGS_WIRE_MESSAGE 0u /* with the u32 chunk-count header (encode_message / decode_message) */
+#define LAGS_WIRE_CHUNK 1u   /* exactly one chunk, no header (encode_chunk / decode_chunk)         */
+
+#define LAGS_WIRE_ERR_TRUNCATED_MESSAGE 1u /* < 4 bytes                  -> StructureError (R: sparsify.py:301-302) */
+#define LAGS_WIRE_ERR_TRUNCATED_HEADER 2u  /* chunk header past the end  -> StructureError (R: sparsify.py:281-282) */
+#define LAGS_WIRE_ERR_TRUNCATED_PAYLOAD 3u /* chunk payload past the end -> StructureError (R: sparsify.py:286-287) */
+#define LAGS_WIRE_ERR_INDEX_RANGE 4u       /* last index >= dim          -> StructureError (R: sparsify.py:48-49)   */
+#define LAGS_WIRE_ERR_INDEX_ORDER 5u       /* not strictly increasing    -> StructureError (R: sparsify.py:50-51)   */
+#define LAGS_WIRE_ERR_TRAILING 6u          /* bytes after the last chunk -> StructureError (R: sparsify.py:308-309) */
+#define LAGS_WIRE_ERR_CAPACITY 7u          /* output / wire buffers too small                                        */
+
+/* Encode nchunks chunks (R: encode_chunk / encode_message, sparsify.py:269-296).  val_dtype
+ * LAGS_F32 or LAGS_F64 (widened exactly to f64).  *wire_len receives the length; nothing is
+ * written (error LAGS_WIRE_ERR_CAPACITY) when it exceeds wire_capacity. */
+int lags_wire_encode(uint32_t mode, int32_t nchunks, const uint32_t* layer_ids, const uint32_t* dims,
+                     const int32_t* counts, const int64_t* first, const int32_t* idx, const void* val,
+                     int32_t val_dtype, void* wire, int64_t wire_capacity, int64_t* wire_len, uint64_t* error,
+                     lags_stream_t stream);
+
+/* Decode wire[offset:wire_len] (R: decode_chunk / decode_message, sparsify.py:279-310) into a
+ * chunk table of at most max_chunks (<= 4096) chunks.  Entries of chunk c go to first[c] with
+ * room caps[c]; with first == NULL they are packed in chunk order into entry_capacity slots.
+ * *end_out = offset after the last decoded chunk (decode_chunk's returned offset). */
+int lags_wire_decode(uint32_t mode, const void* wire, int64_t wire_len, int64_t offset, int32_t max_chunks,
+                     const int64_t* first, const int32_t* caps, int64_t entry_capacity, uint32_t* layer_ids,
+                     uint32_t* dims, int32_t* counts, int32_t* idx, void* val, int32_t val_dtype,
+                     int32_t* nchunks_out, int64_t* end_out, uint64_t* error, lags_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,11 +11,15 @@ from . import _native  # noqa: F401  (raises ImportError when liblagsb200.so is 
 from .engine import Bucket
 from .errors import DivergenceError, StructureError
 from .layered import LayeredVector, LayerShape, concat
-from .sparsify import CompressionPolicy, SparseChunk, decompress, top_k, top_k_device
+from .sparsify import (
+    CompressionPolicy, FusionBuffer, FusionMessage, SparseChunk, decode_chunk, decode_message, decompress, encode_chunk,
+    encode_message, fusion_flush, top_k, top_k_device,
+)
 from .training import StepSizeSchedule, lags_step, slgs_step
 
 __all__ = [
-    "Bucket", "CompressionPolicy", "DivergenceError", "LayeredVector", "LayerShape", "SparseChunk",
-    "StepSizeSchedule", "StructureError", "concat", "decompress", "lags_step", "slgs_step", "top_k", "top_k_device",
+    "Bucket", "CompressionPolicy", "DivergenceError", "FusionBuffer", "FusionMessage", "LayeredVector", "LayerShape",
+    "SparseChunk", "StepSizeSchedule", "StructureError", "concat", "decode_chunk", "decode_message", "decompress",
+    "encode_chunk", "encode_message", "fusion_flush", "lags_step", "slgs_step", "top_k", "top_k_device",
 ]
 __version__ = "0.1.0"

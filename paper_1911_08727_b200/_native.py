@@ -60,6 +60,15 @@ lags_check_finite = _fn("lags_check_finite", C.c_int, _i32, _vp, _i64, _vp, _vp)
 lags_top_k_workspace_bytes = _fn("lags_top_k_workspace_bytes", _sz, _i32, _i64)
 lags_top_k = _fn("lags_top_k", C.c_int, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
 lags_decompress = _fn("lags_decompress", C.c_int, _i32, _vp, _vp, _vp, _i64, _vp, _vp)
+lags_wire_encode = _fn("lags_wire_encode", C.c_int, _u32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i64, _vp,
+                       _vp, _vp)
+lags_wire_decode = _fn("lags_wire_decode", C.c_int, _u32, _vp, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
+                       _vp, _i32, _vp, _vp, _vp, _vp)
+WIRE_MESSAGE, WIRE_CHUNK = 0, 1
+WIRE_MAX_CHUNKS = 4096
+(WIRE_ERR_TRUNCATED_MESSAGE, WIRE_ERR_TRUNCATED_HEADER, WIRE_ERR_TRUNCATED_PAYLOAD, WIRE_ERR_INDEX_RANGE,
+ WIRE_ERR_INDEX_ORDER, WIRE_ERR_TRAILING, WIRE_ERR_CAPACITY) = range(1, 8)
+WIRE_OK = (1 << 64) - 1
 
 EXPORTS = [
     "lags_abi_version", "lags_last_error", "lags_kernel_launches", "lags_bucket_device_bytes",
@@ -67,7 +76,7 @@ EXPORTS = [
     "lags_bucket_decode_update", "lags_bucket_stats", "lags_bucket_step_local", "lags_bucket_set_probe_events",
     "lags_check_finite",
     "lags_top_k_workspace_bytes",
-    "lags_top_k", "lags_decompress",
+    "lags_top_k", "lags_decompress", "lags_wire_encode", "lags_wire_decode",
 ]
 
 

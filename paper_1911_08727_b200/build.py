@@ -15,8 +15,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblagsb200.so")
-SOURCES = ["lags_kernels.cu"]
-HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh", "lags_cluster.cuh"]
+SOURCES = ["lags_kernels.cu", "lags_wire.cu"]
+HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh", "lags_cluster.cuh", "lags_internal.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

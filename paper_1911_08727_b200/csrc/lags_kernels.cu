@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "lags_common.cuh"
+#include "lags_internal.h"
 #include "lags_cluster.cuh"
 #include "lags_fast.cuh"
 #include "lags_select.cuh"
@@ -224,11 +225,18 @@ struct lags_bucket {
 namespace {
 thread_local std::string g_last_error;
 std::atomic<unsigned long long> g_launches{0};
+}  // namespace
 
-int fail(int code, const std::string& msg) {
+int lags::host_fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
+void lags::host_count_launches(int n) {
+  g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed);
+}
+
+namespace {
+int fail(int code, const std::string& msg) { return host_fail(code, msg); }
 
 int cuda_check(const char* where, int launches = 1) {
   g_launches.fetch_add(static_cast<unsigned long long>(launches), std::memory_order_relaxed);
@@ -350,7 +358,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 
 extern "C" {
 
-int lags_abi_version(void) { return 2; }
+int lags_abi_version(void) { return 3; }
 const char* lags_last_error(void) { return g_last_error.c_str(); }
 unsigned long long lags_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 

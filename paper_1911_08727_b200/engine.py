@@ -23,6 +23,7 @@ import numpy as np
 import torch
 
 from . import _native as N
+from .errors import StructureError
 
 
 def value_dtype(mode: int) -> torch.dtype:
@@ -141,6 +142,50 @@ class Bucket:
                                             momentum.data_ptr() if momentum is not None else None, float(mu),
                                             N.DECODE_V64 if v64 else 0, stream_handle(stream)),
                 "lags_bucket_decode_update")
+
+    # -- sparse wire format (R: sparsify.py:260-310) -------------------------------------------
+    def _wire_tables(self, layer_ids):
+        if getattr(self, "_wire", None) is None or self._wire[0] != tuple(layer_ids):
+            from . import wire as W
+
+            self._wire = (tuple(layer_ids), W._u32(layer_ids, self.device), W._u32(self.dims, self.device),
+                          torch.tensor(self.slots, dtype=torch.int64, device=self.device),
+                          torch.tensor(self.ks, dtype=torch.int32, device=self.device))
+        return self._wire[1:]
+
+    def wire_capacity(self) -> int:
+        """Largest encoded message of this bucket (every layer at its full k)."""
+        return 4 + sum(12 + 12 * k for k in self.ks)
+
+    def encode_wire(self, msg: torch.Tensor, layer_ids=None, stream=None):
+        """One message of this bucket in the reference's wire format, on the device (chunk j =
+        layer j with id ``layer_ids[j]``, default 1..L).  Returns (wire uint8 [capacity],
+        length int64 [1], error int64 [1]); stream-ordered, no host synchronisation."""
+        from . import wire as W
+
+        ids = list(layer_ids) if layer_ids is not None else list(range(1, self.nlayers + 1))
+        lids, dims, first, _ = self._wire_tables(ids)
+        return W.encode_table(lids, dims, self.counts_view(msg), first, self.idx_view(msg), self.val_view(msg),
+                              W.MESSAGE, self.wire_capacity(), stream)
+
+    def decode_wire(self, wire: torch.Tensor, length: int, layer_ids=None, msg: torch.Tensor | None = None,
+                    stream=None) -> torch.Tensor:
+        """Inverse of encode_wire into a bucket message (synchronises to check the result).  The
+        chunks must be this bucket's layers in order (ids, dims) with counts <= k."""
+        from . import wire as W
+
+        ids = list(layer_ids) if layer_ids is not None else list(range(1, self.nlayers + 1))
+        lids, dims, first, caps = self._wire_tables(ids)
+        msg = self.new_messages(1) if msg is None else msg
+        out = W.decode_table(wire, int(length), mode=W.MESSAGE, max_chunks=self.nlayers, first=first, caps=caps,
+                             entry_capacity=self.total_k, idx=self.idx_view(msg), val=self.val_view(msg),
+                             stream=stream)
+        W.raise_for(W.error_word(out["error"]), int(out["end"].item()), int(length))
+        n = int(out["nchunks"].item())
+        if n != self.nlayers or not torch.equal(out["layer_ids"], lids) or not torch.equal(out["dims"], dims):
+            raise StructureError("wire message does not hold this bucket's layers in order")
+        self.counts_view(msg).copy_(out["counts"])
+        return msg
 
     # -- host helpers (tests / diagnostics) ----------------------------------------------------
     def set_probe_events(self, before, after) -> None:

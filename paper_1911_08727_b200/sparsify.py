@@ -154,3 +154,140 @@ def decompress(chunk: SparseChunk) -> np.ndarray:
     N.check(N.lags_decompress(mode, idx.data_ptr(), val.data_ptr(), cnt.data_ptr(), chunk.dim, out.data_ptr(),
                               torch.cuda.current_stream().cuda_stream), "lags_decompress")
     return out.cpu().numpy()
+
+
+# --- tensor fusion (R: sparsify.py:199-257) --------------------------------------------------
+
+
+@dataclass(frozen=True)
+class FusionMessage:
+    """Chunks merged into one network message, per-layer identity retained (R: sparsify.py:199-206)."""
+
+    chunks: tuple
+
+    def nbytes(self, value_width: int = VALUE_BYTES_F64) -> int:
+        return sum(c.nbytes(value_width) for c in self.chunks)
+
+
+def fusion_flush(buffer: Sequence[SparseChunk], capacity_bytes: int, first_layer_done: bool,
+                 value_width: int = VALUE_BYTES_F64) -> FusionMessage | None:
+    """Flush rule of R: sparsify.py:209-238: send the buffered chunks when their accounting bytes
+    reach the capacity or the backward pass has produced its final (first) layer; never split or
+    reorder.  The same rule sizes LagsSGD's device buckets (optim.plan_buckets)."""
+    if capacity_bytes <= 0:
+        raise ValueError("capacity_bytes must be positive")
+    chunks = tuple(buffer)
+    seen: set[int] = set()
+    for c in chunks:
+        if c.layer_id in seen:
+            raise StructureError(f"duplicate layer {c.layer_id} in fusion buffer")
+        seen.add(c.layer_id)
+        if c.nbytes(value_width) >= capacity_bytes:
+            raise ValueError(f"capacity {capacity_bytes} does not exceed chunk of {c.nbytes(value_width)} bytes")
+    if not chunks:
+        return None
+    if sum(c.nbytes(value_width) for c in chunks) >= capacity_bytes or first_layer_done:
+        return FusionMessage(chunks)
+    return None
+
+
+class FusionBuffer:
+    """Stateful wrapper around ``fusion_flush`` for streaming use (R: sparsify.py:241-257)."""
+
+    def __init__(self, capacity_bytes: int, value_width: int = VALUE_BYTES_F64):
+        self.capacity_bytes = capacity_bytes
+        self.value_width = value_width
+        self._pending: list[SparseChunk] = []
+
+    def push(self, chunk: SparseChunk, first_layer_done: bool = False) -> FusionMessage | None:
+        self._pending.append(chunk)
+        msg = fusion_flush(self._pending, self.capacity_bytes, first_layer_done, self.value_width)
+        if msg is not None:
+            self._pending.clear()
+        return msg
+
+    def pending_bytes(self) -> int:
+        return sum(c.nbytes(self.value_width) for c in self._pending)
+
+
+# --- wire format (R: sparsify.py:260-310), encoded / decoded by the device kernels -------------
+
+
+def _table(chunks: Sequence[SparseChunk]):
+    from . import wire as W
+
+    for c in chunks:
+        if c.dim > 0x7FFFFFFF:
+            raise ValueError(f"layer {c.layer_id}: dim {c.dim} exceeds the device index range (2^31 - 1)")
+    counts = [len(c) for c in chunks]
+    first = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64) if chunks else np.zeros(1, np.int64)
+    n = max(sum(counts), 1)
+    idx = np.zeros(n, dtype=np.int32)
+    val = np.zeros(n, dtype=np.float64)
+    for c, f in zip(chunks, first):
+        idx[f:f + len(c)] = c.indices
+        val[f:f + len(c)] = c.values  # f32 -> f64 is exact (R: sparsify.py:274)
+    dev = torch.device("cuda")
+    return (W._u32([c.layer_id for c in chunks] or [0], dev), W._u32([c.dim for c in chunks] or [0], dev),
+            torch.tensor(counts or [0], dtype=torch.int32, device=dev), torch.from_numpy(first).to(dev),
+            torch.from_numpy(idx).to(dev), torch.from_numpy(val).to(dev), counts)
+
+
+def _encode(chunks: Sequence[SparseChunk], mode: int) -> bytes:
+    from . import wire as W
+
+    lids, dims, cnts, first, idx, val, counts = _table(chunks)
+    cap = W.wire_bytes(counts, with_header=mode == W.MESSAGE)
+    buf, wlen, err = W.encode_table(lids[:len(chunks)], dims[:len(chunks)], cnts[:len(chunks)], first, idx, val,
+                                    mode=mode, capacity=cap)
+    W.raise_for(W.error_word(err))
+    return buf[: int(wlen.item())].cpu().numpy().tobytes()
+
+
+def encode_chunk(chunk: SparseChunk) -> bytes:
+    """R: sparsify.py:269-274 -- 12-byte header + count x (u32 index, f64 value)."""
+    from . import wire as W
+
+    return _encode([chunk], W.CHUNK)
+
+
+def encode_message(message: FusionMessage) -> bytes:
+    """R: sparsify.py:291-295 -- u32 chunk count + the chunks."""
+    from . import wire as W
+
+    return _encode(list(message.chunks), W.MESSAGE)
+
+
+def _decode(buf: bytes, offset: int, mode: int):
+    from . import wire as W
+
+    raw = bytes(buf)
+    t = torch.frombuffer(bytearray(raw), dtype=torch.uint8) if raw else torch.zeros(1, dtype=torch.uint8)
+    out = W.decode_table(t.cuda(), len(raw), offset=offset, mode=mode)
+    W.raise_for(W.error_word(out["error"]), int(out["end"].item()), len(raw))
+    n = int(out["nchunks"].item())
+    counts = out["counts"][:n].cpu().tolist()
+    lids, dims = W._as_u32(out["layer_ids"][:n]), W._as_u32(out["dims"][:n])
+    idx = out["idx"].cpu().numpy().astype(np.int64)
+    val = out["val"].cpu().numpy()
+    chunks, f = [], 0
+    for lid, dim, c in zip(lids, dims, counts):
+        chunks.append(SparseChunk(lid, dim, idx[f:f + c].copy(), val[f:f + c].copy(), k_target=c))
+        f += c
+    return chunks, int(out["end"].item())
+
+
+def decode_chunk(buf: bytes, offset: int = 0) -> tuple[SparseChunk, int]:
+    """R: sparsify.py:277-288 -- one chunk at ``offset``; returns (chunk, next offset)."""
+    from . import wire as W
+
+    chunks, end = _decode(buf, offset, W.CHUNK)
+    return chunks[0], end
+
+
+def decode_message(buf: bytes) -> FusionMessage:
+    """R: sparsify.py:298-310 -- the whole buffer must be consumed."""
+    from . import wire as W
+
+    chunks, _ = _decode(buf, 0, W.MESSAGE)
+    return FusionMessage(tuple(chunks))

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_functions():
         assert hasattr(lib, name), name
     assert set(N.EXPORTS) == set(declared_functions())
-    assert N.lags_abi_version() == 2
+    assert N.lags_abi_version() == 3
 
 
 def test_argument_errors_map_to_reference_exceptions():
