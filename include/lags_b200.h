@@ -117,6 +117,20 @@ int lags_bucket_set_probe_events(lags_bucket_t* bucket, void* before, void* afte
 #define LAGS_STATS_WORDS 12
 int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 12] */, lags_stream_t stream);
 
+/* ---- diagnostics -------------------------------------------------------------------------------
+ * acc_p = r_p with message p's pairs written back (the accumulated vector before selection, as
+ * R: training.py:329 forms it): P planes of n_total elements, plane_stride elements apart.  r and
+ * acc may not alias.  LAGS_F32 / LAGS_F64 buckets. */
+int lags_bucket_reconstruct(const lags_bucket_t* bucket, const void* msgs, int64_t msg_stride, int32_t P,
+                            const void* r, void* acc, int64_t plane_stride, lags_stream_t stream);
+
+/* Aggregation-quality ratio per layer -- R: analysis.py:24-56 (topk_aggregation_ratio) as the
+ * train loop logs it (R: training.py:320-337): total = sum_p acc_p, agg = sum_p (acc_p - r_p)
+ * (fp64, worker order), out[j] = ||total - agg||^2 / ((1 - k_j/d_j) ||total||^2), NaN where the
+ * denominator vanishes (the reference's None).  out: device double[nlayers]. */
+int lags_bucket_delta(const lags_bucket_t* bucket, const void* acc, const void* r, int64_t plane_stride, int32_t P,
+                      double* out, lags_stream_t stream);
+
 /* ---- single-vector operators ---------------------------------------------------------------- */
 
 /* Finiteness of x[0:n) (R: training.py:174); ORs LAGS_STATUS_NONFINITE into *status. */

@@ -16,10 +16,12 @@ from .sparsify import (
     encode_message, fusion_flush, top_k, top_k_device,
 )
 from .training import StepSizeSchedule, lags_step, slgs_step
+from .analysis import topk_aggregation_ratio
 
 __all__ = [
     "Bucket", "CompressionPolicy", "DivergenceError", "FusionBuffer", "FusionMessage", "LayeredVector", "LayerShape",
     "SparseChunk", "StepSizeSchedule", "StructureError", "concat", "decode_chunk", "decode_message", "decompress",
     "encode_chunk", "encode_message", "fusion_flush", "lags_step", "slgs_step", "top_k", "top_k_device",
+    "topk_aggregation_ratio",
 ]
 __version__ = "0.1.0"

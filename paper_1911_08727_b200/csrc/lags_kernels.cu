@@ -183,6 +183,83 @@ __global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// diagnostics: aggregation-quality ratio delta^(l) (R: analysis.py:24-56, as the train loop
+// evaluates it on the accumulated vectors, R: training.py:320-337).  acc_p = accumulated vector
+// of worker p, r_p = acc_p with its selected entries zeroed (the new residual), so acc_p - r_p is
+// exactly the decompressed top-k pick: total = sum_p acc_p, agg = sum_p (acc_p - r_p) in fp64 in
+// worker order as the reference adds them; per task (one layer slice, one warp) the partial sums
+// of (total - agg)^2 and total^2, reduced per layer in task order (deterministic).
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) delta_partial_kernel(const Task* __restrict__ tasks, int ntasks,
+                                                            const T* __restrict__ acc, const T* __restrict__ r,
+                                                            int64_t stride, int P, double* part) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  griddep_wait();
+  if (w >= ntasks) return;
+  const Task tk = tasks[w];
+  double num = 0.0, den = 0.0;
+  for (int64_t i = tk.start + lane; i < tk.start + tk.len; i += 32) {
+    double tot = static_cast<double>(acc[i]);
+    double agg = __dadd_rn(0.0, __dsub_rn(tot, static_cast<double>(r[i])));
+    for (int p = 1; p < P; ++p) {
+      const double a = static_cast<double>(acc[p * stride + i]);
+      tot = __dadd_rn(tot, a);
+      agg = __dadd_rn(agg, __dsub_rn(a, static_cast<double>(r[p * stride + i])));
+    }
+    const double diff = __dsub_rn(tot, agg);
+    num = __fma_rn(diff, diff, num);
+    den = __fma_rn(tot, tot, den);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    num = __dadd_rn(num, __shfl_down_sync(0xffffffffu, num, o));
+    den = __dadd_rn(den, __shfl_down_sync(0xffffffffu, den, o));
+  }
+  if (lane == 0) {
+    part[2 * w] = num;
+    part[2 * w + 1] = den;
+  }
+}
+
+// delta_l = ||total - agg||^2 / ((1 - k/d) ||total||^2); NaN when the denominator vanishes
+// (the reference returns None there).
+__global__ void delta_final_kernel(const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks,
+                                   int nlayers, const double* __restrict__ part, double* out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  griddep_wait();
+  if (j >= nlayers) return;
+  const int2 tr = layer_tasks[j];
+  double num = 0.0, den = 0.0;
+  for (int t = tr.x; t < tr.y; ++t) {
+    num = __dadd_rn(num, part[2 * t]);
+    den = __dadd_rn(den, part[2 * t + 1]);
+  }
+  const lags_layer_t L = layers[j];
+  const double denom =
+      __dmul_rn(__dsub_rn(1.0, __ddiv_rn(static_cast<double>(L.k), static_cast<double>(L.dim))), den);
+  out[j] = denom == 0.0 ? __longlong_as_double(0x7ff8000000000000ll) : __ddiv_rn(num, denom);
+}
+
+// acc_p[L.offset + idx] = val for every sent pair of message p (acc_p pre-filled with r_p).
+template <typename T>
+__global__ void __launch_bounds__(256) reconstruct_kernel(const lags_layer_t* __restrict__ layers,
+                                                          const int32_t* __restrict__ slot_layer, MsgView msg,
+                                                          int64_t total_k, int P, T* acc, int64_t stride) {
+  griddep_wait();
+  const int64_t gs = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total_k * P; e += gs) {
+    const int p = static_cast<int>(e / total_k);
+    const int64_t s = e - static_cast<int64_t>(p) * total_k;
+    const int j = slot_layer[s];
+    const lags_layer_t L = layers[j];
+    if (s - L.slot >= msg.count(p, j)) continue;
+    acc[p * stride + L.offset + msg.idx(p, s)] = msg.val<T>(p, s);
+  }
+}
+
 }  // namespace lags
 
 // ==========================================================================================
@@ -210,6 +287,7 @@ struct lags_bucket {
   uint32_t* mask = nullptr;
   char* planes = nullptr;
   int32_t* order = nullptr;  // layers by decreasing selection work, group by group (phase-1 schedule)
+  double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
   // fp32 pipeline groups: the selection of group 0 (the layers with the heaviest selection work)
   // runs on `side` while K1 streams group 1 (see compress_impl)
   struct Group {
@@ -276,7 +354,7 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_delta = 0, bytes = 0;
 };
 
 int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, int32_t max_world, Plan* p) {
@@ -320,6 +398,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_mask = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total));
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
   p->o_order = take(sizeof(int32_t) * L);
+  p->o_delta = take(2 * sizeof(double) * nt);
   const bool f32 = dtype == LAGS_F32;
   p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (CoopScratch)
   p->bytes = o;
@@ -400,6 +479,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->mask = reinterpret_cast<uint32_t*>(base + p.o_mask);
   b->planes = base + p.o_planes;
   b->order = reinterpret_cast<int32_t*>(base + p.o_order);
+  b->delta_part = reinterpret_cast<double*>(base + p.o_delta);
   b->coop.work = reinterpret_cast<uint32_t*>(base + p.o_fbc);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
@@ -666,6 +746,46 @@ int lags_bucket_stats(const lags_bucket_t* b, uint32_t* out, lags_stream_t strea
       cudaStreamSynchronize(s) != cudaSuccess)
     return cuda_check("lags_bucket_stats", 0);
   return LAGS_OK;
+}
+
+int lags_bucket_reconstruct(const lags_bucket_t* b, const void* msgs, int64_t msg_stride, int32_t P, const void* r,
+                            void* acc, int64_t plane_stride, lags_stream_t stream) {
+  if (!b || !msgs || !r || !acc) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_reconstruct: null pointer");
+  if (b->dtype == LAGS_F32_ACC64) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_reconstruct: LAGS_F32 or LAGS_F64 bucket");
+  if (P < 1 || plane_stride < b->n_total || msg_stride < b->msg_bytes)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_reconstruct: bad P or strides");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t es = b->dtype == LAGS_F64 ? 8 : 4;
+  if (cudaMemcpy2DAsync(acc, es * plane_stride, r, es * plane_stride, es * b->n_total, P, cudaMemcpyDeviceToDevice,
+                        s) != cudaSuccess)
+    return cuda_check("lags_bucket_reconstruct copy", 0);
+  const MsgView mv{static_cast<const char*>(msgs), msg_stride, b->off_cnt, b->off_idx, b->off_val};
+  const int grid = stream_grid(b->total_k * P, 256, 8);
+  if (b->dtype == LAGS_F64)
+    reconstruct_kernel<double><<<grid, 256, 0, s>>>(b->layers, b->slot_layer, mv, b->total_k, P,
+                                                    static_cast<double*>(acc), plane_stride);
+  else
+    reconstruct_kernel<float><<<grid, 256, 0, s>>>(b->layers, b->slot_layer, mv, b->total_k, P,
+                                                   static_cast<float*>(acc), plane_stride);
+  return cuda_check("reconstruct_kernel");
+}
+
+int lags_bucket_delta(const lags_bucket_t* b, const void* acc, const void* r, int64_t plane_stride, int32_t P,
+                      double* out, lags_stream_t stream) {
+  if (!b || !acc || !r || !out) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_delta: null pointer");
+  if (b->dtype == LAGS_F32_ACC64) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_delta: LAGS_F32 or LAGS_F64 bucket");
+  if (P < 1 || plane_stride < b->n_total) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_delta: bad P or stride");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int blocks = (b->ntasks + 7) / 8;
+  if (b->dtype == LAGS_F64)
+    delta_partial_kernel<double><<<blocks, 256, 0, s>>>(b->tasks, b->ntasks, static_cast<const double*>(acc),
+                                                        static_cast<const double*>(r), plane_stride, P, b->delta_part);
+  else
+    delta_partial_kernel<float><<<blocks, 256, 0, s>>>(b->tasks, b->ntasks, static_cast<const float*>(acc),
+                                                       static_cast<const float*>(r), plane_stride, P, b->delta_part);
+  delta_final_kernel<<<(b->nlayers + 127) / 128, 128, 0, s>>>(b->layers, b->layer_tasks, b->nlayers, b->delta_part,
+                                                              out);
+  return cuda_check("delta kernels", 2);
 }
 
 int lags_check_finite(int32_t dtype, const void* x, int64_t n, uint32_t* status, lags_stream_t stream) {

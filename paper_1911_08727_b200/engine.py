@@ -143,6 +143,34 @@ class Bucket:
                                             N.DECODE_V64 if v64 else 0, stream_handle(stream)),
                 "lags_bucket_decode_update")
 
+    # -- diagnostics (R: analysis.py:24-56, training.py:320-337) ---------------------------------
+    def reconstruct(self, msgs: torch.Tensor, P: int, r: torch.Tensor, acc: torch.Tensor, stream=None,
+                    msg_stride: int | None = None, plane_stride: int | None = None) -> None:
+        """acc_p = r_p with message p's pairs written back: the accumulated vectors of P workers
+        (P planes of ``plane_stride`` elements, default n_total)."""
+        stride = self.n_total if plane_stride is None else int(plane_stride)
+        ms = self.msg_bytes if msg_stride is None else int(msg_stride)
+        if r.dtype != storage_dtype(self.mode) or acc.dtype != r.dtype:
+            raise TypeError("r / acc must have the bucket's storage dtype")
+        if min(r.numel(), acc.numel()) < (P - 1) * stride + self.n_total or msgs.numel() < (P - 1) * ms + self.msg_bytes:
+            raise ValueError("buffers smaller than P planes / messages")
+        N.check(N.lags_bucket_reconstruct(self._h, msgs.data_ptr(), ms, int(P), r.data_ptr(), acc.data_ptr(), stride,
+                                          stream_handle(stream)), "lags_bucket_reconstruct")
+
+    def delta(self, acc: torch.Tensor, r: torch.Tensor, P: int, out: torch.Tensor | None = None, stream=None,
+              plane_stride: int | None = None) -> torch.Tensor:
+        """Per-layer aggregation-quality ratio delta^(l) of P workers (float64 device tensor, NaN
+        where the reference returns None).  acc / r: P accumulated / residual planes."""
+        stride = self.n_total if plane_stride is None else int(plane_stride)
+        if r.dtype != storage_dtype(self.mode) or acc.dtype != r.dtype:
+            raise TypeError("r / acc must have the bucket's storage dtype")
+        if min(r.numel(), acc.numel()) < (P - 1) * stride + self.n_total:
+            raise ValueError("buffers smaller than P planes")
+        out = torch.empty(self.nlayers, dtype=torch.float64, device=self.device) if out is None else out
+        N.check(N.lags_bucket_delta(self._h, acc.data_ptr(), r.data_ptr(), stride, int(P), out.data_ptr(),
+                                    stream_handle(stream)), "lags_bucket_delta")
+        return out
+
     # -- sparse wire format (R: sparsify.py:260-310) -------------------------------------------
     def _wire_tables(self, layer_ids):
         if getattr(self, "_wire", None) is None or self._wire[0] != tuple(layer_ids):

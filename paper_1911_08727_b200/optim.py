@@ -94,7 +94,7 @@ class LagsSGD(torch.optim.Optimizer):
     def __init__(self, params: Iterable[torch.nn.Parameter], lr: float, rho: float | None = None,
                  policy: CompressionPolicy | None = None, momentum: float = 0.0, process_group=None,
                  bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1,
-                 exchange: bool = True):
+                 exchange: bool = True, delta_every: int = 0):
         params = [p for p in params]
         if not params:
             raise ValueError("no parameters")
@@ -118,6 +118,10 @@ class LagsSGD(torch.optim.Optimizer):
         # exchange=False replaces the all-gather by a local no-op (decode of the own message only):
         # a measurement mode for the exposed-communication time, not a training mode
         self.exchange = bool(exchange)
+        # delta_every > 0: every that many steps, log the aggregation-quality ratio delta^(l) of
+        # every layer on the device (R: training.py:320-337, delta_log_every); it all-gathers the
+        # residuals once per logged step (dense traffic, diagnostics only)
+        self.delta_every = int(delta_every)
         # flat per-rank buffers with the reference's layer layout; params and grads become views
         n = sum(self.dims)
         self.offsets = [0]
@@ -155,6 +159,8 @@ class LagsSGD(torch.optim.Optimizer):
         self._hooks = [p.register_post_accumulate_grad_hook(self._on_grad) for p in params]
         self._layer_of_param = {id(p): l for l, p in enumerate(params)}
         self.timing = None  # optional per-bucket CUDA events (see enable_timing)
+        self._delta = torch.full((L,), float("nan"), dtype=torch.float64, device=self.device)
+        self._delta_step = 0
         self._hook_events = None  # optional per-layer CUDA events at gradient readiness
 
     def _build_buckets(self) -> None:
@@ -274,6 +280,8 @@ class LagsSGD(torch.optim.Optimizer):
                 t[1].record(stream)
                 t[2].record(stream)
                 t[3].record(stream)
+            if self._log_delta_now():
+                self._log_delta(b, r, b.msg_local, 1, stream)
             return
         b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=True)
         if t is not None:
@@ -288,6 +296,31 @@ class LagsSGD(torch.optim.Optimizer):
         b.engine.decode(msgs, P, v, momentum=m, mu=self.mu, stream=stream)
         if t is not None:
             t[3].record(stream)
+        if self._log_delta_now():
+            self._log_delta(b, r, msgs, P, stream)
+
+    def _log_delta_now(self) -> bool:
+        return self.delta_every > 0 and (self._steps + 1) % self.delta_every == 0
+
+    def _log_delta(self, b, r, msgs, P, stream) -> None:
+        """delta^(l) of the bucket's layers this step: acc_p = r_p + sent_p rebuilt from the
+        gathered messages and all-gathered residuals (R: training.py:329-337)."""
+        if P > 1:
+            r_all = torch.empty(P * b.numel, dtype=r.dtype, device=r.device)
+            dist.all_gather_into_tensor(r_all, r.contiguous(), group=self.group)
+        else:
+            r_all = r
+        acc = torch.empty(P * b.numel, dtype=r.dtype, device=r.device)
+        b.engine.reconstruct(msgs, P, r_all, acc, stream=stream)
+        b.engine.delta(acc, r_all, P, out=self._delta[b.lo:b.hi + 1], stream=stream)
+        self._delta_step = self._steps + 1
+
+    def last_delta(self):
+        """(step, [delta^(l) or None per layer]) of the last logged step (synchronises)."""
+        if self.side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        vals = self._delta.cpu().tolist()
+        return self._delta_step, [None if v != v else v for v in vals]
 
     def enable_timing(self, on: bool = True) -> None:
         """Record CUDA events around each bucket's compress / exchange / decode."""

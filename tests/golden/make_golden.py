@@ -15,6 +15,7 @@ Fixtures:
   slgs_cases.npz         slgs_step(v, grads, alpha, global_k, res) R: training.py:203-224
   perf_cases.json        select_ratios / comm_time / schedules     R: perf.py:59-260
   wire_cases.json        encode_chunk / fusion_flush               R: sparsify.py:209-310
+  delta_cases.npz        topk_aggregation_ratio (delta^(l))        R: analysis.py:24-56
 """
 
 from __future__ import annotations
@@ -282,7 +283,36 @@ def make_wire():
         json.dump(out, fh, indent=0)
 
 
+def make_delta():
+    from lagsgd.analysis import topk_aggregation_ratio
+
+    rng = np.random.default_rng(24)
+    out = {}
+    n = 0
+    specs = [(1, 50, 5, "normal"), (2, 50, 5, "normal"), (3, 200, 7, "heavy"), (4, 64, 64, "normal"),
+             (2, 64, 3, "ties"), (3, 100, 10, "zeros50"), (2, 30, 4, "allequal"), (4, 1000, 1, "normal"),
+             (2, 1, 1, "normal"), (5, 333, 20, "heavy"), (2, 40, 5, "zerosall")]
+    for P, d, k, kind in specs:
+        for dt in (np.float64, np.float32):
+            if kind == "zerosall":
+                xs = [np.zeros(d, dtype=dt) for _ in range(P)]
+            else:
+                xs = [_dist(rng, kind, d, dt).astype(dt) for _ in range(P)]
+            got = topk_aggregation_ratio(xs, k)
+            out[f"x{n}"] = np.stack(xs)
+            out[f"meta{n}"] = np.array([P, d, k], dtype=np.int64)
+            out[f"delta{n}"] = np.array(np.nan if got is None else got, dtype=np.float64)
+            n += 1
+    out["n"] = np.array(n)
+    np.savez_compressed(os.path.join(HERE, "delta_cases.npz"), **out)
+    return n
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate only the named fixtures, e.g. `make_golden.py delta`
+        for name in sys.argv[1:]:
+            print(name, globals()["make_" + name]())
+        sys.exit(0)
     print("topk cases", make_topk())
     print("lags_step cases", make_lags_step())
     print("config1 iterations", make_config1())

@@ -73,5 +73,32 @@ class OracleStubBucket:
             vn[:] = (vn.astype(np.float64) - total / P).astype(np.float32)
 
 
+    def reconstruct(self, msgs, P, r, acc, stream=None):
+        raw = msgs.numpy()
+        rn, an = r.detach().numpy(), acc.numpy()
+        an[:P * self.n_total] = rn[:P * self.n_total]
+        for p in range(P):
+            m = raw[p * self.msg_bytes:(p + 1) * self.msg_bytes]
+            cnt = m[self.off_cnt:self.off_cnt + 4 * self.nlayers].view(np.int32)
+            idx = m[self.off_idx:self.off_idx + 4 * self.total_k].view(np.int32)
+            val = m[self.off_val:self.off_val + 4 * self.total_k].view(np.float32)
+            for j in range(self.nlayers):
+                s, o = self.slots[j], self.offsets[j]
+                an[p * self.n_total + o + idx[s:s + cnt[j]]] = val[s:s + cnt[j]]
+
+    def delta(self, acc, r, P, out=None, stream=None):
+        an = acc.numpy().reshape(P, self.n_total)
+        res = []
+        for j, (d, k) in enumerate(zip(self.dims, self.ks)):
+            o = self.offsets[j]
+            got = orc.topk_aggregation_ratio([an[p, o:o + d] for p in range(P)], k)
+            res.append(float("nan") if got is None else got)
+        t = torch.tensor(res, dtype=torch.float64)
+        if out is not None:
+            out.copy_(t)
+            return out
+        return t
+
+
 def stub_factory(dims, ks, world, device):
     return OracleStubBucket(dims, ks, world, device)

@@ -121,7 +121,8 @@ def _worker(rank, world, port, steps, out):
     try:
         torch.manual_seed(1 + rank)  # different init per rank: LagsSGD must broadcast rank 0's
         model = Tiny()
-        opt = LagsSGD(model.parameters(), lr=0.05, rho=0.2, bucket_cap_bytes=96, engine_factory=stub_factory)
+        opt = LagsSGD(model.parameters(), lr=0.05, rho=0.2, bucket_cap_bytes=96, engine_factory=stub_factory,
+                      delta_every=2)
         v = opt.flat_param.detach().numpy().copy()
         res = [np.zeros_like(v) for _ in range(world)]
         for t in range(steps):
@@ -132,10 +133,18 @@ def _worker(rank, world, port, steps, out):
             g = torch.from_numpy(consumed_grad(opt))
             gathered = [torch.zeros_like(g) for _ in range(world)]
             dist.all_gather(gathered, g)
+            accs = [res[p] + 0.05 * gathered[p].numpy() for p in range(world)]  # before lags_step mutates res
             v = orc.lags_step(v, [x.numpy() for x in gathered], 0.05, opt.dims, opt.ks, res)
             if opt.flat_param.numpy().tobytes() != v.tobytes():
                 out.put((rank, f"step {t}: params differ from the oracle"))
                 return
+            if (t + 1) % 2 == 0:  # delta^(l) logged on this step (R: training.py:320-337)
+                step, got = opt.last_delta()
+                want = [orc.topk_aggregation_ratio([a[o:o + d] for a in accs], k)
+                        for o, d, k in zip(opt.offsets, opt.dims, opt.ks)]
+                if step != t + 1 or got != want:
+                    out.put((rank, f"step {t}: delta {got} != {want}"))
+                    return
         out.put((rank, opt.flat_param.numpy().tobytes()))
     finally:
         dist.destroy_process_group()

@@ -153,3 +153,20 @@ def test_slgs_golden():
         assert _bits(out).tobytes() == _bits(z[f"v_out{i}"]).tobytes()
         for a, b in zip(res, z[f"r_out{i}"]):
             assert _bits(a).tobytes() == _bits(b).tobytes()
+
+
+def test_delta_golden():
+    """Oracle delta^(l) against the reference's analysis.topk_aggregation_ratio outputs (numpy dot
+    products on both sides: same BLAS, exact agreement expected up to summation order)."""
+    from conftest import load_npz
+
+    z = load_npz("delta_cases.npz")
+    for i in range(int(z["n"])):
+        P, d, k = (int(v) for v in z[f"meta{i}"])
+        xs = list(z[f"x{i}"])
+        want = float(z[f"delta{i}"])
+        got = orc.topk_aggregation_ratio(xs, k)
+        if np.isnan(want):
+            assert got is None
+        else:
+            assert got is not None and abs(got - want) <= 1e-12 * max(1.0, abs(want)), (i, got, want)
