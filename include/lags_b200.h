@@ -111,6 +111,13 @@ int lags_bucket_decode_update(lags_bucket_t* bucket, const void* msgs, int64_t m
  * `after` around its streaming kernel (K1) so callers can time the dominant kernel live. */
 int lags_bucket_set_probe_events(lags_bucket_t* bucket, void* before, void* after);
 
+/* Gradient pointer table (LAGS_F32): `table` is a DEVICE array of nlayers pointers, layer j's
+ * gradient (dim_j contiguous floats, e.g. a framework's per-parameter .grad tensor), read by
+ * every later compress / step_local instead of the flat g (which may then be NULL).  Lets an
+ * autograd engine hand its gradient tensors over without accumulating into a flat buffer.  The
+ * table's contents are read when the kernels run (stream-ordered); NULL switches back to flat g. */
+int lags_bucket_set_grad_table(lags_bucket_t* bucket, const void* table);
+
 /* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls, last select
  * cycles, last path (0 small dense, 1 candidates, 2 dense after a failed prediction), phase
  * cycles, select start / end / CTA launch (%globaltimer ns, low 32 bits), 0} (synchronous). */

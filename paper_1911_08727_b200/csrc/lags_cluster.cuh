@@ -26,23 +26,19 @@ struct ClusterShared {
   uint32_t prefix, pmask, n_gt, need_eq, key2;  // rank 0: the threshold
 };
 
-__global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(SEL_NT, 1) select_cluster_kernel(
-    const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ big,
-    FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
-    const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
-    float* val_out, int32_t* count_out, int smem_words, int force_exact, float* vupd) {
+// One layer by the CTA's cluster (all CLUSTER CTAs call this with the same j).
+__device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ layers,
+                                     const int2* __restrict__ layer_tasks, FastState* state,
+                                     const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
+                                     const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r,
+                                     int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words,
+                                     int force_exact, float* vupd, uint32_t* dyn, CoopSmem& cs, ClusterShared& csh,
+                                     uint32_t t_launch) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ uint32_t dyn[];
-  __shared__ CoopSmem cs;
-  __shared__ ClusterShared csh;
-  const uint32_t t_launch = globaltimer_lo();
-  griddep_wait();                // K1 has completed and its writes are visible
-  griddep_launch_dependents();   // the per-layer selection kernel may start alongside
   const uint32_t t_start = globaltimer_lo();
   const long long t_begin = clock64();
   const int rank = static_cast<int>(cluster.block_rank());
-  const int j = big[blockIdx.x / CLUSTER];
   const lags_layer_t L = layers[j];
   const int2 tr = layer_tasks[j];
   const FastState st = state[j];
@@ -53,7 +49,7 @@ __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(SEL_NT, 1) sel
   // 1. counts
   uint32_t local = 0, over = 0;
   for (int t = t_lo + threadIdx.x; t < t_hi; t += SEL_NT) {
-    const uint32_t c = static_cast<uint32_t>(cand_cnt[t]);
+    const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
     local += min(c, static_cast<uint32_t>(cap));
   }
@@ -107,7 +103,7 @@ __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(SEL_NT, 1) sel
   uint32_t carry = 0;
   for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
     const int nt = min(SEL_NT, t_hi - t0);
-    const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(cand_cnt[t0 + threadIdx.x]) : 0u;
+    const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)) : 0u;
     uint32_t tot;
     const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
     cs.tpos[threadIdx.x] = pos;
@@ -233,6 +229,40 @@ __global__ void __cluster_dims__(CLUSTER, 1, 1) __launch_bounds__(SEL_NT, 1) sel
     state[j] = ns;
   }
   cluster.sync();  // no CTA leaves while others may still read its shared memory
+}
+
+// The whole selection of an fp32 compress in ONE launch (thread-block clusters of CLUSTER CTAs):
+// the first CLUSTER * n_cl CTAs select the largest layers, one cluster per layer; the remaining
+// CTAs walk the other layers persistently (largest estimated work first, first layer by block
+// index, then an atomic counter).  One launch, so no CTA ever waits on another kernel while
+// holding an SM -- this matters when the compress runs beside backprop on a side stream.
+__global__ void __launch_bounds__(SEL_NT, 1) select_kernel(
+    const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ cl_layers,
+    int n_cl, const int32_t* __restrict__ order, int nl, FastState* state, const int32_t* __restrict__ cand_cnt,
+    const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval,
+    float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, CoopScratch sc,
+    float* vupd) {
+  extern __shared__ uint32_t dyn[];
+  __shared__ CoopSmem cs;
+  __shared__ ClusterShared csh;
+  __shared__ int next_pos;
+  const uint32_t t_launch = globaltimer_lo();
+  griddep_wait();  // K1 has completed and its writes are visible (programmatic dependent launch)
+  const int cl_ctas = n_cl * CLUSTER;
+  if (static_cast<int>(blockIdx.x) < cl_ctas) {
+    cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap,
+                         gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh,
+                         t_launch);
+    return;
+  }
+  const int grid = static_cast<int>(gridDim.x) - cl_ctas;
+  for (int pos = static_cast<int>(blockIdx.x) - cl_ctas; pos < nl;) {
+    if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + grid;
+    select_layer(order[pos], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out,
+                 val_out, count_out, dyn, smem_words, force_exact, cs, vupd, t_launch);
+    pos = next_pos;
+    __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
+  }
 }
 
 }  // namespace lags

@@ -114,47 +114,53 @@ __device__ __forceinline__ void emit_candidates(uint32_t bits, float4 vals, int6
 
 // One task of the streaming pass, by one warp (warp-collective): acc = r + alpha * g written back
 // into r, the non-finite flag, and the task's candidate list (entries with key(acc) >= thr[layer],
-// ascending index order) with its count in cand_cnt[tid].
+// ascending index order) with its count in cand_cnt[tid].  gt / rt point at the task's first
+// gradient / residual element (the gradient may live in its own per-layer tensor); 16-byte
+// vectors when both share an alignment, scalar otherwise.
 // ZERO_G: also clear the gradient after reading it (the optimizer's zero_grad fused into the pass;
 // +4 B/element of writes instead of a separate memset pass).
 template <bool ZERO_G, int UNROLL>
 __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, const lags_layer_t* __restrict__ layers,
-                                            const FastState* state, float* __restrict__ g, float* __restrict__ r,
+                                            const FastState* state, float* __restrict__ gt, float* __restrict__ rt,
                                             float alpha, int cap, int32_t* __restrict__ cand_idx,
                                             float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
                                             uint32_t* status) {
-  const int64_t loff = layers[T.layer].offset;
+  const int64_t local0 = T.start - layers[T.layer].offset;  // layer-local index of element 0
   const uint32_t thr0 = state[T.layer].thr;
   const uint32_t thr = thr0 ? thr0 : 0xffffffffu;
   int32_t* cidx = cand_idx + static_cast<int64_t>(tid) * cap;
   float* cval = cand_val + static_cast<int64_t>(tid) * cap;
   uint32_t cnt = 0;
   bool bad = false;
-  const int64_t s = T.start, e = T.start + T.len;
-  // scalar head up to 16-byte alignment (flat buffers are 16-byte aligned)
-  const int64_t h = min(static_cast<int64_t>((4 - (s & 3)) & 3), static_cast<int64_t>(T.len));
-  {
-    uint32_t bits = 0;
-    float a = 0.f;
-    if (lane < h) {
-      const float gi = g[s + lane];
-      if (ZERO_G) g[s + lane] = 0.0f;
-      bad |= nonfinite(gi);
-      a = accum(r[s + lane], gi, alpha);
-      r[s + lane] = a;
-      bits = (Key<float>::of(a) >= thr) ? 1u : 0u;
+  const int n = T.len;
+  const uintptr_t ra = reinterpret_cast<uintptr_t>(rt), ga = reinterpret_cast<uintptr_t>(gt);
+  // scalar head up to 16-byte alignment of r; the whole task scalar if g is aligned differently
+  const int h = ((ra ^ ga) & 15u) == 0 ? min(static_cast<int>(((16u - (ra & 15u)) & 15u) >> 2), n) : n;
+  auto scalar = [&](int lo, int hi) {
+    for (int q0 = lo; q0 < hi; q0 += 32) {  // warp-uniform trip count
+      const int i = q0 + lane;
+      uint32_t bits = 0;
+      float a = 0.f;
+      if (i < hi) {
+        const float gi = gt[i];
+        if (ZERO_G) gt[i] = 0.0f;
+        bad |= nonfinite(gi);
+        a = accum(rt[i], gi, alpha);
+        rt[i] = a;
+        bits = (Key<float>::of(a) >= thr) ? 1u : 0u;
+      }
+      emit_candidates(bits, make_float4(a, a, a, a), local0 + i, lane, cnt, cidx, cval, cap);
     }
-    emit_candidates(bits, make_float4(a, a, a, a), s + lane - loff, lane, cnt, cidx, cval, cap);
-  }
-  const int64_t vb = s + h;
-  const int64_t n4 = (e - vb) >> 2;
-  float4* g4 = reinterpret_cast<float4*>(g + vb);
-  float4* r4 = reinterpret_cast<float4*>(r + vb);
-  for (int64_t q0 = 0; q0 < n4; q0 += 32 * UNROLL) {
+  };
+  scalar(0, h);
+  const int n4 = (n - h) >> 2;
+  float4* g4 = reinterpret_cast<float4*>(gt + h);
+  float4* r4 = reinterpret_cast<float4*>(rt + h);
+  for (int q0 = 0; q0 < n4; q0 += 32 * UNROLL) {
     float4 gv[UNROLL], rv[UNROLL];
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      const int64_t q = q0 + u * 32 + lane;
+      const int q = q0 + u * 32 + lane;
       if (q < n4) {
         gv[u] = __ldcs(g4 + q);
         rv[u] = r4[q];
@@ -163,13 +169,13 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
     if (ZERO_G) {
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) {
-        const int64_t q = q0 + u * 32 + lane;
+        const int q = q0 + u * 32 + lane;
         if (q < n4) __stcs(g4 + q, make_float4(0.f, 0.f, 0.f, 0.f));
       }
     }
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) {
-      const int64_t q = q0 + u * 32 + lane;
+      const int q = q0 + u * 32 + lane;
       uint32_t bits = 0;
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
       if (q < n4) {
@@ -182,41 +188,30 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
         bits = (Key<float>::of(a.x) >= thr ? 1u : 0u) | (Key<float>::of(a.y) >= thr ? 2u : 0u) |
                (Key<float>::of(a.z) >= thr ? 4u : 0u) | (Key<float>::of(a.w) >= thr ? 8u : 0u);
       }
-      if (q0 + u * 32 < n4) emit_candidates(bits, a, vb + 4 * q - loff, lane, cnt, cidx, cval, cap);
+      if (q0 + u * 32 < n4) emit_candidates(bits, a, local0 + h + 4 * static_cast<int64_t>(q), lane, cnt, cidx, cval, cap);
     }
   }
-  // scalar tail
-  {
-    const int64_t t0 = vb + 4 * n4;
-    uint32_t bits = 0;
-    float a = 0.f;
-    if (t0 + lane < e) {
-      const float gi = g[t0 + lane];
-      if (ZERO_G) g[t0 + lane] = 0.0f;
-      bad |= nonfinite(gi);
-      a = accum(r[t0 + lane], gi, alpha);
-      r[t0 + lane] = a;
-      bits = (Key<float>::of(a) >= thr) ? 1u : 0u;
-    }
-    if (t0 < e) emit_candidates(bits, make_float4(a, a, a, a), t0 + lane - loff, lane, cnt, cidx, cval, cap);
-  }
+  scalar(h + 4 * n4, n);  // scalar tail
   if (lane == 0) cand_cnt[tid] = static_cast<int32_t>(cnt);
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
 }
 
-// K1: one warp per task.
+// K1: one warp per task.  gtab (nullable): per-layer gradient pointers replacing the flat g.
 template <bool ZERO_G>
 __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
-    const FastState* __restrict__ state, float* __restrict__ g, float* __restrict__ r, float alpha, int cap,
-    int32_t* __restrict__ cand_idx, float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
-    uint32_t* status, uint32_t* work) {
+    const FastState* __restrict__ state, float* __restrict__ g, float* const* __restrict__ gtab,
+    float* __restrict__ r, float alpha, int cap, int32_t* __restrict__ cand_idx, float* __restrict__ cand_val,
+    int32_t* __restrict__ cand_cnt, uint32_t* status, uint32_t* work) {
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
   griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
   if (wid == 0 && lane == 0) *work = 0u;  // the previous call's selection kernel has completed
   if (wid >= ntasks) return;
-  stream_task<ZERO_G, K1_UNROLL>(tasks[wid], wid, lane, layers, state, g, r, alpha, cap, cand_idx, cand_val, cand_cnt, status);
+  const Task T = tasks[wid];
+  float* gt = gtab ? gtab[T.layer] + (T.start - layers[T.layer].offset) : g + T.start;
+  stream_task<ZERO_G, K1_UNROLL>(T, wid, lane, layers, state, gt, r + T.start, alpha, cap, cand_idx, cand_val,
+                                 cand_cnt, status);
 }
 
 // Block-wide sum; all threads get the result.  Uses sm.warp_tot.
@@ -610,36 +605,6 @@ __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, con
     state[j].t_end = globaltimer_lo();
     state[j].t_launch = t_launch;
   }
-}
-
-// Per-layer selection: persistent CTAs walk the layer list (largest estimated selection work
-// first); the first layer of a CTA is its block index, the following ones are handed out by an
-// atomic counter, so a grid no larger than the free SMs runs the list in one wave, balanced
-// dynamically (longest-processing-time first).  An ordinary launch (not cooperative), so the
-// selection overlaps backprop kernels running on other streams.
-__global__ void __launch_bounds__(SEL_NT, 1) select_phase1_kernel(
-    const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ order,
-    int nl, FastState* state, const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
-    const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out,
-    float* val_out, int32_t* count_out, int smem_keys, int force_exact, CoopScratch sc, float* vupd,
-    int after_cluster) {
-  extern __shared__ uint32_t skeys[];
-  __shared__ CoopSmem cs;
-  __shared__ int next_pos;
-  const uint32_t t_launch = globaltimer_lo();
-  // programmatic dependent launch.  Directly after K1: wait for it here.  After the cluster
-  // kernel (which waited on K1 before triggering this launch): K1's writes are already visible;
-  // wait on the cluster kernel only at the end, so the next kernel on the stream (waiting on this
-  // one) is also ordered after the cluster kernel.
-  if (!after_cluster) griddep_wait();
-  for (int pos = blockIdx.x; pos < nl;) {
-    if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + static_cast<int>(gridDim.x);
-    select_layer(order[pos], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out,
-                 val_out, count_out, skeys, smem_keys, force_exact, cs, vupd, t_launch);
-    pos = next_pos;
-    __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
-  }
-  if (after_cluster) griddep_wait();
 }
 
 }  // namespace lags

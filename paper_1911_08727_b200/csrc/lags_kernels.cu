@@ -2,8 +2,8 @@
 //
 // Kernels (DESIGN.md has the rooflines):
 //   accum_emit_kernel     (lags_fast.cuh) fp32 accumulate + candidate emission (K1)  R: training.py:250,174
-//   select_cluster_kernel (lags_cluster.cuh) largest layers: 4-CTA cluster select    R: sparsify.py:84-90
-//   select_phase1_kernel  (lags_fast.cuh) other layers: persistent per-layer select   R: sparsify.py:84-90
+//   select_kernel         (lags_cluster.cuh) exact top-k from the candidates: 4-CTA clusters
+//                         for the largest layers, persistent per-layer CTAs for the rest   R: sparsify.py:84-90
 //   accum_kernel / select_dense_kernel  exact dense path (fp64, mixed, forced exact)  R: training.py:250-252
 //   decode_* kernels    rank-ordered fp64 accumulation + SGD/momentum update          R: training.py:248,253-254
 #include <cuda_runtime.h>
@@ -298,6 +298,7 @@ struct lags_bucket {
   Group grp[2];
   CoopScratch coop{};  // per-call selection counter (two-kernel path)
   cudaEvent_t probe_before = nullptr, probe_after = nullptr;  // caller-owned, optional
+  float* const* grad_table = nullptr;  // caller-owned device array of per-layer gradient pointers
 };
 
 namespace {
@@ -405,9 +406,8 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   return LAGS_OK;
 }
 
-// Selection groups of an fp32 bucket: 0 = one CTA per layer (select_phase1_kernel), 1 = the
-// largest layers, one thread-block cluster per layer (select_cluster_kernel, run concurrently on
-// the bucket's side stream).
+// Selection groups of an fp32 bucket: 0 = one CTA per layer (select_kernel's persistent role),
+// 1 = the largest layers, one thread-block cluster per layer (select_kernel's cluster role).
 std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
   std::vector<int> gid(L, 0);
   for (int j = 0; j < L; ++j) gid[j] = (dims[j] > SMALL_LAYER && ks[j] >= CLUSTER_MIN_K) ? 1 : 0;
@@ -418,6 +418,27 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
 // previous kernel on the stream drains; it calls griddep_wait() before touching its inputs.
+// The same with a thread-block cluster size (1 = no clusters).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                               int cluster, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -549,14 +570,19 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   }
   if (dtype == LAGS_F32) {
     const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
-    if (cudaFuncSetAttribute(select_phase1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess ||
-        cudaFuncSetAttribute(select_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-            cudaSuccess) {
+    if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess) {
       delete b;
       return cuda_check("select kernel attributes", 0);
     }
-    b->smem_keys = SMEM_KEYS;
+    // shared-memory staging sized to the bucket: small layers are staged whole; a candidate set
+    // (~2k at the adaptive margin) needs value + index words, a cluster layer m + 2 * m_max;
+    // bigger sets fall back to global scratch.  Smaller staging leaves room for backprop kernels
+    // co-resident on the SM when the compress runs beside them.
+    int64_t words = 4096;
+    for (int j = 0; j < nlayers; ++j)
+      words = std::max<int64_t>(words, dims[j] <= SMALL_LAYER ? dims[j] : (15 * static_cast<int64_t>(ks[j])) / 2);
+    b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), SMEM_KEYS));
   }
   *out = b;
   return LAGS_OK;
@@ -578,8 +604,11 @@ int lags_bucket_message_layout(const lags_bucket_t* b, int64_t* off_counts, int6
 // selection epilogue (lags_bucket_step_local).
 static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, void* v_update, lags_stream_t stream) {
-  if (!b || !g || !r || !msg || !status) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
-  if (!aligned16(g) || !aligned16(r) || !aligned16(msg))
+  const bool table = b && b->grad_table && b->dtype == LAGS_F32;
+  if (!b || (!g && !table) || !r || !msg || !status)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
+  if (table) g = nullptr;  // the per-layer table replaces the flat gradient
+  if ((g && !aligned16(g)) || !aligned16(r) || !aligned16(msg))
     return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: buffers must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* m = static_cast<char*>(msg);
@@ -602,43 +631,35 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       const int64_t cb = static_cast<int64_t>(G.task_base) * b->cap;
       if (zg)
         return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
-                          G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
-                          b->cand_cnt + G.task_base, status, b->coop.work);
+                          G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
+                          b->cand_val + cb, b->cand_cnt + G.task_base, status, b->coop.work);
       return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
-                        G.ntasks, b->layers, b->state, gg, rr, a, b->cap, b->cand_idx + cb, b->cand_val + cb,
-                        b->cand_cnt + G.task_base, status, b->coop.work);
-    };
-    // K2 over one group's layers (a layer whose candidates fail the proof runs the dense path in
-    // its own CTA)
-    auto k2 = [&](const lags_bucket::Group& G, cudaStream_t st) -> cudaError_t {
-      if (G.nlayers == 0) return cudaSuccess;
-      // persistent CTAs: one wave on the SMs the cluster kernel leaves free (1 CTA per SM)
-      const int busy = b->ngroups == 2 ? b->grp[1].nlayers * CLUSTER : 0;
-      const int grid = std::min(G.nlayers, std::max(num_sms() - busy, num_sms() / 2));
-      return launch_pdl(select_phase1_kernel, dim3(grid), dim3(SEL_NT),
-                        static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), st, b->layers, b->layer_tasks,
-                        b->order + G.order_base, G.nlayers, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap,
-                        b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->coop, vu, b->ngroups == 2 ? 1 : 0);
+                        G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
+                        b->cand_val + cb, b->cand_cnt + G.task_base, status, b->coop.work);
     };
     cudaError_t e = cudaSuccess;
-    int launches = 2;
     lags_bucket::Group all = b->grp[0];  // K1 streams every task (group 0's then group 1's)
     all.task_base = 0;
     all.ntasks = b->grp[0].ntasks + b->grp[1].ntasks;
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
     if (e == cudaSuccess) e = k1(all, s);
     if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
-    if (b->ngroups == 2 && e == cudaSuccess) {
-      // the largest layers: one 4-CTA cluster each; it waits on K1, then triggers the launch of
-      // the per-layer selection of the other layers, which runs alongside (PDL, same stream)
-      const lags_bucket::Group& G = b->grp[1];
-      e = launch_pdl(select_cluster_kernel, dim3(G.nlayers * CLUSTER), dim3(SEL_NT),
-                     static_cast<size_t>(b->smem_keys) * sizeof(uint32_t), s, b->layers, b->layer_tasks,
-                     b->order + G.order_base, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx,
-                     b->gval, rr, idx, vals, cnt, b->smem_keys, fe, vu);
-      launches = 3;
+    if (e == cudaSuccess) {
+      // the selection: one launch (PDL behind K1).  Group 1 (the largest layers): one 4-CTA
+      // cluster each; group 0: persistent CTAs, one wave on the SMs the clusters leave free.
+      const lags_bucket::Group& G0 = b->grp[0];
+      const lags_bucket::Group& G1 = b->grp[1];
+      const int ncl = b->ngroups == 2 ? G1.nlayers : 0;
+      const int cl = ncl > 0 ? CLUSTER : 1;
+      int per = std::min(G0.nlayers, std::max(num_sms() - ncl * CLUSTER, num_sms() / 2));
+      per = (per + cl - 1) / cl * cl;  // the grid is a whole number of clusters
+      const int grid = ncl * CLUSTER + per;
+      e = launch_pdl_cluster(select_kernel, dim3(grid), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s, cl,
+                             b->layers, b->layer_tasks, b->order + G1.order_base, ncl, b->order + G0.order_base,
+                             G0.nlayers, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval,
+                             rr, idx, vals, cnt, b->smem_keys, fe, b->coop, vu);
     }
-    if (e == cudaSuccess) e = k2(b->grp[0], s);
+    const int launches = 2;
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
     return cuda_check("lags_bucket_compress(f32)", launches);
   }
@@ -736,6 +757,14 @@ int lags_bucket_set_probe_events(lags_bucket_t* b, void* before, void* after) {
   if (!b) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_set_probe_events: null bucket");
   b->probe_before = static_cast<cudaEvent_t>(before);
   b->probe_after = static_cast<cudaEvent_t>(after);
+  return LAGS_OK;
+}
+
+int lags_bucket_set_grad_table(lags_bucket_t* b, const void* table) {
+  if (!b) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_set_grad_table: null bucket");
+  if (table && b->dtype != LAGS_F32)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_set_grad_table: LAGS_F32 buckets only");
+  b->grad_table = static_cast<float* const*>(table);
   return LAGS_OK;
 }
 

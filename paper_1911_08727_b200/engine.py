@@ -106,27 +106,39 @@ class Bucket:
                  status: torch.Tensor, stream=None, exact: bool = False, zero_grad: bool = False) -> None:
         """acc = r + alpha*g; per-layer top-k; r <- acc with selected entries +0.0; msg <- pairs.
         ``zero_grad`` clears g in the same pass (the optimizer's fused zero_grad)."""
-        sd = storage_dtype(self.mode)
-        if g.dtype != sd or r.dtype != sd:
-            raise TypeError(f"bucket mode {self.mode} expects {sd} buffers")
-        if g.numel() < self.n_total or r.numel() < self.n_total or msg.numel() < self.msg_bytes:
-            raise ValueError("buffer smaller than the bucket")
+        self._check_buffers(g, r, None, msg)
         flags = (N.COMPRESS_EXACT if exact else 0) | (N.COMPRESS_ZERO_GRAD if zero_grad else 0)
-        N.check(N.lags_bucket_compress(self._h, g.data_ptr(), r.data_ptr(), float(alpha), msg.data_ptr(),
-                                       status.data_ptr(), flags, stream_handle(stream)), "lags_bucket_compress")
+        N.check(N.lags_bucket_compress(self._h, g.data_ptr() if g is not None else None, r.data_ptr(), float(alpha),
+                                       msg.data_ptr(), status.data_ptr(), flags, stream_handle(stream)),
+                "lags_bucket_compress")
 
     def step_local(self, g: torch.Tensor, r: torch.Tensor, alpha: float, v: torch.Tensor, msg: torch.Tensor,
                    status: torch.Tensor, stream=None, exact: bool = False, zero_grad: bool = False) -> None:
         """Single rank (P = 1): compress with v <- v - sent fused into the selection epilogue."""
-        sd = storage_dtype(self.mode)
-        if g.dtype != sd or r.dtype != sd or v.dtype != sd:
-            raise TypeError(f"bucket mode {self.mode} expects {sd} buffers")
-        if min(g.numel(), r.numel(), v.numel()) < self.n_total or msg.numel() < self.msg_bytes:
-            raise ValueError("buffer smaller than the bucket")
+        self._check_buffers(g, r, v, msg)
         flags = (N.COMPRESS_EXACT if exact else 0) | (N.COMPRESS_ZERO_GRAD if zero_grad else 0)
-        N.check(N.lags_bucket_step_local(self._h, g.data_ptr(), r.data_ptr(), float(alpha), v.data_ptr(),
-                                         msg.data_ptr(), status.data_ptr(), flags, stream_handle(stream)),
-                "lags_bucket_step_local")
+        N.check(N.lags_bucket_step_local(self._h, g.data_ptr() if g is not None else None, r.data_ptr(), float(alpha),
+                                         v.data_ptr(), msg.data_ptr(), status.data_ptr(), flags,
+                                         stream_handle(stream)), "lags_bucket_step_local")
+
+    def _check_buffers(self, g, r, v, msg) -> None:
+        sd = storage_dtype(self.mode)
+        if g is None and getattr(self, "_grad_table", None) is None:
+            raise ValueError("g is required unless a gradient table is set (set_grad_table)")
+        for t in (g, r, v):
+            if t is not None and (t.dtype != sd or t.numel() < self.n_total):
+                raise TypeError(f"bucket mode {self.mode} expects {sd} buffers of >= {self.n_total} elements")
+        if msg.numel() < self.msg_bytes:
+            raise ValueError("message buffer smaller than the bucket's message")
+
+    def set_grad_table(self, table: torch.Tensor | None) -> None:
+        """Read gradients through a device int64 tensor of nlayers per-layer gradient pointers
+        (lags_bucket_set_grad_table); compress / step_local then take g=None.  None: flat g again."""
+        if table is not None and (table.dtype != torch.int64 or table.numel() < self.nlayers or not table.is_cuda):
+            raise ValueError("the gradient table is a CUDA int64 tensor of nlayers pointers")
+        N.check(N.lags_bucket_set_grad_table(self._h, table.data_ptr() if table is not None else None),
+                "lags_bucket_set_grad_table")
+        self._grad_table = table  # keep it alive while the library holds the pointer
 
     def decode(self, msgs: torch.Tensor, P: int, v: torch.Tensor, momentum: torch.Tensor | None = None,
                mu: float = 0.0, stream=None, msg_stride: int | None = None) -> None:

@@ -75,6 +75,12 @@ class _BucketRT:
     engine: object
     msg_local: torch.Tensor
     msg_all: torch.Tensor | None
+    gtab: torch.Tensor | None = None   # grads="tensors": device table of per-layer gradient pointers
+    ring: list | None = None           # pinned host staging slots for the table, with their events
+    slot: int = 0
+
+
+_RING = 4  # host staging slots per bucket (a slot is reused only after its copy has completed)
 
 
 class LagsSGD(torch.optim.Optimizer):
@@ -94,7 +100,7 @@ class LagsSGD(torch.optim.Optimizer):
     def __init__(self, params: Iterable[torch.nn.Parameter], lr: float, rho: float | None = None,
                  policy: CompressionPolicy | None = None, momentum: float = 0.0, process_group=None,
                  bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1,
-                 exchange: bool = True, delta_every: int = 0):
+                 exchange: bool = True, delta_every: int = 0, grads: str = "auto"):
         params = [p for p in params]
         if not params:
             raise ValueError("no parameters")
@@ -122,24 +128,6 @@ class LagsSGD(torch.optim.Optimizer):
         # every layer on the device (R: training.py:320-337, delta_log_every); it all-gathers the
         # residuals once per logged step (dense traffic, diagnostics only)
         self.delta_every = int(delta_every)
-        # flat per-rank buffers with the reference's layer layout; params and grads become views
-        n = sum(self.dims)
-        self.offsets = [0]
-        for d in self.dims[:-1]:
-            self.offsets.append(self.offsets[-1] + d)
-        with torch.no_grad():
-            self.flat_param = torch.empty(n, dtype=torch.float32, device=self.device)
-            self.flat_grad = torch.zeros(n, dtype=torch.float32, device=self.device)
-            self.residual = torch.zeros(n, dtype=torch.float32, device=self.device)
-            self.momentum_buf = torch.zeros(n, dtype=torch.float32, device=self.device) if self.mu else None
-            for p, off, d in zip(params, self.offsets, self.dims):
-                if p.dtype != torch.float32:
-                    raise TypeError("LagsSGD keeps fp32 parameters")
-                self.flat_param[off:off + d].copy_(p.detach().reshape(-1))
-                p.data = self.flat_param[off:off + d].view_as(p)
-                p.grad = self.flat_grad[off:off + d].view_as(p)
-        if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
-            dist.broadcast(self.flat_param, src=0, group=process_group)
         if engine_factory is None:
             from . import _native as N
             from .engine import Bucket
@@ -147,6 +135,35 @@ class LagsSGD(torch.optim.Optimizer):
             def engine_factory(dims, ks, world, device):
                 return Bucket(dims, ks, N.F32, device=device, max_world=world)
 
+        # gradients: "flat" -- p.grad are views of one flat buffer that autograd accumulates into
+        # and the compress clears; "tensors" -- autograd's own per-parameter tensors, read by the
+        # compress through a device pointer table and released afterwards (no accumulate kernels,
+        # no flat gradient buffer).  "auto" = tensors when the engine supports the table.
+        if grads not in ("auto", "flat", "tensors"):
+            raise ValueError(f"grads must be 'auto', 'flat' or 'tensors', got {grads!r}")
+        if grads == "auto":
+            probe = engine_factory([4], [1], 1, self.device)
+            grads = "tensors" if hasattr(probe, "set_grad_table") and self.device.type == "cuda" else "flat"
+            del probe
+        self.grads_mode = grads
+        # flat per-rank buffers with the reference's layer layout; params (and flat grads) are views
+        n = sum(self.dims)
+        self.offsets = [0]
+        for d in self.dims[:-1]:
+            self.offsets.append(self.offsets[-1] + d)
+        with torch.no_grad():
+            self.flat_param = torch.empty(n, dtype=torch.float32, device=self.device)
+            self.flat_grad = torch.zeros(n, dtype=torch.float32, device=self.device) if grads == "flat" else None
+            self.residual = torch.zeros(n, dtype=torch.float32, device=self.device)
+            self.momentum_buf = torch.zeros(n, dtype=torch.float32, device=self.device) if self.mu else None
+            for p, off, d in zip(params, self.offsets, self.dims):
+                if p.dtype != torch.float32:
+                    raise TypeError("LagsSGD keeps fp32 parameters")
+                self.flat_param[off:off + d].copy_(p.detach().reshape(-1))
+                p.data = self.flat_param[off:off + d].view_as(p)
+                p.grad = self.flat_grad[off:off + d].view_as(p) if grads == "flat" else None
+        if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
+            dist.broadcast(self.flat_param, src=0, group=process_group)
         self.engine_factory = engine_factory
         self.bucket_cap_bytes = int(bucket_cap_bytes)
         self._build_buckets()
@@ -172,6 +189,12 @@ class LagsSGD(torch.optim.Optimizer):
             msg_local = eng.new_messages(1)
             msg_all = eng.new_messages(self.world) if self.world > 1 else None
             b = _BucketRT(lo, hi, self.offsets[lo], sum(self.dims[lo:hi + 1]), eng, msg_local, msg_all)
+            if self.grads_mode == "tensors":
+                nl = hi - lo + 1
+                b.gtab = torch.zeros(nl, dtype=torch.int64, device=self.device)
+                b.ring = [(torch.zeros(nl, dtype=torch.int64, pin_memory=True), torch.cuda.Event())
+                          for _ in range(_RING)]
+                eng.set_grad_table(b.gtab)
             for l in range(lo, hi + 1):
                 self._bucket_of_param[id(self.params[l])] = len(self.buckets)
             self.buckets.append(b)
@@ -257,25 +280,53 @@ class LagsSGD(torch.optim.Optimizer):
     def _launch(self, i: int) -> None:
         b = self.buckets[i]
         lr = self.param_groups[0]["lr"]
-        g = self.flat_grad[b.offset:b.offset + b.numel]
         r = self.residual[b.offset:b.offset + b.numel]
         v = self.flat_param[b.offset:b.offset + b.numel]
         m = self.momentum_buf[b.offset:b.offset + b.numel] if self.momentum_buf is not None else None
         if self.side is None:
-            self._run_bucket(i, b, g, r, v, m, lr, None)
+            self._run_bucket(i, b, self.flat_grad[b.offset:b.offset + b.numel], r, v, m, lr, None)
             return
         cur = torch.cuda.current_stream(self.device)
         self.side.wait_stream(cur)  # the bucket's gradients are complete on the compute stream
         with torch.cuda.stream(self.side):
-            self._run_bucket(i, b, g, r, v, m, lr, self.side)
+            if self.grads_mode == "tensors":
+                held = self._stage_grad_table(b)
+                self._run_bucket(i, b, None, r, v, m, lr, self.side)
+                for p, gt in held:  # released to autograd: the next backward hands over a fresh tensor
+                    gt.record_stream(self.side)
+                    p.grad = None
+            else:
+                self._run_bucket(i, b, self.flat_grad[b.offset:b.offset + b.numel], r, v, m, lr, self.side)
+
+    def _stage_grad_table(self, b):
+        """Point the bucket's device table at its parameters' autograd gradient tensors (a pinned
+        host slot, copied on the side stream); unused parameters get zeros."""
+        host, ev = b.ring[b.slot]
+        ev.synchronize()  # this slot's previous copy (_RING launches ago) has completed
+        held = []
+        ptrs = host.numpy()
+        for q, l in enumerate(range(b.lo, b.hi + 1)):
+            p = self.params[l]
+            gt = p.grad
+            if gt is None:
+                gt = torch.zeros(self.dims[l], dtype=torch.float32, device=self.device)
+            elif gt.dtype != torch.float32 or not gt.is_contiguous():
+                gt = gt.float().contiguous()
+            held.append((p, gt))
+            ptrs[q] = gt.data_ptr()
+        b.gtab.copy_(host, non_blocking=True)
+        ev.record(self.side)
+        b.slot = (b.slot + 1) % _RING
+        return held
 
     def _run_bucket(self, i, b, g, r, v, m, lr, stream):
         t = self.timing[i] if self.timing is not None else None
         if t is not None:
             t[0].record(stream)
         local = self.world == 1 or not self.exchange
+        zg = g is not None  # flat gradients are cleared by the compress (fused zero_grad)
         if local and m is None and hasattr(b.engine, "step_local"):  # P = 1: update fused into selection
-            b.engine.step_local(g, r, lr, v, b.msg_local, self.status, stream=stream, zero_grad=True)
+            b.engine.step_local(g, r, lr, v, b.msg_local, self.status, stream=stream, zero_grad=zg)
             if t is not None:
                 t[1].record(stream)
                 t[2].record(stream)
@@ -283,7 +334,7 @@ class LagsSGD(torch.optim.Optimizer):
             if self._log_delta_now():
                 self._log_delta(b, r, b.msg_local, 1, stream)
             return
-        b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=True)
+        b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=zg)
         if t is not None:
             t[1].record(stream)
         if self.world > 1 and self.exchange:

@@ -54,7 +54,10 @@ def test_lagssgd_matches_oracle(L):
         v = orc.lags_step(v, [g], 0.05, opt.dims, opt.ks, res)
         assert opt.flat_param.cpu().numpy().tobytes() == v.tobytes(), t
         assert opt.residual.cpu().numpy().tobytes() == res[0].tobytes(), t
-        assert not torch.any(opt.flat_grad), "compress clears the gradients"
+        if opt.flat_grad is not None:
+            assert not torch.any(opt.flat_grad), "compress clears the gradients"
+        else:
+            assert all(p.grad is None for p in opt.params), "gradient tensors are released to autograd"
     # the model's parameters are views of the updated flat buffer
     w = model.l1.weight.detach().reshape(-1).cpu().numpy()
     assert w.tobytes() == v[:w.size].tobytes()
@@ -76,3 +79,41 @@ def test_lagssgd_divergence(L):
             model(torch.randn(4, 256, device="cuda")).sum().backward()
             opt.step()
             torch.cuda.synchronize()
+
+
+class Odd(torch.nn.Module):
+    """Odd parameter sizes: layer offsets that are not multiples of 4 elements (the per-layer
+    gradient tensors are then aligned differently from the flat residual -> scalar K1 tasks)."""
+
+    def __init__(self):
+        super().__init__()
+        self.a = torch.nn.Linear(37, 301)
+        self.b = torch.nn.Linear(301, 7)
+        self.c = torch.nn.Linear(7, 3)
+
+    def forward(self, x):
+        return self.c(torch.tanh(self.b(torch.tanh(self.a(x)))))
+
+
+@pytest.mark.parametrize("model_cls", [MLP, Odd])
+def test_grad_modes_bit_identical(L, model_cls):
+    """grads="tensors" (autograd tensors through the device pointer table) == grads="flat"."""
+    from paper_1911_08727_b200.optim import LagsSGD
+
+    outs = {}
+    for mode in ("flat", "tensors"):
+        torch.manual_seed(3)
+        model = model_cls().cuda()
+        opt = LagsSGD(model.parameters(), lr=0.05, rho=0.02, bucket_cap_bytes=2048, grads=mode)
+        assert opt.grads_mode == mode
+        gen = torch.Generator(device="cuda").manual_seed(9)
+        nin = model.l1.in_features if hasattr(model, "l1") else model.a.in_features
+        for t in range(6):
+            x = torch.randn(16, nin, device="cuda", generator=gen)
+            y = torch.randint(0, 3, (16,), device="cuda", generator=gen)
+            torch.nn.functional.cross_entropy(model(x), y).backward()
+            opt.step()
+        torch.cuda.synchronize()
+        outs[mode] = (opt.flat_param.cpu().numpy().tobytes(), opt.residual.cpu().numpy().tobytes())
+        opt.remove_hooks()
+    assert outs["flat"] == outs["tensors"]
