@@ -543,9 +543,15 @@ def measure_e2e(args, dims, ks, L, dev):
     torch.cuda.synchronize(dev)
     dt = (time.perf_counter() - t0) / steps
     comp_b, dec_b = algorithmic_bytes(n, ks, sum(ks), 1)
-    return {"value": round((comp_b + dec_b) / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": 3 * 4 * n,
-            "d2h_bytes_per_step": 2 * 4 * n, "ms_per_step": round(dt * 1e3, 3),
+    # bytes over PCIe per step: g and r up, the new r down (chunk-pipelined); v stays on the host
+    # (host threads copy it into the pinned output) and the decode reads / writes only the
+    # selected entries of that output through its device mapping (4 B each way per entry)
+    nsel = sum(ks)
+    return {"value": round((comp_b + dec_b) / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": 2 * 4 * n + 4 * nsel,
+            "d2h_bytes_per_step": 4 * n + 4 * nsel, "ms_per_step": round(dt * 1e3, 3),
             "api": "paper_1911_08727_b200.lags_step (drop-in for R: training.py:227) on host numpy LayeredVectors",
+            "transfer": "g, r up and r down in layer chunks on 2 copy streams; v copied host-side, selected "
+                        "entries of the pinned output updated in place by the decode (UVA)",
             "steps": steps, "world_used": 1}
 
 

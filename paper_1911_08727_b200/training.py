@@ -13,6 +13,7 @@ messages are decoded in rank order, and the results are copied back.
 
 from __future__ import annotations
 
+import os
 from collections import OrderedDict
 from dataclasses import dataclass
 from typing import Sequence
@@ -68,7 +69,7 @@ def _bucket_for(dims: tuple, ks: tuple, mode: int, world: int) -> Bucket:
     key = (dims, ks, mode, world, torch.cuda.current_device())
     b = _BUCKETS.get(key)
     if b is None:
-        if len(_BUCKETS) > 16:
+        if len(_BUCKETS) > 64:
             _BUCKETS.clear()
         b = Bucket(dims, ks, mode, max_world=world)
         _BUCKETS[key] = b
@@ -128,6 +129,26 @@ class HostPinner:
             t = st
         return t.to(device, non_blocking=True)
 
+    def source(self, arr: np.ndarray) -> torch.Tensor:
+        """A pinned CPU tensor holding arr's data (arr itself when page-locked, else a staged copy)."""
+        arr = np.ascontiguousarray(arr).reshape(-1)
+        t = torch.from_numpy(arr)
+        if self.pinned(arr):
+            return t
+        st = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        st.copy_(t)
+        return st
+
+    def dest(self, arr: np.ndarray, finish: list) -> torch.Tensor:
+        """A pinned CPU tensor to copy results into for arr (arr itself when page-locked; else a
+        staging buffer whose contents a finisher appended to ``finish`` copies into arr)."""
+        flat = arr.reshape(-1)
+        if arr.flags.c_contiguous and self.pinned(arr):
+            return torch.from_numpy(flat)
+        st = torch.empty(flat.shape, dtype=torch.from_numpy(flat[:0]).dtype, pin_memory=True)
+        finish.append(lambda: np.copyto(flat, st.numpy()))
+        return st
+
     def d2h_into(self, arr: np.ndarray, src: torch.Tensor):
         """Copy src into the numpy array; returns a finisher to call after synchronising."""
         if self.pinned(arr):
@@ -139,6 +160,154 @@ class HostPinner:
 
 
 _PINNER = HostPinner()
+
+
+_CHUNK_ELEMS = 4 << 20  # ~16 MB of fp32 per pipeline stage
+_STREAMS: dict = {}
+
+
+def _chunk_plan(dims: tuple) -> list:
+    """Consecutive layer ranges of about _CHUNK_ELEMS elements: (lo, hi_exclusive, elem_lo, elem_hi)."""
+    out, lo, acc, e0 = [], 0, 0, 0
+    for j, d in enumerate(dims):
+        acc += d
+        if acc - e0 >= _CHUNK_ELEMS or j == len(dims) - 1:
+            out.append((lo, j + 1, e0, acc))
+            lo, e0 = j + 1, acc
+    return out
+
+
+def _streams(dev):
+    key = dev.index
+    if key not in _STREAMS:
+        _STREAMS[key] = tuple(torch.cuda.Stream(dev) for _ in range(3))  # h2d, compute, d2h
+    return _STREAMS[key]
+
+
+_COPY_POOL = None
+_COPY_THREADS = 8  # host threads copying v into the pinned output of the drop-in step
+# diagnostics: set to a list to collect (phase, time.perf_counter()) marks of _pipelined_step
+PIPELINE_TRACE = None
+
+
+def _mark(label: str) -> None:
+    if PIPELINE_TRACE is not None:
+        import time
+
+        PIPELINE_TRACE.append((label, time.perf_counter()))
+
+
+def _host_copy(dst: np.ndarray, src: np.ndarray, plan: list) -> list:
+    """dst[:] = src (with dtype conversion) on host threads, chunk by chunk of ``plan`` in order;
+    returns one joiner per chunk."""
+    global _COPY_POOL
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _COPY_POOL = ThreadPoolExecutor(max_workers=min(_COPY_THREADS, os.cpu_count() or 1))
+    joins = []
+    for (_, _, e0, e1) in plan:
+        parts = max(1, min(4, (e1 - e0) // (1 << 20)))
+        bounds = [e0 + (e1 - e0) * i // parts for i in range(parts + 1)]
+        futs = [_COPY_POOL.submit(np.copyto, dst[a:b], src[a:b], "unsafe") for a, b in zip(bounds, bounds[1:])]
+        joins.append(lambda futs=futs: [f.result() for f in futs])
+    return joins
+
+
+def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
+    """The drop-in step with its host transfers overlapped, chunk by chunk of layers.
+
+    PCIe carries only what must cross it: the gradients and residuals up, the new residuals down
+    (R: training.py:252 updates them in place).  The new parameters differ from v only at the
+    selected entries, so v never crosses the link: host threads copy v into the (pinned) output
+    while the GPU works, and the decode then updates the selected entries of that output in place
+    through its device mapping (pinned host memory is device-addressable under UVA).
+    Order (R: training.py:174-175): every gradient goes up and is checked for finiteness before
+    any residual is written back; residual chunks stream up behind the gradients, each chunk's
+    compress runs as soon as it has arrived, and its new residual streams back on a third stream
+    while later chunks still upload (the copy engines run both directions at once)."""
+    _mark("start")
+    P = len(grads)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    s_up, s_cmp, s_down = _streams(dev)
+    cur = torch.cuda.current_stream(dev)
+    for s in (s_up, s_cmp, s_down):
+        s.wait_stream(cur)
+    pin = _PINNER
+    plan = _chunk_plan(dims)
+    out_dtype = np.float64 if promote_v else v.dtype
+    out = torch.empty(v.shape, dtype=torch.from_numpy(np.empty(0, out_dtype)).dtype, pin_memory=True)
+    join_copy = _host_copy(out.numpy(), v.reshape(-1), plan)  # per chunk; overlaps everything below
+    g_src = [pin.source(g) for g in grads]
+    r_src = [pin.source(r) for r in residuals]
+    with torch.cuda.stream(s_up):
+        g_dev = [[torch.empty(e1 - e0, dtype=g.dtype, device=dev) for (_, _, e0, e1) in plan] for g in g_src]
+        for p in range(P):
+            for (_, _, e0, e1), gd in zip(plan, g_dev[p]):
+                gd.copy_(g_src[p][e0:e1], non_blocking=True)
+        ev_g = torch.cuda.Event()
+        ev_g.record(s_up)
+        r_dev, ev_in = [], []
+        for (_, _, e0, e1) in plan:
+            r_dev.append([r_src[p][e0:e1].to(dev, non_blocking=True) for p in range(P)])
+            e = torch.cuda.Event()
+            e.record(s_up)
+            ev_in.append(e)
+    with torch.cuda.stream(s_cmp):
+        s_cmp.wait_event(ev_g)
+        pre = torch.zeros(P, dtype=torch.int32, device=dev)
+        for p in range(P):
+            for gd in g_dev[p]:
+                N.check(N.lags_check_finite(N.F64 if gd.dtype == torch.float64 else N.F32, gd.data_ptr(), gd.numel(),
+                                            pre[p:p + 1].data_ptr(), s_cmp.cuda_stream), "lags_check_finite")
+        pre_h = torch.empty(P, dtype=torch.int32, pin_memory=True)
+        pre_h.copy_(pre, non_blocking=True)
+        ev_pre = torch.cuda.Event()
+        ev_pre.record(s_cmp)
+        # every chunk's compress is queued now (it writes device buffers only), so it runs the
+        # moment the chunk has arrived, whatever the host is doing
+        status = torch.zeros(P, dtype=torch.int32, device=dev)
+        staged = []
+        for c, (lo, hi, e0, e1) in enumerate(plan):
+            bucket = _bucket_for(dims[lo:hi], ks[lo:hi], mode, P)
+            s_cmp.wait_event(ev_in[c])
+            msgs = bucket.new_messages(P)
+            for p in range(P):
+                bucket.compress(g_dev[p][c], r_dev[c][p], alpha, msgs[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes],
+                                status[p:p + 1], stream=s_cmp)
+            done = torch.cuda.Event()
+            done.record(s_cmp)
+            staged.append((bucket, msgs, e0, e1, done))
+    _mark("uploads and compress enqueued")
+    ev_pre.synchronize()
+    _mark("gradients checked")
+    bad = [p for p in range(P) if pre_h[p] & N.STATUS_NONFINITE]
+    if bad:  # R: training.py:174-175 -- raised before any residual is written back
+        for j in join_copy:
+            j()
+        for s in (s_up, s_cmp, s_down):
+            s.synchronize()
+        raise DivergenceError(f"worker {bad[0] + 1} produced a non-finite gradient", iteration=t)
+    finish = []
+    r_dst = [pin.dest(r, finish) for r in residuals]
+    with torch.cuda.stream(s_down):  # new residuals back, chunk by chunk as they are computed
+        for c, (_, _, e0, e1, done) in enumerate(staged):
+            s_down.wait_event(done)
+            for p in range(P):
+                r_dst[p][e0:e1].copy_(r_dev[c][p], non_blocking=True)
+    with torch.cuda.stream(s_cmp):
+        for c, (bucket, msgs, e0, e1, _) in enumerate(staged):
+            join_copy[c]()  # this chunk of the output holds v: update its selected entries in place
+            bucket.decode(msgs, P, out[e0:e1], stream=s_cmp)
+    _mark("chunks enqueued")
+    s_cmp.synchronize()
+    _mark("decode done")
+    s_down.synchronize()
+    _mark("residuals down")
+    for f in finish:
+        f()
+    cur.wait_stream(s_down)
+    return out
 
 
 def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: int | None = None):
@@ -205,35 +374,6 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
         if not 1 <= k <= d:  # R: sparsify.py:82-83 (raised before any residual is touched)
             raise ValueError(f"k={k} outside 1..{d}")
         ks.append(k)
-    bucket = _bucket_for(dims, tuple(ks), mode, P)
-
-    dev = torch.device("cuda", torch.cuda.current_device())
-    pin = _PINNER
-    v_d = pin.h2d(v.data, dev)
-    if _promote_v and v_d.dtype == torch.float32:
-        v_d = v_d.double()
-    msgs = bucket.new_messages(P)
-    r_devs = []
-    fused = P == 1 and mode == N.F32 and v_d.dtype == torch.float32
-    for p in range(P):
-        g_d = pin.h2d(grads[p].data, dev)
-        r_d = pin.h2d(residuals[p].data, dev)
-        msg_p = msgs[p * bucket.msg_bytes:(p + 1) * bucket.msg_bytes]
-        if fused:  # one worker: the update is fused into the selection epilogue
-            bucket.step_local(g_d, r_d, alpha, v_d, msg_p, status[p:p + 1])
-        else:
-            bucket.compress(g_d, r_d, alpha, msg_p, status[p:p + 1])
-        r_devs.append(r_d)
-    if not fused:
-        bucket.decode(msgs, P, v_d)
-    out = torch.empty(v_d.shape, dtype=v_d.dtype, pin_memory=True)
-    out.copy_(v_d, non_blocking=True)
-    st = status.cpu().numpy()  # synchronises: inputs copied, compress + decode done
-    for p in range(P):
-        if st[p] & N.STATUS_NONFINITE:  # residuals untouched on the host, as in the reference
-            raise DivergenceError(f"worker {p + 1} produced a non-finite gradient", iteration=t)
-    finish = [pin.d2h_into(res.data, r_d) for r_d, res in zip(r_devs, residuals)]
-    torch.cuda.current_stream(dev).synchronize()
-    for f in finish:
-        f()
+    out = _pipelined_step(v.data, [g.data for g in grads], [r.data for r in residuals], alpha, dims, tuple(ks),
+                          mode, t, _promote_v)
     return type(v)(v.shape, out.numpy())
