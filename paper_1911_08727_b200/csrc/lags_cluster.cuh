@@ -232,13 +232,15 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
 }
 
 // The whole selection of an fp32 compress in ONE launch (thread-block clusters of CLUSTER CTAs):
-// the first CLUSTER * n_cl CTAs select the largest layers, one cluster per layer; the remaining
-// CTAs walk the other layers persistently (largest estimated work first, first layer by block
+// the first CLUSTER * n_cl CTAs select the largest layers, one cluster per layer; the next CTAs
+// select the tiny layers, one warp per layer (warp_topk_layer); the remaining CTAs walk the
+// other layers persistently (largest estimated work first, first layer by block
 // index, then an atomic counter).  One launch, so no CTA ever waits on another kernel while
 // holding an SM -- this matters when the compress runs beside backprop on a side stream.
-__global__ void __launch_bounds__(SEL_NT, 1) select_kernel(
+__global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
     const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks, const int32_t* __restrict__ cl_layers,
-    int n_cl, const int32_t* __restrict__ order, int nl, FastState* state, const int32_t* __restrict__ cand_cnt,
+    int n_cl, const int32_t* __restrict__ tiny_layers, int n_tiny, const int32_t* __restrict__ order, int nl,
+    FastState* state, const int32_t* __restrict__ cand_cnt,
     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval,
     float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, CoopScratch sc,
     float* vupd) {
@@ -255,8 +257,20 @@ __global__ void __launch_bounds__(SEL_NT, 1) select_kernel(
                          t_launch);
     return;
   }
-  const int grid = static_cast<int>(gridDim.x) - cl_ctas;
-  for (int pos = static_cast<int>(blockIdx.x) - cl_ctas; pos < nl;) {
+  // tiny layers: one warp each, in the CTAs right after the clusters (all in the first wave)
+  constexpr int NW = SEL_NT / 32;
+  const int tiny_ctas = (n_tiny + NW - 1) / NW;
+  if (static_cast<int>(blockIdx.x) < cl_ctas + tiny_ctas) {
+    const int t = (static_cast<int>(blockIdx.x) - cl_ctas) * NW + static_cast<int>(threadIdx.x >> 5);
+    if (t < n_tiny) {
+      const int j = tiny_layers[t];
+      warp_topk_layer(j, layers[j], state, r, idx_out, val_out, count_out, vupd, t_launch);
+    }
+    return;
+  }
+  const int base = cl_ctas + tiny_ctas;
+  const int grid = static_cast<int>(gridDim.x) - base;
+  for (int pos = static_cast<int>(blockIdx.x) - base; pos < nl;) {
     if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + grid;
     select_layer(order[pos], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out,
                  val_out, count_out, dyn, smem_words, force_exact, cs, vupd, t_launch);

@@ -26,7 +26,8 @@ namespace lags {
 #define LAGS_K1_UNROLL 4
 #endif
 constexpr int TASK_ELEMS = LAGS_TASK_ELEMS;  // elements per streaming task (one warp)
-constexpr int SMALL_LAYER = 16384; // layers up to this size always take the dense exact path
+constexpr int SMALL_LAYER = 16384; // layers up to this size stage their dense exact path in smem
+constexpr int TINY_LAYER = 4096;   // layers up to this size always take it (cheaper than candidates)
 constexpr int K1_WARPS = 8;        // warps per K1 CTA
 constexpr int K1_UNROLL = LAGS_K1_UNROLL;        // float4 loads in flight per lane per operand (K1)
 constexpr int PRED_FACTOR = 3;     // predicted threshold targets PRED_FACTOR * k candidates
@@ -258,40 +259,6 @@ __device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32
     for (int u = 0; u < B; ++u)
       if (ix[u] >= 0) vl[ix[u]] = single_rank_update(w[u], x[u]);
   }
-}
-
-// Dense exact top-k of a small layer staged once in shared memory (`sv`, >= d floats): every
-// radix pass and the compaction then read shared memory instead of L2.
-__device__ uint32_t small_dense_select(float* data, int64_t d, uint32_t k, int32_t* oidx, float* oval, float* sv,
-                                       CoopSmem& cs, float* vl) {
-  const bool vec = ((reinterpret_cast<uintptr_t>(data) & 15u) == 0u);
-  if (vec) {
-    const float4* d4 = reinterpret_cast<const float4*>(data);
-    float4* s4 = reinterpret_cast<float4*>(sv);
-    const int64_t n4 = d >> 2;
-#pragma unroll 4
-    for (int64_t i = threadIdx.x; i < n4; i += SEL_NT) s4[i] = __ldcg(d4 + i);
-    for (int64_t i = 4 * n4 + threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
-  } else {
-#pragma unroll 4
-    for (int64_t i = threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
-  }
-  __syncthreads();
-  auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
-  const auto th = radix_select<uint32_t, 31, Key<float>::RB>(key_at, d, k, cs.sm, 0, nullptr, true);
-  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
-    *x = sv[i];
-    *key = Key<float>::of(*x);
-    *ix = i;
-  };
-  auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
-    oidx[pos] = static_cast<int32_t>(i);
-    oval[pos] = x;
-    data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
-  };
-  const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
-  if (vl) apply_single_rank_updates(vl, oidx, oval, cnt);
-  return cnt;
 }
 
 // Two ranks in one set of radix passes over m keys (shared memory): the exact threshold of the
@@ -566,6 +533,208 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
   }
 }
 
+// Dense exact path of a small layer (d <= SMALL_LAYER): staged once in shared memory, so the
+// radix passes and the compaction read shared memory; the same dual-rank select predicts the
+// next candidate threshold (small layers then take the candidate path like the big ones).
+__device__ void small_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
+                                      float* val_out, int32_t* count_out, FastState* state, bool force_exact, int why,
+                                      CoopSmem& cs, float* vupd, float* sv, bool predict) {
+  float* data = r + L.offset;
+  const int64_t d = L.dim;
+  const uint32_t k = static_cast<uint32_t>(L.k);
+  if ((reinterpret_cast<uintptr_t>(data) & 15u) == 0u) {
+    const float4* d4 = reinterpret_cast<const float4*>(data);
+    float4* s4 = reinterpret_cast<float4*>(sv);
+    const int64_t n4 = d >> 2;
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < n4; i += SEL_NT) s4[i] = __ldcg(d4 + i);
+    for (int64_t i = 4 * n4 + threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
+  } else {
+#pragma unroll 4
+    for (int64_t i = threadIdx.x; i < d; i += SEL_NT) sv[i] = __ldcg(data + i);
+  }
+  __syncthreads();
+  const bool predicted = st.thr != 0u && !force_exact;
+  const float pf_next = !predicted ? pred_factor(st)
+                                   : (why == FB_OVERFLOW ? 0.5f * pred_factor(st) : 2.0f * pred_factor(st));
+  const int64_t pk = static_cast<int64_t>(fmaxf(pf_next, 1.0f) * static_cast<float>(k));
+  const uint32_t k2 = static_cast<uint32_t>(pk < d ? (pk > k ? pk : k + 1) : d);
+  auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
+  SelectThreshold<uint32_t> th;
+  uint32_t key2;
+  radix_select_dual(key_at, d, k, k2, cs, &th, &key2, true);
+  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
+    *x = sv[i];
+    *key = Key<float>::of(*x);
+    *ix = i;
+  };
+  int32_t* oidx = idx_out + L.slot;
+  float* oval = val_out + L.slot;
+  auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
+    oidx[pos] = static_cast<int32_t>(i);
+    oval[pos] = x;
+    data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+  };
+  const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
+  if (vupd) apply_single_rank_updates(vupd + L.offset, oidx, oval, cnt);
+  if (threadIdx.x == 0) {
+    count_out[j] = static_cast<int32_t>(cnt);
+    FastState ns = st;
+    ns.thr = predict ? max(key2, 1u) : 0u;  // 1: every nonzero entry is a candidate (layer mostly zeros)
+    ns.fallbacks += predicted ? 1u : 0u;
+    ns.last_cands = 0;
+    ns.calls += 1;
+    ns.pf256 = pf_encode(pf_next);
+    state[j] = ns;
+  }
+}
+
+// Exact top-k of a tiny layer (d <= TINY_LAYER, k <= WARP_TOPK) by ONE warp, no barriers: every
+// lane keeps its WARP_TOPK largest (|x| key, index) of a lane-strided scan in registers (an
+// insertion chain; on equal keys the earlier = lower index stays ahead), then k rounds of a warp
+// argmax over the lanes' heads (key, then lower index) take the layer's top-k; zero keys are
+// never selected (R: sparsify.py:84-90).  Output in ascending index order, residual zeroed, the
+// optional fused P = 1 update applied.
+#ifndef LAGS_WARP_B
+#define LAGS_WARP_B 2  // small unrolls: the code footprint (instruction cache) dominates this path
+#endif
+#ifndef LAGS_WARP_TOPK
+#define LAGS_WARP_TOPK 8
+#endif
+constexpr int WARP_TOPK = LAGS_WARP_TOPK;
+
+__device__ void warp_topk_layer(int j, const lags_layer_t& L, FastState* state, float* r, int32_t* idx_out,
+                                float* val_out, int32_t* count_out, float* vupd, uint32_t t_launch) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t t_start = globaltimer_lo();
+  const long long c0 = clock64();
+  float* data = r + L.offset;
+  float val[WARP_TOPK];
+  int32_t ix[WARP_TOPK];
+#pragma unroll
+  for (int q = 0; q < WARP_TOPK; ++q) {
+    val[q] = 0.0f;
+    ix[q] = 0x7fffffff;
+  }
+  const int d = static_cast<int>(L.dim);
+  const uint32_t k = static_cast<uint32_t>(L.k);
+  const bool vec = (reinterpret_cast<uintptr_t>(data) & 15u) == 0u;
+  const float4* d4 = reinterpret_cast<const float4*>(data);
+  const int n4 = vec ? d >> 2 : 0;
+  // every lane visits its elements in ascending index order (the tie rule needs it); the loads
+  // of a batch are issued together (LAGS_WARP_B x 16 B per lane in flight)
+  constexpr int B = LAGS_WARP_B;
+  auto scan = [&](auto&& visit) {
+    for (int q0 = lane; q0 < n4; q0 += 32 * B) {
+      float4 x[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) x[u] = q0 + 32 * u < n4 ? __ldcg(d4 + q0 + 32 * u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int e = 4 * (q0 + 32 * u);
+        visit(x[u].x, e);
+        visit(x[u].y, e + 1);
+        visit(x[u].z, e + 2);
+        visit(x[u].w, e + 3);
+      }
+    }
+    for (int i0 = 4 * n4 + lane; i0 < d; i0 += 32 * B) {
+      float x[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) x[u] = i0 + 32 * u < d ? __ldcg(data + i0 + 32 * u) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < B; ++u) visit(x[u], i0 + 32 * u);
+    }
+  };
+  // pass 1: a warp-wide lower bound of the k-th largest key -- the k-th largest of the 32 lane
+  // maxima (at least k elements reach it); zero keys are never selected
+  uint32_t lmax = 0;
+  scan([&](float x, int) { lmax = max(lmax, Key<float>::of(x)); });
+  uint32_t bound = 0, m = lmax;
+  for (uint32_t q = 0; q < k && q < 32u; ++q) {
+    bound = __reduce_max_sync(0xffffffffu, m);
+    const unsigned who = __ballot_sync(0xffffffffu, m == bound);
+    if (lane == __ffs(who) - 1) m = 0;
+  }
+  bound = max(bound, 1u);
+  // pass 2: each lane keeps its WARP_TOPK largest entries at or above the bound (rarely more
+  // than a few), an insertion chain where equal keys keep the earlier = lower index ahead
+  scan([&](float cv, int ci) {
+    if (Key<float>::of(cv) >= bound && Key<float>::of(cv) > Key<float>::of(val[WARP_TOPK - 1])) {
+#pragma unroll
+      for (int q = 0; q < WARP_TOPK; ++q) {
+        if (Key<float>::of(cv) > Key<float>::of(val[q])) {
+          const float tv = val[q];
+          const int32_t ti = ix[q];
+          val[q] = cv;
+          ix[q] = ci;
+          cv = tv;
+          ci = ti;
+        }
+      }
+    }
+  });
+  const long long c1 = clock64();
+  // merge: round q's winner is kept by lane q
+  float my_val = 0.0f;
+  int32_t my_ix = 0x7fffffff;
+  uint32_t cnt = 0;
+  for (uint32_t q = 0; q < k; ++q) {
+    const uint32_t key = Key<float>::of(val[0]);
+    unsigned long long best = (static_cast<unsigned long long>(key) << 32) | static_cast<uint32_t>(~ix[0]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other > best ? other : best;
+    }
+    if ((best >> 32) == 0ull) break;  // no nonzero key left
+    const int32_t wi = static_cast<int32_t>(~static_cast<uint32_t>(best));
+    const bool mine = key == static_cast<uint32_t>(best >> 32) && ix[0] == wi;
+    const unsigned wl = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+    const float wv = __shfl_sync(0xffffffffu, val[0], wl);
+    if (lane == static_cast<int>(q)) {
+      my_val = wv;
+      my_ix = wi;
+    }
+    if (mine) {  // pop the head
+#pragma unroll
+      for (int t = 0; t + 1 < WARP_TOPK; ++t) {
+        val[t] = val[t + 1];
+        ix[t] = ix[t + 1];
+      }
+      val[WARP_TOPK - 1] = 0.0f;
+      ix[WARP_TOPK - 1] = 0x7fffffff;
+    }
+    ++cnt;
+  }
+  const long long c2 = clock64();
+  // ascending index order: a winner's position = winners with a smaller index
+  uint32_t pos = 0;
+  for (uint32_t q = 0; q < cnt; ++q) pos += __shfl_sync(0xffffffffu, my_ix, q) < my_ix ? 1u : 0u;
+  if (static_cast<uint32_t>(lane) < cnt) {
+    idx_out[L.slot + pos] = my_ix;
+    val_out[L.slot + pos] = my_val;
+    data[my_ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    if (vupd) vupd[L.offset + my_ix] = single_rank_update(vupd[L.offset + my_ix], my_val);
+  }
+  if (lane == 0) {
+    const long long c3 = clock64();
+    auto q64 = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
+    count_out[j] = static_cast<int32_t>(cnt);
+    FastState ns = state[j];
+    ns.thr = 0u;
+    ns.last_cands = 0u;
+    ns.calls += 1;
+    ns.path = 0u;
+    ns.cycles = static_cast<uint32_t>(c3 - c0);
+    ns.reserved = q64(c1 - c0) | (q64(c2 - c1) << 11) | (q64(c3 - c2) << 22);
+    ns.t_start = t_start;
+    ns.t_end = globaltimer_lo();
+    ns.t_launch = t_launch;
+    state[j] = ns;
+  }
+}
+
 // Selection of layer j by the whole CTA (all paths), with its diagnostic timeline entry.
 __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks,
                              FastState* state, const int32_t* cand_cnt, const int32_t* cand_idx, const float* cand_val,
@@ -576,27 +745,19 @@ __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, con
   const lags_layer_t L = layers[j];
   const FastState st = state[j];
   const long long t_begin = clock64();
-  uint32_t path;
-  if (L.dim <= SMALL_LAYER) {  // SMALL_LAYER <= shared-memory staging capacity
-    const uint32_t cnt = small_dense_select(r + L.offset, L.dim, static_cast<uint32_t>(L.k), idx_out + L.slot,
-                                            val_out + L.slot, reinterpret_cast<float*>(skeys), cs,
-                                            vupd ? vupd + L.offset : nullptr);
-    if (threadIdx.x == 0) {
-      count_out[j] = static_cast<int32_t>(cnt);
-      FastState ns = st;
-      ns.calls += 1;
-      state[j] = ns;
-    }
-    path = 0u;
-  } else {
-    const int why = (force_exact || st.thr == 0u)
-                        ? FB_TOO_FEW
-                        : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
-                                           idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
-    // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA
-    if (why) dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
-    path = why ? 2u : 1u;
-  }
+  const bool tiny = L.dim <= TINY_LAYER;
+  const int why = (force_exact || st.thr == 0u || tiny)
+                      ? FB_TOO_FEW
+                      : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
+                                         idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
+  // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA (small
+  // layers staged in shared memory; SMALL_LAYER <= the staging capacity)
+  if (why && L.dim <= SMALL_LAYER)
+    small_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd,
+                          reinterpret_cast<float*>(skeys), !tiny);
+  else if (why)
+    dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
+  const uint32_t path = why ? (L.dim <= SMALL_LAYER ? 0u : 2u) : 1u;
   __syncthreads();
   if (threadIdx.x == 0) {
     state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);

@@ -294,8 +294,7 @@ struct lags_bucket {
     int task_base = 0, ntasks = 0;    // contiguous range of the task table
     int order_base = 0, nlayers = 0;  // contiguous range of `order`
   };
-  int ngroups = 1;
-  Group grp[2];
+  Group grp[3];
   CoopScratch coop{};  // per-call selection counter (two-kernel path)
   cudaEvent_t probe_before = nullptr, probe_after = nullptr;  // caller-owned, optional
   float* const* grad_table = nullptr;  // caller-owned device array of per-layer gradient pointers
@@ -362,7 +361,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "unknown dtype");
   if (!dims || !ks || L <= 0) return fail(LAGS_ERR_INVALID_ARG, "empty bucket");
   if (max_world < 1 || max_world > 32) return fail(LAGS_ERR_INVALID_ARG, "max_world must be in 1..32");
-  double max_density = 0.0;
+  double max_per_task = 0.0;  // expected selected entries in one task of a layer
   for (int j = 0; j < L; ++j) {
     if (dims[j] < 1) return fail(LAGS_ERR_STRUCTURE, "layer " + std::to_string(j + 1) + ": dim must be positive");
     if (dims[j] > 0x7fffffffLL) return fail(LAGS_ERR_INVALID_ARG, "layer dim exceeds the int32 index range");
@@ -371,10 +370,11 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
     p->n_total += dims[j];
     p->total_k += ks[j];
     p->ntasks += static_cast<int32_t>((dims[j] + TASK_ELEMS - 1) / TASK_ELEMS);
-    if (dims[j] > SMALL_LAYER) max_density = std::max(max_density, static_cast<double>(ks[j]) / dims[j]);
+    max_per_task = std::max(max_per_task, static_cast<double>(ks[j]) * std::min<int64_t>(dims[j], TASK_ELEMS) / dims[j]);
   }
-  // per-task candidate capacity: 16x the expected PRED_FACTOR*k/d share, power of two in [256, TASK]
-  const double want = 16.0 * PRED_FACTOR * max_density * TASK_ELEMS;
+  // per-task candidate capacity: 16x the expected PRED_FACTOR * (selected per task), power of two
+  // in [256, TASK]
+  const double want = 16.0 * PRED_FACTOR * max_per_task;
   int cap = 256;
   while (cap < want && cap < TASK_ELEMS) cap <<= 1;
   p->cap = dtype == LAGS_F32 ? cap : 0;
@@ -407,10 +407,14 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
 }
 
 // Selection groups of an fp32 bucket: 0 = one CTA per layer (select_kernel's persistent role),
-// 1 = the largest layers, one thread-block cluster per layer (select_kernel's cluster role).
+// 1 = the largest layers, one thread-block cluster per layer (select_kernel's cluster role),
+// 2 = tiny layers with k <= WARP_TOPK, one warp per layer (select_kernel's warp role).
 std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
   std::vector<int> gid(L, 0);
-  for (int j = 0; j < L; ++j) gid[j] = (dims[j] > SMALL_LAYER && ks[j] >= CLUSTER_MIN_K) ? 1 : 0;
+  for (int j = 0; j < L; ++j) {
+    if (dims[j] > SMALL_LAYER && ks[j] >= CLUSTER_MIN_K) gid[j] = 1;
+    else if (dims[j] <= TINY_LAYER && ks[j] <= WARP_TOPK) gid[j] = 2;
+  }
   return gid;
 }
 
@@ -523,7 +527,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     off += dims[j];
     slot += ks[j];
   }
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < 3; ++g) {
     b->grp[g].task_base = static_cast<int>(tasks.size());
     for (int j = 0; j < nlayers; ++j) {
       if (gid[j] != g) continue;
@@ -539,7 +543,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   std::vector<double> cost(nlayers);
   for (int j = 0; j < nlayers; ++j)
     cost[j] = dims[j] <= SMALL_LAYER ? 5.0 * dims[j] : 40.0 * ks[j] + 64.0 * (ltasks[j].y - ltasks[j].x);
-  for (int g = 0; g < 2; ++g) {
+  for (int g = 0; g < 3; ++g) {
     b->grp[g].order_base = static_cast<int>(order.size());
     std::vector<int32_t> og;
     for (int j = 0; j < nlayers; ++j)
@@ -548,7 +552,6 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     order.insert(order.end(), og.begin(), og.end());
     b->grp[g].nlayers = static_cast<int>(og.size());
   }
-  b->ngroups = b->grp[1].nlayers > 0 ? 2 : 1;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool ok =
       cudaMemcpyAsync(b->layers, layers.data(), sizeof(lags_layer_t) * nlayers, cudaMemcpyHostToDevice, s) ==
@@ -640,24 +643,27 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     cudaError_t e = cudaSuccess;
     lags_bucket::Group all = b->grp[0];  // K1 streams every task (group 0's then group 1's)
     all.task_base = 0;
-    all.ntasks = b->grp[0].ntasks + b->grp[1].ntasks;
+    all.ntasks = b->grp[0].ntasks + b->grp[1].ntasks + b->grp[2].ntasks;
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
     if (e == cudaSuccess) e = k1(all, s);
     if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
     if (e == cudaSuccess) {
       // the selection: one launch (PDL behind K1).  Group 1 (the largest layers): one 4-CTA
-      // cluster each; group 0: persistent CTAs, one wave on the SMs the clusters leave free.
+      // cluster each; group 2 (tiny layers): one warp each; group 0: persistent CTAs, one wave
+      // on the SMs the others leave free.
       const lags_bucket::Group& G0 = b->grp[0];
       const lags_bucket::Group& G1 = b->grp[1];
-      const int ncl = b->ngroups == 2 ? G1.nlayers : 0;
+      const lags_bucket::Group& G2 = b->grp[2];
+      const int ncl = G1.nlayers;
       const int cl = ncl > 0 ? CLUSTER : 1;
-      int per = std::min(G0.nlayers, std::max(num_sms() - ncl * CLUSTER, num_sms() / 2));
-      per = (per + cl - 1) / cl * cl;  // the grid is a whole number of clusters
-      const int grid = ncl * CLUSTER + per;
+      const int tiny_ctas = (G2.nlayers + SEL_NT / 32 - 1) / (SEL_NT / 32);
+      const int fixed = ncl * CLUSTER + tiny_ctas;
+      const int per = std::min(G0.nlayers, std::max(SEL_MINB * num_sms() - fixed, num_sms() / 2));
+      const int grid = (fixed + per + cl - 1) / cl * cl;  // a whole number of clusters
       e = launch_pdl_cluster(select_kernel, dim3(grid), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s, cl,
-                             b->layers, b->layer_tasks, b->order + G1.order_base, ncl, b->order + G0.order_base,
-                             G0.nlayers, b->state, b->cand_cnt, b->cand_idx, b->cand_val, b->cap, b->gidx, b->gval,
-                             rr, idx, vals, cnt, b->smem_keys, fe, b->coop, vu);
+                             b->layers, b->layer_tasks, b->order + G1.order_base, ncl, b->order + G2.order_base,
+                             G2.nlayers, b->order + G0.order_base, G0.nlayers, b->state, b->cand_cnt, b->cand_idx,
+                             b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->coop, vu);
     }
     const int launches = 2;
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));

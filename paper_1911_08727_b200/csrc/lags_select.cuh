@@ -12,7 +12,11 @@ namespace lags {
 #ifndef LAGS_SEL_NT
 #define LAGS_SEL_NT 512
 #endif
-constexpr int SEL_NT = LAGS_SEL_NT;  // threads per selection CTA (512 measured faster than 1024)
+#ifndef LAGS_SEL_MINB
+#define LAGS_SEL_MINB 1
+#endif
+constexpr int SEL_NT = LAGS_SEL_NT;      // threads per selection CTA (512 measured faster than 1024)
+constexpr int SEL_MINB = LAGS_SEL_MINB;  // selection CTAs resident per SM (launch bounds)
 constexpr int SEL_VEC = 4;    // consecutive elements per thread per compaction chunk
 
 // Select (key & pmask) > prefix, plus the first `need_eq` (in scan order) with

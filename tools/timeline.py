@@ -100,7 +100,7 @@ def main():
         big = max(js, key=lambda j: dims[j])
         print(f"  path {names.get(p, p)}: {len(js)} layers, us per layer median {np.median(du):.2f} max {du.max():.2f}"
               f" sum {du.sum():.1f}; largest dim {dims[big]} took {end[big] - start[big]:.2f}")
-        if p in (1, 3):
+        if p in (0, 1, 3):
             print("    phases of the 4 largest:",
                   [(dims[j], ph(s[j, 7])) for j in sorted(js, key=lambda j: -dims[j])[:4]])
 
