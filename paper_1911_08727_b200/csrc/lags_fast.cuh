@@ -28,7 +28,14 @@ namespace lags {
 constexpr int TASK_ELEMS = LAGS_TASK_ELEMS;  // elements per streaming task (one warp)
 constexpr int SMALL_LAYER = 16384; // layers up to this size stage their dense exact path in smem
 constexpr int TINY_LAYER = 4096;   // layers up to this size always take it (cheaper than candidates)
-constexpr int K1_WARPS = 8;        // warps per K1 CTA
+#ifndef LAGS_K1_WARPS
+#define LAGS_K1_WARPS 8
+#endif
+#ifndef LAGS_K1_MINB
+#define LAGS_K1_MINB 1
+#endif
+constexpr int K1_WARPS = LAGS_K1_WARPS;  // warps per K1 CTA
+constexpr int K1_MINB = LAGS_K1_MINB;    // K1 CTAs per SM the register allocation must allow
 constexpr int K1_UNROLL = LAGS_K1_UNROLL;        // float4 loads in flight per lane per operand (K1)
 constexpr int PRED_FACTOR = 3;     // predicted threshold targets PRED_FACTOR * k candidates
 constexpr int F32_PASSES = 3;      // radix passes for 31-bit keys with 11-bit digits
@@ -199,7 +206,7 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
 
 // K1: one warp per task.  gtab (nullable): per-layer gradient pointers replacing the flat g.
 template <bool ZERO_G>
-__global__ void __launch_bounds__(K1_WARPS * 32) accum_emit_kernel(
+__global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
     const FastState* __restrict__ state, float* __restrict__ g, float* const* __restrict__ gtab,
     float* __restrict__ r, float alpha, int cap, int32_t* __restrict__ cand_idx, float* __restrict__ cand_val,

@@ -93,6 +93,8 @@ def main():
     print("  start after griddep wait: min %.2f max %.2f" % (min(start), max(start)))
     ph = lambda w: (int(w) & 2047, (int(w) >> 11) & 2047, (int(w) >> 22) & 2047)  # noqa: E731
     print("  phases x64 cycles (gather, select, compact) of the slowest:", [ph(s[j, 7]) for j in rows[:6]])
+    fb = [(dims[j], ks[j], int(s[j, 1]), int(s[j, 3])) for j in range(len(dims)) if s[j, 1]]
+    print("  layers with dense fallbacks (dim, k, fallbacks, calls):", fb[:12])
     names = {0: "small-dense", 1: "candidate", 2: "dense-fallback", 3: "cluster"}
     for p in sorted(set(int(x) for x in s[:, 5])):
         js = [j for j in range(len(dims)) if s[j, 5] == p]
