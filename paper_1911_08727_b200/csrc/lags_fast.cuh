@@ -5,12 +5,14 @@
 //    once (16-byte vectors), writes acc back into r, ORs the non-finite flag, and appends every
 //    entry with key(acc) >= thr[layer] to the task's candidate list in ascending index order
 //    (warp ballot + shuffle scan, no atomics).  Algorithmic traffic: 12 B/element.
-// K2a (select_phase1_kernel, one CTA per layer, largest work first): a big layer whose candidate
-//    set provably holds its top-k (count >= k, no task overflow) is selected from the candidates
-//    alone (dual-rank radix select in shared memory, ordered compaction, residual zeroing by
-//    scatter) and predicts its next threshold; small layers run the dense exact path staged in
-//    shared memory; other big layers are queued.
-//    A layer whose candidate set fails the proof runs the dense exact path over r in its CTA.
+// Selection (select_kernel, lags_cluster.cuh, one launch) per layer:
+//  - tiny layers: warp_topk_layer, one warp, register top-k (no prediction needed);
+//  - other layers with a prediction: candidate_select (or cluster_select_layer for the largest),
+//    when the candidate set provably holds the top-k (count >= k, no task overflow): dual-rank
+//    radix select in shared memory, ordered compaction, residual zeroing by scatter, and the
+//    next threshold;
+//  - otherwise the dense exact path in the same CTA (small_fallback_select staged in shared
+//    memory, dense_fallback_select over r), which also yields the next prediction.
 // Every path returns exactly the reference's selection: the candidate set contains every top-k
 // element, and the dense paths scan all of r.  All launches are ordinary (not cooperative), so
 // the selection can share the GPU with backprop kernels on other streams.
@@ -38,7 +40,6 @@ constexpr int K1_WARPS = LAGS_K1_WARPS;  // warps per K1 CTA
 constexpr int K1_MINB = LAGS_K1_MINB;    // K1 CTAs per SM the register allocation must allow
 constexpr int K1_UNROLL = LAGS_K1_UNROLL;        // float4 loads in flight per lane per operand (K1)
 constexpr int PRED_FACTOR = 3;     // predicted threshold targets PRED_FACTOR * k candidates
-constexpr int F32_PASSES = 3;      // radix passes for 31-bit keys with 11-bit digits
 constexpr int F32_BINS = 1 << Key<float>::RB;
 
 struct Task {
@@ -53,7 +54,7 @@ struct FastState {
   uint32_t last_cands;  // candidates at the last call (0 = dense path)
   uint32_t calls;
   uint32_t cycles;      // SM cycles the layer's phase-1 work took at the last call (diagnostic)
-  uint32_t path;        // last path: 0 small dense, 1 candidates, 2 queued for the grid-wide dense path
+  uint32_t path;        // last path: 0 small / tiny dense, 1 candidates, 2 dense over r, 3 cluster
   uint32_t pf256;       // adaptive prediction rank factor x256 (0 = PRED_FACTOR)
   uint32_t reserved;    // candidate-path phase cycles (diagnostic)
   uint32_t t_start;     // %globaltimer (ns, low 32 bits) when the layer's CTA started / ended its
@@ -376,9 +377,9 @@ __device__ __forceinline__ FastState candidate_state(const FastState& st, uint32
   return ns;
 }
 
-// Candidate path of one big layer inside one CTA.  Returns 0 on success, or why the candidate set
-// cannot be proven to hold the top-k (FB_TOO_FEW / FB_OVERFLOW); the caller then queues the layer
-// for the grid-wide dense path.  Candidates are gathered once into shared memory (value + index,
+// Candidate path of one layer inside one CTA.  Returns 0 on success, or why the candidate set
+// cannot be proven to hold the top-k (FB_TOO_FEW / FB_OVERFLOW); the caller then runs a dense
+// exact path in the same CTA.  Candidates are gathered once into shared memory (value + index,
 // ascending index order) when they fit (2*m words <= smem_words), else into global scratch.
 constexpr int FB_TOO_FEW = 1, FB_OVERFLOW = 2;
 

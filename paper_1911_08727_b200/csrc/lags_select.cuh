@@ -101,16 +101,6 @@ __device__ __forceinline__ K block_or(K v, RadixSmem<RB>& sm) {
   return static_cast<K>((static_cast<uint64_t>(hi) << 32) | lo);
 }
 
-// Histogram increment aggregated over the lanes of a warp that hit the same bin (candidate keys
-// crowd into a few bins; plain shared atomics would serialise).  Warp-collective.
-__device__ __forceinline__ void hist_add_warp(uint32_t* hist, uint32_t bin, bool act) {
-  const unsigned am = __ballot_sync(0xffffffffu, act);
-  if (act) {
-    const unsigned peers = __match_any_sync(am, bin);
-    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(hist + bin, static_cast<uint32_t>(__popc(peers)));
-  }
-}
-
 // skip_common_prefix: first OR-reduce key ^ key(0) over all m keys and start the radix passes
 // below the highest differing bit (cheap when keys live in shared memory and crowd together).
 template <typename K, int BITS, int RB, typename KeyAt>
