@@ -331,3 +331,46 @@ def test_slgs_step_golden(L):
         assert _same_bits(out.data, z[f"v_out{i}"])
         for a, b in zip(res, z[f"r_out{i}"]):
             assert _same_bits(a.data, b)
+
+
+def test_tiny_layer_warp_path_vs_oracle(L):
+    """Tiny layers (d <= 4096, k <= 8) take one warp each (register top-k) -- checked against the
+    oracle's top_k on every call: odd sizes (unaligned layer offsets), k from 1 to 8, ties across
+    lanes, all-equal layers, zeros, signed zeros, subnormals, a layer with fewer nonzeros than k."""
+    from paper_1911_08727_b200 import _native as N
+
+    rng = np.random.default_rng(17)
+    dims = [1, 3, 7, 64, 65, 127, 256, 511, 1000, 1023, 2048, 4095, 4096, 33, 97, 600]
+    ks = [1, 1, 3, 8, 5, 2, 4, 8, 1, 7, 2, 8, 4, 8, 6, 3]
+    b = L.Bucket(dims, ks, N.F32)
+    n = sum(dims)
+    off = np.concatenate([[0], np.cumsum(dims)]).astype(np.int64)
+    r = np.zeros(n, dtype=np.float32)
+    r_d = torch.zeros(n, device="cuda")
+    msg = b.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    alpha = 0.25
+    for it in range(12):
+        g = rng.standard_normal(n).astype(np.float32)
+        if it % 4 == 1:  # heavy ties: few distinct magnitudes across lanes
+            g = rng.integers(-3, 4, size=n).astype(np.float32)
+        if it % 4 == 2:
+            g[off[5]:off[6]] = -1.5  # all-equal layer (plus whatever residual it carries)
+            g[off[7]:off[8]] = 0.0
+            g[off[12]:off[13]] = np.where(rng.random(dims[12]) < 0.5, -0.0, 0.0)
+            g[off[12] + 5] = 2.0  # fewer nonzeros than k there
+        if it % 4 == 3:
+            g[off[10]:off[11]] = (rng.integers(-40, 41, size=dims[10]) * np.finfo(np.float32).smallest_subnormal)
+        acc = (r + np.float32(alpha) * g).astype(np.float32)
+        b.compress(torch.from_numpy(g).cuda(), r_d, alpha, msg, st)
+        got = b.unpack(msg)
+        for j, (d, k) in enumerate(zip(dims, ks)):
+            idx, val = orc.top_k(acc[off[j]:off[j + 1]], k)
+            np.testing.assert_array_equal(got[j][0], idx, err_msg=f"iteration {it} layer {j}")
+            assert _same_bits(got[j][1], val), (it, j)
+        r = acc.copy()
+        for j in range(len(dims)):
+            r[off[j] + got[j][0]] = 0.0
+        assert _same_bits(r_d.cpu().numpy(), r), it
+    s = b.stats()
+    assert all(int(s[j, 5]) == 0 for j in range(len(dims)))  # every layer on the warp / dense-small path
