@@ -108,7 +108,6 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
     cs.tpos[threadIdx.x] = pos;
     __syncthreads();
-    constexpr int GATHER_ILP = 8;
     for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
       int64_t src[GATHER_ILP];
 #pragma unroll

@@ -56,8 +56,43 @@ __device__ __forceinline__ bool nonfinite(double g) {
 // Block-wide exclusive scan of one uint32 per thread (NT threads, multiple of 32).
 // `warp_tot` must hold 33 uint32 of shared memory.  Returns the exclusive prefix and writes the
 // block total into *total.  Contains two __syncthreads().
+// Inlining of the block-wide helpers (instruction footprint vs call overhead), per helper:
+// LAGS_INL_<NAME> = 1 inline, 0 out of line.
+#ifndef LAGS_INL_SCAN
+#define LAGS_INL_SCAN 1
+#endif
+#ifndef LAGS_INL_FINDBIN
+#define LAGS_INL_FINDBIN 1
+#endif
+#ifndef LAGS_INL_SUM
+#define LAGS_INL_SUM 1
+#endif
+#ifndef LAGS_INL_OR
+#define LAGS_INL_OR 1
+#endif
+#if LAGS_INL_SCAN
+#define LAGS_SCAN_ATTR __forceinline__
+#else
+#define LAGS_SCAN_ATTR __noinline__
+#endif
+#if LAGS_INL_FINDBIN
+#define LAGS_FINDBIN_ATTR __forceinline__
+#else
+#define LAGS_FINDBIN_ATTR __noinline__
+#endif
+#if LAGS_INL_SUM
+#define LAGS_SUM_ATTR __forceinline__
+#else
+#define LAGS_SUM_ATTR __noinline__
+#endif
+#if LAGS_INL_OR
+#define LAGS_OR_ATTR __forceinline__
+#else
+#define LAGS_OR_ATTR __noinline__
+#endif
+
 template <int NT>
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot, uint32_t* total) {
+__device__ LAGS_SCAN_ATTR uint32_t block_exclusive_scan(uint32_t v, uint32_t* warp_tot, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll

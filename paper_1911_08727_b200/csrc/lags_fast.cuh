@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
 
 // Block-wide sum; all threads get the result.  Uses sm.warp_tot.
 template <int RB>
-__device__ __forceinline__ uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
+__device__ LAGS_SUM_ATTR uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
   uint32_t tot;
   block_exclusive_scan<SEL_NT>(v, sm.warp_tot, &tot);
   __syncthreads();
@@ -251,7 +251,7 @@ __device__ __forceinline__ float single_rank_update(float v, float x) {
 __device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32_t* oidx, const float* oval,
                                                           uint32_t cnt) {
   __syncthreads();  // the block's compaction writes are visible
-  constexpr int B = 4;
+  constexpr int B = UPDATE_B;
   for (uint32_t q0 = 0; q0 < cnt; q0 += SEL_NT * B) {
     int32_t ix[B];
     float x[B], w[B];
@@ -423,8 +423,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       __syncthreads();
       // batches of GATHER_ILP entries per thread: all source addresses first, then all loads in
       // flight together, then the stores (the destination may alias global scratch)
-      constexpr int GATHER_ILP = 8;
-      for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
+        for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
         int64_t src[GATHER_ILP];
 #pragma unroll
         for (int u = 0; u < GATHER_ILP; ++u) {

@@ -17,7 +17,18 @@ namespace lags {
 #endif
 constexpr int SEL_NT = LAGS_SEL_NT;      // threads per selection CTA (512 measured faster than 1024)
 constexpr int SEL_MINB = LAGS_SEL_MINB;  // selection CTAs resident per SM (launch bounds)
-constexpr int SEL_VEC = 4;    // consecutive elements per thread per compaction chunk
+#ifndef LAGS_SEL_VEC
+#define LAGS_SEL_VEC 4
+#endif
+#ifndef LAGS_GATHER_ILP
+#define LAGS_GATHER_ILP 2
+#endif
+#ifndef LAGS_UPDATE_B
+#define LAGS_UPDATE_B 1
+#endif
+constexpr int SEL_VEC = LAGS_SEL_VEC;        // consecutive elements per thread per compaction chunk
+constexpr int GATHER_ILP = LAGS_GATHER_ILP;  // candidate loads in flight per thread in the gathers
+constexpr int UPDATE_B = LAGS_UPDATE_B;      // weight loads in flight per thread in the P = 1 update
 
 // Select (key & pmask) > prefix, plus the first `need_eq` (in scan order) with
 // (key & pmask) == prefix.  `full_key` is the resolved threshold (valid when pmask is full).
@@ -41,7 +52,7 @@ struct RadixSmem {
 // Bin holding the rank-th largest (1-based) of the histogram (descending scan).  All threads.
 // `hist` (shared, NB bins) defaults to sm.hist.
 template <int RB>
-__device__ __forceinline__ void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint32_t* bin, uint32_t* above,
+__device__ LAGS_FINDBIN_ATTR void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint32_t* bin, uint32_t* above,
                                          uint32_t* in_bin, const uint32_t* hist = nullptr) {
   constexpr int NB = RadixSmem<RB>::NB;
   constexpr int PER = NB / SEL_NT;  // 2 (fp32) or 8 (fp64) bins per thread
@@ -79,7 +90,7 @@ __device__ __forceinline__ void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint3
 // holds the pred_rank-th largest key (used to predict next call's candidate threshold).
 // Block-wide OR of one key per thread (all threads get the result).  Uses sm.warp_tot.
 template <typename K, int RB>
-__device__ __forceinline__ K block_or(K v, RadixSmem<RB>& sm) {
+__device__ LAGS_OR_ATTR K block_or(K v, RadixSmem<RB>& sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(v));
   uint32_t hi = sizeof(K) > 4 ? __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(static_cast<uint64_t>(v) >> 32)) : 0u;
