@@ -17,8 +17,14 @@
 
 namespace lags {
 
-constexpr int CLUSTER = 4;             // CTAs per cluster layer
-constexpr int CLUSTER_MIN_K = 512;     // layers with at least this k (and > SMALL_LAYER) use clusters
+#ifndef LAGS_CLUSTER
+#define LAGS_CLUSTER 4
+#endif
+#ifndef LAGS_CLUSTER_MIN_K
+#define LAGS_CLUSTER_MIN_K 512
+#endif
+constexpr int CLUSTER = LAGS_CLUSTER;              // CTAs per cluster layer
+constexpr int CLUSTER_MIN_K = LAGS_CLUSTER_MIN_K;  // layers with at least this k (and > SMALL_LAYER) use clusters
 
 struct ClusterShared {
   uint32_t m, over;          // this CTA's candidate count / overflow
