@@ -3,9 +3,12 @@
 // of the selection (gather + compaction of ~2k candidates in one CTA); here the CTAs of a cluster
 // each own a contiguous quarter of the layer's K1 task lists (= a contiguous index range):
 //   1. candidate counts are exchanged over DSMEM (cluster.sync) -> the exactness proof, prefixes;
-//   2. every CTA gathers its candidates (value, index) into its own shared memory and pushes the
-//      keys into rank 0's shared memory at its prefix offset (remote DSMEM stores);
-//   3. rank 0 runs the dual-rank radix select (k-th key + next prediction) on all keys;
+//   2. every CTA gathers its candidates (value, index) into its own shared memory and, when rank 0
+//      has room for all m keys ("central"), pushes the keys into rank 0's shared memory at its
+//      prefix offset (remote DSMEM stores);
+//   3. rank 0 runs the dual-rank radix select (k-th key + next prediction) on all keys: its own
+//      copy, or -- for candidate sets too large for one CTA (k in the tens of thousands) -- the
+//      keys read in place from every CTA's shared memory over DSMEM;
 //   4. the threshold is read back over DSMEM, per-CTA (gt, eq) counts are exchanged, and every CTA
 //      compacts its own range in order with the carried counts (global output positions), zeroes
 //      the selected residuals and applies the optional fused P = 1 update.
@@ -67,6 +70,8 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   }
   cluster.sync();
   uint32_t m = 0, pre = 0, m_max = 0, over_any = 0;
+  uint32_t rpre[CLUSTER + 1];  // prefix of the ranks' candidate counts (remote key reads)
+  rpre[0] = 0;
   for (int q = 0; q < CLUSTER; ++q) {
     const ClusterShared* o = cluster.map_shared_rank(&csh, q);
     const uint32_t mq = o->m;
@@ -74,9 +79,13 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     m += mq;
     m_max = max(m_max, mq);
     over_any |= o->over;
+    rpre[q + 1] = rpre[q] + mq;
   }
   cluster.sync();  // every CTA has read the counts
-  const bool fits = static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
+  // central: rank 0 holds a copy of all m keys (plus its own values / indices); otherwise every
+  // CTA holds only its own candidates and rank 0's radix passes read the keys over DSMEM
+  const bool central = static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
+  const bool fits = central || 2ull * m_max <= static_cast<uint64_t>(smem_words);
   int why = 0;
   if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
   else if (over_any) why = FB_OVERFLOW;
@@ -100,11 +109,13 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     }
     return;
   }
-  // 2. gather: own (value, index) at [m, m + mr) / [m + mr, m + 2 mr) of dyn; keys -> rank 0's dyn
+  // 2. gather: own (value, index) at [m, m + mr) / [m + mr, m + 2 mr) of dyn and the keys into
+  // rank 0's dyn (central), or own (value, index) at [0, m_max) / [m_max, m_max + mr) (remote)
   const long long c0 = clock64();
   const uint32_t mr = local;
-  float* sv = reinterpret_cast<float*>(dyn + m);
-  int32_t* si = reinterpret_cast<int32_t*>(dyn + m + mr);
+  const uint32_t vbase = central ? m : 0u, ibase = central ? m + mr : m_max;
+  float* sv = reinterpret_cast<float*>(dyn + vbase);
+  int32_t* si = reinterpret_cast<int32_t*>(dyn + ibase);
   uint32_t* keys0 = cluster.map_shared_rank(dyn, 0);
   uint32_t carry = 0;
   for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
@@ -145,7 +156,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
           const uint32_t e = carry + e0 + u * SEL_NT + threadIdx.x;
           sv[e] = xv[u];
           si[e] = xi[u];
-          keys0[pre + e] = Key<float>::of(xv[u]);
+          if (central) keys0[pre + e] = Key<float>::of(xv[u]);
         }
       }
     }
@@ -157,11 +168,23 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   // 3. rank 0 selects
   const uint32_t k2 = pred_rank(st, k);
   if (rank == 0) {
-    const uint32_t* keys = dyn;
-    auto key_at = [=](int64_t i) { return keys[i]; };
     SelectThreshold<uint32_t> th;
     uint32_t key2;
-    radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+    if (central) {
+      const uint32_t* keys = dyn;
+      auto key_at = [=](int64_t i) { return keys[i]; };
+      radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+    } else {
+      const float* rsv[CLUSTER];
+      for (int q = 0; q < CLUSTER; ++q) rsv[q] = reinterpret_cast<const float*>(cluster.map_shared_rank(dyn, q));
+      auto key_at = [=](int64_t i) {
+        int q = 0;
+#pragma unroll
+        for (int t = 1; t < CLUSTER; ++t) q += i >= static_cast<int64_t>(rpre[t]) ? 1 : 0;
+        return Key<float>::of(rsv[q][i - rpre[q]]);
+      };
+      radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+    }
     if (threadIdx.x == 0) {
       csh.prefix = th.prefix;
       csh.pmask = th.pmask;

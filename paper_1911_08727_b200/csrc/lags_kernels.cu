@@ -347,7 +347,21 @@ int stream_grid(int64_t work_items, int threads, int per_sm) {
 bool valid_dtype(int32_t dtype) { return dtype == LAGS_F32 || dtype == LAGS_F64 || dtype == LAGS_F32_ACC64; }
 size_t val_size(int32_t dtype) { return dtype == LAGS_F32 ? 4 : 8; }
 
-constexpr int SMEM_KEYS = 40960;  // candidate keys kept in shared memory by select_fast_kernel (160 KB)
+// Shared-memory staging words of select_kernel: the device's opt-in maximum per block minus the
+// kernel's static shared memory (B200: ~48 k words = ~190 KB).
+int select_smem_words_max() {
+  static int words = 0;
+  if (words == 0) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, select_kernel);
+    words = static_cast<int>((static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024) / sizeof(uint32_t)) / 1024 * 1024;
+    if (words < 16384) words = 16384;
+  }
+  return words;
+}
 
 // Device memory layout shared by lags_bucket_device_bytes and lags_bucket_create.
 struct Plan {
@@ -572,7 +586,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     return cuda_check("lags_bucket_create upload", 0);
   }
   if (dtype == LAGS_F32) {
-    const int smem = SMEM_KEYS * static_cast<int>(sizeof(uint32_t));
+    const int smem = select_smem_words_max() * static_cast<int>(sizeof(uint32_t));
     if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
         cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess) {
       delete b;
@@ -585,7 +599,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     int64_t words = 4096;
     for (int j = 0; j < nlayers; ++j)
       words = std::max<int64_t>(words, dims[j] <= SMALL_LAYER ? dims[j] : (15 * static_cast<int64_t>(ks[j])) / 2);
-    b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), SMEM_KEYS));
+    b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), select_smem_words_max()));
   }
   *out = b;
   return LAGS_OK;

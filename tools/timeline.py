@@ -37,8 +37,19 @@ def show(title, ks, last=12):
 
 
 def main():
-    dims = resnet50_dims()
-    ks = ks_for(dims)
+    # optional workload: resnet50 (default) | resnet50:RHO | lstm | vgg16
+    arg = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
+    name, _, rho = arg.partition(":")
+    rho = float(rho) if rho else 0.001
+    if name == "lstm":
+        from paper_1911_08727_b200.workloads import LSTMPTB
+        dims = [p.numel() for p in LSTMPTB().parameters()]
+    elif name == "vgg16":
+        from paper_1911_08727_b200.workloads import vgg16_cifar
+        dims = [p.numel() for p in vgg16_cifar().parameters()]
+    else:
+        dims = resnet50_dims()
+    ks = ks_for(dims, rho)
     n = sum(dims)
     b = L.Bucket(dims, ks, N.F32)
     gen = torch.Generator(device="cuda").manual_seed(1)
