@@ -35,6 +35,121 @@ struct ClusterShared {
   uint32_t prefix, pmask, n_gt, need_eq, key2;  // rank 0: the threshold
 };
 
+// Dual-rank radix select over a cluster's candidates when every CTA holds only its own keys
+// (sv[0..mr)): per pass every CTA histograms its keys, rank 0 adds the CLUSTER histograms over
+// DSMEM and resolves the bins of both ranks (radix_select_dual's rule), every CTA reads the
+// digits back -- two cluster barriers per pass, no key moves between CTAs.  Same result as
+// radix_select_dual over all m keys.  Called by every thread of every CTA of the cluster.
+struct ClusterRadix {
+  uint32_t bin[2], above[2], in_bin[2];
+  uint32_t diff;
+};
+
+__device__ void cluster_radix_select_dual(cooperative_groups::cluster_group& cluster, int rank, const float* sv,
+                                          uint32_t mr, uint32_t m, uint32_t key0, uint32_t k, uint32_t k2,
+                                          CoopSmem& cs, ClusterRadix& cr, SelectThreshold<uint32_t>* th_out,
+                                          uint32_t* key2_out) {
+  constexpr int RB = Key<float>::RB;
+  constexpr uint32_t FULL = 0x7fffffffu;
+  RadixSmem<RB>& sm = cs.sm;
+  uint32_t diff = 0;
+  for (uint32_t i = threadIdx.x; i < mr; i += SEL_NT) diff |= Key<float>::of(sv[i]) ^ key0;
+  diff = block_or<uint32_t, RB>(diff, sm);
+  if (threadIdx.x == 0) cr.diff = diff;
+  cluster.sync();
+  diff = 0;
+  for (int q = 0; q < CLUSTER; ++q) diff |= cluster.map_shared_rank(&cr, q)->diff;
+  uint32_t prefix[2], pmask[2];
+  uint32_t rank_[2] = {k < m ? k : m, k2 < m ? k2 : m};
+  uint32_t n_gt0 = 0;
+  bool done[2] = {false, false};
+  int shift = 0, width = 0;
+  if (diff == 0) {
+    prefix[0] = prefix[1] = key0;
+    pmask[0] = pmask[1] = FULL;
+  } else {
+    const int h = 31 - __clz(static_cast<int>(diff));
+    const uint32_t pm = FULL & ~((1u << (h + 1)) - 1u);
+    prefix[0] = prefix[1] = key0 & pm;
+    pmask[0] = pmask[1] = pm;
+    shift = h + 1 > RB ? h + 1 - RB : 0;
+    width = h + 1 - shift;
+  }
+  while (width > 0 && !(done[0] && done[1])) {
+    const bool same = !done[0] && !done[1] && prefix[0] == prefix[1] && pmask[0] == pmask[1];
+    const bool second = !same && !done[1];
+    for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
+      sm.hist[b] = 0;
+      cs.hist2[b] = 0;
+    }
+    __syncthreads();
+    const uint32_t dmask = (1u << width) - 1u;
+    for (uint32_t i = threadIdx.x; i < mr; i += SEL_NT) {
+      const uint32_t key = Key<float>::of(sv[i]);
+      const uint32_t bin = (key >> shift) & dmask;
+      if (!done[0] && (key & pmask[0]) == prefix[0]) atomicAdd(&sm.hist[bin], 1u);
+      if (second && (key & pmask[1]) == prefix[1]) atomicAdd(&cs.hist2[bin], 1u);
+    }
+    __syncthreads();
+    cluster.sync();  // every CTA's histograms are complete
+    if (rank == 0) {
+      const uint32_t* rh[CLUSTER];
+      const uint32_t* rh2[CLUSTER];
+      for (int q = 1; q < CLUSTER; ++q) {
+        rh[q] = cluster.map_shared_rank(sm.hist, q);
+        rh2[q] = cluster.map_shared_rank(cs.hist2, q);
+      }
+      for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
+        uint32_t h = sm.hist[b], h2 = second ? cs.hist2[b] : 0u;
+#pragma unroll
+        for (int q = 1; q < CLUSTER; ++q) {
+          h += rh[q][b];
+          if (second) h2 += rh2[q][b];
+        }
+        sm.hist[b] = h;
+        if (second) cs.hist2[b] = h2;
+      }
+      __syncthreads();
+      for (int q = 0; q < 2; ++q) {
+        if (done[q]) continue;
+        uint32_t bin, above, in_bin;
+        find_bin<RB>(sm, rank_[q], &bin, &above, &in_bin, (q == 0 || same) ? sm.hist : cs.hist2);
+        if (threadIdx.x == 0) {
+          cr.bin[q] = bin;
+          cr.above[q] = above;
+          cr.in_bin[q] = in_bin;
+        }
+      }
+    }
+    cluster.sync();  // rank 0's digits are visible; the histograms are no longer read remotely
+    const ClusterRadix* r0 = cluster.map_shared_rank(&cr, 0);
+    for (int q = 0; q < 2; ++q) {
+      if (done[q]) continue;
+      const uint32_t bin = r0->bin[q], above = r0->above[q], in_bin = r0->in_bin[q];
+      prefix[q] |= bin << shift;
+      pmask[q] |= dmask << shift;
+      rank_[q] -= above;
+      if (q == 0) n_gt0 += above;
+      if (shift == 0 || (in_bin == rank_[q] && prefix[q] != 0u)) done[q] = true;
+    }
+    const int ns = shift > RB ? shift - RB : 0;
+    width = shift - ns;
+    shift = ns;
+  }
+  if (k >= m) {  // every nonzero key is selected
+    th_out->prefix = 0u;
+    th_out->pmask = 0xffffffffu;
+    th_out->n_gt = 0;
+    th_out->need_eq = 0;
+  } else {
+    th_out->prefix = prefix[0];
+    th_out->pmask = pmask[0];
+    th_out->n_gt = n_gt0;
+    th_out->need_eq = prefix[0] == 0u ? 0u : rank_[0];
+  }
+  *key2_out = prefix[1];
+}
+
 // One layer by the CTA's cluster (all CLUSTER CTAs call this with the same j).
 __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ layers,
                                      const int2* __restrict__ layer_tasks, FastState* state,
@@ -42,6 +157,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                                      const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r,
                                      int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words,
                                      int force_exact, float* vupd, uint32_t* dyn, CoopSmem& cs, ClusterShared& csh,
+                                     ClusterRadix& cr,
                                      uint32_t t_launch) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -84,7 +200,8 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   cluster.sync();  // every CTA has read the counts
   // central: rank 0 holds a copy of all m keys (plus its own values / indices); otherwise every
   // CTA holds only its own candidates and rank 0's radix passes read the keys over DSMEM
-  const bool central = static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
+  constexpr uint32_t CENTRAL_MAX = 16384;  // larger sets: the distributed select is faster
+  const bool central = m <= CENTRAL_MAX && static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
   const bool fits = central || 2ull * m_max <= static_cast<uint64_t>(smem_words);
   int why = 0;
   if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
@@ -167,25 +284,29 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   const long long c1 = clock64();
   // 3. rank 0 selects
   const uint32_t k2 = pred_rank(st, k);
-  if (rank == 0) {
-    SelectThreshold<uint32_t> th;
-    uint32_t key2;
-    if (central) {
+  if (central) {
+    if (rank == 0) {
+      SelectThreshold<uint32_t> th;
+      uint32_t key2;
       const uint32_t* keys = dyn;
       auto key_at = [=](int64_t i) { return keys[i]; };
       radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
-    } else {
-      const float* rsv[CLUSTER];
-      for (int q = 0; q < CLUSTER; ++q) rsv[q] = reinterpret_cast<const float*>(cluster.map_shared_rank(dyn, q));
-      auto key_at = [=](int64_t i) {
-        int q = 0;
-#pragma unroll
-        for (int t = 1; t < CLUSTER; ++t) q += i >= static_cast<int64_t>(rpre[t]) ? 1 : 0;
-        return Key<float>::of(rsv[q][i - rpre[q]]);
-      };
-      radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+      if (threadIdx.x == 0) {
+        csh.prefix = th.prefix;
+        csh.pmask = th.pmask;
+        csh.n_gt = th.n_gt;
+        csh.need_eq = th.need_eq;
+        csh.key2 = key2;
+      }
     }
-    if (threadIdx.x == 0) {
+  } else {  // every CTA holds its own keys: the distributed select (all CTAs)
+    int q0 = 0;
+    while (rpre[q0 + 1] == rpre[q0]) ++q0;  // the first rank with candidates (m > 0)
+    const uint32_t key0 = Key<float>::of(cluster.map_shared_rank(reinterpret_cast<const float*>(dyn), q0)[0]);
+    SelectThreshold<uint32_t> th;
+    uint32_t key2;
+    cluster_radix_select_dual(cluster, rank, sv, mr, m, key0, k, k2, cs, cr, &th, &key2);
+    if (rank == 0 && threadIdx.x == 0) {
       csh.prefix = th.prefix;
       csh.pmask = th.pmask;
       csh.n_gt = th.n_gt;
@@ -275,13 +396,14 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
   extern __shared__ uint32_t dyn[];
   __shared__ CoopSmem cs;
   __shared__ ClusterShared csh;
+  __shared__ ClusterRadix cr;
   __shared__ int next_pos;
   const uint32_t t_launch = globaltimer_lo();
   griddep_wait();  // K1 has completed and its writes are visible (programmatic dependent launch)
   const int cl_ctas = n_cl * CLUSTER;
   if (static_cast<int>(blockIdx.x) < cl_ctas) {
     cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap,
-                         gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh,
+                         gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh, cr,
                          t_launch);
     return;
   }

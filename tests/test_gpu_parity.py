@@ -374,3 +374,32 @@ def test_tiny_layer_warp_path_vs_oracle(L):
         assert _same_bits(r_d.cpu().numpy(), r), it
     s = b.stats()
     assert all(int(s[j, 5]) == 0 for j in range(len(dims)))  # every layer on the warp / dense-small path
+
+
+def test_large_k_cluster_modes_equal_exact_path(L):
+    """Large k (rho = 0.01 on multi-million-element layers): the cluster selection's candidate
+    sets exceed one CTA's shared memory, so the CTAs keep their own keys and run the distributed
+    radix select -- bit-identical to the dense exact path on every call, incl. mispredictions."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [2359296, 1048576, 3000001, 70000]
+    ks = [d // 100 for d in dims]
+    fast = L.Bucket(dims, ks, N.F32)
+    exact = L.Bucket(dims, ks, N.F32)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    r_f = torch.zeros(n, device="cuda")
+    r_e = torch.zeros(n, device="cuda")
+    m_f, m_e = fast.new_messages(1), exact.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for it in range(10):
+        g = torch.randn(n, device="cuda", generator=gen)
+        if it == 6:
+            g *= 1e-3  # scale drop -> too few candidates -> dense fallback, then recovery
+        fast.compress(g, r_f, 0.05, m_f, st)
+        exact.compress(g, r_e, 0.05, m_e, st, exact=True)
+        assert torch.equal(m_f, m_e), f"messages differ at iteration {it}"
+        assert torch.equal(r_f.view(torch.int32), r_e.view(torch.int32)), f"residuals differ at {it}"
+    s = fast.stats()
+    assert sum(1 for j in range(3) if s[j, 5] == 3) >= 2, s  # the big layers ran on clusters
+    assert int(st.item()) == 0
