@@ -21,10 +21,10 @@ constexpr int SEL_MINB = LAGS_SEL_MINB;  // selection CTAs resident per SM (laun
 #define LAGS_SEL_VEC 4
 #endif
 #ifndef LAGS_GATHER_ILP
-#define LAGS_GATHER_ILP 2
+#define LAGS_GATHER_ILP 4
 #endif
 #ifndef LAGS_UPDATE_B
-#define LAGS_UPDATE_B 1
+#define LAGS_UPDATE_B 4
 #endif
 constexpr int SEL_VEC = LAGS_SEL_VEC;        // consecutive elements per thread per compaction chunk
 constexpr int GATHER_ILP = LAGS_GATHER_ILP;  // candidate loads in flight per thread in the gathers
