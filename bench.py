@@ -397,6 +397,24 @@ def run_ours(args, dims, ks, world, rank, local):
         sel_mean = sel_local
     comp_b, dec_b = algorithmic_bytes(n, [sel_mean], union, world)
     value = (comp_b + dec_b) * args.steps / (ms / 1e3) / 1e9
+    exchange = None
+    if world > 1:  # the all-gather alone (NCCL convention: algBW = P * msg / t, busBW = algBW (P-1)/P)
+        ex0, ex1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(10):
+            dist.all_gather_into_tensor(msgs, msg_local)
+        torch.cuda.synchronize(dev)
+        ex0.record(stream)
+        for _ in range(50):
+            dist.all_gather_into_tensor(msgs, msg_local)
+        ex1.record(stream)
+        torch.cuda.synchronize(dev)
+        ex_us = torch.tensor([ex0.elapsed_time(ex1) / 50 * 1e3], dtype=torch.float64, device=dev)
+        dist.all_reduce(ex_us, op=dist.ReduceOp.MAX)
+        ex_us = float(ex_us)
+        alg = world * bucket.msg_bytes / (ex_us * 1e-6) / 1e9
+        exchange = {"what": "NCCL all-gather of the fixed-size sparse messages (one bucket)",
+                    "bytes_per_rank": int(bucket.msg_bytes), "us": round(ex_us, 2), "alg_GBs": round(alg, 2),
+                    "bus_GBs": round(alg * (world - 1) / world, 2), "nvlink_GBs_per_direction": 900}
     peak, peak_src = read_peaks()
     comp_bytes_rank = 12 * n + 8 * sel_local
     achieved = comp_bytes_rank / (comp_ms / 1e3) / 1e9
@@ -437,6 +455,7 @@ def run_ours(args, dims, ks, world, rank, local):
             "launch_mode": "cuda graph replay (one captured step per gradient buffer)" if graphs is not None
             else "eager (ctypes -> cudaLaunchKernelEx with programmatic dependent launch)",
             "resnet50_train": train,
+            "exchange": exchange,
             "selection": {"layers": len(dims),
                           "dense_fallbacks_in_timed_region": int(stats[:, 1].sum() - stats0[:, 1].sum()),
                           "candidate_path_layers": int((stats[:, 2] > 0).sum()),

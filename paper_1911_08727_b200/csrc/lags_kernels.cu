@@ -113,54 +113,50 @@ __global__ void __launch_bounds__(256) decode_single_kernel(const lags_layer_t* 
   }
 }
 
+// Work is tiled per (layer chunk, rank): CTA (t, p) handles pairs [c * DEC_NT, (c + 1) * DEC_NT)
+// of rank p's list of layer j = tiles[t].x (c = tiles[t].y), one pair per thread, so a thread's
+// dependent-load chain is tile -> (layer, count) -> pair -> planes (the latency-bound part).
+constexpr int DEC_NT = 256;
+
 template <typename TVal>
-__global__ void __launch_bounds__(256) decode_scatter_kernel(const lags_layer_t* __restrict__ layers,
-                                                             const int32_t* __restrict__ slot_layer, MsgView msg,
-                                                             int64_t total_k, int P, TVal* planes, int64_t n,
-                                                             uint32_t* mask) {
+__global__ void __launch_bounds__(DEC_NT) decode_scatter_kernel(const lags_layer_t* __restrict__ layers,
+                                                                const int2* __restrict__ tiles, MsgView msg, int P,
+                                                                TVal* planes, int64_t n, uint32_t* mask) {
   griddep_wait();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t work = total_k * P;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < work; e += stride) {
-    const int p = static_cast<int>(e / total_k);
-    const int64_t s = e - static_cast<int64_t>(p) * total_k;
-    const int j = slot_layer[s];
-    const lags_layer_t L = layers[j];
-    if (s - L.slot >= msg.count(p, j)) continue;
-    const int64_t i = L.offset + msg.idx(p, s);
-    planes[static_cast<int64_t>(p) * n + i] = msg.val<TVal>(p, s);
-    atomicOr(mask + i, 1u << p);
-  }
+  const int p = static_cast<int>(blockIdx.x) % P;
+  const int2 tc = tiles[blockIdx.x / P];
+  const lags_layer_t L = layers[tc.x];
+  const int e = tc.y * DEC_NT + static_cast<int>(threadIdx.x);
+  if (e >= msg.count(p, tc.x)) return;
+  const int64_t s = L.slot + e;
+  const int64_t i = L.offset + msg.idx(p, s);
+  planes[static_cast<int64_t>(p) * n + i] = msg.val<TVal>(p, s);
+  atomicOr(mask + i, 1u << p);
 }
 
 template <typename TV, typename TVal>
-__global__ void __launch_bounds__(256) decode_update_kernel(const lags_layer_t* __restrict__ layers,
-                                                            const int32_t* __restrict__ slot_layer, MsgView msg,
-                                                            int64_t total_k, int P, const TVal* planes, int64_t n,
-                                                            uint32_t* mask, TV* v) {
+__global__ void __launch_bounds__(DEC_NT) decode_update_kernel(const lags_layer_t* __restrict__ layers,
+                                                               const int2* __restrict__ tiles, MsgView msg, int P,
+                                                               const TVal* planes, int64_t n, uint32_t* mask, TV* v) {
   griddep_wait();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t work = total_k * P;
-  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < work; e += stride) {
-    const int p = static_cast<int>(e / total_k);
-    const int64_t s = e - static_cast<int64_t>(p) * total_k;
-    const int j = slot_layer[s];
-    const lags_layer_t L = layers[j];
-    if (s - L.slot >= msg.count(p, j)) continue;
-    const int64_t i = L.offset + msg.idx(p, s);
-    const uint32_t bits = mask[i];
-    if (bits == 0 || (__ffs(bits) - 1) != p) continue;  // only the lowest holding rank applies
-    double total = 0.0;
-    for (uint32_t b = bits; b; b &= b - 1) {
-      const int q = __ffs(b) - 1;
-      total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
-    }
-    v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), __ddiv_rn(total, static_cast<double>(P))));
-    mask[i] = 0u;
+  const int p = static_cast<int>(blockIdx.x) % P;
+  const int2 tc = tiles[blockIdx.x / P];
+  const lags_layer_t L = layers[tc.x];
+  const int e = tc.y * DEC_NT + static_cast<int>(threadIdx.x);
+  if (e >= msg.count(p, tc.x)) return;
+  const int64_t i = L.offset + msg.idx(p, L.slot + e);
+  const uint32_t bits = mask[i];
+  if (bits == 0 || (__ffs(bits) - 1) != p) return;  // only the lowest holding rank applies
+  const double vi = static_cast<double>(v[i]);
+  double total = 0.0;
+  for (uint32_t b = bits; b; b &= b - 1) {
+    const int q = __ffs(b) - 1;
+    total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
   }
+  v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
+  mask[i] = 0u;
 }
 
-// Momentum (mu > 0, parity unpinned): dense over the bucket after decode_scatter.
 template <typename TV, typename TVal>
 __global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes, int64_t n, uint32_t* mask, int P,
                                                               TV* v, TV* mom, double mu) {
@@ -287,6 +283,8 @@ struct lags_bucket {
   uint32_t* mask = nullptr;
   char* planes = nullptr;
   int32_t* order = nullptr;  // layers by decreasing selection work, group by group (phase-1 schedule)
+  int2* tiles_dec = nullptr;  // decode tiles: (layer, chunk of DEC_NT slots)
+  int dec_tiles = 0;
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
   // fp32 pipeline groups: the selection of group 0 (the layers with the heaviest selection work)
   // runs on `side` while K1 streams group 1 (see compress_impl)
@@ -368,7 +366,8 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_delta = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_delta = 0, o_tiles = 0, bytes = 0;
+  int32_t ntiles = 0;
 };
 
 int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, int32_t max_world, Plan* p) {
@@ -384,6 +383,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
     p->n_total += dims[j];
     p->total_k += ks[j];
     p->ntasks += static_cast<int32_t>((dims[j] + TASK_ELEMS - 1) / TASK_ELEMS);
+    p->ntiles += (ks[j] + DEC_NT - 1) / DEC_NT;
     max_per_task = std::max(max_per_task, static_cast<double>(ks[j]) * std::min<int64_t>(dims[j], TASK_ELEMS) / dims[j]);
   }
   // per-task candidate capacity: 16x the expected PRED_FACTOR * (selected per task), power of two
@@ -414,6 +414,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
   p->o_order = take(sizeof(int32_t) * L);
   p->o_delta = take(2 * sizeof(double) * nt);
+  p->o_tiles = take(sizeof(int2) * static_cast<size_t>(p->ntiles));
   const bool f32 = dtype == LAGS_F32;
   p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (CoopScratch)
   p->bytes = o;
@@ -519,6 +520,8 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->planes = base + p.o_planes;
   b->order = reinterpret_cast<int32_t*>(base + p.o_order);
   b->delta_part = reinterpret_cast<double*>(base + p.o_delta);
+  b->tiles_dec = reinterpret_cast<int2*>(base + p.o_tiles);
+  b->dec_tiles = p.ntiles;
   b->coop.work = reinterpret_cast<uint32_t*>(base + p.o_fbc);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
@@ -566,6 +569,9 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     order.insert(order.end(), og.begin(), og.end());
     b->grp[g].nlayers = static_cast<int>(og.size());
   }
+  std::vector<int2> tiles;  // decode tiles
+  for (int j = 0; j < nlayers; ++j)
+    for (int c = 0; c * DEC_NT < ks[j]; ++c) tiles.push_back(make_int2(j, c));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool ok =
       cudaMemcpyAsync(b->layers, layers.data(), sizeof(lags_layer_t) * nlayers, cudaMemcpyHostToDevice, s) ==
@@ -576,6 +582,8 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       cudaMemcpyAsync(b->slot_layer, slot_layer.data(), sizeof(int32_t) * slot_layer.size(), cudaMemcpyHostToDevice,
                       s) == cudaSuccess &&
       cudaMemcpyAsync(b->order, order.data(), sizeof(int32_t) * nlayers, cudaMemcpyHostToDevice, s) ==
+          cudaSuccess &&
+      cudaMemcpyAsync(b->tiles_dec, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, s) ==
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
@@ -713,7 +721,7 @@ int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* m
   const int gwork = stream_grid(S * P, 256, 8);
   TVal* planes = reinterpret_cast<TVal*>(b->planes);
   if (mu != 0.0) {
-    decode_scatter_kernel<TVal><<<gwork, 256, 0, s>>>(b->layers, b->slot_layer, mv, S, P, planes, n, b->mask);
+    decode_scatter_kernel<TVal><<<P * b->dec_tiles, DEC_NT, 0, s>>>(b->layers, b->tiles_dec, mv, P, planes, n, b->mask);
     decode_momentum_kernel<TV, TVal><<<stream_grid(n, 256, 8), 256, 0, s>>>(
         planes, n, b->mask, P, static_cast<TV*>(v), static_cast<TV*>(momentum), mu);
     return cuda_check("decode(momentum)", 2);
@@ -725,11 +733,11 @@ int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* m
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
     return cuda_check("decode(single)", 1);
   }
-  e = launch_pdl(decode_scatter_kernel<TVal>, dim3(gwork), dim3(256), 0, s, b->layers, b->slot_layer, mv, S, P,
-                 planes, n, b->mask);
+  e = launch_pdl(decode_scatter_kernel<TVal>, dim3(P * b->dec_tiles), dim3(DEC_NT), 0, s, b->layers, b->tiles_dec, mv,
+                 P, planes, n, b->mask);
   if (e == cudaSuccess)
-    e = launch_pdl(decode_update_kernel<TV, TVal>, dim3(gwork), dim3(256), 0, s, b->layers, b->slot_layer, mv, S, P,
-                   static_cast<const TVal*>(planes), n, b->mask, static_cast<TV*>(v));
+    e = launch_pdl(decode_update_kernel<TV, TVal>, dim3(P * b->dec_tiles), dim3(DEC_NT), 0, s, b->layers,
+                   b->tiles_dec, mv, P, static_cast<const TVal*>(planes), n, b->mask, static_cast<TV*>(v));
   if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("decode launch: ") + cudaGetErrorString(e));
   return cuda_check("decode", 2);
 }

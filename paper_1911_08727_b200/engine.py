@@ -84,8 +84,9 @@ class Bucket:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            N.lags_bucket_destroy(h)
+        destroy = getattr(N, "lags_bucket_destroy", None)
+        if h and destroy is not None:  # at interpreter shutdown the binding may already be gone
+            destroy(h)
             self._h = None
 
     # -- message views ---------------------------------------------------------------------
