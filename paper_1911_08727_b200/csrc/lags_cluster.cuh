@@ -47,7 +47,7 @@ struct ClusterRadix {
 
 __device__ void cluster_radix_select_dual(cooperative_groups::cluster_group& cluster, int rank, const float* sv,
                                           uint32_t mr, uint32_t m, uint32_t key0, uint32_t k, uint32_t k2,
-                                          CoopSmem& cs, ClusterRadix& cr, SelectThreshold<uint32_t>* th_out,
+                                          SelectSmem& cs, ClusterRadix& cr, SelectThreshold<uint32_t>* th_out,
                                           uint32_t* key2_out) {
   constexpr int RB = Key<float>::RB;
   constexpr uint32_t FULL = 0x7fffffffu;
@@ -156,7 +156,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                                      const int32_t* __restrict__ cand_cnt, const int32_t* __restrict__ cand_idx,
                                      const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r,
                                      int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words,
-                                     int force_exact, float* vupd, uint32_t* dyn, CoopSmem& cs, ClusterShared& csh,
+                                     int force_exact, float* vupd, uint32_t* dyn, SelectSmem& cs, ClusterShared& csh,
                                      ClusterRadix& cr,
                                      uint32_t t_launch) {
   namespace cg = cooperative_groups;
@@ -391,10 +391,10 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
     int n_cl, const int32_t* __restrict__ tiny_layers, int n_tiny, const int32_t* __restrict__ order, int nl,
     FastState* state, const int32_t* __restrict__ cand_cnt,
     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval,
-    float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, CoopScratch sc,
+    float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, SelectCounters sc,
     float* vupd) {
   extern __shared__ uint32_t dyn[];
-  __shared__ CoopSmem cs;
+  __shared__ SelectSmem cs;
   __shared__ ClusterShared csh;
   __shared__ ClusterRadix cr;
   __shared__ int next_pos;

@@ -53,7 +53,7 @@ struct FastState {
   uint32_t fallbacks;   // dense-path executions after a prediction existed (diagnostic)
   uint32_t last_cands;  // candidates at the last call (0 = dense path)
   uint32_t calls;
-  uint32_t cycles;      // SM cycles the layer's phase-1 work took at the last call (diagnostic)
+  uint32_t cycles;      // SM cycles the layer's selection took at the last call (diagnostic)
   uint32_t path;        // last path: 0 small / tiny dense, 1 candidates, 2 dense over r, 3 cluster
   uint32_t pf256;       // adaptive prediction rank factor x256 (0 = PRED_FACTOR)
   uint32_t reserved;    // candidate-path phase cycles (diagnostic)
@@ -87,7 +87,7 @@ __device__ __forceinline__ uint32_t pf_encode(float pf) {
 
 // Per-call counter of the selection kernel (device memory of the bucket, reset by the next
 // call's accum_emit_kernel): next position of the LPT layer list to hand out (persistent CTAs).
-struct CoopScratch {
+struct SelectCounters {
   uint32_t* work;
 };
 
@@ -232,7 +232,7 @@ __device__ LAGS_SUM_ATTR uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
   return tot;
 }
 
-struct CoopSmem {
+struct SelectSmem {
   RadixSmem<Key<float>::RB> sm;
   uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
   uint32_t tpos[SEL_NT];     // candidate gather: per-task output position / count
@@ -274,7 +274,7 @@ __device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32
 // Passes start below the common prefix of all keys (candidates crowd just above the threshold).
 // skip_prefix = false (dense data in global memory) starts at the top bit without the OR pass.
 template <typename KeyAt>
-__device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t k2, CoopSmem& cs,
+__device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t k2, SelectSmem& cs,
                                   SelectThreshold<uint32_t>* th_out, uint32_t* key2_out, bool skip_prefix = true) {
   constexpr int RB = Key<float>::RB;
   constexpr uint32_t FULL = 0x7fffffffu;
@@ -386,7 +386,7 @@ constexpr int FB_TOO_FEW = 1, FB_OVERFLOW = 2;
 __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
                                 const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
                                 int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
-                                int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, CoopSmem& cs,
+                                int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, SelectSmem& cs,
                                 float* vupd) {
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
@@ -499,7 +499,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
 // prediction rank over r, then an ordered compaction that zeroes the selected residuals.
 __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
                                       float* val_out, int32_t* count_out, FastState* state, bool force_exact,
-                                      int why, CoopSmem& cs, float* vupd) {
+                                      int why, SelectSmem& cs, float* vupd) {
   float* data = r + L.offset;
   const int64_t d = L.dim;
   const uint32_t k = static_cast<uint32_t>(L.k);
@@ -545,7 +545,7 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
 // next candidate threshold (small layers then take the candidate path like the big ones).
 __device__ void small_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
                                       float* val_out, int32_t* count_out, FastState* state, bool force_exact, int why,
-                                      CoopSmem& cs, float* vupd, float* sv, bool predict) {
+                                      SelectSmem& cs, float* vupd, float* sv, bool predict) {
   float* data = r + L.offset;
   const int64_t d = L.dim;
   const uint32_t k = static_cast<uint32_t>(L.k);
@@ -746,7 +746,7 @@ __device__ void warp_topk_layer(int j, const lags_layer_t& L, FastState* state, 
 __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, const int2* __restrict__ layer_tasks,
                              FastState* state, const int32_t* cand_cnt, const int32_t* cand_idx, const float* cand_val,
                              int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
-                             int32_t* count_out, uint32_t* skeys, int smem_keys, int force_exact, CoopSmem& cs,
+                             int32_t* count_out, uint32_t* skeys, int smem_keys, int force_exact, SelectSmem& cs,
                              float* vupd, uint32_t t_launch) {
   const uint32_t t_start = globaltimer_lo();
   const lags_layer_t L = layers[j];

@@ -282,7 +282,7 @@ struct lags_bucket {
   double* acc64 = nullptr;
   uint32_t* mask = nullptr;
   char* planes = nullptr;
-  int32_t* order = nullptr;  // layers by decreasing selection work, group by group (phase-1 schedule)
+  int32_t* order = nullptr;  // layers by decreasing selection work, group by group (persistent-role schedule)
   int2* tiles_dec = nullptr;  // decode tiles: (layer, chunk of DEC_NT slots)
   int dec_tiles = 0;
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
@@ -293,7 +293,7 @@ struct lags_bucket {
     int order_base = 0, nlayers = 0;  // contiguous range of `order`
   };
   Group grp[3];
-  CoopScratch coop{};  // per-call selection counter (two-kernel path)
+  SelectCounters sel_ctr{};  // per-call selection counter (persistent role)
   cudaEvent_t probe_before = nullptr, probe_after = nullptr;  // caller-owned, optional
   float* const* grad_table = nullptr;  // caller-owned device array of per-layer gradient pointers
 };
@@ -366,7 +366,7 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_fbc = 0, o_delta = 0, o_tiles = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0, bytes = 0;
   int32_t ntiles = 0;
 };
 
@@ -416,7 +416,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_delta = take(2 * sizeof(double) * nt);
   p->o_tiles = take(sizeof(int2) * static_cast<size_t>(p->ntiles));
   const bool f32 = dtype == LAGS_F32;
-  p->o_fbc = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (CoopScratch)
+  p->o_ctr = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (SelectCounters)
   p->bytes = o;
   return LAGS_OK;
 }
@@ -522,7 +522,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->delta_part = reinterpret_cast<double*>(base + p.o_delta);
   b->tiles_dec = reinterpret_cast<int2*>(base + p.o_tiles);
   b->dec_tiles = p.ntiles;
-  b->coop.work = reinterpret_cast<uint32_t*>(base + p.o_fbc);
+  b->sel_ctr.work = reinterpret_cast<uint32_t*>(base + p.o_ctr);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -555,7 +555,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     }
     b->grp[g].ntasks = static_cast<int>(tasks.size()) - b->grp[g].task_base;
   }
-  // phase-1 schedule of the selection kernel: longest (estimated) work first, group by group
+  // schedule of the selection kernel's persistent role: longest (estimated) work first, group by group
   std::vector<int32_t> order;
   std::vector<double> cost(nlayers);
   for (int j = 0; j < nlayers; ++j)
@@ -587,7 +587,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
-      (dtype != LAGS_F32 || cudaMemsetAsync(b->coop.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
+      (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
       cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) {
     delete b;
@@ -657,10 +657,10 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       if (zg)
         return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                           G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
-                          b->cand_val + cb, b->cand_cnt + G.task_base, status, b->coop.work);
+                          b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work);
       return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                         G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
-                        b->cand_val + cb, b->cand_cnt + G.task_base, status, b->coop.work);
+                        b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work);
     };
     cudaError_t e = cudaSuccess;
     lags_bucket::Group all = b->grp[0];  // K1 streams every task (group 0's then group 1's)
@@ -685,7 +685,7 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       e = launch_pdl_cluster(select_kernel, dim3(grid), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s, cl,
                              b->layers, b->layer_tasks, b->order + G1.order_base, ncl, b->order + G2.order_base,
                              G2.nlayers, b->order + G0.order_base, G0.nlayers, b->state, b->cand_cnt, b->cand_idx,
-                             b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->coop, vu);
+                             b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->sel_ctr, vu);
     }
     const int launches = 2;
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
