@@ -286,8 +286,8 @@ struct lags_bucket {
   int2* tiles_dec = nullptr;  // decode tiles: (layer, chunk of DEC_NT slots)
   int dec_tiles = 0;
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
-  // fp32 pipeline groups: the selection of group 0 (the layers with the heaviest selection work)
-  // runs on `side` while K1 streams group 1 (see compress_impl)
+  // selection groups of an fp32 bucket (plan_groups): 0 persistent role, 1 cluster role, 2 warp
+  // role; each group's tasks and `order` entries are contiguous
   struct Group {
     int task_base = 0, ntasks = 0;    // contiguous range of the task table
     int order_base = 0, nlayers = 0;  // contiguous range of `order`
@@ -366,7 +366,8 @@ struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
-         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0, bytes = 0;
+         o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
+         bytes = 0;
   int32_t ntiles = 0;
 };
 
@@ -527,8 +528,8 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
   b->msg_bytes = static_cast<int64_t>(align_up(b->off_val + val_size(dtype) * static_cast<size_t>(p.total_k), 16));
-  // host tables.  fp32 buckets are split into two pipeline groups; the task table holds group 0's
-  // tasks first so each group's tasks (and candidate lists) are one contiguous range.
+  // host tables.  fp32 buckets are split into selection groups (plan_groups); the task table holds
+  // them group after group, so each group's tasks (and candidate lists) are one contiguous range.
   const std::vector<int> gid = dtype == LAGS_F32 ? plan_groups(dims, ks, nlayers) : std::vector<int>(nlayers, 0);
   std::vector<lags_layer_t> layers(nlayers);
   std::vector<int2> ltasks(nlayers);
