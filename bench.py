@@ -428,7 +428,7 @@ def run_ours(args, dims, ks, world, rank, local):
         train = measure_train(args, world, rank, local, dev)
     if rank == 0 and not args.no_e2e:
         e2e = measure_e2e(args, dims, ks, L, dev)
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
         threads = os.cpu_count() or 1
         s = cpu_oracle_step_rate(dims, ks, 1, threads, steps=1)
         cb, dbb = algorithmic_bytes(n, ks, sum(ks), 1)
