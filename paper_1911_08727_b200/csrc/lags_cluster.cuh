@@ -197,10 +197,13 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     over_any |= o->over;
     rpre[q + 1] = rpre[q] + mq;
   }
-  cluster.sync();  // every CTA has read the counts
+  // (no barrier here: csh.m / csh.over are not written again; the early exit below has its own)
   // central: rank 0 holds a copy of all m keys (plus its own values / indices); otherwise every
   // CTA holds only its own candidates and rank 0's radix passes read the keys over DSMEM
-  constexpr uint32_t CENTRAL_MAX = 16384;  // larger sets: the distributed select is faster
+#ifndef LAGS_CENTRAL_MAX
+#define LAGS_CENTRAL_MAX 16384
+#endif
+  constexpr uint32_t CENTRAL_MAX = LAGS_CENTRAL_MAX;  // larger sets: the distributed select is faster
   const bool central = m <= CENTRAL_MAX && static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
   const bool fits = central || 2ull * m_max <= static_cast<uint64_t>(smem_words);
   int why = 0;
@@ -208,6 +211,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   else if (over_any) why = FB_OVERFLOW;
   else if (m < k && st.thr > 1u) why = FB_TOO_FEW;
   if (why || !fits || m == 0) {  // uniform across the cluster; rank 0 finishes the layer alone
+    cluster.sync();  // no CTA leaves while another may still read its counts
     if (rank == 0) {
       if (why) {
         dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
