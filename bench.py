@@ -154,9 +154,10 @@ def dist_setup():
     return world, rank, local
 
 
-def cpu_oracle_step_rate(dims, ks, world, threads, steps=1, seed=0):
-    """Time the reference algorithm (numpy oracle port) for `steps` full steps of the workload
-    with `world` simulated workers; returns seconds per step (best of `steps`)."""
+def cpu_oracle_step_rate(dims, ks, world, threads, budget=10.0, seed=0):
+    """Time the reference algorithm (numpy oracle port) on full steps of the workload with `world`
+    simulated workers, repeating until about `budget` seconds have run; returns (mean seconds per
+    step, steps timed)."""
     from oracle import lagsgd_oracle as orc
 
     rng = np.random.default_rng(seed)
@@ -164,12 +165,14 @@ def cpu_oracle_step_rate(dims, ks, world, threads, steps=1, seed=0):
     v = rng.standard_normal(n).astype(np.float32)
     grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
     res = [(0.01 * rng.standard_normal(n)).astype(np.float32) for _ in range(world)]
-    best = float("inf")
-    for _ in range(steps):
+    orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)  # warm-up (page faults, pools)
+    total, reps = 0.0, 0
+    while reps == 0 or total < budget:
         t0 = time.perf_counter()
-        orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
-        best = min(best, time.perf_counter() - t0)
-    return best
+        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
+        total += time.perf_counter() - t0
+        reps += 1
+    return total / reps, reps
 
 
 def run_reference(args, dims, ks, world, rank):
@@ -426,14 +429,15 @@ def run_ours(args, dims, ks, world, rank, local):
         del g_bufs
         torch.cuda.empty_cache()
         train = measure_train(args, world, rank, local, dev)
-    if rank == 0 and not args.no_e2e:
-        e2e = measure_e2e(args, dims, ks, L, dev)
+    if not args.no_e2e:  # all ranks: at N > 1 each rank is one worker of the drop-in (NCCL group)
+        e2e = measure_e2e(args, dims, ks, L, dev, world, rank, union)
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
         threads = os.cpu_count() or 1
-        s = cpu_oracle_step_rate(dims, ks, 1, threads, steps=1)
+        s, reps = cpu_oracle_step_rate(dims, ks, 1, threads, budget=args.cpu_budget)
         cb, dbb = algorithmic_bytes(n, ks, sum(ks), 1)
         cpu = {"value": round((cb + dbb) / s / 1e9, 4), "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"1 full ResNet-50-shaped lags_step, P=1 ({s:.2f} s; numpy oracle of R: training.py:227-255)"}
+               "sample": f"{reps} full ResNet-50-shaped lags_steps, P=1 ({reps * s:.1f} s, mean {s:.3f} s/step; "
+                         f"numpy oracle of R: training.py:227-255)"}
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -464,6 +468,9 @@ def run_ours(args, dims, ks, world, rank, local):
         print(json.dumps(out), flush=True)
 
 
+TRAIN_WINDOWS = 5
+
+
 def measure_train(args, world, rank, local, dev):
     """ResNet-50 (config 4) training iterations/s, batch 64/GPU, bf16 autocast, synthetic data:
     LagsSGD (hook-driven sparse exchange) vs dense S-SGD (torch DDP, NCCL all-reduce, 25 MB
@@ -477,6 +484,8 @@ def measure_train(args, world, rank, local, dev):
 
     torch.backends.cudnn.benchmark = True
     x, y = synthetic_images(64, 224, 1000, dev, seed=rank)
+
+    all_windows = {}
 
     def run(kind):
         torch.manual_seed(0)
@@ -503,15 +512,22 @@ def measure_train(args, world, rank, local, dev):
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.train_steps):
-            it()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        ms = torch.tensor([e0.elapsed_time(e1) / args.train_steps], device=dev)
-        if world > 1:
-            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        # TRAIN_WINDOWS windows of train_steps iterations, each max over ranks; the median window
+        # is reported (one transient stall of a shared box must not decide a 20-iteration number)
+        windows = []
+        for _ in range(TRAIN_WINDOWS):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.train_steps):
+                it()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            w = torch.tensor([e0.elapsed_time(e1) / args.train_steps], device=dev)
+            if world > 1:
+                dist.all_reduce(w, op=dist.ReduceOp.MAX)
+            windows.append(float(w))
+        ms = sorted(windows)[len(windows) // 2]
+        all_windows[kind] = [round(w, 3) for w in windows]
         comm = None
         if kind == "lags":
             opt.enable_timing(True)
@@ -528,7 +544,7 @@ def measure_train(args, world, rank, local, dev):
             nb = None
         del opt, net, model
         torch.cuda.empty_cache()
-        return float(ms), comm, nb
+        return ms, comm, nb
 
     lags_ms, comm, nb = run("lags")
     nx_ms, _, _ = run("lags_noexchange")
@@ -539,44 +555,60 @@ def measure_train(args, world, rank, local, dev):
            "dense_ddp_iter_per_s": round(1e3 / dense_ms, 3), "dense_ms_per_iter": round(dense_ms, 3),
            "lags_no_exchange_ms_per_iter": round(nx_ms, 3),
            "sum_compress_ms": round(comm[1], 3), "sum_exchange_ms": round(comm[0], 3),
-           "sum_decode_ms": round(comm[2], 3)}
+           "sum_decode_ms": round(comm[2], 3), "windows": TRAIN_WINDOWS, "ms_per_iter_windows": all_windows}
     if world > 1 and comm[0] > 0:
         exposed = max(0.0, lags_ms - nx_ms)
         out["exchange_hidden_fraction"] = round(max(0.0, min(1.0, 1.0 - exposed / comm[0])), 4)
     return out
 
 
-def measure_e2e(args, dims, ks, L, dev):
-    """Same metric through the reference-facing drop-in lags_step with host numpy buffers."""
+def measure_e2e(args, dims, ks, L, dev, world=1, rank=0, union=None):
+    """Same metric through the reference-facing drop-in lags_step with host numpy buffers.  At
+    N > 1 every rank is one worker (``group=``: its own gradient and residual, the replica of v;
+    messages all-gathered over NCCL); the step time is the max over ranks of each rank's own
+    host-clock time (the host copies are part of what is measured)."""
     import torch
 
     n = sum(dims)
     shape = [L.LayerShape(i + 1, d) for i, d in enumerate(dims)]
-    rng = np.random.default_rng(7)
-    v = L.LayeredVector(shape, rng.standard_normal(n).astype(np.float32))
+    v = L.LayeredVector(shape, np.random.default_rng(7).standard_normal(n).astype(np.float32))
+    rng = np.random.default_rng(8 + rank)
     gs = [L.LayeredVector(shape, rng.standard_normal(n).astype(np.float32)) for _ in range(2)]
     res = [L.LayeredVector.zeros(shape, np.float32)]
     counts = {i + 1: k for i, k in enumerate(ks)}
     steps = max(3, min(args.steps, 10))
+    grp = None
+    if world > 1:
+        import torch.distributed as dist
+
+        grp = dist.group.WORLD
     for t in range(5):  # past the one-time page-locking of the reused host buffers
-        v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res)
+        v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res, group=grp)
     torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for t in range(steps):
-        v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res)
+        v = L.lags_step(v, [gs[t % 2]], 0.1, counts, res, group=grp)
     torch.cuda.synchronize(dev)
     dt = (time.perf_counter() - t0) / steps
-    comp_b, dec_b = algorithmic_bytes(n, ks, sum(ks), 1)
-    # bytes over PCIe per step: g and r up, the new r down (chunk-pipelined); v stays on the host
-    # (host threads copy it into the pinned output) and the decode reads / writes only the
-    # selected entries of that output through its device mapping (4 B each way per entry)
+    if world > 1:
+        mx = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dt = float(mx)
     nsel = sum(ks)
-    return {"value": round((comp_b + dec_b) / dt / 1e9, 3), "unit": UNIT, "h2d_bytes_per_step": 2 * 4 * n + 4 * nsel,
-            "d2h_bytes_per_step": 4 * n + 4 * nsel, "ms_per_step": round(dt * 1e3, 3),
-            "api": "paper_1911_08727_b200.lags_step (drop-in for R: training.py:227) on host numpy LayeredVectors",
+    comp_b, dec_b = algorithmic_bytes(n, ks, nsel if union is None or world == 1 else union, world)
+    # bytes over PCIe per step (all ranks): g and r up, the new r down (chunk-pipelined); v stays
+    # on the host (host threads copy it into the pinned output) and the decode reads / writes only
+    # the selected entries of that output through its device mapping (4 B each way per entry)
+    return {"value": round((comp_b + dec_b) / dt / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": world * (2 * 4 * n + 4 * nsel), "d2h_bytes_per_step": world * (4 * n + 4 * nsel),
+            "ms_per_step": round(dt * 1e3, 3),
+            "api": "paper_1911_08727_b200.lags_step (drop-in for R: training.py:227) on host numpy LayeredVectors"
+                   + (f", group= NCCL world {world} (one worker per rank)" if world > 1 else ""),
             "transfer": "g, r up and r down in layer chunks on 2 copy streams; v copied host-side, selected "
                         "entries of the pinned output updated in place by the decode (UVA)",
-            "steps": steps, "world_used": 1}
+            "steps": steps, "world_used": world}
 
 
 def main():
@@ -585,6 +617,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds for the --impl reference run")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work for cpu_baseline")
     ap.add_argument("--soak", type=float, default=1.0, help="untimed busy seconds before timing (clocks)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")

@@ -214,7 +214,7 @@ def _host_copy(dst: np.ndarray, src: np.ndarray, plan: list) -> list:
     return joins
 
 
-def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
+def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v, group=None):
     """The drop-in step with its host transfers overlapped, chunk by chunk of layers.
 
     PCIe carries only what must cross it: the gradients and residuals up, the new residuals down
@@ -225,9 +225,21 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
     Order (R: training.py:174-175): every gradient goes up and is checked for finiteness before
     any residual is written back; residual chunks stream up behind the gradients, each chunk's
     compress runs as soon as it has arrived, and its new residual streams back on a third stream
-    while later chunks still upload (the copy engines run both directions at once)."""
+    while later chunks still upload (the copy engines run both directions at once).
+
+    With a process group this process is ONE worker (``grads``/``residuals`` hold its own): the
+    finiteness flags of all workers are all-gathered before any residual is written back, and each
+    chunk's fixed-size message is all-gathered over NCCL before the rank-ordered decode, so every
+    rank computes the same new parameters as the single-process P-worker step."""
     _mark("start")
     P = len(grads)
+    world, me = 1, 0
+    if group is not None:
+        import torch.distributed as dist
+
+        world, me = dist.get_world_size(group), dist.get_rank(group)
+        if P != 1:
+            raise ValueError("with a process group each rank passes exactly its own gradient and residual")
     dev = torch.device("cuda", torch.cuda.current_device())
     s_up, s_cmp, s_down = _streams(dev)
     cur = torch.cuda.current_stream(dev)
@@ -260,7 +272,11 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
             for gd in g_dev[p]:
                 N.check(N.lags_check_finite(N.F64 if gd.dtype == torch.float64 else N.F32, gd.data_ptr(), gd.numel(),
                                             pre[p:p + 1].data_ptr(), s_cmp.cuda_stream), "lags_check_finite")
-        pre_h = torch.empty(P, dtype=torch.int32, pin_memory=True)
+        if world > 1:  # every worker's flags, in rank order (R: training.py:174-175 names the first)
+            pre_all = torch.empty(world, dtype=torch.int32, device=dev)
+            dist.all_gather_into_tensor(pre_all, pre, group=group)
+            pre = pre_all
+        pre_h = torch.empty(world * P, dtype=torch.int32, pin_memory=True)
         pre_h.copy_(pre, non_blocking=True)
         ev_pre = torch.cuda.Event()
         ev_pre.record(s_cmp)
@@ -269,7 +285,7 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
         status = torch.zeros(P, dtype=torch.int32, device=dev)
         staged = []
         for c, (lo, hi, e0, e1) in enumerate(plan):
-            bucket = _bucket_for(dims[lo:hi], ks[lo:hi], mode, P)
+            bucket = _bucket_for(dims[lo:hi], ks[lo:hi], mode, world * P)
             s_cmp.wait_event(ev_in[c])
             msgs = bucket.new_messages(P)
             for p in range(P):
@@ -281,7 +297,7 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
     _mark("uploads and compress enqueued")
     ev_pre.synchronize()
     _mark("gradients checked")
-    bad = [p for p in range(P) if pre_h[p] & N.STATUS_NONFINITE]
+    bad = [p for p in range(world * P) if pre_h[p] & N.STATUS_NONFINITE]
     if bad:  # R: training.py:174-175 -- raised before any residual is written back
         for j in join_copy:
             j()
@@ -297,8 +313,12 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
                 r_dst[p][e0:e1].copy_(r_dev[c][p], non_blocking=True)
     with torch.cuda.stream(s_cmp):
         for c, (bucket, msgs, e0, e1, _) in enumerate(staged):
+            if world > 1:  # every worker's message for this chunk, rank order
+                allm = bucket.new_messages(world)
+                dist.all_gather_into_tensor(allm, msgs, group=group)
+                msgs = allm
             join_copy[c]()  # this chunk of the output holds v: update its selected entries in place
-            bucket.decode(msgs, P, out[e0:e1], stream=s_cmp)
+            bucket.decode(msgs, world * P, out[e0:e1], stream=s_cmp)
     _mark("chunks enqueued")
     s_cmp.synchronize()
     _mark("decode done")
@@ -310,7 +330,8 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v):
     return out
 
 
-def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: int | None = None):
+def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: int | None = None, *,
+              group=None):
     """Single-layer (whole stacked vector) selection with error feedback -- R: training.py:203-224.
 
     The same kernels with one "layer" spanning the flat vector: R: training.py:216-217 checks k
@@ -330,16 +351,21 @@ def slgs_step(v, grads: Sequence, alpha, global_k: int, residuals: Sequence, t: 
     one = (LayerShape(1, dim),)
     for p, g in enumerate(grads, start=1):  # layout check against the real layer split first
         if layout_of(g) != layout_of(v):
-            return lags_step(v, grads, alpha, {ls.layer_id: 1 for ls in v.shape}, residuals, t)
+            return lags_step(v, grads, alpha, {ls.layer_id: 1 for ls in v.shape}, residuals, t, group=group)
     flat_res = [_Flat(one, r.data) for r in residuals]
     out = lags_step(_Flat(one, v.data), [_Flat(one, g.data) for g in grads], alpha, {1: int(global_k)}, flat_res, t,
-                    _promote_v=True)
+                    group=group, _promote_v=True)
     return type(v)(v.shape, out.data)
 
 
 def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: int | None = None, *,
-              _promote_v: bool = False):
+              group=None, _promote_v: bool = False):
     """Per-layer selection with error feedback on the B200; R: training.py:227-255.
+
+    ``group`` (a torch.distributed NCCL process group): run as one worker of a multi-process job --
+    ``grads``/``residuals`` hold this rank's own single gradient and residual, ``v`` the replica;
+    the workers are the ranks in group order, and every rank returns the parameters the
+    single-process step over all of their gradients would return (same bits).
 
     (_promote_v: return float32 parameters as the unrounded float64 ``v - total / P``, which is
     what the reference's slgs_step does, R: training.py:224.)"""
@@ -375,5 +401,5 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
             raise ValueError(f"k={k} outside 1..{d}")
         ks.append(k)
     out = _pipelined_step(v.data, [g.data for g in grads], [r.data for r in residuals], alpha, dims, tuple(ks),
-                          mode, t, _promote_v)
+                          mode, t, _promote_v, group)
     return type(v)(v.shape, out.numpy())

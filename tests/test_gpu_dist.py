@@ -1,0 +1,93 @@
+"""Multi-process drop-in: ``lags_step(..., group=...)`` with one worker per GPU (NCCL) must return,
+on every rank, the bits the single-process P-worker step returns (checked against the pinned
+oracle), update each rank's own residual exactly, and raise the same DivergenceError on every rank
+before any residual is written back.  Needs 2 GPUs (``gpurun --gpus 2``); skipped otherwise."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import lagsgd_oracle as orc  # noqa: E402
+
+WORLD = 2
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _case(it):
+    rng = np.random.default_rng(500 + it)
+    dtype = [np.float32, np.float64][it % 2]
+    dims = [int(x) for x in rng.integers(1, 300_000, size=int(rng.integers(1, 9)))]
+    if it == 2:
+        dims = [5_000_000, 3, 70_000]  # spans several pipeline chunks
+    n = sum(dims)
+    counts = [max(1, d // int(rng.choice([1, 10, 100, 1000]))) for d in dims]
+    v = rng.standard_normal(n).astype(dtype)
+    grads = [(rng.standard_normal(n) * np.exp(rng.standard_normal(n))).astype(dtype) for _ in range(WORLD)]
+    res = [(0.01 * rng.standard_normal(n)).astype(dtype) for _ in range(WORLD)]
+    alpha = float(rng.uniform(0.01, 1.0))
+    return dims, counts, v, grads, res, alpha
+
+
+def _worker(rank, port, out_dir):
+    import torch.distributed as dist
+
+    import paper_1911_08727_b200 as L
+
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=WORLD)
+    grp = dist.group.WORLD
+    lv = lambda dims, a: L.LayeredVector([L.LayerShape(i + 1, d) for i, d in enumerate(dims)], a)  # noqa: E731
+    save = {}
+    for it in range(4):
+        dims, counts, v, grads, res, alpha = _case(it)
+        r = lv(dims, res[rank].copy())
+        vv = lv(dims, v)
+        for t in range(2):  # two chained steps (residuals carry over)
+            vv = L.lags_step(vv, [lv(dims, grads[rank] * (t + 1))], alpha, {i + 1: k for i, k in enumerate(counts)},
+                             [r], t=t, group=grp)
+        save[f"v{it}"] = vv.data
+        save[f"r{it}"] = r.data
+    # divergence: rank 1's gradient is non-finite -> both ranks raise naming worker 2, residuals untouched
+    dims = [1000]
+    g = np.ones(1000, np.float32)
+    if rank == 1:
+        g[7] = np.nan
+    r = lv(dims, np.full(1000, 0.5, np.float32))
+    try:
+        L.lags_step(lv(dims, np.zeros(1000, np.float32)), [lv(dims, g)], 0.1, {1: 3}, [r], t=9, group=grp)
+        save["div"] = np.array("no error")
+    except L.DivergenceError as e:
+        save["div"] = np.array(f"{e.iteration}:{e}")
+    save["div_res_ok"] = np.array(bool(np.all(r.data == 0.5)))
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **save)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < WORLD, reason="needs 2 GPUs")
+def test_two_rank_nccl_lags_step_matches_oracle(tmp_path):
+    import torch.multiprocessing as mp
+
+    mp.spawn(_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
+    outs = [np.load(tmp_path / f"rank{p}.npz") for p in range(WORLD)]
+    for it in range(4):
+        dims, counts, v, grads, res, alpha = _case(it)
+        for t in range(2):
+            v = orc.lags_step(v, [g * (t + 1) for g in grads], alpha, dims, counts, res)
+        for p in range(WORLD):
+            assert outs[p][f"v{it}"].tobytes() == v.tobytes(), (it, p)
+            assert outs[p][f"r{it}"].tobytes() == res[p].tobytes(), (it, p)
+    for p in range(WORLD):
+        msg = str(outs[p]["div"])
+        assert msg.startswith("9:") and "worker 2" in msg, msg
+        assert bool(outs[p]["div_res_ok"])
