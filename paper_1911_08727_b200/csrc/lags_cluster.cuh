@@ -29,10 +29,19 @@ namespace lags {
 constexpr int CLUSTER = LAGS_CLUSTER;              // CTAs per cluster layer
 constexpr int CLUSTER_MIN_K = LAGS_CLUSTER_MIN_K;  // layers with at least this k (and > SMALL_LAYER) use clusters
 
+// Execution-only cluster barrier: no release/acquire (cluster.sync()'s arrive is a release, which
+// waits for every earlier global store of the thread to drain).  For the barriers that only keep a
+// CTA resident while its peers finish reading its shared memory -- reads whose values the peers
+// have already consumed before arriving.
+__device__ __forceinline__ void cluster_sync_exec() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 struct ClusterShared {
   uint32_t m, over;          // this CTA's candidate count / overflow
   uint32_t gt, eq;           // this CTA's compaction counts
   uint32_t prefix, pmask, n_gt, need_eq, key2;  // rank 0: the threshold
+  uint32_t diff;             // OR of key ^ key0 over this CTA's candidates
 };
 
 // Dual-rank radix select over a cluster's candidates when every CTA holds only its own keys
@@ -179,7 +188,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     local += min(c, static_cast<uint32_t>(cap));
   }
   local = block_sum(local, cs.sm);
-  over = block_sum(over, cs.sm);
+  over = __syncthreads_or(over) ? 1u : 0u;
   if (threadIdx.x == 0) {
     csh.m = local;
     csh.over = over;
@@ -211,7 +220,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   else if (over_any) why = FB_OVERFLOW;
   else if (m < k && st.thr > 1u) why = FB_TOO_FEW;
   if (why || !fits || m == 0) {  // uniform across the cluster; rank 0 finishes the layer alone
-    cluster.sync();  // no CTA leaves while another may still read its counts
+    cluster_sync_exec();  // no CTA leaves while another may still read its counts
     if (rank == 0) {
       if (why) {
         dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
@@ -239,6 +248,8 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   int32_t* si = reinterpret_cast<int32_t*>(dyn + ibase);
   uint32_t* keys0 = cluster.map_shared_rank(dyn, 0);
   uint32_t carry = 0;
+  const uint32_t key0 = st.thr;  // reference key of the common-prefix OR
+  if (threadIdx.x == 0) cs.sm.diff_acc = 0u;
   for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
     const int nt = min(SEL_NT, t_hi - t0);
     const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)) : 0u;
@@ -246,6 +257,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
     cs.tpos[threadIdx.x] = pos;
     __syncthreads();
+    uint32_t dx = 0u;
     for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
       int64_t src[GATHER_ILP];
 #pragma unroll
@@ -278,12 +290,16 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
           sv[e] = xv[u];
           si[e] = xi[u];
           if (central) keys0[pre + e] = Key<float>::of(xv[u]);
+          dx |= Key<float>::of(xv[u]) ^ key0;
         }
       }
     }
+    dx = __reduce_or_sync(0xffffffffu, dx);
+    if ((threadIdx.x & 31) == 0 && dx) atomicOr(&cs.sm.diff_acc, dx);
     carry += tot;
     __syncthreads();
   }
+  if (threadIdx.x == 0) csh.diff = cs.sm.diff_acc;
   cluster.sync();  // all keys are in rank 0
   const long long c1 = clock64();
   // 3. rank 0 selects
@@ -294,7 +310,9 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       uint32_t key2;
       const uint32_t* keys = dyn;
       auto key_at = [=](int64_t i) { return keys[i]; };
-      radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+      uint32_t dk[2] = {0u, key0};
+      for (int q = 0; q < CLUSTER; ++q) dk[0] |= cluster.map_shared_rank(&csh, q)->diff;
+      radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
       if (threadIdx.x == 0) {
         csh.prefix = th.prefix;
         csh.pmask = th.pmask;
@@ -330,20 +348,16 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   }
   const uint32_t key2 = cluster.map_shared_rank(&csh, 0)->key2;
   // 4. ordered compaction of the own range with the carried counts of the lower ranks
-  uint32_t lgt = 0, leq = 0;
+  uint32_t lge = 0;  // gt count | eq count << 16 (mr < 65536: it fits the shared memory)
   for (uint32_t i = threadIdx.x; i < mr; i += SEL_NT) {
     const uint32_t key = Key<float>::of(sv[i]);
     const uint32_t hk = key & th.pmask;
-    if (key != 0u) {
-      lgt += hk > th.prefix ? 1u : 0u;
-      leq += hk == th.prefix ? 1u : 0u;
-    }
+    if (key != 0u) lge += hk > th.prefix ? 1u : (hk == th.prefix ? 0x10000u : 0u);
   }
-  lgt = block_sum(lgt, cs.sm);
-  leq = block_sum(leq, cs.sm);
+  lge = block_sum(lge, cs.sm);
   if (threadIdx.x == 0) {
-    csh.gt = lgt;
-    csh.eq = leq;
+    csh.gt = lge & 0xffffu;
+    csh.eq = lge >> 16;
   }
   cluster.sync();
   uint32_t cg0 = 0, ce0 = 0;
@@ -372,8 +386,12 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   if (rank == CLUSTER - 1 && threadIdx.x == 0) count_out[j] = static_cast<int32_t>(end);
   if (rank == 0 && threadIdx.x == 0) {
     auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
-    FastState ns = candidate_state(st, next_threshold(st, m, k, k2, th.prefix, key2), m, k,
-                                   q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22));
+#ifdef LAGS_DBG_SELECT
+    const uint32_t ph = cs.sm.dbg;
+#else
+    const uint32_t ph = q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22);
+#endif
+    FastState ns = candidate_state(st, next_threshold(st, m, k, k2, th.prefix, key2), m, k, ph);
     ns.cycles = static_cast<uint32_t>(clock64() - t_begin);
     ns.path = 3u;
     ns.t_start = t_start;
@@ -381,7 +399,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     ns.t_launch = t_launch;
     state[j] = ns;
   }
-  cluster.sync();  // no CTA leaves while others may still read its shared memory
+  cluster_sync_exec();  // no CTA leaves while others may still read its shared memory
 }
 
 // The whole selection of an fp32 compress in ONE launch (thread-block clusters of CLUSTER CTAs):

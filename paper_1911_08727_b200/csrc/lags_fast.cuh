@@ -272,16 +272,27 @@ __device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32
 // Two ranks in one set of radix passes over m keys (shared memory): the exact threshold of the
 // k largest (select form) and a lower bound of the k2-th largest key (the next prediction).
 // Passes start below the common prefix of all keys (candidates crowd just above the threshold).
-// skip_prefix = false (dense data in global memory) starts at the top bit without the OR pass.
+// skip_prefix = false (dense data in global memory) starts at the top bit without the OR pass;
+// diff_key0 = {OR of key ^ key0 over all keys, key0} (computed by the caller's gather) skips it.
+// coarse_key2: the prediction is the lower edge of its first-pass bin (candidate sets, where a
+// first-pass bin holds a few keys) instead of being refined in the later passes.
+// Once the threshold's bin holds at most BIN_LIST_MAX keys, the remaining passes are replaced by
+// one pass that lists the bin's keys and a direct rank count among them.
+constexpr uint32_t BIN_LIST_MAX = 128;
+
 template <typename KeyAt>
 __device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t k2, SelectSmem& cs,
-                                  SelectThreshold<uint32_t>* th_out, uint32_t* key2_out, bool skip_prefix = true) {
+                                  SelectThreshold<uint32_t>* th_out, uint32_t* key2_out, bool skip_prefix = true,
+                                  const uint32_t* diff_key0 = nullptr, bool coarse_key2 = false) {
   constexpr int RB = Key<float>::RB;
   constexpr uint32_t FULL = 0x7fffffffu;
   RadixSmem<RB>& sm = cs.sm;
-  const uint32_t key0 = skip_prefix ? key_at(0) : 0u;
-  uint32_t diff = FULL;
-  if (skip_prefix) {
+  uint32_t key0 = 0u, diff = FULL;
+  if (diff_key0) {
+    diff = diff_key0[0];
+    key0 = diff_key0[1];
+  } else if (skip_prefix) {
+    key0 = key_at(0);
     diff = 0;
     for (int64_t i = threadIdx.x; i < m; i += SEL_NT) diff |= key_at(i) ^ key0;
     diff = block_or<uint32_t, RB>(diff, sm);
@@ -305,32 +316,80 @@ __device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t 
   }
   while (width > 0 && !(done[0] && done[1])) {
     const bool same = !done[0] && !done[1] && prefix[0] == prefix[1] && pmask[0] == pmask[1];
+    const bool second = !same && !done[1];
     for (int b = threadIdx.x; b < F32_BINS; b += SEL_NT) {
       sm.hist[b] = 0;
-      cs.hist2[b] = 0;
+      if (second) cs.hist2[b] = 0;
     }
+    if (threadIdx.x == 0) sm.list_n = 0;
     __syncthreads();
     const uint32_t dmask = (1u << width) - 1u;
     for (int64_t i = threadIdx.x; i < m; i += SEL_NT) {
       const uint32_t key = key_at(i);
       const uint32_t bin = (key >> shift) & dmask;
       if (!done[0] && (key & pmask[0]) == prefix[0]) atomicAdd(&sm.hist[bin], 1u);
-      if (!same && !done[1] && (key & pmask[1]) == prefix[1]) atomicAdd(&cs.hist2[bin], 1u);
+      if (second && (key & pmask[1]) == prefix[1]) atomicAdd(&cs.hist2[bin], 1u);
     }
     __syncthreads();
+    uint32_t bin[2], above[2], in_bin[2];
+    if (same) {
+      find_bin2<RB>(sm, sm.hist, rank[0], rank[1], bin, above, in_bin);
+    } else {
+      for (int q = 0; q < 2; ++q)
+        if (!done[q]) find_bin<RB>(sm, rank[q], &bin[q], &above[q], &in_bin[q], q == 0 ? sm.hist : cs.hist2);
+    }
     for (int q = 0; q < 2; ++q) {
       if (done[q]) continue;
-      uint32_t bin, above, in_bin;
-      find_bin<RB>(sm, rank[q], &bin, &above, &in_bin, (q == 0 || same) ? sm.hist : cs.hist2);
-      prefix[q] |= bin << shift;
+      prefix[q] |= bin[q] << shift;
       pmask[q] |= dmask << shift;
-      rank[q] -= above;
-      if (q == 0) n_gt0 += above;
-      if (shift == 0 || (in_bin == rank[q] && prefix[q] != 0u)) done[q] = true;
+      rank[q] -= above[q];
+      if (q == 0) n_gt0 += above[q];
+      if (shift == 0 || (in_bin[q] == rank[q] && prefix[q] != 0u)) done[q] = true;
     }
+    if (coarse_key2) done[1] = true;
+#ifdef LAGS_DBG_SELECT
+    if (threadIdx.x == 0) {
+      if (shift + width == (diff ? 32 - __clz(static_cast<int>(diff)) : 0))  // first pass
+        sm.dbg = min(in_bin[0], 4095u) | (static_cast<uint32_t>(diff ? 31 - __clz(static_cast<int>(diff)) : 0) << 12);
+      sm.dbg += 1u << 18;  // passes
+    }
+#endif
     const int ns = shift > RB ? shift - RB : 0;
     width = shift - ns;
     shift = ns;
+    if (!done[0] && done[1] && in_bin[0] <= BIN_LIST_MAX) {
+      // bin-list finish: the threshold bin's keys, then the rank[0]-th largest by direct count
+      uint32_t* list = cs.hist2;
+      for (int64_t i = threadIdx.x; i < m; i += SEL_NT) {
+        const uint32_t key = key_at(i);
+        if ((key & pmask[0]) == prefix[0]) list[atomicAdd(&sm.list_n, 1u)] = key;
+      }
+      __syncthreads();
+      const uint32_t c = in_bin[0];
+      if (threadIdx.x < c) {
+        const uint32_t mine = list[threadIdx.x];
+        uint32_t gt = 0, eq = 0;
+        for (uint32_t q = 0; q < c; ++q) {
+          const uint32_t x = list[q];
+          gt += x > mine ? 1u : 0u;
+          eq += x == mine ? 1u : 0u;
+        }
+        if (gt < rank[0] && rank[0] <= gt + eq) {  // equal keys write equal values
+          sm.list_key = mine;
+          sm.list_gt = gt;
+        }
+      }
+      __syncthreads();
+      prefix[0] = sm.list_key;
+      pmask[0] = FULL;
+      rank[0] -= sm.list_gt;
+      n_gt0 += sm.list_gt;
+      done[0] = true;
+#ifdef LAGS_DBG_SELECT
+      if (threadIdx.x == 0) sm.dbg |= 1u << 22;
+#endif
+      __syncthreads();  // list_key / list_gt / the list are read before any reuse
+    }
   }
   if (static_cast<int64_t>(k) >= m) {  // every nonzero candidate is selected
     th_out->prefix = 0u;
@@ -397,8 +456,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     local += min(c, static_cast<uint32_t>(cap));
   }
   const uint32_t m = block_sum(local, sm);
-  over = block_sum(over, sm);
-  if (over) return FB_OVERFLOW;
+  if (__syncthreads_or(over)) return FB_OVERFLOW;
   if (m < k && st.thr > 1u) return FB_TOO_FEW;
   float* data = r + L.offset;
   uint32_t cnt = 0;
@@ -412,8 +470,11 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     float* sv = in_smem ? reinterpret_cast<float*>(dyn) : gval + gbase;
     int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + m : gidx + gbase;
     // gather: positions by a block scan over task counts, then one thread per entry (the owning
-    // task is found by binary search over the positions), every load independent
+    // task is found by binary search over the positions), every load independent; the keys'
+    // common prefix (OR of key ^ key0, key0 = the candidate threshold) is accumulated on the way
     uint32_t carry = 0;
+    const uint32_t key0 = st.thr;
+    if (threadIdx.x == 0) sm.diff_acc = 0u;
     for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
       const int nt = min(SEL_NT, tr.y - t0);
       const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)) : 0u;
@@ -423,7 +484,8 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       __syncthreads();
       // batches of GATHER_ILP entries per thread: all source addresses first, then all loads in
       // flight together, then the stores (the destination may alias global scratch)
-        for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
+      uint32_t dx = 0u;
+      for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
         int64_t src[GATHER_ILP];
 #pragma unroll
         for (int u = 0; u < GATHER_ILP; ++u) {
@@ -454,9 +516,12 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
             const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
             sv[carry + e] = xv[u];
             si[carry + e] = xi[u];
+            dx |= Key<float>::of(xv[u]) ^ key0;
           }
         }
       }
+      dx = __reduce_or_sync(0xffffffffu, dx);
+      if ((threadIdx.x & 31) == 0 && dx) atomicOr(&sm.diff_acc, dx);
       carry += tot;
       __syncthreads();
     }
@@ -464,7 +529,8 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     SelectThreshold<uint32_t> th;
     uint32_t key2;
     const long long c1 = clock64();
-    radix_select_dual(key_at, m, k, k2, cs, &th, &key2);
+    const uint32_t dk[2] = {sm.diff_acc, key0};
+    radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
     const long long c2 = clock64();
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
       *x = sv[i];
@@ -484,6 +550,9 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     const long long c3 = clock64();
     auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
     phases = q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22);
+#ifdef LAGS_DBG_SELECT
+    phases = sm.dbg;
+#endif
     pred = next_threshold(st, m, k, k2, th.prefix, key2);
   }
   if (threadIdx.x == 0) {

@@ -47,6 +47,10 @@ struct RadixSmem {
   uint32_t warp_tot[33];
   uint32_t above, bin_count;
   int found;
+  uint32_t found2[2], above2[2], count2[2];  // find_bin2
+  uint32_t list_n, list_key, list_gt;         // bin-list finish of radix_select_dual
+  uint32_t diff_acc;                          // key ^ key0 OR-accumulated by the candidate gathers
+  uint32_t dbg;                               // -DLAGS_DBG_SELECT: radix_select_dual's shape
 };
 
 // Bin holding the rank-th largest (1-based) of the histogram (descending scan).  All threads.
@@ -82,6 +86,50 @@ __device__ LAGS_FINDBIN_ATTR void find_bin(RadixSmem<RB>& sm, uint32_t rank, uin
   *bin = static_cast<uint32_t>(sm.found);
   *above = sm.above;
   *in_bin = sm.bin_count;
+  __syncthreads();
+}
+
+// Both ranks' bins in one scan of the histogram (the first pass of a dual select, where both
+// ranks share the prefix).  bin/above/in_bin are arrays of 2.  All threads.
+template <int RB>
+__device__ LAGS_FINDBIN_ATTR void find_bin2(RadixSmem<RB>& sm, const uint32_t* H, uint32_t r0, uint32_t r1,
+                                          uint32_t* bin, uint32_t* above, uint32_t* in_bin) {
+  constexpr int NB = RadixSmem<RB>::NB;
+  constexpr int PER = NB / SEL_NT;
+  const int t = threadIdx.x;
+  uint32_t h[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    h[q] = H[NB - 1 - t * PER - q];
+    s += h[q];
+  }
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan<SEL_NT>(s, sm.warp_tot, &tot);
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const uint32_t r = w ? r1 : r0;
+    if (ex < r && r <= ex + s) {
+      uint32_t c = ex;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        if (r <= c + h[q]) {
+          sm.count2[w] = h[q];
+          sm.above2[w] = c;
+          sm.found2[w] = static_cast<uint32_t>(NB - 1 - t * PER - q);
+          break;
+        }
+        c += h[q];
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    bin[w] = sm.found2[w];
+    above[w] = sm.above2[w];
+    in_bin[w] = sm.count2[w];
+  }
   __syncthreads();
 }
 
