@@ -37,11 +37,32 @@ __device__ __forceinline__ void cluster_sync_exec() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 
+// -DLAGS_DBG_STAMPS: clock64 / globaltimer at the phase boundaries of the first cluster layer,
+// per rank (read back by lags_dbg_stamps_read; diagnostic builds only).
+#ifdef LAGS_DBG_STAMPS
+__device__ unsigned long long lags_dbg_stamps[CLUSTER][2][24];
+#define LAGS_STAMP(i)                                                   \
+  do {                                                                  \
+    if (blockIdx.x < CLUSTER && threadIdx.x == 0) {                     \
+      lags_dbg_stamps[blockIdx.x][0][i] = clock64();                    \
+      unsigned long long g_;                                            \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));            \
+      lags_dbg_stamps[blockIdx.x][1][i] = g_;                           \
+    }                                                                   \
+  } while (0)
+#else
+#define LAGS_STAMP(i) \
+  do {                \
+  } while (0)
+#endif
+
 struct ClusterShared {
   uint32_t m, over;          // this CTA's candidate count / overflow
   uint32_t gt, eq;           // this CTA's compaction counts
   uint32_t prefix, pmask, n_gt, need_eq, key2;  // rank 0: the threshold
   uint32_t diff;             // OR of key ^ key0 over this CTA's candidates
+  uint32_t qsum[CLUSTER];    // the ranks' candidate counts (every CTA computes all of them)
+  uint32_t qdiff[CLUSTER];   // central: every rank's OR word (pushed by each rank before the barrier)
 };
 
 // Dual-rank radix select over a cluster's candidates when every CTA holds only its own keys
@@ -180,33 +201,49 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   const int T = tr.y - tr.x;
   const int t_lo = tr.x + static_cast<int>((static_cast<int64_t>(T) * rank) / CLUSTER);
   const int t_hi = tr.x + static_cast<int>((static_cast<int64_t>(T) * (rank + 1)) / CLUSTER);
-  // 1. counts
-  uint32_t local = 0, over = 0;
-  for (int t = t_lo + threadIdx.x; t < t_hi; t += SEL_NT) {
+  // every CTA of the cluster must be running before any remote shared-memory access: arrive now,
+  // wait just before the first remote store (the counts below overlap the barrier)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  LAGS_STAMP(0);
+  // 1. counts: every CTA reads ALL of the layer's task counts (one load per thread for layers
+  // up to SEL_NT tasks) and derives m, the ranks' sums and its own offset -- no exchange
+  int bnd[CLUSTER + 1];
+#pragma unroll
+  for (int q = 0; q <= CLUSTER; ++q) bnd[q] = tr.x + static_cast<int>((static_cast<int64_t>(T) * q) / CLUSTER);
+  if (threadIdx.x < CLUSTER) csh.qsum[threadIdx.x] = 0u;
+  uint32_t qs[CLUSTER];
+#pragma unroll
+  for (int q = 0; q < CLUSTER; ++q) qs[q] = 0u;
+  uint32_t over = 0;
+  for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
-    local += min(c, static_cast<uint32_t>(cap));
+    const uint32_t cc = min(c, static_cast<uint32_t>(cap));
+#pragma unroll
+    for (int q = 0; q < CLUSTER; ++q) qs[q] += (t >= bnd[q] && t < bnd[q + 1]) ? cc : 0u;
   }
-  local = block_sum(local, cs.sm);
-  over = __syncthreads_or(over) ? 1u : 0u;
-  if (threadIdx.x == 0) {
-    csh.m = local;
-    csh.over = over;
+  LAGS_STAMP(1);
+  __syncthreads();  // qsum / qge zeroed
+#pragma unroll
+  for (int q = 0; q < CLUSTER; ++q) {
+    const uint32_t w = __reduce_add_sync(0xffffffffu, qs[q]);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(&csh.qsum[q], w);
   }
-  cluster.sync();
-  uint32_t m = 0, pre = 0, m_max = 0, over_any = 0;
+  const uint32_t over_any = __syncthreads_or(over) ? 1u : 0u;
+  LAGS_STAMP(2);
+  LAGS_STAMP(3);
+  uint32_t m = 0, pre = 0, m_max = 0;
   uint32_t rpre[CLUSTER + 1];  // prefix of the ranks' candidate counts (remote key reads)
   rpre[0] = 0;
+#pragma unroll
   for (int q = 0; q < CLUSTER; ++q) {
-    const ClusterShared* o = cluster.map_shared_rank(&csh, q);
-    const uint32_t mq = o->m;
+    const uint32_t mq = csh.qsum[q];
     if (q < rank) pre += mq;
     m += mq;
     m_max = max(m_max, mq);
-    over_any |= o->over;
     rpre[q + 1] = rpre[q] + mq;
   }
-  // (no barrier here: csh.m / csh.over are not written again; the early exit below has its own)
+  const uint32_t local = csh.qsum[rank];
   // central: rank 0 holds a copy of all m keys (plus its own values / indices); otherwise every
   // CTA holds only its own candidates and rank 0's radix passes read the keys over DSMEM
 #ifndef LAGS_CENTRAL_MAX
@@ -219,9 +256,9 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
   else if (over_any) why = FB_OVERFLOW;
   else if (m < k && st.thr > 1u) why = FB_TOO_FEW;
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // all CTAs of the cluster are running
   if (why || !fits || m == 0) {  // uniform across the cluster; rank 0 finishes the layer alone
-    cluster_sync_exec();  // no CTA leaves while another may still read its counts
-    if (rank == 0) {
+    if (rank == 0) {  // (no shared memory of another CTA was touched: the others just leave)
       if (why) {
         dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
       } else {  // too many candidates for the cluster's shared memory, or none: one-CTA path
@@ -240,13 +277,17 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     return;
   }
   // 2. gather: own (value, index) at [m, m + mr) / [m + mr, m + 2 mr) of dyn and the keys into
-  // rank 0's dyn (central), or own (value, index) at [0, m_max) / [m_max, m_max + mr) (remote)
+  // EVERY CTA's dyn at the own prefix offset (central), or own (value, index) at [0, m_max) /
+  // [m_max, m_max + mr) (distributed)
   const long long c0 = clock64();
+  LAGS_STAMP(4);
   const uint32_t mr = local;
   const uint32_t vbase = central ? m : 0u, ibase = central ? m + mr : m_max;
   float* sv = reinterpret_cast<float*>(dyn + vbase);
   int32_t* si = reinterpret_cast<int32_t*>(dyn + ibase);
-  uint32_t* keys0 = cluster.map_shared_rank(dyn, 0);
+  uint32_t* keysq[CLUSTER];
+#pragma unroll
+  for (int q = 0; q < CLUSTER; ++q) keysq[q] = cluster.map_shared_rank(dyn, q) + pre;
   uint32_t carry = 0;
   const uint32_t key0 = st.thr;  // reference key of the common-prefix OR
   if (threadIdx.x == 0) cs.sm.diff_acc = 0u;
@@ -287,10 +328,14 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       for (int u = 0; u < GATHER_ILP; ++u) {
         if (src[u] >= 0) {
           const uint32_t e = carry + e0 + u * SEL_NT + threadIdx.x;
+          const uint32_t key = Key<float>::of(xv[u]);
           sv[e] = xv[u];
           si[e] = xi[u];
-          if (central) keys0[pre + e] = Key<float>::of(xv[u]);
-          dx |= Key<float>::of(xv[u]) ^ key0;
+          if (central) {
+#pragma unroll
+            for (int q = 0; q < CLUSTER; ++q) keysq[q][e] = key;
+          }
+          dx |= key ^ key0;
         }
       }
     }
@@ -299,35 +344,49 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) csh.diff = cs.sm.diff_acc;
-  cluster.sync();  // all keys are in rank 0
+  if (central) {  // the own OR word into every CTA (read locally after the barrier)
+    if (threadIdx.x < CLUSTER) cluster.map_shared_rank(&csh, static_cast<int>(threadIdx.x))->qdiff[rank] = cs.sm.diff_acc;
+  }
+  LAGS_STAMP(5);
+  cluster.sync();  // central: all keys are in every CTA
+  LAGS_STAMP(6);
   const long long c1 = clock64();
-  // 3. rank 0 selects
   const uint32_t k2 = pred_rank(st, k);
+  SelectThreshold<uint32_t> th;
+  uint32_t key2;
+  uint32_t cg0 = 0, ce0 = 0;
   if (central) {
-    if (rank == 0) {
-      SelectThreshold<uint32_t> th;
-      uint32_t key2;
-      const uint32_t* keys = dyn;
-      auto key_at = [=](int64_t i) { return keys[i]; };
-      uint32_t dk[2] = {0u, key0};
-      for (int q = 0; q < CLUSTER; ++q) dk[0] |= cluster.map_shared_rank(&csh, q)->diff;
-      radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
-      if (threadIdx.x == 0) {
-        csh.prefix = th.prefix;
-        csh.pmask = th.pmask;
-        csh.n_gt = th.n_gt;
-        csh.need_eq = th.need_eq;
-        csh.key2 = key2;
-      }
+    // 3. every CTA selects on its own full copy (same keys, same order: the same threshold), then
+    // counts the lower ranks' entries itself -- nothing crosses CTAs after the gather barrier
+    const uint32_t* keys = dyn;
+    auto key_at = [=](int64_t i) { return keys[i]; };
+    uint32_t dk[2] = {0u, key0};
+#pragma unroll
+    for (int q = 0; q < CLUSTER; ++q) dk[0] |= csh.qdiff[q];
+    radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
+#ifdef LAGS_DBG_TWICE  // the same select again with a warm instruction cache (diagnostic)
+    LAGS_STAMP(16);
+    radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
+    LAGS_STAMP(17);
+#endif
+    LAGS_STAMP(7);
+    LAGS_STAMP(8);
+    uint32_t lge = 0;  // gt | eq << 16 over the lower ranks' keys [0, pre) (m <= CENTRAL_MAX < 65536)
+    for (uint32_t i = threadIdx.x; i < pre; i += SEL_NT) {
+      const uint32_t key = keys[i];
+      const uint32_t hk = key & th.pmask;
+      if (key != 0u) lge += hk > th.prefix ? 1u : (hk == th.prefix ? 0x10000u : 0u);
     }
+    lge = block_sum(lge, cs.sm);
+    cg0 = lge & 0xffffu;
+    ce0 = lge >> 16;
+    LAGS_STAMP(9);
+    LAGS_STAMP(10);
   } else {  // every CTA holds its own keys: the distributed select (all CTAs)
     int q0 = 0;
     while (rpre[q0 + 1] == rpre[q0]) ++q0;  // the first rank with candidates (m > 0)
-    const uint32_t key0 = Key<float>::of(cluster.map_shared_rank(reinterpret_cast<const float*>(dyn), q0)[0]);
-    SelectThreshold<uint32_t> th;
-    uint32_t key2;
-    cluster_radix_select_dual(cluster, rank, sv, mr, m, key0, k, k2, cs, cr, &th, &key2);
+    const uint32_t dkey0 = Key<float>::of(cluster.map_shared_rank(reinterpret_cast<const float*>(dyn), q0)[0]);
+    cluster_radix_select_dual(cluster, rank, sv, mr, m, dkey0, k, k2, cs, cr, &th, &key2);
     if (rank == 0 && threadIdx.x == 0) {
       csh.prefix = th.prefix;
       csh.pmask = th.pmask;
@@ -335,37 +394,39 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       csh.need_eq = th.need_eq;
       csh.key2 = key2;
     }
+    LAGS_STAMP(7);
+    cluster.sync();
+    LAGS_STAMP(8);
+    {
+      const ClusterShared* o = cluster.map_shared_rank(&csh, 0);
+      th.prefix = o->prefix;
+      th.pmask = o->pmask;
+      th.n_gt = o->n_gt;
+      th.need_eq = o->need_eq;
+      key2 = o->key2;
+    }
+    uint32_t lge = 0;  // gt count | eq count << 16 (mr < 65536: it fits the shared memory)
+    for (uint32_t i = threadIdx.x; i < mr; i += SEL_NT) {
+      const uint32_t key = Key<float>::of(sv[i]);
+      const uint32_t hk = key & th.pmask;
+      if (key != 0u) lge += hk > th.prefix ? 1u : (hk == th.prefix ? 0x10000u : 0u);
+    }
+    lge = block_sum(lge, cs.sm);
+    LAGS_STAMP(9);
+    if (threadIdx.x == 0) {
+      csh.gt = lge & 0xffffu;
+      csh.eq = lge >> 16;
+    }
+    cluster.sync();
+    LAGS_STAMP(10);
+    for (int q = 0; q < rank; ++q) {
+      const ClusterShared* o = cluster.map_shared_rank(&csh, q);
+      cg0 += o->gt;
+      ce0 += o->eq;
+    }
   }
-  cluster.sync();
   const long long c2 = clock64();
-  SelectThreshold<uint32_t> th;
-  {
-    const ClusterShared* o = cluster.map_shared_rank(&csh, 0);
-    th.prefix = o->prefix;
-    th.pmask = o->pmask;
-    th.n_gt = o->n_gt;
-    th.need_eq = o->need_eq;
-  }
-  const uint32_t key2 = cluster.map_shared_rank(&csh, 0)->key2;
   // 4. ordered compaction of the own range with the carried counts of the lower ranks
-  uint32_t lge = 0;  // gt count | eq count << 16 (mr < 65536: it fits the shared memory)
-  for (uint32_t i = threadIdx.x; i < mr; i += SEL_NT) {
-    const uint32_t key = Key<float>::of(sv[i]);
-    const uint32_t hk = key & th.pmask;
-    if (key != 0u) lge += hk > th.prefix ? 1u : (hk == th.prefix ? 0x10000u : 0u);
-  }
-  lge = block_sum(lge, cs.sm);
-  if (threadIdx.x == 0) {
-    csh.gt = lge & 0xffffu;
-    csh.eq = lge >> 16;
-  }
-  cluster.sync();
-  uint32_t cg0 = 0, ce0 = 0;
-  for (int q = 0; q < rank; ++q) {
-    const ClusterShared* o = cluster.map_shared_rank(&csh, q);
-    cg0 += o->gt;
-    ce0 += o->eq;
-  }
   float* data = r + L.offset;
   int32_t* oidx = idx_out + L.slot;
   float* oval = val_out + L.slot;
@@ -374,14 +435,26 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     *key = Key<float>::of(*x);
     *ix = si[i];
   };
-  auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
-    oidx[pos] = static_cast<int32_t>(ix);
-    oval[pos] = x;
-    data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
-  };
-  const uint32_t first = cg0 + min(ce0, th.need_eq);
-  const uint32_t end = ordered_compact<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0);
-  if (vupd) apply_single_rank_updates(vupd + L.offset, oidx + first, oval + first, end - first);
+  uint32_t end;
+  if (vupd) {  // fused P = 1 update: the weights are loaded before the compaction's scan
+    float* vl = vupd + L.offset;
+    auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
+      oidx[pos] = static_cast<int32_t>(ix);
+      oval[pos] = x;
+      data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+      vl[ix] = single_rank_update(w, x);
+    };
+    end = ordered_compact_pf<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0, [=](int64_t ix) { return vl[ix]; });
+  } else {
+    auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
+      oidx[pos] = static_cast<int32_t>(ix);
+      oval[pos] = x;
+      data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    };
+    end = ordered_compact<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0);
+  }
+  LAGS_STAMP(11);
+  LAGS_STAMP(12);
   const long long c3 = clock64();
   if (rank == CLUSTER - 1 && threadIdx.x == 0) count_out[j] = static_cast<int32_t>(end);
   if (rank == 0 && threadIdx.x == 0) {
@@ -399,7 +472,10 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     ns.t_launch = t_launch;
     state[j] = ns;
   }
-  cluster_sync_exec();  // no CTA leaves while others may still read its shared memory
+  // distributed: no CTA leaves while others may still read its shared memory (central: nothing is
+  // read remotely after the gather barrier)
+  if (!central) cluster_sync_exec();
+  LAGS_STAMP(13);
 }
 
 // The whole selection of an fp32 compress in ONE launch (thread-block clusters of CLUSTER CTAs):
@@ -421,7 +497,9 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
   __shared__ ClusterRadix cr;
   __shared__ int next_pos;
   const uint32_t t_launch = globaltimer_lo();
+  LAGS_STAMP(14);
   griddep_wait();  // K1 has completed and its writes are visible (programmatic dependent launch)
+  LAGS_STAMP(15);
   const int cl_ctas = n_cl * CLUSTER;
   if (static_cast<int>(blockIdx.x) < cl_ctas) {
     cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap,

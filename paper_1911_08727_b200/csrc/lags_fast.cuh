@@ -442,6 +442,21 @@ __device__ __forceinline__ FastState candidate_state(const FastState& st, uint32
 // ascending index order) when they fit (2*m words <= smem_words), else into global scratch.
 constexpr int FB_TOO_FEW = 1, FB_OVERFLOW = 2;
 
+#ifdef LAGS_DBG_STAMPS
+#ifndef LAGS_DBG_J
+#define LAGS_DBG_J 78
+#endif
+__device__ unsigned long long lags_dbg_cstamps[16];
+#define LAGS_CSTAMP(i)                                           \
+  do {                                                           \
+    if (j == LAGS_DBG_J && threadIdx.x == 0) lags_dbg_cstamps[i] = clock64(); \
+  } while (0)
+#else
+#define LAGS_CSTAMP(i) \
+  do {                 \
+  } while (0)
+#endif
+
 __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
                                 const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
                                 int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
@@ -450,13 +465,16 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
   uint32_t local = 0, over = 0;
+  LAGS_CSTAMP(0);
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
     local += min(c, static_cast<uint32_t>(cap));
   }
+  LAGS_CSTAMP(1);
   const uint32_t m = block_sum(local, sm);
   if (__syncthreads_or(over)) return FB_OVERFLOW;
+  LAGS_CSTAMP(2);
   if (m < k && st.thr > 1u) return FB_TOO_FEW;
   float* data = r + L.offset;
   uint32_t cnt = 0;
@@ -529,6 +547,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     SelectThreshold<uint32_t> th;
     uint32_t key2;
     const long long c1 = clock64();
+    LAGS_CSTAMP(3);
     const uint32_t dk[2] = {sm.diff_acc, key0};
     radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
     const long long c2 = clock64();
@@ -540,13 +559,26 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     int32_t* oidx = idx_out + L.slot;
     float* oval = val_out + L.slot;
     float* vl = vupd ? vupd + L.offset : nullptr;
-    auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
-      oidx[pos] = static_cast<int32_t>(ix);
-      oval[pos] = x;
-      data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
-    };
-    cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
-    if (vl) apply_single_rank_updates(vl, oidx, oval, cnt);
+    LAGS_CSTAMP(4);
+    if (vl) {  // fused P = 1 update: the weights are loaded before the compaction's scan
+      auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
+        oidx[pos] = static_cast<int32_t>(ix);
+        oval[pos] = x;
+        data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+        vl[ix] = single_rank_update(w, x);
+      };
+      cnt = ordered_compact_pf<uint32_t, float>(m, th, load, emit, sm, 0u, 0u,
+                                                [=](int64_t ix) { return vl[ix]; });
+    } else {
+      auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
+        oidx[pos] = static_cast<int32_t>(ix);
+        oval[pos] = x;
+        data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+      };
+      cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
+    }
+    LAGS_CSTAMP(5);
+    LAGS_CSTAMP(6);
     const long long c3 = clock64();
     auto q = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
     phases = q(c1 - c0) | (q(c2 - c1) << 11) | (q(c3 - c2) << 22);
@@ -560,6 +592,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     count_out[j] = static_cast<int32_t>(cnt);
   }
   __syncthreads();
+  LAGS_CSTAMP(7);
   return 0;
 }
 
@@ -818,6 +851,7 @@ __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, con
                              int32_t* count_out, uint32_t* skeys, int smem_keys, int force_exact, SelectSmem& cs,
                              float* vupd, uint32_t t_launch) {
   const uint32_t t_start = globaltimer_lo();
+  LAGS_CSTAMP(8);
   const lags_layer_t L = layers[j];
   const FastState st = state[j];
   const long long t_begin = clock64();

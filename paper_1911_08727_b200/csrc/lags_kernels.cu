@@ -906,3 +906,13 @@ int lags_decompress(int32_t dtype, const int32_t* idx, const void* val, const in
 }
 
 }  // extern "C"
+
+#ifdef LAGS_DBG_STAMPS
+// Diagnostic builds only: the phase stamps of the first cluster layer ([rank][clock|globaltimer][16]).
+extern "C" int lags_dbg_stamps_read(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_stamps, sizeof(lags::lags_dbg_stamps)));
+}
+extern "C" int lags_dbg_cstamps_read(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_cstamps, sizeof(lags::lags_dbg_cstamps)));
+}
+#endif

@@ -249,6 +249,60 @@ __device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, 
 // load(i, &key, &val, &index) fetches entry i; emit(pos, i, index, val) writes selected entry i
 // to output position pos.  Returns the selected count (all threads).
 // carry_gt0 / carry_eq0: counts of gt / eq entries before entry 0 (multi-CTA compaction).
+// Without a prefetch functor the emit is emit(pos, i, index, val).  ordered_compact_pf takes
+// pf(index) -> W, called for every entry at or above the threshold BEFORE the block scan (so its
+// loads are in flight across the scan's barriers), and calls emit(pos, i, index, val, w).
+struct NoPrefetch {
+  __device__ __forceinline__ float operator()(int64_t) const { return 0.0f; }
+};
+
+template <typename K, typename T, typename Load, typename Emit, int RB, typename Pf = NoPrefetch>
+__device__ uint32_t ordered_compact_pf(int64_t m, const SelectThreshold<K>& th, Load load, Emit emit,
+                                       RadixSmem<RB>& sm, uint32_t carry_gt0, uint32_t carry_eq0, Pf pf) {
+  uint32_t carry_gt = carry_gt0, carry_eq = carry_eq0;
+  const int64_t chunk = static_cast<int64_t>(SEL_NT) * SEL_VEC;
+  for (int64_t base = 0; base < m; base += chunk) {
+    const int64_t i0 = base + static_cast<int64_t>(threadIdx.x) * SEL_VEC;
+    T x[SEL_VEC];
+    int64_t ix[SEL_VEC];
+    uint32_t gtm = 0, eqm = 0;
+#pragma unroll
+    for (int v = 0; v < SEL_VEC; ++v) {
+      const int64_t i = i0 + v;
+      K key = 0;
+      x[v] = T(0);
+      ix[v] = 0;
+      if (i < m) load(i, &key, &x[v], &ix[v]);
+      const K hi = key & th.pmask;
+      if (key != 0) {
+        if (hi > th.prefix) gtm |= 1u << v;
+        else if (hi == th.prefix) eqm |= 1u << v;
+      }
+    }
+    decltype(pf(0)) w[SEL_VEC];
+#pragma unroll
+    for (int v = 0; v < SEL_VEC; ++v) w[v] = ((gtm | eqm) >> v) & 1u ? pf(ix[v]) : decltype(pf(0))(0);
+    const uint32_t packed = (static_cast<uint32_t>(__popc(eqm)) << 16) | static_cast<uint32_t>(__popc(gtm));
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<SEL_NT>(packed, sm.warp_tot, &tot);
+    uint32_t gt_before = carry_gt + (ex & 0xffffu);
+    uint32_t eq_before = carry_eq + (ex >> 16);
+    if (gtm | eqm) {
+#pragma unroll
+      for (int v = 0; v < SEL_VEC; ++v) {
+        const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
+        if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), i0 + v, ix[v], x[v], w[v]);
+        gt_before += g;
+        eq_before += e;
+      }
+    }
+    carry_gt += tot & 0xffffu;
+    carry_eq += tot >> 16;
+    __syncthreads();  // warp_tot reuse by the next scan
+  }
+  return carry_gt + min(carry_eq, th.need_eq);
+}
+
 template <typename K, typename T, typename Load, typename Emit, int RB>
 __device__ uint32_t ordered_compact(int64_t m, const SelectThreshold<K>& th, Load load, Emit emit,
                                     RadixSmem<RB>& sm, uint32_t carry_gt0 = 0, uint32_t carry_eq0 = 0) {
