@@ -278,7 +278,10 @@ __device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32
 // first-pass bin holds a few keys) instead of being refined in the later passes.
 // Once the threshold's bin holds at most BIN_LIST_MAX keys, the remaining passes are replaced by
 // one pass that lists the bin's keys and a direct rank count among them.
-constexpr uint32_t BIN_LIST_MAX = 128;
+#ifndef LAGS_BIN_LIST_MAX
+#define LAGS_BIN_LIST_MAX 128
+#endif
+constexpr uint32_t BIN_LIST_MAX = LAGS_BIN_LIST_MAX;
 
 template <typename KeyAt>
 __device__ void radix_select_dual(KeyAt key_at, int64_t m, uint32_t k, uint32_t k2, SelectSmem& cs,

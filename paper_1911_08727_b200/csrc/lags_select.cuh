@@ -21,7 +21,7 @@ constexpr int SEL_MINB = LAGS_SEL_MINB;  // selection CTAs resident per SM (laun
 #define LAGS_SEL_VEC 4
 #endif
 #ifndef LAGS_GATHER_ILP
-#define LAGS_GATHER_ILP 4
+#define LAGS_GATHER_ILP 2
 #endif
 #ifndef LAGS_UPDATE_B
 #define LAGS_UPDATE_B 4
