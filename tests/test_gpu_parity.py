@@ -239,6 +239,36 @@ def test_fast_path_equals_exact_path(L):
     assert int(st.item()) == 0
 
 
+def test_fast_path_ties_equal_exact_path(L):
+    """Tie-heavy data through the fast paths (cluster layers, candidate layers, small fallbacks):
+    integer gradients with alpha = 1 keep every accumulated value an integer, so the threshold's
+    radix bin (and the bin-list finish) holds many equal keys, and zeros are frequent.  The
+    selection must still take the lower indices first among equal keys, exactly as the dense path."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [600_000, 300_000, 9_000, 2_100_000, 40_000, 1_000]
+    ks = [max(1, d // 1000) for d in dims]
+    fast = L.Bucket(dims, ks, N.F32)
+    exact = L.Bucket(dims, ks, N.F32)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    r_f = torch.zeros(n, device="cuda")
+    r_e = torch.zeros(n, device="cuda")
+    m_f, m_e = fast.new_messages(1), exact.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for it in range(20):
+        g = torch.randint(-6, 7, (n,), device="cuda", generator=gen).float()
+        if it % 5 == 4:
+            g[::3] = 0.0
+        fast.compress(g, r_f, 1.0, m_f, st)
+        exact.compress(g, r_e, 1.0, m_e, st, exact=True)
+        assert torch.equal(m_f, m_e), f"messages differ at iteration {it}"
+        assert torch.equal(r_f.view(torch.int32), r_e.view(torch.int32)), f"residuals differ at {it}"
+    s = fast.stats()
+    assert int((s[:, 5] == 3).sum()) >= 1, s  # a cluster layer took the cluster path
+    assert int(st.item()) == 0
+
+
 def test_fast_path_decode_multi_rank_equals_oracle(L):
     """P simulated ranks through one bucket: fast compress per rank, rank-ordered decode."""
     from paper_1911_08727_b200 import _native as N
