@@ -290,6 +290,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   for (int q = 0; q < CLUSTER; ++q) keysq[q] = cluster.map_shared_rank(dyn, q) + pre;
   uint32_t carry = 0;
   const uint32_t key0 = st.thr;  // reference key of the common-prefix OR
+  const float* vpf = vupd ? vupd + L.offset : nullptr;  // P = 1: prefetch the candidates' weights
   if (threadIdx.x == 0) cs.sm.diff_acc = 0u;
   for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
     const int nt = min(SEL_NT, t_hi - t0);
@@ -331,6 +332,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
           const uint32_t key = Key<float>::of(xv[u]);
           sv[e] = xv[u];
           si[e] = xi[u];
+          if (vpf) asm volatile("prefetch.global.L2 [%0];" ::"l"(vpf + xi[u]));  // fused update's weight
           if (central) {
 #pragma unroll
             for (int q = 0; q < CLUSTER; ++q) keysq[q][e] = key;

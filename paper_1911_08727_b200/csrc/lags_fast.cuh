@@ -537,6 +537,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
             const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
             sv[carry + e] = xv[u];
             si[carry + e] = xi[u];
+            if (vupd) asm volatile("prefetch.global.L2 [%0];" ::"l"(vupd + L.offset + xi[u]));  // P = 1 weight
             dx |= Key<float>::of(xv[u]) ^ key0;
           }
         }
