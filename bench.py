@@ -4,8 +4,9 @@ One *step* = one pass of the hot path over one batch of synthetic per-rank gradi
 ResNet-50 layer shapes (BASELINE.json configs[3]; 161 tensors, 25,557,032 fp32 elements,
 rho = 0.001 -> c = 1000, k_l = min(d, max(1, d // 1000)) as R: sparsify.py:182-184):
 
-    compress (K1 accumulate + K2 select/compact, per layer)  ->  NCCL all-gather of the fixed-size
-    sparse messages (N > 1)  ->  rank-ordered decode + SGD update of the parameters
+    compress (K1 accumulate + K2 select/compact, per layer)  ->  exchange of the fixed-size sparse
+    messages (N > 1: peer-memory push over CUDA IPC / NVLink, or --exchange nccl for the NCCL
+    all-gather)  ->  rank-ordered decode + SGD update of the parameters
 
 `value` = algorithmic bytes of all ranks / device time (GB/s), inputs resident in HBM.
 `e2e`   = the same metric through the reference-facing drop-in `lags_step` with HOST numpy
@@ -268,6 +269,20 @@ def run_ours(args, dims, ks, world, rank, local):
     msg_local = bucket.new_messages(1)
     msgs = bucket.new_messages(world) if world > 1 else msg_local
     status = torch.zeros(1, dtype=torch.int32, device=dev)
+    peer = None
+    if world > 1 and args.exchange == "p2p":  # peer-memory exchange (CUDA IPC over NVLink / NVSwitch)
+        from paper_1911_08727_b200.p2p import PeerExchange
+
+        try:
+            peer = PeerExchange(bucket.msg_bytes, ctas_per_peer=args.p2p_ctas)
+        except Exception as exc:  # IPC unavailable on this box: the NCCL all-gather instead (reported)
+            print(f"peer-memory exchange unavailable ({exc}); using the NCCL all-gather", file=sys.stderr)
+            peer = None
+        ok = torch.tensor([1 if peer is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank must use the same exchange
+        if int(ok.item()) == 0 and peer is not None:
+            peer.close()
+            peer = None
     alpha = 0.1
     stream = torch.cuda.current_stream(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -283,8 +298,11 @@ def run_ours(args, dims, ks, world, rank, local):
         bucket.compress(g_bufs[t % NG], r, alpha, msg_local, status, stream=stream)
         if timed:
             ev[t][1].record(stream)
-        dist.all_gather_into_tensor(msgs, msg_local)
-        bucket.decode(msgs, world, v, stream=stream)
+        if peer is not None:
+            bucket.decode(peer.exchange(msg_local, stream=stream), world, v, stream=stream)
+        else:
+            dist.all_gather_into_tensor(msgs, msg_local)
+            bucket.decode(msgs, world, v, stream=stream)
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -306,28 +324,44 @@ def run_ours(args, dims, ks, world, rank, local):
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
-    # N = 1: the step is captured once per gradient buffer into CUDA graphs and replayed (the
-    # selection state lives on the device, so replays are real steps); no host launch overhead.
+    # The step is captured into CUDA graphs and replayed (the selection state lives on the device,
+    # so replays are real steps; no host launch overhead): N = 1 one graph per gradient buffer;
+    # N > 1 with the peer-memory exchange (all launches are this library's, the exchange epoch is
+    # device-resident) one per (gradient buffer, receive parity), replayed in capture order.
     graphs = None
     l_graph = 0
-    if world == 1 and not args.no_graph:
+    n_replay = 0
+    if not args.no_graph and (world == 1 or (peer is not None and args.graph_mgpu)):
         try:
             cap = torch.cuda.Stream(dev)
             cap.wait_stream(stream)
             graphs = []
             lc0 = N.lags_kernel_launches()
-            for i in range(NG):
+            c0 = peer.calls if peer is not None else 0
+            NGR = NG if world == 1 else 2 * NG
+            for i in range(NGR):
                 gr = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gr, stream=cap):
-                    bucket.step_local(g_bufs[i], r, alpha, v, msg_local, status, stream=cap)
+                    if world == 1:
+                        bucket.step_local(g_bufs[i], r, alpha, v, msg_local, status, stream=cap)
+                    else:
+                        bucket.compress(g_bufs[i % NG], r, alpha, msg_local, status, stream=cap)
+                        bucket.decode(peer.exchange(msg_local, stream=cap), world, v, stream=cap)
                 graphs.append(gr)
-            l_graph = (N.lags_kernel_launches() - lc0) // NG  # our kernels per captured step
-            for i in range(2 * NG):  # graph warm-up replays (steps like any other)
-                graphs[i % NG].replay()
+            if peer is not None:
+                peer.calls = c0  # captured, not executed: replays advance it
+            l_graph = (N.lags_kernel_launches() - lc0) // NGR  # our kernels per captured step
+            for i in range(2 * NGR):  # graph warm-up replays (steps like any other)
+                graphs[n_replay % NGR].replay()
+                n_replay += 1
             torch.cuda.synchronize(dev)
         except Exception as exc:  # pragma: no cover - report and time eagerly
             print(f"cuda graph capture failed ({exc}); timing eager launches", file=sys.stderr)
             graphs = None
+            if peer is not None:  # a failed capture must not leave the exchange state behind
+                raise
+    if world > 1:
+        dist.barrier()
     stats0 = bucket.stats()
     l0 = N.lags_kernel_launches()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -338,7 +372,8 @@ def run_ours(args, dims, ks, world, rank, local):
     start.record(stream)
     for t in range(args.steps):
         if graphs is not None:
-            graphs[t % NG].replay()
+            graphs[n_replay % len(graphs)].replay()
+            n_replay += 1
         else:
             step(t)
     stop.record(stream)
@@ -350,7 +385,9 @@ def run_ours(args, dims, ks, world, rank, local):
     clk = clocks.stop(wall0, wall1)
     stats = bucket.stats()
     ms = start.elapsed_time(stop)
-    if graphs is not None:
+    if peer is not None:
+        peer.advance(n_replay)  # the replayed exchanges (receive parity bookkeeping)
+    if graphs is not None and world == 1:
         comp_ms = ms / args.steps  # at N = 1 the whole step is the compress (update fused)
     else:  # the compress alone, from events around it in extra untimed steps (events in the timed
         # steps would break the programmatic-dependent-launch chain between steps)
@@ -364,6 +401,8 @@ def run_ours(args, dims, ks, world, rank, local):
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms, comp_ms = float(t_ms[0]), float(t_ms[1])
     assert int(status.item()) == 0
+    if peer is not None:
+        assert int(peer.status.item()) == 0, "peer exchange timed out"
     # dominant kernel (K1, the streaming pass) timed live: the library records these events
     # around K1 inside every compress call (eager steps after the timed region, all ranks)
     probes = []
@@ -386,6 +425,7 @@ def run_ours(args, dims, ks, world, rank, local):
     sel_local = int(counts.sum())
     union = sel_local if world == 1 else None
     if world > 1:
+        dist.all_gather_into_tensor(msgs, msg_local)  # every rank's last message (statistics only)
         allmsg = msgs
         idx_all = []
         for p in range(world):
@@ -415,9 +455,28 @@ def run_ours(args, dims, ks, world, rank, local):
         dist.all_reduce(ex_us, op=dist.ReduceOp.MAX)
         ex_us = float(ex_us)
         alg = world * bucket.msg_bytes / (ex_us * 1e-6) / 1e9
-        exchange = {"what": "NCCL all-gather of the fixed-size sparse messages (one bucket)",
-                    "bytes_per_rank": int(bucket.msg_bytes), "us": round(ex_us, 2), "alg_GBs": round(alg, 2),
-                    "bus_GBs": round(alg * (world - 1) / world, 2), "nvlink_GBs_per_direction": 900}
+        exchange = {"in_step": "peer-memory push + flag wait (lags_p2p_push / lags_p2p_wait, CUDA IPC)"
+                               if peer is not None else "NCCL all_gather_into_tensor",
+                    "nccl_all_gather": {"bytes_per_rank": int(bucket.msg_bytes), "us": round(ex_us, 2),
+                                        "alg_GBs": round(alg, 2), "bus_GBs": round(alg * (world - 1) / world, 2)},
+                    "nvlink_GBs_per_direction": 900}
+        if peer is not None:  # the peer-memory exchange alone, same convention
+            for _ in range(10):
+                peer.exchange(msg_local, stream=stream)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            ex0.record(stream)
+            for _ in range(50):
+                peer.exchange(msg_local, stream=stream)
+            ex1.record(stream)
+            torch.cuda.synchronize(dev)
+            p_us = torch.tensor([ex0.elapsed_time(ex1) / 50 * 1e3], dtype=torch.float64, device=dev)
+            dist.all_reduce(p_us, op=dist.ReduceOp.MAX)
+            p_us = float(p_us)
+            palg = world * bucket.msg_bytes / (p_us * 1e-6) / 1e9
+            exchange["peer_memory"] = {"bytes_per_rank": int(bucket.msg_bytes), "us": round(p_us, 2),
+                                       "alg_GBs": round(palg, 2), "bus_GBs": round(palg * (world - 1) / world, 2)}
+            assert int(peer.status.item()) == 0, "peer exchange timed out"
     peak, peak_src = read_peaks()
     comp_bytes_rank = 12 * n + 8 * sel_local
     achieved = comp_bytes_rank / (comp_ms / 1e3) / 1e9
@@ -456,7 +515,8 @@ def run_ours(args, dims, ks, world, rank, local):
                                       "algorithmic_bytes_per_call": int(comp_bytes_rank),
                                       "ms_per_call": round(comp_ms, 4)}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
-            "launch_mode": "cuda graph replay (one captured step per gradient buffer)" if graphs is not None
+            "launch_mode": ("cuda graph replay (one captured step per gradient buffer"
+                            + (")" if world == 1 else " and receive parity; peer-memory exchange)")) if graphs is not None
             else "eager (ctypes -> cudaLaunchKernelEx with programmatic dependent launch)",
             "resnet50_train": train,
             "exchange": exchange,
@@ -466,6 +526,8 @@ def run_ours(args, dims, ks, world, rank, local):
                           "candidates_per_step": int(stats[:, 2].sum())},
         }
         print(json.dumps(out), flush=True)
+    if peer is not None:
+        peer.close()  # collective
 
 
 TRAIN_WINDOWS = 5
@@ -624,6 +686,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the ResNet-50 training-iteration measurement")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graph replay")
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="N > 1: peer-memory exchange (own kernels over CUDA IPC) or NCCL all-gather")
+    ap.add_argument("--p2p-ctas", type=int, default=4, help="peer-memory exchange: CTAs per destination rank")
+    ap.add_argument("--graph-mgpu", action="store_true",
+                    help="N > 1 with the peer-memory exchange: replay CUDA graphs (measured slower than eager)")
     ap.add_argument("--train-steps", type=int, default=20)
     ap.add_argument("--train-warmup", type=int, default=8)
     ap.add_argument("--bucket-cap", type=int, default=1 << 16, help="fusion capacity (bytes) for LagsSGD")

@@ -47,6 +47,7 @@ typedef enum {
 typedef enum { LAGS_F32 = 0, LAGS_F64 = 1, LAGS_F32_ACC64 = 2 } lags_dtype_t;
 
 /* Status bits OR-ed into the caller's device status word. */
+#define LAGS_STATUS_P2P_TIMEOUT 0x100u /* lags_p2p_wait: a peer's message did not arrive in time */
 #define LAGS_STATUS_NONFINITE 0x1u /* a gradient entry was inf/nan -> DivergenceError (R: training.py:174-175) */
 
 /* lags_bucket_compress flags */
@@ -188,6 +189,28 @@ int lags_wire_decode(uint32_t mode, const void* wire, int64_t wire_len, int64_t 
                      const int64_t* first, const int32_t* caps, int64_t entry_capacity, uint32_t* layer_ids,
                      uint32_t* dims, int32_t* counts, int32_t* idx, void* val, int32_t val_dtype,
                      int32_t* nchunks_out, int64_t* end_out, uint64_t* error, lags_stream_t stream);
+
+/* ---- peer-memory exchange (one process per GPU, CUDA IPC over NVLink / NVSwitch) -------------
+ * Replaces the all-gather of the fixed-size bucket messages (R: training.py:245-248 gathers every
+ * worker's sparse chunks) with direct stores into every peer's receive area:
+ *   area = [flags: P * G u32, padded to flags_bytes (multiple of 256)] [parity 0: P messages] [parity 1: P messages]
+ * lags_ipc_malloc allocates a zeroed area and its 64-byte IPC handle; peers map it with
+ * lags_ipc_open.  lags_p2p_push (G = ctas_per_peer CTAs per destination; bases = device array of
+ * the P areas, own included) writes the message into slot `rank` of parity (epoch & 1) of every
+ * area and publishes the epoch in flag [rank * G + g] (system-scope release).  lags_p2p_wait
+ * acquires the local P * G flags (>= epoch, wrap-safe); on timeout it ORs LAGS_STATUS_P2P_TIMEOUT
+ * into *status.  The decode that follows on the stream then reads the parity's P messages in rank order.
+ * The epoch lives in device memory (*epoch, u32, starts at 0): the push uses *epoch + 1, the wait
+ * waits for it and then stores it, so a step's launches have fixed arguments (graph-capturable);
+ * the receiving parity is then (exchange count) & 1. */
+int lags_ipc_malloc(size_t bytes, void** ptr, void* handle64);
+int lags_ipc_open(const void* handle64, void** ptr);
+int lags_ipc_close(void* ptr);
+int lags_ipc_free(void* ptr);
+int lags_p2p_push(const void* msg, int64_t msg_bytes, const uint64_t* bases, int P, int rank, int ctas_per_peer,
+                  uint64_t flags_bytes, const uint32_t* epoch, lags_stream_t stream);
+int lags_p2p_wait(const uint32_t* flags, int nflags, uint32_t* epoch, int32_t* status, uint64_t timeout_ns,
+                  lags_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,13 @@ lags_wire_encode = _fn("lags_wire_encode", C.c_int, _u32, _i32, _vp, _vp, _vp, _
                        _vp, _vp)
 lags_wire_decode = _fn("lags_wire_decode", C.c_int, _u32, _vp, _i64, _i64, _i32, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
                        _vp, _i32, _vp, _vp, _vp, _vp)
+lags_ipc_malloc = _fn("lags_ipc_malloc", C.c_int, _sz, C.POINTER(_vp), _vp)
+lags_ipc_open = _fn("lags_ipc_open", C.c_int, _vp, C.POINTER(_vp))
+lags_ipc_close = _fn("lags_ipc_close", C.c_int, _vp)
+lags_ipc_free = _fn("lags_ipc_free", C.c_int, _vp)
+lags_p2p_push = _fn("lags_p2p_push", C.c_int, _vp, _i64, _vp, _i32, _i32, _i32, C.c_uint64, _vp, _vp)
+lags_p2p_wait = _fn("lags_p2p_wait", C.c_int, _vp, _i32, _vp, _vp, C.c_uint64, _vp)
+STATUS_P2P_TIMEOUT = 0x100
 WIRE_MESSAGE, WIRE_CHUNK = 0, 1
 WIRE_MAX_CHUNKS = 4096
 (WIRE_ERR_TRUNCATED_MESSAGE, WIRE_ERR_TRUNCATED_HEADER, WIRE_ERR_TRUNCATED_PAYLOAD, WIRE_ERR_INDEX_RANGE,
@@ -80,6 +87,7 @@ EXPORTS = [
     "lags_check_finite", "lags_bucket_reconstruct", "lags_bucket_delta",
     "lags_top_k_workspace_bytes",
     "lags_top_k", "lags_decompress", "lags_wire_encode", "lags_wire_decode",
+    "lags_ipc_malloc", "lags_ipc_open", "lags_ipc_close", "lags_ipc_free", "lags_p2p_push", "lags_p2p_wait",
 ]
 
 

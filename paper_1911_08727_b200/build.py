@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblagsb200.so")
-SOURCES = ["lags_kernels.cu", "lags_wire.cu"]
+SOURCES = ["lags_kernels.cu", "lags_wire.cu", "lags_p2p.cu"]
 HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh", "lags_cluster.cuh", "lags_internal.h"]
 
 NVCC_FLAGS = [
