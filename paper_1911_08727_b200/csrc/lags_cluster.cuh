@@ -1,17 +1,18 @@
 // Selection of the largest layers by a thread-block cluster (CLUSTER CTAs, distributed shared
 // memory).  One CTA per layer made the handful of ~2 M-element ResNet-50 layers the critical path
-// of the selection (gather + compaction of ~2k candidates in one CTA); here the CTAs of a cluster
-// each own a contiguous quarter of the layer's K1 task lists (= a contiguous index range):
-//   1. candidate counts are exchanged over DSMEM (cluster.sync) -> the exactness proof, prefixes;
-//   2. every CTA gathers its candidates (value, index) into its own shared memory and, when rank 0
-//      has room for all m keys ("central"), pushes the keys into rank 0's shared memory at its
-//      prefix offset (remote DSMEM stores);
-//   3. rank 0 runs the dual-rank radix select (k-th key + next prediction) on all keys: its own
-//      copy, or -- for candidate sets too large for one CTA (k in the tens of thousands) -- the
-//      keys read in place from every CTA's shared memory over DSMEM;
-//   4. the threshold is read back over DSMEM, per-CTA (gt, eq) counts are exchanged, and every CTA
-//      compacts its own range in order with the carried counts (global output positions), zeroes
-//      the selected residuals and applies the optional fused P = 1 update.
+// of the selection; here the CTAs of a cluster each own a contiguous quarter of the layer's K1
+// task lists (= a contiguous index range):
+//   1. every CTA reads ALL of the layer's task counts and derives the candidate total m, every
+//      rank's share and its own offset (no exchange);
+//   2. every CTA gathers its candidates (value, index) into its own shared memory and -- central
+//      mode, m <= LAGS_CENTRAL_MAX -- stores their keys into EVERY CTA's shared memory at its
+//      offset (remote DSMEM stores), plus its common-prefix OR word; one cluster barrier;
+//   3. central: every CTA runs the same dual-rank radix select on its own full key copy (same
+//      keys, same order: the same threshold and prediction) and counts the lower ranks' gt / eq
+//      entries itself -- nothing crosses CTAs after the barrier.  Distributed mode (larger sets):
+//      per-pass histograms summed by rank 0 over DSMEM, threshold and counts exchanged;
+//   4. every CTA compacts its own range in order with the carried counts (global output
+//      positions), zeroes the selected residuals and applies the optional fused P = 1 update.
 // Results are identical to the single-CTA candidate path (same keys, same order, same rule).
 #pragma once
 #include <cooperative_groups.h>
@@ -57,10 +58,8 @@ __device__ unsigned long long lags_dbg_stamps[CLUSTER][2][24];
 #endif
 
 struct ClusterShared {
-  uint32_t m, over;          // this CTA's candidate count / overflow
-  uint32_t gt, eq;           // this CTA's compaction counts
-  uint32_t prefix, pmask, n_gt, need_eq, key2;  // rank 0: the threshold
-  uint32_t diff;             // OR of key ^ key0 over this CTA's candidates
+  uint32_t gt, eq;           // distributed mode: this CTA's compaction counts
+  uint32_t prefix, pmask, n_gt, need_eq, key2;  // distributed mode, rank 0: the threshold
   uint32_t qsum[CLUSTER];    // the ranks' candidate counts (every CTA computes all of them)
   uint32_t qdiff[CLUSTER];   // central: every rank's OR word (pushed by each rank before the barrier)
 };
