@@ -1,5 +1,6 @@
-"""Kernel timeline of the N > 1 bench step on rank 0 (CUPTI via torch.profiler): compress, NCCL
-all-gather, decode, and the gaps between them.  Run under torchrun.  Diagnostic only."""
+"""Kernel timeline of the N > 1 bench step on rank 0 (CUPTI via torch.profiler): compress, the
+exchange (NCCL all-gather, or `p2p` as argument: the peer-memory push + wait), decode, and the
+gaps between them.  Run under torchrun.  Diagnostic only."""
 
 import json
 import os
@@ -32,10 +33,19 @@ def main():
     msgs = b.new_messages(world)
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
 
+    peer = None
+    if len(sys.argv) > 1 and sys.argv[1] == "p2p":
+        from paper_1911_08727_b200.p2p import PeerExchange
+
+        peer = PeerExchange(b.msg_bytes)
+
     def step(t):
         b.compress(gs[t % 3], r, 0.1, msg, st)
-        dist.all_gather_into_tensor(msgs, msg)
-        b.decode(msgs, world, v)
+        if peer is not None:
+            b.decode(peer.exchange(msg), world, v)
+        else:
+            dist.all_gather_into_tensor(msgs, msg)
+            b.decode(msgs, world, v)
 
     for t in range(300):
         step(t)
@@ -50,7 +60,7 @@ def main():
         prof.export_chrome_trace(path)
         ev = [e for e in json.load(open(path))["traceEvents"] if e.get("cat") == "kernel"]
         ev.sort(key=lambda e: e["ts"])
-        ev = ev[-12:]
+        ev = ev[-15:]
         t0 = ev[0]["ts"]
         prev = None
         for e in ev:
@@ -58,6 +68,8 @@ def main():
             print(f"  +{e['ts'] - t0:8.1f} us  dur {e['dur']:6.1f}  gap {gap:5.1f}  {e['name'][:70]}")
             prev = e["ts"] + e["dur"]
     dist.barrier()
+    if peer is not None:
+        peer.close()
     dist.destroy_process_group()
 
 
