@@ -40,7 +40,13 @@ __global__ void __launch_bounds__(P2P_NT) p2p_push_kernel(const uint4* __restric
   for (int64_t i = lo + threadIdx.x; i < hi; i += P2P_NT) dst[i] = __ldg(src + i);
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's stores (barrier-ordered before this thread) first
+    // st.release.sys = fence.acq_rel.sys + relaxed store: cumulative over what this thread has
+    // observed, which after the barrier includes every store of the CTA (a separate
+    // __threadfence_system() here measured 2 us slower per exchange and orders nothing more;
+    // -DLAGS_P2P_SC_FENCE restores it)
+#ifdef LAGS_P2P_SC_FENCE
+    __threadfence_system();
+#endif
     uint32_t* flag = reinterpret_cast<uint32_t*>(base) + rank * G + gq;
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
   }

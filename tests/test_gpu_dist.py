@@ -115,7 +115,7 @@ def _p2p_worker(rank, port, out_dir):
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     ex = PeerExchange(b.msg_bytes, ctas_per_peer=2, timeout_s=10.0)
     ok = True
-    for t in range(12):
+    for t in range(40):
         g = torch.randn(n, device="cuda", generator=gen)
         b.compress(g, r, 0.1, msg, st)
         b.decode(ex.exchange(msg), WORLD, v_p2p)  # peer-memory exchange
@@ -132,7 +132,7 @@ def _p2p_worker(rank, port, out_dir):
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < WORLD, reason="needs 2 GPUs")
 def test_two_rank_peer_memory_exchange_equals_nccl(tmp_path):
     """The peer-memory exchange (CUDA IPC push + flag wait, double-buffered) delivers exactly the
-    NCCL all-gather's messages: decoded weights bit-identical on every rank, 12 chained steps."""
+    NCCL all-gather's messages: decoded weights bit-identical on every rank, 40 chained steps."""
     import torch.multiprocessing as mp
 
     mp.spawn(_p2p_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, join=True)
