@@ -38,6 +38,19 @@ def _case(it):
     return dims, counts, v, grads, res, alpha
 
 
+SLGS_K = 50
+
+
+def _slgs_case():
+    rng = np.random.default_rng(900)
+    dims = [30_000, 5_000, 17]
+    n = sum(dims)
+    v = rng.standard_normal(n).astype(np.float32)
+    grads = [rng.standard_normal(n).astype(np.float32) for _ in range(WORLD)]
+    res = [(0.01 * rng.standard_normal(n)).astype(np.float32) for _ in range(WORLD)]
+    return dims, v, grads, res, 0.3
+
+
 def _worker(rank, port, out_dir):
     import torch.distributed as dist
 
@@ -57,6 +70,12 @@ def _worker(rank, port, out_dir):
                              [r], t=t, group=grp)
         save[f"v{it}"] = vv.data
         save[f"r{it}"] = r.data
+    # SLGS arm in group mode (whole-vector selection, fp64 parameters out)
+    dims, v, grads, res, alpha = _slgs_case()
+    r = lv(dims, res[rank].copy())
+    out = L.slgs_step(lv(dims, v), [lv(dims, grads[rank])], alpha, SLGS_K, [r], t=0, group=grp)
+    save["slgs_v"] = out.data
+    save["slgs_r"] = r.data
     # divergence: rank 1's gradient is non-finite -> both ranks raise naming worker 2, residuals untouched
     dims = [1000]
     g = np.ones(1000, np.float32)
@@ -87,6 +106,11 @@ def test_two_rank_nccl_lags_step_matches_oracle(tmp_path):
         for p in range(WORLD):
             assert outs[p][f"v{it}"].tobytes() == v.tobytes(), (it, p)
             assert outs[p][f"r{it}"].tobytes() == res[p].tobytes(), (it, p)
+    dims, v, grads, res, alpha = _slgs_case()
+    want = orc.slgs_step(v, grads, alpha, SLGS_K, res)
+    for p in range(WORLD):
+        assert outs[p]["slgs_v"].dtype == want.dtype and outs[p]["slgs_v"].tobytes() == want.tobytes(), p
+        assert outs[p]["slgs_r"].tobytes() == res[p].tobytes(), p
     for p in range(WORLD):
         msg = str(outs[p]["div"])
         assert msg.startswith("9:") and "worker 2" in msg, msg
