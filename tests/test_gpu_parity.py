@@ -433,3 +433,55 @@ def test_large_k_cluster_modes_equal_exact_path(L):
     s = fast.stats()
     assert sum(1 for j in range(3) if s[j, 5] == 3) >= 2, s  # the big layers ran on clusters
     assert int(st.item()) == 0
+
+
+@pytest.mark.parametrize("config", ["resnet20", "vgg16", "resnet50", "resnet50-rho0.01", "lstm"])
+def test_survey_config_full_size_vs_oracle(L, config):
+    """Every SURVEY config's full layer shapes (BASELINE.json configs 2-5) through the bench's
+    path (fast candidate / cluster / warp selection): 10 chained compress calls bit-identical to
+    the dense exact path, and calls 0 and 9 checked per layer against the oracle's top_k
+    (R: sparsify.py:71-90) and residual rule (R: training.py:250-252) on the same fp32 inputs."""
+    from paper_1911_08727_b200 import _native as N
+    from paper_1911_08727_b200.workloads import LSTMPTB, resnet20, resnet50, vgg16_cifar
+
+    make = {"resnet20": resnet20, "vgg16": vgg16_cifar, "resnet50": resnet50,
+            "resnet50-rho0.01": resnet50, "lstm": LSTMPTB}[config]
+    rho = 0.01 if config.endswith("0.01") else 0.001
+    dims = [p.numel() for p in make().parameters()]
+    ks = [orc.selection_count(d, 1.0 / rho) for d in dims]
+    n = sum(dims)
+    off = np.concatenate([[0], np.cumsum(dims)])
+    fast = L.Bucket(dims, ks, N.F32)
+    exact = L.Bucket(dims, ks, N.F32)
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    # per-layer gradient scales spread over 4 decades, like a real backward pass
+    scale = torch.repeat_interleave(
+        torch.logspace(-2, 2, len(dims), device="cuda")[torch.randperm(len(dims), device="cuda", generator=gen)],
+        torch.tensor(dims, device="cuda"))
+    r_f = torch.zeros(n, device="cuda")
+    r_e = torch.zeros(n, device="cuda")
+    m_f, m_e = fast.new_messages(1), exact.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    alpha = 0.1
+    for it in range(10):
+        g = torch.randn(n, device="cuda", generator=gen) * scale
+        check = it in (0, 9)
+        if check:
+            g_h, r_h = g.cpu().numpy(), r_f.cpu().numpy()
+            acc = r_h + np.float32(alpha) * g_h  # two fp32 roundings, as the kernel (-fmad=false)
+        fast.compress(g, r_f, alpha, m_f, st)
+        exact.compress(g, r_e, alpha, m_e, st, exact=True)
+        assert torch.equal(m_f, m_e), f"{config}: messages differ at call {it}"
+        assert torch.equal(r_f.view(torch.int32), r_e.view(torch.int32)), f"{config}: residuals differ at {it}"
+        if check:
+            got = fast.unpack(m_f)
+            r_new = r_f.cpu().numpy()
+            want_r = acc.copy()
+            for j, (idx, val) in enumerate(got):
+                a = acc[off[j]:off[j + 1]]
+                w_idx, w_val = orc.top_k(a, ks[j])
+                assert np.array_equal(idx, w_idx), (config, it, j)
+                assert _same_bits(val, w_val), (config, it, j)
+                want_r[off[j] + w_idx] = 0.0
+            assert _same_bits(r_new, want_r), (config, it)
+    assert int(st.item()) == 0
