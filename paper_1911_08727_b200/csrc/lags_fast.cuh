@@ -70,6 +70,18 @@ __device__ __forceinline__ uint32_t globaltimer_lo() {
 }
 
 constexpr float PRED_TARGET = 2.0f;  // wanted candidates per selected entry (m / k)
+#ifndef LAGS_PRED_SIGMAS
+#define LAGS_PRED_SIGMAS 3.0f
+#endif
+// Plus this many sqrt(m) of margin: at small k the candidate count's spread alone dropped it
+// below k about once per 100 steps (k = 9 / 16 layers, tools/fallback_trace.py).
+constexpr float PRED_SIGMAS = LAGS_PRED_SIGMAS;
+
+// Wanted candidate count for a layer selecting k: PRED_TARGET * k plus a Poisson-style margin.
+__device__ __forceinline__ float pred_target_count(uint32_t k) {
+  const float m = PRED_TARGET * static_cast<float>(k);
+  return m + PRED_SIGMAS * sqrtf(m);
+}
 
 __device__ __forceinline__ float pred_factor(const FastState& st) {
   return st.pf256 ? st.pf256 / 256.0f : static_cast<float>(PRED_FACTOR);
@@ -422,8 +434,8 @@ __device__ __forceinline__ uint32_t next_threshold(const FastState& st, uint32_t
 }
 
 // State after a candidate-path selection; the rank factor gets feedback: the threshold set last
-// call (rank pf*k) produced m candidates now, steer the next toward PRED_TARGET * k (geometric
-// mean of the old and the corrected factor).
+// call (rank pf*k) produced m candidates now, steer the next toward pred_target_count(k)
+// (geometric mean of the old and the corrected factor).
 __device__ __forceinline__ FastState candidate_state(const FastState& st, uint32_t pred, uint32_t m, uint32_t k,
                                                      uint32_t phases) {
   FastState ns = st;
@@ -433,7 +445,7 @@ __device__ __forceinline__ FastState candidate_state(const FastState& st, uint32
   ns.reserved = phases;
   if (m > 0) {
     const float pf = pred_factor(st);
-    const float corrected = pf * PRED_TARGET * static_cast<float>(k) / static_cast<float>(m);
+    const float corrected = pf * pred_target_count(k) / static_cast<float>(m);
     ns.pf256 = pf_encode(sqrtf(pf * fmaxf(corrected, 0.25f)));
   }
   return ns;
