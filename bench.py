@@ -32,9 +32,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 RHO = 0.001
-# DRAM bytes of one K1 launch from the committed ncu --set full capture (profiles/r1d_ncu_full_raw.csv:
-# dram__bytes_read.sum 204.616704 MB + dram__bytes_write.sum 51.038720 MB; ncu flushes caches per replay)
-K1_DRAM_TRAFFIC = 255_655_424
+# DRAM bytes of one K1 launch from the committed ncu --set full capture (profiles/r1e_ncu_full_raw.csv:
+# dram__bytes_read.sum 204.637440 MB + dram__bytes_write.sum 50.829568 MB; ncu flushes caches per replay)
+K1_DRAM_TRAFFIC = 255_467_008
 METRIC ="LAGS sparsify/decode GB/s (ResNet-50 layer shapes, rho=0.001); iter/s of the hot-path step"
 UNIT = "GB/s"
 
@@ -508,7 +508,7 @@ def run_ours(args, dims, ks, world, rank, local):
                          "bound": "hbm", "achieved": round(12 * n / (k1_ms / 1e3) / 1e9, 2), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(12 * n / (k1_ms / 1e3) / 1e9 / peak, 4), "traffic": K1_DRAM_TRAFFIC,
-                         "traffic_source": "profiles/r1d_ncu_full_raw.csv dram__bytes_read.sum + dram__bytes_write.sum",
+                         "traffic_source": "profiles/r1e_ncu_full_raw.csv dram__bytes_read.sum + dram__bytes_write.sum",
                          "algorithmic_bytes_per_launch": int(12 * n), "ms_per_launch": round(k1_ms, 4),
                          "compress": {"what": "K1 + K2 select/compact (+fused P=1 update at N=1)",
                                       "achieved": round(achieved, 2), "frac": round(achieved / peak, 4),
