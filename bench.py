@@ -531,6 +531,7 @@ def run_ours(args, dims, ks, world, rank, local):
 
 
 TRAIN_WINDOWS = 5
+TRAIN_KINDS = ("lags", "lags_noexchange", "dense")
 
 
 def measure_train(args, world, rank, local, dev):
@@ -547,9 +548,9 @@ def measure_train(args, world, rank, local, dev):
     torch.backends.cudnn.benchmark = True
     x, y = synthetic_images(64, 224, 1000, dev, seed=rank)
 
-    all_windows = {}
+    all_windows = {k: [] for k in TRAIN_KINDS}
 
-    def run(kind):
+    def setup(kind):
         torch.manual_seed(0)
         model = resnet50().to(dev)
         if kind == "dense":
@@ -572,54 +573,61 @@ def measure_train(args, world, rank, local, dev):
         for _ in range(args.train_warmup):
             it()
         torch.cuda.synchronize(dev)
+        return {"model": model, "net": net, "opt": opt, "it": it}
+
+    def window(it):
         if world > 1:
             dist.barrier()
-        # TRAIN_WINDOWS windows of train_steps iterations, each max over ranks; the median window
-        # is reported (one transient stall of a shared box must not decide a 20-iteration number)
-        windows = []
-        for _ in range(TRAIN_WINDOWS):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(args.train_steps):
-                it()
-            e1.record()
-            torch.cuda.synchronize(dev)
-            w = torch.tensor([e0.elapsed_time(e1) / args.train_steps], device=dev)
-            if world > 1:
-                dist.all_reduce(w, op=dist.ReduceOp.MAX)
-            windows.append(float(w))
-        ms = sorted(windows)[len(windows) // 2]
-        all_windows[kind] = [round(w, 3) for w in windows]
-        comm = None
-        if kind == "lags":
-            opt.enable_timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.train_steps):
             it()
-            times = opt.bucket_times_ms()
-            comm = torch.tensor([sum(t[1] for t in times), sum(t[0] for t in times), sum(t[2] for t in times)],
-                                device=dev)
-            if world > 1:
-                dist.all_reduce(comm, op=dist.ReduceOp.MAX)
-            comm = [float(c) for c in comm]
-            nb = len(opt.buckets)
-            opt.remove_hooks()
-        else:
-            nb = None
-        del opt, net, model
-        torch.cuda.empty_cache()
-        return ms, comm, nb
+        e1.record()
+        torch.cuda.synchronize(dev)
+        w = torch.tensor([e0.elapsed_time(e1) / args.train_steps], device=dev)
+        if world > 1:
+            dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        return float(w)
 
-    lags_ms, comm, nb = run("lags")
-    nx_ms, _, _ = run("lags_noexchange")
-    dense_ms, _, _ = run("dense")
+    # All three arms live side by side and their windows are interleaved (lags, no-exchange, dense,
+    # lags, ...), so box drift between windows hits every arm alike.  Each window is max over
+    # ranks; the median window is reported, and the exposed exchange is the median of the paired
+    # per-round differences lags - no-exchange.
+    arms = {k: setup(k) for k in TRAIN_KINDS}
+    for _ in range(TRAIN_WINDOWS):
+        for k in TRAIN_KINDS:
+            all_windows[k].append(window(arms[k]["it"]))
+    med = {k: sorted(w)[len(w) // 2] for k, w in all_windows.items()}
+    lags_ms, nx_ms, dense_ms = med["lags"], med["lags_noexchange"], med["dense"]
+    diffs = sorted(a - b for a, b in zip(all_windows["lags"], all_windows["lags_noexchange"]))
+    exposed_ms = diffs[len(diffs) // 2]
+    opt = arms["lags"]["opt"]
+    opt.enable_timing(True)
+    per_it = []  # the per-bucket side-stream spans include waiting for the slowest rank: median of 5
+    for _ in range(5):
+        arms["lags"]["it"]()
+        times = opt.bucket_times_ms()
+        c = torch.tensor([sum(t[1] for t in times), sum(t[0] for t in times), sum(t[2] for t in times)], device=dev)
+        if world > 1:
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        per_it.append([float(v) for v in c])
+    comm = [sorted(col)[len(col) // 2] for col in zip(*per_it)]
+    nb = len(opt.buckets)
+    for k in ("lags", "lags_noexchange"):
+        arms[k]["opt"].remove_hooks()
+    del arms, opt
+    torch.cuda.empty_cache()
+    all_windows = {k: [round(w, 3) for w in v] for k, v in all_windows.items()}
     out = {"model": "resnet50 (torchvision, random init)", "batch_per_gpu": 64, "amp": "bf16 autocast, fp32 weights",
            "rho": RHO, "buckets": nb, "bucket_cap_bytes": args.bucket_cap, "steps": args.train_steps,
            "lags_iter_per_s": round(1e3 / lags_ms, 3), "lags_ms_per_iter": round(lags_ms, 3),
            "dense_ddp_iter_per_s": round(1e3 / dense_ms, 3), "dense_ms_per_iter": round(dense_ms, 3),
            "lags_no_exchange_ms_per_iter": round(nx_ms, 3),
            "sum_compress_ms": round(comm[1], 3), "sum_exchange_ms": round(comm[0], 3),
-           "sum_decode_ms": round(comm[2], 3), "windows": TRAIN_WINDOWS, "ms_per_iter_windows": all_windows}
+           "sum_decode_ms": round(comm[2], 3), "windows": TRAIN_WINDOWS, "window_order": "interleaved",
+           "ms_per_iter_windows": all_windows, "exposed_exchange_ms": round(exposed_ms, 3)}
     if world > 1 and comm[0] > 0:
-        exposed = max(0.0, lags_ms - nx_ms)
+        exposed = max(0.0, exposed_ms)
         out["exchange_hidden_fraction"] = round(max(0.0, min(1.0, 1.0 - exposed / comm[0])), 4)
     return out
 
