@@ -15,7 +15,8 @@
  *    (thread-local).  No C++ exception crosses the ABI.
  *  - A bucket is a contiguous run of layers of the flat per-worker buffers (the reference's
  *    LayeredVector layout, R: layered.py:46-107): layer j occupies [offset_j, offset_j + dim_j),
- *    offsets being the prefix sums of dims.  Flat buffers must be 16-byte aligned.
+ *    offsets being the prefix sums of dims.  Flat buffers need only their element alignment
+ *    (4 bytes fp32, 8 bytes fp64); 16-byte aligned buffers take the vector path throughout.
  */
 #ifndef LAGS_B200_H
 #define LAGS_B200_H

@@ -4,13 +4,14 @@
 // task lists (= a contiguous index range):
 //   1. every CTA reads ALL of the layer's task counts and derives the candidate total m, every
 //      rank's share and its own offset (no exchange);
-//   2. every CTA gathers its candidates (value, index) into its own shared memory and -- central
-//      mode, m <= LAGS_CENTRAL_MAX -- stores their keys into EVERY CTA's shared memory at its
-//      offset (remote DSMEM stores), plus its common-prefix OR word; one cluster barrier;
-//   3. central: every CTA runs the same dual-rank radix select on its own full key copy (same
-//      keys, same order: the same threshold and prediction) and counts the lower ranks' gt / eq
-//      entries itself -- nothing crosses CTAs after the barrier.  Distributed mode (larger sets):
-//      per-pass histograms summed by rank 0 over DSMEM, threshold and counts exchanged;
+//   2. every CTA reads K1's histogram of the layer's candidate keys and locates the bin of the k-th
+//      largest (the same cut everywhere), then gathers its candidates (value, index) into its own
+//      shared memory, counting those above the cut bin and listing the cut bin's keys (a handful);
+//      it pushes that count and list into every CTA (DSMEM); one cluster barrier;
+//   3. every CTA resolves the exact threshold from the listed keys and the lower ranks' carried
+//      counts itself -- nothing crosses CTAs after the barrier.  A cut in the open top bin or a
+//      crowded bin (ties) takes the distributed radix select instead: per-pass histograms summed
+//      by rank 0 over DSMEM, threshold and counts exchanged;
 //   4. every CTA compacts its own range in order with the carried counts (global output
 //      positions), zeroes the selected residuals and applies the optional fused P = 1 update.
 // Results are identical to the single-CTA candidate path (same keys, same order, same rule).
@@ -61,7 +62,9 @@ struct ClusterShared {
   uint32_t gt, eq;           // distributed mode: this CTA's compaction counts
   uint32_t prefix, pmask, n_gt, need_eq, key2;  // distributed mode, rank 0: the threshold
   uint32_t qsum[CLUSTER];    // the ranks' candidate counts (every CTA computes all of them)
-  uint32_t qdiff[CLUSTER];   // central: every rank's OR word (pushed by each rank before the barrier)
+  uint32_t gtb[CLUSTER];     // histogram cut: every rank's count above the cut bin (pushed)
+  uint32_t lc[CLUSTER];      //   and its keys in the cut bin (pushed)
+  uint32_t lists[CLUSTER][BIN_LIST_MAX];
 };
 
 // Dual-rank radix select over a cluster's candidates when every CTA holds only its own keys
@@ -74,7 +77,7 @@ struct ClusterRadix {
   uint32_t diff;
 };
 
-__device__ void cluster_radix_select_dual(cooperative_groups::cluster_group& cluster, int rank, const float* sv,
+__device__ LAGS_COLD void cluster_radix_select_dual(cooperative_groups::cluster_group& cluster, int rank, const float* sv,
                                           uint32_t mr, uint32_t m, uint32_t key0, uint32_t k, uint32_t k2,
                                           SelectSmem& cs, ClusterRadix& cr, SelectThreshold<uint32_t>* th_out,
                                           uint32_t* key2_out) {
@@ -186,8 +189,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                                      const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r,
                                      int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words,
                                      int force_exact, float* vupd, uint32_t* dyn, SelectSmem& cs, ClusterShared& csh,
-                                     ClusterRadix& cr,
-                                     uint32_t t_launch) {
+                                     ClusterRadix& cr, uint32_t t_launch, uint32_t* hist) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t t_start = globaltimer_lo();
@@ -200,10 +202,13 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   const int T = tr.y - tr.x;
   const int t_lo = tr.x + static_cast<int>((static_cast<int64_t>(T) * rank) / CLUSTER);
   const int t_hi = tr.x + static_cast<int>((static_cast<int64_t>(T) * (rank + 1)) / CLUSTER);
+  // K1 counted this layer's candidates into its histogram iff it had a threshold
+  uint32_t* hl = hist && st.thr != 0u ? hist + static_cast<int64_t>(j) * HIST_BINS : nullptr;
   // every CTA of the cluster must be running before any remote shared-memory access: arrive now,
-  // wait just before the first remote store (the counts below overlap the barrier)
+  // wait just before the first remote store (the loads below overlap the barrier)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   LAGS_STAMP(0);
+  if (hl) stage_hist(hl, cs);  // every CTA its own copy, in flight together with the counts
   // 1. counts: every CTA reads ALL of the layer's task counts (one load per thread for layers
   // up to SEL_NT tasks) and derives m, the ranks' sums and its own offset -- no exchange
   int bnd[CLUSTER + 1];
@@ -214,25 +219,26 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
 #pragma unroll
   for (int q = 0; q < CLUSTER; ++q) qs[q] = 0u;
   uint32_t over = 0;
+  const bool cache = T <= SEL_NT;  // the counts stay in shared memory for the gather
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
+    if (cache) cs.tcache[t - tr.x] = c;
     const uint32_t cc = min(c, static_cast<uint32_t>(cap));
 #pragma unroll
     for (int q = 0; q < CLUSTER; ++q) qs[q] += (t >= bnd[q] && t < bnd[q + 1]) ? cc : 0u;
   }
   LAGS_STAMP(1);
-  __syncthreads();  // qsum / qge zeroed
+  __syncthreads();  // qsum zeroed
 #pragma unroll
   for (int q = 0; q < CLUSTER; ++q) {
     const uint32_t w = __reduce_add_sync(0xffffffffu, qs[q]);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(&csh.qsum[q], w);
   }
-  const uint32_t over_any = __syncthreads_or(over) ? 1u : 0u;
+  const uint32_t over_any = __syncthreads_or(over) ? 1u : 0u;  // (also publishes the staged histogram)
   LAGS_STAMP(2);
-  LAGS_STAMP(3);
   uint32_t m = 0, pre = 0, m_max = 0;
-  uint32_t rpre[CLUSTER + 1];  // prefix of the ranks' candidate counts (remote key reads)
+  uint32_t rpre[CLUSTER + 1];  // prefix of the ranks' candidate counts
   rpre[0] = 0;
 #pragma unroll
   for (int q = 0; q < CLUSTER; ++q) {
@@ -242,29 +248,24 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     m_max = max(m_max, mq);
     rpre[q + 1] = rpre[q] + mq;
   }
-  const uint32_t local = csh.qsum[rank];
-  // central: rank 0 holds a copy of all m keys (plus its own values / indices); otherwise every
-  // CTA holds only its own candidates and rank 0's radix passes read the keys over DSMEM
-#ifndef LAGS_CENTRAL_MAX
-#define LAGS_CENTRAL_MAX 16384
-#endif
-  constexpr uint32_t CENTRAL_MAX = LAGS_CENTRAL_MAX;  // larger sets: the distributed select is faster
-  const bool central = m <= CENTRAL_MAX && static_cast<uint64_t>(m) + 2ull * m_max <= static_cast<uint64_t>(smem_words);
-  const bool fits = central || 2ull * m_max <= static_cast<uint64_t>(smem_words);
+  const uint32_t mr = csh.qsum[rank];
+  const bool fits = 2ull * m_max <= static_cast<uint64_t>(smem_words);  // own values + indices
   int why = 0;
   if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
   else if (over_any) why = FB_OVERFLOW;
   else if (m < k && st.thr > 1u) why = FB_TOO_FEW;
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // all CTAs of the cluster are running
+  LAGS_STAMP(3);
   if (why || !fits || m == 0) {  // uniform across the cluster; rank 0 finishes the layer alone
     if (rank == 0) {  // (no shared memory of another CTA was touched: the others just leave)
       if (why) {
         dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
       } else {  // too many candidates for the cluster's shared memory, or none: one-CTA path
         candidate_select(j, L, tr, st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out, val_out, count_out,
-                         state, dyn, smem_words, cs, vupd);
+                         state, dyn, smem_words, cs, vupd, hl);
       }
       __syncthreads();
+      if (hl) zero_hist(hl, 0, HIST_BINS);
       if (threadIdx.x == 0) {
         state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
         state[j].path = why ? 2u : 1u;
@@ -275,115 +276,107 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     }
     return;
   }
-  // 2. gather: own (value, index) at [m, m + mr) / [m + mr, m + 2 mr) of dyn and the keys into
-  // EVERY CTA's dyn at the own prefix offset (central), or own (value, index) at [0, m_max) /
-  // [m_max, m_max + mr) (distributed)
+  // 2. the histogram cut (every CTA the same, from its own copy), then the gather of the own
+  // quarter: values at [0, mr), indices at [m_max, m_max + mr) of dyn; entries above the cut bin
+  // are counted and the cut bin's keys listed on the way
   const long long c0 = clock64();
-  LAGS_STAMP(4);
-  const uint32_t mr = local;
-  const uint32_t vbase = central ? m : 0u, ibase = central ? m + mr : m_max;
-  float* sv = reinterpret_cast<float*>(dyn + vbase);
-  int32_t* si = reinterpret_cast<int32_t*>(dyn + ibase);
-  uint32_t* keysq[CLUSTER];
-#pragma unroll
-  for (int q = 0; q < CLUSTER; ++q) keysq[q] = cluster.map_shared_rank(dyn, q) + pre;
-  uint32_t carry = 0;
-  const uint32_t key0 = st.thr;  // reference key of the common-prefix OR
-  const float* vpf = vupd ? vupd + L.offset : nullptr;  // P = 1: prefetch the candidates' weights
-  if (threadIdx.x == 0) cs.sm.diff_acc = 0u;
-  for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
-    const int nt = min(SEL_NT, t_hi - t0);
-    const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)) : 0u;
-    uint32_t tot;
-    const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
-    cs.tpos[threadIdx.x] = pos;
-    __syncthreads();
-    uint32_t dx = 0u;
-    for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
-      int64_t src[GATHER_ILP];
-#pragma unroll
-      for (int u = 0; u < GATHER_ILP; ++u) {
-        const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
-        src[u] = -1;
-        if (e < tot) {
-          int lo = 0, hi = nt - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (cs.tpos[mid] <= e) lo = mid;
-            else hi = mid - 1;
-          }
-          src[u] = static_cast<int64_t>(t0 + lo) * cap + (e - cs.tpos[lo]);
-        }
-      }
-      float xv[GATHER_ILP];
-      int32_t xi[GATHER_ILP];
-#pragma unroll
-      for (int u = 0; u < GATHER_ILP; ++u) {
-        if (src[u] >= 0) {
-          xv[u] = __ldcg(cand_val + src[u]);
-          xi[u] = __ldcg(cand_idx + src[u]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < GATHER_ILP; ++u) {
-        if (src[u] >= 0) {
-          const uint32_t e = carry + e0 + u * SEL_NT + threadIdx.x;
-          const uint32_t key = Key<float>::of(xv[u]);
-          sv[e] = xv[u];
-          si[e] = xi[u];
-          if (vpf) asm volatile("prefetch.global.L2 [%0];" ::"l"(vpf + xi[u]));  // fused update's weight
-          if (central) {
-#pragma unroll
-            for (int q = 0; q < CLUSTER; ++q) keysq[q][e] = key;
-          }
-          dx |= key ^ key0;
-        }
-      }
-    }
-    dx = __reduce_or_sync(0xffffffffu, dx);
-    if ((threadIdx.x & 31) == 0 && dx) atomicOr(&cs.sm.diff_acc, dx);
-    carry += tot;
-    __syncthreads();
-  }
-  if (central) {  // the own OR word into every CTA (read locally after the barrier)
-    if (threadIdx.x < CLUSTER) cluster.map_shared_rank(&csh, static_cast<int>(threadIdx.x))->qdiff[rank] = cs.sm.diff_acc;
-  }
-  LAGS_STAMP(5);
-  cluster.sync();  // central: all keys are in every CTA
-  LAGS_STAMP(6);
-  const long long c1 = clock64();
   const uint32_t k2 = pred_rank(st, k);
-  SelectThreshold<uint32_t> th;
-  uint32_t key2;
-  uint32_t cg0 = 0, ce0 = 0;
-  if (central) {
-    // 3. every CTA selects on its own full copy (same keys, same order: the same threshold), then
-    // counts the lower ranks' entries itself -- nothing crosses CTAs after the gather barrier
-    const uint32_t* keys = dyn;
-    auto key_at = [=](int64_t i) { return keys[i]; };
-    uint32_t dk[2] = {0u, key0};
-#pragma unroll
-    for (int q = 0; q < CLUSTER; ++q) dk[0] |= csh.qdiff[q];
-    radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
-#ifdef LAGS_DBG_TWICE  // the same select again with a warm instruction cache (diagnostic)
-    LAGS_STAMP(16);
-    radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
-    LAGS_STAMP(17);
-#endif
-    LAGS_STAMP(7);
-    LAGS_STAMP(8);
-    uint32_t lge = 0;  // gt | eq << 16 over the lower ranks' keys [0, pre) (m <= CENTRAL_MAX < 65536)
-    for (uint32_t i = threadIdx.x; i < pre; i += SEL_NT) {
-      const uint32_t key = keys[i];
-      const uint32_t hk = key & th.pmask;
-      if (key != 0u) lge += hk > th.prefix ? 1u : (hk == th.prefix ? 0x10000u : 0u);
+  const uint32_t base = st.thr >> HIST_SHIFT;
+  HistCut hc{~0u, 0u, 0u, 0u};
+  bool cut = hl != nullptr && k < m;
+  if (cut) {
+    hc = hist_cut(cs, k, k2, m);
+    cut = hc.bin < HIST_BINS - 1u && hc.in_bin <= BIN_LIST_MAX;
+  }
+  if (threadIdx.x == 0) {
+    cs.sm.list_n = 0u;
+    cs.sm.gtb = 0u;
+  }
+  __syncthreads();
+  LAGS_STAMP(4);
+  float* sv = reinterpret_cast<float*>(dyn);
+  int32_t* si = reinterpret_cast<int32_t*>(dyn + m_max);
+  gather_candidates(t_lo, t_hi, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
+                    &cs.sm.gtb, cs.hist2, &cs.sm.list_n, vupd ? vupd + L.offset : nullptr,
+                    cache ? cs.tcache : nullptr, tr.x);
+  __syncthreads();
+  LAGS_STAMP(5);
+  if (cut) {  // push the own count above the cut and the cut bin's keys into every CTA
+    const uint32_t lc = min(cs.sm.list_n, BIN_LIST_MAX), per = lc + 1;
+    for (uint32_t e = threadIdx.x; e < CLUSTER * per; e += SEL_NT) {
+      ClusterShared* o = cluster.map_shared_rank(&csh, static_cast<int>(e / per));
+      const uint32_t i = e % per;
+      if (i < lc) {
+        o->lists[rank][i] = cs.hist2[i];
+      } else {
+        o->gtb[rank] = cs.sm.gtb;
+        o->lc[rank] = cs.sm.list_n;
+      }
     }
-    lge = block_sum(lge, cs.sm);
-    cg0 = lge & 0xffffu;
-    ce0 = lge >> 16;
-    LAGS_STAMP(9);
-    LAGS_STAMP(10);
-  } else {  // every CTA holds its own keys: the distributed select (all CTAs)
+  }
+  LAGS_STAMP(6);
+  cluster.sync();  // the pushed counts and lists are visible (the histogram copies are consumed)
+  LAGS_STAMP(7);
+  const long long c1 = clock64();
+  SelectThreshold<uint32_t> th;
+  uint32_t key2 = 0u;
+  uint32_t cg0 = 0, ce0 = 0;
+  bool resolved = false;
+  if (k >= m) {  // every candidate (all nonzero: keys >= the threshold >= 1) is selected
+    th.prefix = 0u;
+    th.pmask = 0xffffffffu;
+    th.n_gt = 0u;
+    th.need_eq = 0u;
+    cg0 = pre;
+    resolved = true;
+  } else if (cut) {
+    uint32_t off[CLUSTER + 1], gsum = 0;
+    off[0] = 0;
+#pragma unroll
+    for (int q = 0; q < CLUSTER; ++q) {
+      off[q + 1] = off[q] + csh.lc[q];
+      gsum += csh.gtb[q];
+    }
+    if (off[CLUSTER] == hc.in_bin && gsum == hc.above) {  // uniform: the same pushed data everywhere
+      const uint32_t c = off[CLUSTER];
+      uint32_t* list = cs.hist2;  // the cut bin's keys of all ranks, contiguous
+      for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) {
+        int q = 0;
+        while (i >= off[q + 1]) ++q;
+        list[i] = csh.lists[q][i - off[q]];
+      }
+      __syncthreads();
+      th = resolve_cut(list, c, k - hc.above, hc.above, cs);
+      LAGS_STAMP(8);
+      // carried counts of the lower ranks: their entries above the cut bin plus their listed keys
+      // above / equal to the threshold (c <= BIN_LIST_MAX < SEL_NT: one key per thread)
+      uint32_t lge = 0u;
+      if (threadIdx.x < c && threadIdx.x < off[rank]) {
+        const uint32_t x = list[threadIdx.x];
+        lge = x > th.prefix ? 1u : (x == th.prefix ? 0x10000u : 0u);
+      }
+      lge = block_sum(lge, cs.sm);
+      for (int q = 0; q < rank; ++q) cg0 += csh.gtb[q];
+      cg0 += lge & 0xffffu;
+      ce0 = lge >> 16;
+      key2 = (base + hc.bin2) << HIST_SHIFT;  // lower edge of the k2-th candidate's bin
+      resolved = true;
+      LAGS_STAMP(9);
+      LAGS_STAMP(10);
+    }
+  }
+  const bool hard = !resolved;  // uniform
+  uint32_t cut_diag = 0u;  // why the cut did not resolve (diagnostic): 1 no histogram, 2 top bin or
+                           // crowded, 4 counts mismatch; bits 8.. the cut bin's count
+  if (hard) {
+    if (!hl) cut_diag = 1u;
+    else if (!cut) cut_diag = 2u;
+    else cut_diag = 4u;
+    if (hl && k < m) cut_diag |= min(hc.in_bin, 0xffffffu) << 8;
+    if (cut_diag == 4u && threadIdx.x == 0 && rank == 0)
+      cut_diag |= (min(csh.lc[0] + csh.lc[1] + csh.lc[2] + csh.lc[3], 255u) << 16) | (hc.in_bin == 0 ? 0x80u : 0u);
+  }
+  if (hard) {  // top (open) bin or a crowded one: the distributed radix select over every CTA's keys
     int q0 = 0;
     while (rpre[q0 + 1] == rpre[q0]) ++q0;  // the first rank with candidates (m > 0)
     const uint32_t dkey0 = Key<float>::of(cluster.map_shared_rank(reinterpret_cast<const float*>(dyn), q0)[0]);
@@ -395,9 +388,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       csh.need_eq = th.need_eq;
       csh.key2 = key2;
     }
-    LAGS_STAMP(7);
     cluster.sync();
-    LAGS_STAMP(8);
     {
       const ClusterShared* o = cluster.map_shared_rank(&csh, 0);
       th.prefix = o->prefix;
@@ -413,13 +404,11 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       if (key != 0u) lge += hk > th.prefix ? 1u : (hk == th.prefix ? 0x10000u : 0u);
     }
     lge = block_sum(lge, cs.sm);
-    LAGS_STAMP(9);
     if (threadIdx.x == 0) {
       csh.gt = lge & 0xffffu;
       csh.eq = lge >> 16;
     }
     cluster.sync();
-    LAGS_STAMP(10);
     for (int q = 0; q < rank; ++q) {
       const ClusterShared* o = cluster.map_shared_rank(&csh, q);
       cg0 += o->gt;
@@ -427,7 +416,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     }
   }
   const long long c2 = clock64();
-  // 4. ordered compaction of the own range with the carried counts of the lower ranks
+  // 3. ordered compaction of the own range with the carried counts of the lower ranks
   float* data = r + L.offset;
   int32_t* oidx = idx_out + L.slot;
   float* oval = val_out + L.slot;
@@ -442,7 +431,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
       oidx[pos] = static_cast<int32_t>(ix);
       oval[pos] = x;
-      data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+      data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       vl[ix] = single_rank_update(w, x);
     };
     end = ordered_compact_pf<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0, [=](int64_t ix) { return vl[ix]; });
@@ -450,11 +439,12 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
       oidx[pos] = static_cast<int32_t>(ix);
       oval[pos] = x;
-      data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+      data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
     };
     end = ordered_compact<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0);
   }
   LAGS_STAMP(11);
+  if (hl) zero_hist(hl, rank * (HIST_BINS / CLUSTER), (rank + 1) * (HIST_BINS / CLUSTER));
   LAGS_STAMP(12);
   const long long c3 = clock64();
   if (rank == CLUSTER - 1 && threadIdx.x == 0) count_out[j] = static_cast<int32_t>(end);
@@ -467,15 +457,16 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
 #endif
     FastState ns = candidate_state(st, next_threshold(st, m, k, k2, th.prefix, key2), m, k, ph);
     ns.cycles = static_cast<uint32_t>(clock64() - t_begin);
-    ns.path = 3u;
+    ns.path = hard ? 4u : 3u;
+    ns.cut = cut_diag | (hard && cut ? (min(csh.gtb[0] + csh.gtb[1] + csh.gtb[2] + csh.gtb[3], 0xffu) << 24) : 0u);
     ns.t_start = t_start;
     ns.t_end = globaltimer_lo();
     ns.t_launch = t_launch;
     state[j] = ns;
   }
-  // distributed: no CTA leaves while others may still read its shared memory (central: nothing is
-  // read remotely after the gather barrier)
-  if (!central) cluster_sync_exec();
+  // the distributed select reads other CTAs' shared memory up to its last barrier: no CTA leaves
+  // before every CTA is past it (the cut path reads only its own after the gather barrier)
+  if (hard) cluster_sync_exec();
   LAGS_STAMP(13);
 }
 
@@ -491,26 +482,26 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
     FastState* state, const int32_t* __restrict__ cand_cnt,
     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval,
     float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, SelectCounters sc,
-    float* vupd) {
+    float* vupd, uint32_t* hist) {
   extern __shared__ uint32_t dyn[];
   __shared__ SelectSmem cs;
   __shared__ ClusterShared csh;
   __shared__ ClusterRadix cr;
   __shared__ int next_pos;
   const uint32_t t_launch = globaltimer_lo();
+  const int cl_ctas = n_cl * CLUSTER;
+  constexpr int NW = SEL_NT / 32;
+  const int tiny_ctas = (n_tiny + NW - 1) / NW;
   LAGS_STAMP(14);
   griddep_wait();  // K1 has completed and its writes are visible (programmatic dependent launch)
   LAGS_STAMP(15);
-  const int cl_ctas = n_cl * CLUSTER;
   if (static_cast<int>(blockIdx.x) < cl_ctas) {
     cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap,
                          gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh, cr,
-                         t_launch);
+                         t_launch, hist);
     return;
   }
   // tiny layers: one warp each, in the CTAs right after the clusters (all in the first wave)
-  constexpr int NW = SEL_NT / 32;
-  const int tiny_ctas = (n_tiny + NW - 1) / NW;
   if (static_cast<int>(blockIdx.x) < cl_ctas + tiny_ctas) {
     const int t = (static_cast<int>(blockIdx.x) - cl_ctas) * NW + static_cast<int>(threadIdx.x >> 5);
     if (t < n_tiny) {
@@ -524,7 +515,7 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
   for (int pos = static_cast<int>(blockIdx.x) - base; pos < nl;) {
     if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + grid;
     select_layer(order[pos], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out,
-                 val_out, count_out, dyn, smem_words, force_exact, cs, vupd, t_launch);
+                 val_out, count_out, dyn, smem_words, force_exact, cs, vupd, t_launch, hist);
     pos = next_pos;
     __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
   }

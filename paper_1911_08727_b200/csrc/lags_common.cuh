@@ -16,24 +16,35 @@ struct lags_layer_t {
 
 namespace lags {
 
-// |x| as an unsigned key: monotone in magnitude for finite x, 0 only for +-0.
-// Ties on equal keys are broken by lower index (R: sparsify.py:85-87).
+// |x| as an unsigned key: monotone in magnitude for finite x and +-inf, 0 for +-0 and NaN.
+// Ties on equal keys are broken by lower index (R: sparsify.py:85-87).  NaN maps to 0 (never
+// selected): the reference's stable argsort of -|x| puts NaN after every number and its
+// `mag > 0` filter then drops it (R: sparsify.py:87-88).
 template <typename T> struct Key;
 template <> struct Key<float> {
   using K = uint32_t;
   static constexpr int BITS = 31;  // sign bit dropped
   static constexpr int RB = 12;    // radix digit width -> <= 3 passes (12, 12, 7); crowded
                                    // candidate keys (common prefix skipped) usually need 2
-  __device__ __forceinline__ static K of(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+  __device__ __forceinline__ static K of(float x) {
+    const K k = __float_as_uint(x) & 0x7fffffffu;
+    return k > 0x7f800000u ? 0u : k;
+  }
 };
 template <> struct Key<double> {
   using K = unsigned long long;
   static constexpr int BITS = 63;
   static constexpr int RB = 13;  // 5 passes (13, 13, 13, 13, 11)
   __device__ __forceinline__ static K of(double x) {
-    return static_cast<K>(__double_as_longlong(x)) & 0x7fffffffffffffffull;
+    const K k = static_cast<K>(__double_as_longlong(x)) & 0x7fffffffffffffffull;
+    return k > 0x7ff0000000000000ull ? 0ull : k;
   }
 };
+
+// Residual of a selected entry, acc - sent with sent = acc (R: training.py:252): +0.0 for finite
+// acc, NaN for an overflowed +-inf (inf - inf), exactly as numpy computes it.
+__device__ __forceinline__ float sent_residual(float x) { return __fsub_rn(x, x); }
+__device__ __forceinline__ double sent_residual(double x) { return __dsub_rn(x, x); }
 
 // acc = r + alpha * g rounded twice (numpy evaluates `alpha * g` then `+`; no FMA).
 __device__ __forceinline__ float accum(float r, float g, float a) { return __fadd_rn(r, __fmul_rn(a, g)); }
@@ -89,6 +100,15 @@ __device__ __forceinline__ bool nonfinite(double g) {
 #define LAGS_OR_ATTR __forceinline__
 #else
 #define LAGS_OR_ATTR __noinline__
+#endif
+
+// Rarely executed selection paths (dense fallbacks, radix selects behind a failed histogram cut)
+// are kept out of line: every path of the selection kernel runs once per launch with a cold
+// instruction cache, so inlining them would only spread the hot path over more cache lines.
+#ifdef LAGS_COLD_INLINE
+#define LAGS_COLD __forceinline__
+#else
+#define LAGS_COLD __noinline__
 #endif
 
 template <int NT>

@@ -36,6 +36,16 @@ constexpr int TINY_LAYER = 4096;   // layers up to this size always take it (che
 #ifndef LAGS_K1_MINB
 #define LAGS_K1_MINB 1
 #endif
+// K1's residual traffic (read + write of r, 8 B/element) streams through L2 with evict-first
+// priority like the gradient: normal-priority lines (the candidate lists and histograms K1 writes,
+// the weights, the selection kernel's own code) then stay in L2 for the selection that follows.
+#ifndef LAGS_R_NORMAL
+#define LAGS_R_LOAD(p) __ldcs(p)
+#define LAGS_R_STORE(p, v) __stcs((p), (v))
+#else
+#define LAGS_R_LOAD(p) (*(p))
+#define LAGS_R_STORE(p, v) (*(p) = (v))
+#endif
 constexpr int K1_WARPS = LAGS_K1_WARPS;  // warps per K1 CTA
 constexpr int K1_MINB = LAGS_K1_MINB;    // K1 CTAs per SM the register allocation must allow
 constexpr int K1_UNROLL = LAGS_K1_UNROLL;        // float4 loads in flight per lane per operand (K1)
@@ -60,7 +70,7 @@ struct FastState {
   uint32_t t_start;     // %globaltimer (ns, low 32 bits) when the layer's CTA started / ended its
   uint32_t t_end;       //   selection work at the last call (diagnostic timeline)
   uint32_t t_launch;    // %globaltimer when the CTA entered the kernel (before griddepcontrol.wait)
-  uint32_t pad;
+  uint32_t cut;         // histogram-cut diagnostic: in_bin << 8 | code (0 resolved, see cut_code)
 };
 
 __device__ __forceinline__ uint32_t globaltimer_lo() {
@@ -112,21 +122,40 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
   return x;
 }
 
+// K1's per-layer histogram of its candidate keys -- the selection's first cut without a pass over
+// the candidates: HIST_BINS bins of 2^HIST_SHIFT consecutive keys, counted up from the layer's
+// candidate threshold (8192 bins per octave of |x|, so the 4096 bins span keys up to sqrt(2) times
+// the threshold; larger keys share the top bin).  Error feedback piles the accumulated magnitudes
+// up just below the threshold, so the bins must be fine there (at 1024 per octave the cut bin of a
+// 2.4 M-element layer held 150-220 keys).  HIST_BINS equals the radix histogram size, so the radix
+// find_bin2 resolves ranks on it.
+#ifndef LAGS_HIST_SHIFT
+#define LAGS_HIST_SHIFT 10
+#endif
+constexpr int HIST_SHIFT = LAGS_HIST_SHIFT;
+constexpr int HIST_BINS = F32_BINS;
+__device__ __forceinline__ uint32_t hist_bin(uint32_t key, uint32_t base) {
+  return min((key >> HIST_SHIFT) - base, static_cast<uint32_t>(HIST_BINS - 1));
+}
+
 // Append this lane's candidate bits (ascending element order within the lane, lanes in index
-// order) to the task list.  Warp-collective.  The lane's (up to 4) values come by value: a
-// dynamically indexed array would live in local memory.
+// order) to the task list, and count each in the layer histogram hl (nullable; base = the
+// threshold's bin).  Warp-collective.  The lane's (up to 4) values come by value: a dynamically
+// indexed array would live in local memory.
 __device__ __forceinline__ void emit_candidates(uint32_t bits, float4 vals, int64_t local0, int lane, uint32_t& cnt,
-                                                int32_t* cidx, float* cval, int cap) {
+                                                int32_t* cidx, float* cval, int cap, uint32_t* hl, uint32_t base) {
   if (__ballot_sync(0xffffffffu, bits != 0) == 0u) return;
   const uint32_t c = __popc(bits);
   const uint32_t inc = warp_inclusive_scan(c, lane);
   uint32_t pos = cnt + inc - c;
   while (bits) {
     const int b = __ffs(bits) - 1;
+    const float x = b == 0 ? vals.x : b == 1 ? vals.y : b == 2 ? vals.z : vals.w;
     if (pos < static_cast<uint32_t>(cap)) {
       cidx[pos] = static_cast<int32_t>(local0 + b);
-      cval[pos] = b == 0 ? vals.x : b == 1 ? vals.y : b == 2 ? vals.z : vals.w;
+      cval[pos] = x;
     }
+    if (hl) atomicAdd(hl + hist_bin(Key<float>::of(x), base), 1u);
     ++pos;
     bits &= bits - 1;
   }
@@ -145,10 +174,12 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
                                             const FastState* state, float* __restrict__ gt, float* __restrict__ rt,
                                             float alpha, int cap, int32_t* __restrict__ cand_idx,
                                             float* __restrict__ cand_val, int32_t* __restrict__ cand_cnt,
-                                            uint32_t* status) {
+                                            uint32_t* status, uint32_t* hist) {
   const int64_t local0 = T.start - layers[T.layer].offset;  // layer-local index of element 0
   const uint32_t thr0 = state[T.layer].thr;
   const uint32_t thr = thr0 ? thr0 : 0xffffffffu;
+  uint32_t* hl = hist ? hist + static_cast<int64_t>(T.layer) * HIST_BINS : nullptr;
+  const uint32_t hbase = thr0 >> HIST_SHIFT;
   int32_t* cidx = cand_idx + static_cast<int64_t>(tid) * cap;
   float* cval = cand_val + static_cast<int64_t>(tid) * cap;
   uint32_t cnt = 0;
@@ -170,7 +201,7 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
         rt[i] = a;
         bits = (Key<float>::of(a) >= thr) ? 1u : 0u;
       }
-      emit_candidates(bits, make_float4(a, a, a, a), local0 + i, lane, cnt, cidx, cval, cap);
+      emit_candidates(bits, make_float4(a, a, a, a), local0 + i, lane, cnt, cidx, cval, cap, hl, hbase);
     }
   };
   scalar(0, h);
@@ -184,7 +215,7 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
       const int q = q0 + u * 32 + lane;
       if (q < n4) {
         gv[u] = __ldcs(g4 + q);
-        rv[u] = r4[q];
+        rv[u] = LAGS_R_LOAD(r4 + q);
       }
     }
     if (ZERO_G) {
@@ -205,11 +236,12 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
         a.y = accum(rv[u].y, gv[u].y, alpha);
         a.z = accum(rv[u].z, gv[u].z, alpha);
         a.w = accum(rv[u].w, gv[u].w, alpha);
-        r4[q] = a;
+        LAGS_R_STORE(r4 + q, a);
         bits = (Key<float>::of(a.x) >= thr ? 1u : 0u) | (Key<float>::of(a.y) >= thr ? 2u : 0u) |
                (Key<float>::of(a.z) >= thr ? 4u : 0u) | (Key<float>::of(a.w) >= thr ? 8u : 0u);
       }
-      if (q0 + u * 32 < n4) emit_candidates(bits, a, local0 + h + 4 * static_cast<int64_t>(q), lane, cnt, cidx, cval, cap);
+      if (q0 + u * 32 < n4)
+        emit_candidates(bits, a, local0 + h + 4 * static_cast<int64_t>(q), lane, cnt, cidx, cval, cap, hl, hbase);
     }
   }
   scalar(h + 4 * n4, n);  // scalar tail
@@ -223,16 +255,21 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
     const FastState* __restrict__ state, float* __restrict__ g, float* const* __restrict__ gtab,
     float* __restrict__ r, float alpha, int cap, int32_t* __restrict__ cand_idx, float* __restrict__ cand_val,
-    int32_t* __restrict__ cand_cnt, uint32_t* status, uint32_t* work) {
+    int32_t* __restrict__ cand_cnt, uint32_t* status, uint32_t* work, uint32_t* hist) {
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
   griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
+  // let the selection kernel (PDL) be scheduled: it is launched once the last K1 CTA has started,
+  // so its CTAs take SMs as K1's last wave drains, and it waits for K1's completion itself
+#ifndef LAGS_NO_EARLY_TRIGGER
+  griddep_launch_dependents();
+#endif
   if (wid == 0 && lane == 0) *work = 0u;  // the previous call's selection kernel has completed
   if (wid >= ntasks) return;
   const Task T = tasks[wid];
   float* gt = gtab ? gtab[T.layer] + (T.start - layers[T.layer].offset) : g + T.start;
   stream_task<ZERO_G, K1_UNROLL>(T, wid, lane, layers, state, gt, r + T.start, alpha, cap, cand_idx, cand_val,
-                                 cand_cnt, status);
+                                 cand_cnt, status, hist);
 }
 
 // Block-wide sum; all threads get the result.  Uses sm.warp_tot.
@@ -249,6 +286,7 @@ struct SelectSmem {
   uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
   uint32_t tpos[SEL_NT];     // candidate gather: per-task output position / count
   uint32_t tcnt[SEL_NT];
+  uint32_t tcache[SEL_NT];   // the layer's task counts from the counting pass (layers of <= SEL_NT tasks)
 };
 
 // P = 1 update fused into the selection epilogue (no exchange, no separate decode): exactly the
@@ -291,7 +329,7 @@ __device__ __forceinline__ void apply_single_rank_updates(float* vl, const int32
 // Once the threshold's bin holds at most BIN_LIST_MAX keys, the remaining passes are replaced by
 // one pass that lists the bin's keys and a direct rank count among them.
 #ifndef LAGS_BIN_LIST_MAX
-#define LAGS_BIN_LIST_MAX 128
+#define LAGS_BIN_LIST_MAX 256
 #endif
 constexpr uint32_t BIN_LIST_MAX = LAGS_BIN_LIST_MAX;
 
@@ -451,10 +489,154 @@ __device__ __forceinline__ FastState candidate_state(const FastState& st, uint32
   return ns;
 }
 
+// Histogram cut of a candidate set (K1's per-layer histogram, staged in cs.sm.hist): the bins
+// holding the k-th and the k2-th largest candidate (k, k2 <= m).
+struct HistCut {
+  uint32_t bin, above, in_bin;  // rank k: its bin, the candidates in higher bins, the bin's count
+  uint32_t bin2;                // rank k2 (the next prediction): its bin
+};
+
+// Stage the layer's histogram into cs.sm.hist (16-byte loads; the caller synchronises).
+__device__ __forceinline__ void stage_hist(const uint32_t* hl, SelectSmem& cs) {
+  const uint4* src = reinterpret_cast<const uint4*>(hl);
+  uint4* dst = reinterpret_cast<uint4*>(cs.sm.hist);
+  for (int i = threadIdx.x; i < HIST_BINS / 4; i += SEL_NT) dst[i] = __ldcg(src + i);
+}
+
+// Clear bins [lo, hi) of a layer histogram for the next call's K1 (16-byte stores).
+__device__ __forceinline__ void zero_hist(uint32_t* hl, int lo, int hi) {
+  uint4* dst = reinterpret_cast<uint4*>(hl);
+  for (int i = lo / 4 + threadIdx.x; i < hi / 4; i += SEL_NT) dst[i] = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// All threads; the staged histogram must be visible (after a barrier).
+__device__ __forceinline__ HistCut hist_cut(SelectSmem& cs, uint32_t k, uint32_t k2, uint32_t m) {
+  uint32_t bin[2], above[2], in_bin[2];
+  find_bin2<Key<float>::RB>(cs.sm, cs.sm.hist, min(k, m), min(k2, m), bin, above, in_bin);
+  return HistCut{bin[0], above[0], in_bin[0], bin[1]};
+}
+
+// The exact threshold from the keys of the cut bin (list[0..c), any order): the r-th largest of
+// them (1 <= r <= c) is T; the selection is every key > T (n_gt = above + those in the list) plus
+// the first need_eq entries equal to T in index order (R: sparsify.py:85-88, lowest index wins).
+// All threads; ends with a barrier.  Uses cs.sm.list_key / list_gt.
+__device__ __forceinline__ SelectThreshold<uint32_t> resolve_cut(const uint32_t* list, uint32_t c, uint32_t r,
+                                                                 uint32_t above, SelectSmem& cs) {
+  for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) {
+    const uint32_t mine = list[i];
+    uint32_t gt = 0, eq = 0;
+    for (uint32_t q = 0; q < c; ++q) {
+      const uint32_t x = list[q];
+      gt += x > mine ? 1u : 0u;
+      eq += x == mine ? 1u : 0u;
+    }
+    if (gt < r && r <= gt + eq) {  // equal keys write equal values
+      cs.sm.list_key = mine;
+      cs.sm.list_gt = gt;
+    }
+  }
+  __syncthreads();
+  SelectThreshold<uint32_t> th;
+  th.prefix = cs.sm.list_key;
+  th.pmask = 0x7fffffffu;
+  th.n_gt = above + cs.sm.list_gt;
+  th.need_eq = r - cs.sm.list_gt;
+  __syncthreads();  // list_key / list_gt are read before any reuse
+  return th;
+}
+
+// Candidate gather of tasks [t_lo, t_hi) into sv / si (ascending index order): positions by a
+// block scan over the task counts, then one warp per task copies the task's list (lane l takes
+// entries l, l + 32, ...: coalesced), GATHER_TASKS tasks per warp in flight.  On the way, against
+// the histogram cut (cut_bin, base; cut_bin == ~0u: no cut): the entries in higher bins are
+// counted into *gtb (shared), the keys of the cut bin are appended to list (shared, *list_n), and
+// the weights of possibly selected entries are prefetched into L2 (vpf, P = 1 update).  The keys'
+// common-prefix OR against key0 goes to cs.sm.diff_acc (radix fallback).  tc (nullable): the task
+// counts already in shared memory, tc[t - t_base] for every task of the range.  Returns the
+// number gathered.  All threads.
+#ifndef LAGS_GATHER_TASKS
+#define LAGS_GATHER_TASKS 6
+#endif
+constexpr int GATHER_TASKS = LAGS_GATHER_TASKS;
+
+__device__ uint32_t gather_candidates(int t_lo, int t_hi, const int32_t* __restrict__ cand_cnt,
+                                      const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
+                                      float* sv, int32_t* si, SelectSmem& cs, uint32_t key0, uint32_t base,
+                                      uint32_t cut_bin, uint32_t* gtb, uint32_t* list, uint32_t* list_n,
+                                      const float* vpf, const uint32_t* tc, int t_base) {
+  constexpr int NW = SEL_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t carry = 0, my_gt = 0, dx = 0;
+  if (threadIdx.x == 0) cs.sm.diff_acc = 0u;
+  auto take = [&](float x, int32_t ix, uint32_t e) {
+    const uint32_t key = Key<float>::of(x);
+    sv[e] = x;
+    si[e] = ix;
+    dx |= key ^ key0;
+    const uint32_t b = hist_bin(key, base);
+    if (cut_bin == ~0u || b >= cut_bin) {
+      if (vpf) asm volatile("prefetch.global.L2 [%0];" ::"l"(vpf + ix));  // P = 1 weight
+      if (cut_bin != ~0u) {
+        if (b > cut_bin) {
+          ++my_gt;
+        } else {
+          const uint32_t at = atomicAdd(list_n, 1u);
+          if (at < BIN_LIST_MAX) list[at] = key;
+        }
+      }
+    }
+  };
+  for (int t0 = t_lo; t0 < t_hi; t0 += SEL_NT) {
+    const int nt = min(SEL_NT, t_hi - t0);
+    uint32_t c = 0u;
+    if (threadIdx.x < nt) c = tc ? tc[t0 - t_base + threadIdx.x] : static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x));
+    c = min(c, static_cast<uint32_t>(cap));
+    uint32_t tot;
+    const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
+    cs.tpos[threadIdx.x] = carry + pos;
+    cs.tcnt[threadIdx.x] = c;
+    __syncthreads();
+    for (int tb = warp; tb < nt; tb += NW * GATHER_TASKS) {
+      uint32_t cc[GATHER_TASKS], pp[GATHER_TASKS];
+      float xv[GATHER_TASKS];
+      int32_t xi[GATHER_TASKS];
+#pragma unroll
+      for (int u = 0; u < GATHER_TASKS; ++u) {
+        const int tt = tb + u * NW;
+        cc[u] = tt < nt ? cs.tcnt[tt] : 0u;
+        pp[u] = tt < nt ? cs.tpos[tt] : 0u;
+        if (static_cast<uint32_t>(lane) < cc[u]) {
+          const int64_t src = static_cast<int64_t>(t0 + tt) * cap + lane;
+          xv[u] = __ldcg(cand_val + src);
+          xi[u] = __ldcg(cand_idx + src);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GATHER_TASKS; ++u)
+        if (static_cast<uint32_t>(lane) < cc[u]) take(xv[u], xi[u], pp[u] + lane);
+#pragma unroll 1
+      for (int u = 0; u < GATHER_TASKS; ++u) {  // lists longer than a warp (rare)
+        const int64_t row = static_cast<int64_t>(t0 + tb + u * NW) * cap;
+        for (uint32_t e = 32u + lane; e < cc[u]; e += 32u) take(__ldcg(cand_val + row + e), __ldcg(cand_idx + row + e), pp[u] + e);
+      }
+    }
+    carry += tot;
+    __syncthreads();  // tpos / tcnt reuse
+  }
+  dx = __reduce_or_sync(0xffffffffu, dx);
+  if (lane == 0 && dx) atomicOr(&cs.sm.diff_acc, dx);
+  my_gt = __reduce_add_sync(0xffffffffu, my_gt);
+  if (gtb && lane == 0 && my_gt) atomicAdd(gtb, my_gt);
+  return carry;
+}
+
 // Candidate path of one layer inside one CTA.  Returns 0 on success, or why the candidate set
 // cannot be proven to hold the top-k (FB_TOO_FEW / FB_OVERFLOW); the caller then runs a dense
 // exact path in the same CTA.  Candidates are gathered once into shared memory (value + index,
 // ascending index order) when they fit (2*m words <= smem_words), else into global scratch.
+// The threshold: K1's histogram locates the bin of the k-th largest candidate and the gather lists
+// that bin's keys (a handful), so one count among them resolves it exactly; a cut in the top
+// (open-ended) bin or a crowded bin (ties) takes the radix select over the gathered keys instead.
 constexpr int FB_TOO_FEW = 1, FB_OVERFLOW = 2;
 
 #ifdef LAGS_DBG_STAMPS
@@ -472,22 +654,35 @@ __device__ unsigned long long lags_dbg_cstamps[16];
   } while (0)
 #endif
 
+// The radix select over gathered candidates sv[0..m) (a cut in the open top bin, a crowded bin, or
+// k >= m): out of line, the histogram cut resolves the common case.
+__device__ LAGS_COLD void candidate_radix(const float* sv, uint32_t m, uint32_t k, uint32_t k2, uint32_t diff,
+                                          uint32_t key0, SelectSmem& cs, SelectThreshold<uint32_t>* th,
+                                          uint32_t* key2) {
+  auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
+  const uint32_t dk[2] = {diff, key0};
+  radix_select_dual(key_at, m, k, k2, cs, th, key2, true, dk, true);
+}
+
 __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState st, const int32_t* cand_cnt,
                                 const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap,
                                 int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
                                 int32_t* count_out, FastState* state, uint32_t* dyn, int smem_words, SelectSmem& cs,
-                                float* vupd) {
+                                float* vupd, const uint32_t* hl) {
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
   uint32_t local = 0, over = 0;
   LAGS_CSTAMP(0);
+  if (hl) stage_hist(hl, cs);  // in flight together with the counts
+  const bool cache = tr.y - tr.x <= SEL_NT;  // the counts stay in shared memory for the gather
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
     local += min(c, static_cast<uint32_t>(cap));
+    if (cache) cs.tcache[t - tr.x] = c;
   }
   LAGS_CSTAMP(1);
-  const uint32_t m = block_sum(local, sm);
+  const uint32_t m = block_sum(local, sm);  // (its barriers also publish the staged histogram)
   if (__syncthreads_or(over)) return FB_OVERFLOW;
   LAGS_CSTAMP(2);
   if (m < k && st.thr > 1u) return FB_TOO_FEW;
@@ -502,70 +697,33 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
     float* sv = in_smem ? reinterpret_cast<float*>(dyn) : gval + gbase;
     int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + m : gidx + gbase;
-    // gather: positions by a block scan over task counts, then one thread per entry (the owning
-    // task is found by binary search over the positions), every load independent; the keys'
-    // common prefix (OR of key ^ key0, key0 = the candidate threshold) is accumulated on the way
-    uint32_t carry = 0;
-    const uint32_t key0 = st.thr;
-    if (threadIdx.x == 0) sm.diff_acc = 0u;
-    for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
-      const int nt = min(SEL_NT, tr.y - t0);
-      const uint32_t c = threadIdx.x < nt ? static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)) : 0u;
-      uint32_t tot;
-      const uint32_t pos = block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
-      cs.tpos[threadIdx.x] = pos;
-      __syncthreads();
-      // batches of GATHER_ILP entries per thread: all source addresses first, then all loads in
-      // flight together, then the stores (the destination may alias global scratch)
-      uint32_t dx = 0u;
-      for (uint32_t e0 = 0; e0 < tot; e0 += SEL_NT * GATHER_ILP) {
-        int64_t src[GATHER_ILP];
-#pragma unroll
-        for (int u = 0; u < GATHER_ILP; ++u) {
-          const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
-          src[u] = -1;
-          if (e < tot) {
-            int lo = 0, hi = nt - 1;  // last task whose start position <= e
-            while (lo < hi) {
-              const int mid = (lo + hi + 1) >> 1;
-              if (cs.tpos[mid] <= e) lo = mid;
-              else hi = mid - 1;
-            }
-            src[u] = static_cast<int64_t>(t0 + lo) * cap + (e - cs.tpos[lo]);
-          }
-        }
-        float xv[GATHER_ILP];
-        int32_t xi[GATHER_ILP];
-#pragma unroll
-        for (int u = 0; u < GATHER_ILP; ++u) {
-          if (src[u] >= 0) {
-            xv[u] = __ldcg(cand_val + src[u]);
-            xi[u] = __ldcg(cand_idx + src[u]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < GATHER_ILP; ++u) {
-          if (src[u] >= 0) {
-            const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
-            sv[carry + e] = xv[u];
-            si[carry + e] = xi[u];
-            if (vupd) asm volatile("prefetch.global.L2 [%0];" ::"l"(vupd + L.offset + xi[u]));  // P = 1 weight
-            dx |= Key<float>::of(xv[u]) ^ key0;
-          }
-        }
-      }
-      dx = __reduce_or_sync(0xffffffffu, dx);
-      if ((threadIdx.x & 31) == 0 && dx) atomicOr(&sm.diff_acc, dx);
-      carry += tot;
-      __syncthreads();
+    const uint32_t base = st.thr >> HIST_SHIFT;
+    // the histogram cut (uniform): usable when the k-th candidate is in a closed bin with few keys
+    HistCut hc{~0u, 0u, 0u, 0u};
+    bool cut = hl != nullptr && k < m;
+    if (cut) {
+      hc = hist_cut(cs, k, k2, m);
+      cut = hc.bin < HIST_BINS - 1u && hc.in_bin <= BIN_LIST_MAX;
     }
-    auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
-    SelectThreshold<uint32_t> th;
-    uint32_t key2;
+    if (threadIdx.x == 0) {
+      sm.list_n = 0u;
+      sm.gtb = 0u;  // entries above the cut bin, counted by the gather
+    }
+    __syncthreads();
+    uint32_t* list = cs.hist2;
+    gather_candidates(tr.x, tr.y, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
+                      &sm.gtb, list, &sm.list_n, vupd ? vupd + L.offset : nullptr, cache ? cs.tcache : nullptr, tr.x);
+    __syncthreads();  // the gather's counts (gtb, list_n) are complete: one uniform decision below
     const long long c1 = clock64();
     LAGS_CSTAMP(3);
-    const uint32_t dk[2] = {sm.diff_acc, key0};
-    radix_select_dual(key_at, m, k, k2, cs, &th, &key2, true, dk, true);
+    SelectThreshold<uint32_t> th;
+    uint32_t key2 = 0u;
+    if (cut && sm.list_n == hc.in_bin && sm.gtb == hc.above) {
+      th = resolve_cut(list, hc.in_bin, k - hc.above, hc.above, cs);
+      key2 = (base + hc.bin2) << HIST_SHIFT;  // lower edge of the k2-th candidate's bin
+    } else {
+      candidate_radix(sv, m, k, k2, sm.diff_acc, st.thr, cs, &th, &key2);
+    }
     const long long c2 = clock64();
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
       *x = sv[i];
@@ -580,7 +738,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
         oidx[pos] = static_cast<int32_t>(ix);
         oval[pos] = x;
-        data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+        data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
         vl[ix] = single_rank_update(w, x);
       };
       cnt = ordered_compact_pf<uint32_t, float>(m, th, load, emit, sm, 0u, 0u,
@@ -589,7 +747,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
         oidx[pos] = static_cast<int32_t>(ix);
         oval[pos] = x;
-        data[ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+        data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       };
       cnt = ordered_compact<uint32_t, float>(m, th, load, emit, sm);
     }
@@ -615,7 +773,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
 // Dense exact path of one big layer inside one CTA (first call of a layer, failed prediction or
 // forced exact mode): radix select of the k-th key and, in the same passes, of the next
 // prediction rank over r, then an ordered compaction that zeroes the selected residuals.
-__device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
+__device__ LAGS_COLD void dense_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
                                       float* val_out, int32_t* count_out, FastState* state, bool force_exact,
                                       int why, SelectSmem& cs, float* vupd) {
   float* data = r + L.offset;
@@ -642,7 +800,7 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
   auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
     oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
-    data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    data[i] = sent_residual(x);  // acc - acc (R: training.py:252)
   };
   const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
   if (vl) apply_single_rank_updates(vl, oidx, oval, cnt);
@@ -661,7 +819,7 @@ __device__ void dense_fallback_select(int j, const lags_layer_t& L, FastState st
 // Dense exact path of a small layer (d <= SMALL_LAYER): staged once in shared memory, so the
 // radix passes and the compaction read shared memory; the same dual-rank select predicts the
 // next candidate threshold (small layers then take the candidate path like the big ones).
-__device__ void small_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
+__device__ LAGS_COLD void small_fallback_select(int j, const lags_layer_t& L, FastState st, float* r, int32_t* idx_out,
                                       float* val_out, int32_t* count_out, FastState* state, bool force_exact, int why,
                                       SelectSmem& cs, float* vupd, float* sv, bool predict) {
   float* data = r + L.offset;
@@ -698,7 +856,7 @@ __device__ void small_fallback_select(int j, const lags_layer_t& L, FastState st
   auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
     oidx[pos] = static_cast<int32_t>(i);
     oval[pos] = x;
-    data[i] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    data[i] = sent_residual(x);  // acc - acc (R: training.py:252)
   };
   const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
   if (vupd) apply_single_rank_updates(vupd + L.offset, oidx, oval, cnt);
@@ -839,7 +997,7 @@ __device__ void warp_topk_layer(int j, const lags_layer_t& L, FastState* state, 
   if (static_cast<uint32_t>(lane) < cnt) {
     idx_out[L.slot + pos] = my_ix;
     val_out[L.slot + pos] = my_val;
-    data[my_ix] = 0.0f;  // acc - acc == +0.0 (R: training.py:252)
+    data[my_ix] = sent_residual(my_val);  // acc - acc (R: training.py:252)
     if (vupd) vupd[L.offset + my_ix] = single_rank_update(vupd[L.offset + my_ix], my_val);
   }
   if (lane == 0) {
@@ -865,17 +1023,19 @@ __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, con
                              FastState* state, const int32_t* cand_cnt, const int32_t* cand_idx, const float* cand_val,
                              int cap, int32_t* gidx, float* gval, float* r, int32_t* idx_out, float* val_out,
                              int32_t* count_out, uint32_t* skeys, int smem_keys, int force_exact, SelectSmem& cs,
-                             float* vupd, uint32_t t_launch) {
+                             float* vupd, uint32_t t_launch, uint32_t* hist) {
   const uint32_t t_start = globaltimer_lo();
   LAGS_CSTAMP(8);
   const lags_layer_t L = layers[j];
   const FastState st = state[j];
   const long long t_begin = clock64();
   const bool tiny = L.dim <= TINY_LAYER;
+  // K1 counted this layer's candidates into its histogram iff it had a threshold
+  uint32_t* hl = hist && st.thr != 0u ? hist + static_cast<int64_t>(j) * HIST_BINS : nullptr;
   const int why = (force_exact || st.thr == 0u || tiny)
                       ? FB_TOO_FEW
                       : candidate_select(j, L, layer_tasks[j], st, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r,
-                                         idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd);
+                                         idx_out, val_out, count_out, state, skeys, smem_keys, cs, vupd, hl);
   // the candidate set cannot be proven to hold the top-k: dense exact path, same CTA (small
   // layers staged in shared memory; SMALL_LAYER <= the staging capacity)
   if (why && L.dim <= SMALL_LAYER)
@@ -885,6 +1045,7 @@ __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, con
     dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
   const uint32_t path = why ? (L.dim <= SMALL_LAYER ? 0u : 2u) : 1u;
   __syncthreads();
+  if (hl) zero_hist(hl, 0, HIST_BINS);  // every path: the staged copy has been consumed
   if (threadIdx.x == 0) {
     state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
     state[j].path = path;

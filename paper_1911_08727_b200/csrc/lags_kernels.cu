@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <atomic>
 #include <string>
 #include <vector>
@@ -286,6 +288,7 @@ struct lags_bucket {
   int2* tiles_dec = nullptr;  // decode tiles: (layer, chunk of DEC_NT slots)
   int dec_tiles = 0;
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
+  uint32_t* hist = nullptr;       // fp32: per-layer candidate-key histograms (K1 -> select_kernel)
   // selection groups of an fp32 bucket (plan_groups): 0 persistent role, 1 cluster role, 2 warp
   // role; each group's tasks and `order` entries are contiguous
   struct Group {
@@ -367,7 +370,7 @@ struct Plan {
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
          o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
-         bytes = 0;
+         o_hist = 0, bytes = 0;
   int32_t ntiles = 0;
 };
 
@@ -418,6 +421,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_tiles = take(sizeof(int2) * static_cast<size_t>(p->ntiles));
   const bool f32 = dtype == LAGS_F32;
   p->o_ctr = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (SelectCounters)
+  p->o_hist = take(f32 ? sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(L) : 0);
   p->bytes = o;
   return LAGS_OK;
 }
@@ -435,6 +439,7 @@ std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+bool aligned_to(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; }
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
 // previous kernel on the stream drains; it calls griddep_wait() before touching its inputs.
@@ -524,6 +529,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->tiles_dec = reinterpret_cast<int2*>(base + p.o_tiles);
   b->dec_tiles = p.ntiles;
   b->sel_ctr.work = reinterpret_cast<uint32_t*>(base + p.o_ctr);
+  b->hist = dtype == LAGS_F32 ? reinterpret_cast<uint32_t*>(base + p.o_hist) : nullptr;
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -589,6 +595,8 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
       (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
+      (dtype != LAGS_F32 ||
+       cudaMemsetAsync(b->hist, 0, sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(nlayers), s) == cudaSuccess) &&
       cudaStreamSynchronize(s) == cudaSuccess;
   if (!ok) {
     delete b;
@@ -634,8 +642,12 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
   if (!b || (!g && !table) || !r || !msg || !status)
     return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
   if (table) g = nullptr;  // the per-layer table replaces the flat gradient
-  if ((g && !aligned16(g)) || !aligned16(r) || !aligned16(msg))
-    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: buffers must be 16-byte aligned");
+  // g / r / v need only their element alignment (the streaming pass peels a scalar head up to
+  // 16 bytes); the message is the library's own layout and stays 16-byte aligned
+  const size_t ea = b->dtype == LAGS_F64 ? 8 : 4;
+  if ((g && !aligned_to(g, ea)) || !aligned_to(r, ea) || (v_update && !aligned_to(v_update, ea)) || !aligned16(msg))
+    return fail(LAGS_ERR_INVALID_ARG,
+                "lags_bucket_compress: g / r / v must be element-aligned and msg 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* m = static_cast<char*>(msg);
   int32_t* cnt = reinterpret_cast<int32_t*>(m + b->off_cnt);
@@ -658,10 +670,10 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       if (zg)
         return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                           G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
-                          b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work);
+                          b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work, b->hist);
       return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
                         G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
-                        b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work);
+                        b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work, b->hist);
     };
     cudaError_t e = cudaSuccess;
     lags_bucket::Group all = b->grp[0];  // K1 streams every task (group 0's then group 1's)
@@ -686,7 +698,8 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       e = launch_pdl_cluster(select_kernel, dim3(grid), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s, cl,
                              b->layers, b->layer_tasks, b->order + G1.order_base, ncl, b->order + G2.order_base,
                              G2.nlayers, b->order + G0.order_base, G0.nlayers, b->state, b->cand_cnt, b->cand_idx,
-                             b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->sel_ctr, vu);
+                             b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->sel_ctr, vu,
+                             b->hist);
     }
     const int launches = 2;
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));

@@ -20,14 +20,10 @@ constexpr int SEL_MINB = LAGS_SEL_MINB;  // selection CTAs resident per SM (laun
 #ifndef LAGS_SEL_VEC
 #define LAGS_SEL_VEC 4
 #endif
-#ifndef LAGS_GATHER_ILP
-#define LAGS_GATHER_ILP 2
-#endif
 #ifndef LAGS_UPDATE_B
 #define LAGS_UPDATE_B 4
 #endif
 constexpr int SEL_VEC = LAGS_SEL_VEC;        // consecutive elements per thread per compaction chunk
-constexpr int GATHER_ILP = LAGS_GATHER_ILP;  // candidate loads in flight per thread in the gathers
 constexpr int UPDATE_B = LAGS_UPDATE_B;      // weight loads in flight per thread in the P = 1 update
 
 // Select (key & pmask) > prefix, plus the first `need_eq` (in scan order) with
@@ -43,13 +39,14 @@ struct SelectThreshold {
 template <int RB>
 struct RadixSmem {
   static constexpr int NB = 1 << RB;
-  uint32_t hist[NB];
+  alignas(16) uint32_t hist[NB];
   uint32_t warp_tot[33];
   uint32_t above, bin_count;
   int found;
   uint32_t found2[2], above2[2], count2[2];  // find_bin2
   uint32_t list_n, list_key, list_gt;         // bin-list finish of radix_select_dual
   uint32_t diff_acc;                          // key ^ key0 OR-accumulated by the candidate gathers
+  uint32_t gtb;                               // candidates above the histogram cut (gathers)
   uint32_t dbg;                               // -DLAGS_DBG_SELECT: radix_select_dual's shape
 };
 
@@ -365,7 +362,7 @@ __device__ uint32_t exact_topk_dense(T* data, int64_t d, uint32_t k, int32_t* id
   auto emit = [=](uint32_t pos, int64_t i, int64_t ix, T x) {
     idx_out[pos] = static_cast<int32_t>(ix);
     val_out[pos] = static_cast<TOut>(x);
-    if (zero_selected) data[i] = T(0);  // acc - acc == +0.0 (R: training.py:252)
+    if (zero_selected) data[i] = sent_residual(x);  // acc - acc (R: training.py:252)
   };
   return ordered_compact<K, T>(d, th, load, emit, sm);
 }

@@ -32,6 +32,7 @@ from .errors import DivergenceError
 from .sparsify import CompressionPolicy
 
 CHUNK_HEADER_BYTES = 8  # R: sparsify.py:23 (accounting header of a chunk)
+MAX_WORLD = 32  # ranks one decode can combine (lags_bucket_create: max_world <= 32)
 INDEX_BYTES = 4
 
 
@@ -119,6 +120,9 @@ class LagsSGD(torch.optim.Optimizer):
         self.group = process_group
         self.world = dist.get_world_size(process_group) if dist.is_available() and dist.is_initialized() else 1
         self.rank = dist.get_rank(process_group) if self.world > 1 else 0
+        if self.world > MAX_WORLD:
+            raise ValueError(f"LagsSGD exchanges among at most {MAX_WORLD} ranks (the decode's rank bitmask is "
+                             f"32 bits), got {self.world}")
         self.check_every = max(1, int(check_every))
         self.mu = float(momentum)
         # exchange=False replaces the all-gather by a local no-op (decode of the own message only):
@@ -146,29 +150,22 @@ class LagsSGD(torch.optim.Optimizer):
             grads = "tensors" if hasattr(probe, "set_grad_table") and self.device.type == "cuda" else "flat"
             del probe
         self.grads_mode = grads
-        # flat per-rank buffers with the reference's layer layout; params (and flat grads) are views
-        n = sum(self.dims)
-        self.offsets = [0]
-        for d in self.dims[:-1]:
-            self.offsets.append(self.offsets[-1] + d)
-        with torch.no_grad():
-            self.flat_param = torch.empty(n, dtype=torch.float32, device=self.device)
-            self.flat_grad = torch.zeros(n, dtype=torch.float32, device=self.device) if grads == "flat" else None
-            self.residual = torch.zeros(n, dtype=torch.float32, device=self.device)
-            self.momentum_buf = torch.zeros(n, dtype=torch.float32, device=self.device) if self.mu else None
-            for p, off, d in zip(params, self.offsets, self.dims):
-                if p.dtype != torch.float32:
-                    raise TypeError("LagsSGD keeps fp32 parameters")
-                self.flat_param[off:off + d].copy_(p.detach().reshape(-1))
-                p.data = self.flat_param[off:off + d].view_as(p)
-                p.grad = self.flat_grad[off:off + d].view_as(p) if grads == "flat" else None
-        if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
-            dist.broadcast(self.flat_param, src=0, group=process_group)
+        # flat per-rank buffers with the reference's layer layout (R: layered.py:46-107) -- layers
+        # back to back inside a fusion bucket, every bucket starting 16-byte aligned (so the
+        # streaming pass takes its vector path); params (and flat grads) are views
+        for p in params:
+            if p.dtype != torch.float32:
+                raise TypeError("LagsSGD keeps fp32 parameters")
         self.engine_factory = engine_factory
         self.bucket_cap_bytes = int(bucket_cap_bytes)
+        self.flat_param = self.flat_grad = self.residual = self.momentum_buf = None
+        self.offsets = None
+        self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
+        self._relayout(plan_buckets(self.dims, self.ks, self.bucket_cap_bytes))
+        if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
+            dist.broadcast(self.flat_param, group=process_group, group_src=0)
         self._build_buckets()
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=self.device.type == "cuda")
         self._status_event = None
         self._status_step = 0
@@ -180,11 +177,81 @@ class LagsSGD(torch.optim.Optimizer):
         self._delta_step = 0
         self._hook_events = None  # optional per-layer CUDA events at gradient readiness
 
+    @staticmethod
+    def _bucket_offsets(dims, ranges):
+        """Layer offsets with every bucket's first layer at a multiple of 4 elements."""
+        offsets, pos = [0] * len(dims), 0
+        for lo, hi in sorted(ranges):
+            pos = (pos + 3) // 4 * 4
+            for l in range(lo, hi + 1):
+                offsets[l] = pos
+                pos += dims[l]
+        return offsets, pos
+
+    @torch.no_grad()
+    def _relayout(self, ranges) -> None:
+        """Place the flat buffers for these bucket ranges, carrying params, residual and momentum
+        (and flat gradients) over layer by layer when the layout changes."""
+        offsets, n = self._bucket_offsets(self.dims, ranges)
+        if offsets == self.offsets and self.flat_param is not None and self.flat_param.numel() == n:
+            return
+        old = self.offsets
+
+        def moved(buf, fill_params=False):
+            new = torch.zeros(n, dtype=torch.float32, device=self.device)
+            for l, d in enumerate(self.dims):
+                dst = new[offsets[l]:offsets[l] + d]
+                if buf is not None:
+                    dst.copy_(buf[old[l]:old[l] + d])
+                elif fill_params:
+                    dst.copy_(self.params[l].detach().reshape(-1))
+            return new
+
+        flat_mode = self.grads_mode == "flat"
+        self.flat_param = moved(self.flat_param, fill_params=True)
+        self.residual = moved(self.residual)
+        self.momentum_buf = moved(self.momentum_buf) if self.mu else None
+        self.flat_grad = moved(self.flat_grad) if flat_mode else None
+        self.offsets = offsets
+        for l, (p, d) in enumerate(zip(self.params, self.dims)):
+            off = offsets[l]
+            p.data = self.flat_param[off:off + d].view_as(p)
+            if flat_mode:
+                p.grad = self.flat_grad[off:off + d].view_as(p)
+            elif old is None:
+                p.grad = None
+
+    def _per_layer(self, buf) -> torch.Tensor:
+        """The flat buffer without inter-bucket padding (the reference's layer layout)."""
+        if self.side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        return torch.cat([buf[o:o + d] for o, d in zip(self.offsets, self.dims)])
+
+    @property
+    def ref_offsets(self) -> list[int]:
+        """Layer offsets of the reference's LayeredVector layout (prefix sums of dims)."""
+        out = [0]
+        for d in self.dims[:-1]:
+            out.append(out[-1] + d)
+        return out
+
+    def params_vector(self) -> torch.Tensor:
+        """The parameters as the reference's flat LayeredVector data (a copy, no padding)."""
+        return self._per_layer(self.flat_param)
+
+    def residual_vector(self) -> torch.Tensor:
+        """The error-feedback residual in the reference's layer layout (a copy, no padding)."""
+        return self._per_layer(self.residual)
+
     def _build_buckets(self) -> None:
         """(Re)plan fusion buckets for the current ks; residual and momentum state are kept."""
+        ranges = plan_buckets(self.dims, self.ks, self.bucket_cap_bytes)
+        if self.side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._relayout(ranges)
         self.buckets: list[_BucketRT] = []
         self._bucket_of_param = {}
-        for lo, hi in plan_buckets(self.dims, self.ks, self.bucket_cap_bytes):
+        for lo, hi in ranges:
             eng = self.engine_factory(self.dims[lo:hi + 1], self.ks[lo:hi + 1], self.world, self.device)
             msg_local = eng.new_messages(1)
             msg_all = eng.new_messages(self.world) if self.world > 1 else None
@@ -227,7 +294,7 @@ class LagsSGD(torch.optim.Optimizer):
         ratios = torch.tensor([pol.ratio_for(i + 1) for i in range(len(self.params))], dtype=torch.float64,
                               device=self.device)
         if self.world > 1:
-            dist.broadcast(ratios, src=0, group=self.group)
+            dist.broadcast(ratios, group=self.group, group_src=0)
         pol = CompressionPolicy({i + 1: float(c) for i, c in enumerate(ratios.tolist())}, ratio_cap)
         self.set_policy(pol)
         return pol
@@ -269,6 +336,11 @@ class LagsSGD(torch.optim.Optimizer):
         b = self._bucket_of_param.get(id(p))
         if b is None:
             return
+        if self._pending[b] <= 0:
+            # the bucket already launched this step: its gradients were consumed (and cleared) by
+            # the compress, so a second backward before step() would be silently lost
+            raise RuntimeError("LagsSGD consumes gradients during backward: call step() after every backward() "
+                               "(gradient accumulation over several backward passes is not supported)")
         if self._hook_events is not None:
             self._hook_events[self._layer_of_param[id(p)]].record(torch.cuda.current_stream(self.device))
         self._pending[b] -= 1
@@ -433,19 +505,38 @@ class LagsSGD(torch.optim.Optimizer):
         return None
 
     def state_dict(self):
+        """Optimizer state plus the error-feedback residual and momentum in the reference's layer
+        layout (R: layered.py:46-107, no padding) and the per-layer ratios: a true resume (the
+        reference saves only final parameters, R: experiment.py:501-502)."""
+        if self.side is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self.side)
         sd = super().state_dict()
-        sd["lags"] = {"residual": self.residual.clone(), "momentum": None if self.momentum_buf is None
-                      else self.momentum_buf.clone(), "steps": self._steps, "ks": list(self.ks)}
+        sd["lags"] = {"residual": self._per_layer(self.residual),
+                      "momentum": None if self.momentum_buf is None else self._per_layer(self.momentum_buf),
+                      "steps": self._steps, "ks": list(self.ks), "ratios": list(self.ratios)}
         return sd
 
     def load_state_dict(self, state_dict):
         lags = state_dict.pop("lags", None)
         super().load_state_dict(state_dict)
         if lags is not None:
-            self.residual.copy_(lags["residual"])
+            if "ratios" in lags and list(lags["ratios"]) != list(self.ratios):
+                cap = max(self.policy.ratio_cap, max(lags["ratios"]))
+                self.set_policy(CompressionPolicy({i + 1: float(c) for i, c in enumerate(lags["ratios"])}, cap))
+            self._load_per_layer(self.residual, lags["residual"])
             if self.momentum_buf is not None and lags["momentum"] is not None:
-                self.momentum_buf.copy_(lags["momentum"])
+                self._load_per_layer(self.momentum_buf, lags["momentum"])
             self._steps = int(lags["steps"])
+
+    @torch.no_grad()
+    def _load_per_layer(self, buf, src) -> None:
+        src = src.to(buf.device, buf.dtype).reshape(-1)
+        if src.numel() != sum(self.dims):
+            raise ValueError("saved LagsSGD state does not match the parameters")
+        pos = 0
+        for o, d in zip(self.offsets, self.dims):
+            buf[o:o + d].copy_(src[pos:pos + d])
+            pos += d
 
     def remove_hooks(self):
         for h in self._hooks:

@@ -47,3 +47,24 @@ def step_cases():
 @pytest.fixture(scope="session")
 def config1():
     return load_npz("config1_trajectory.npz")
+
+
+def same_bits_nan(a, b) -> bool:
+    """Bit equality except that any NaN matches any NaN at the same position (the NaN payload of
+    inf - inf is platform-defined: x86 numpy yields 0xffc00000, the GPU 0x7fffffff)."""
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    if a.dtype != b.dtype or a.shape != b.shape:
+        return False
+    na, nb = np.isnan(a), np.isnan(b)
+    return bool(np.array_equal(na, nb)) and a[~na].tobytes() == b[~nb].tobytes()
+
+
+@pytest.fixture(scope="session")
+def nonfinite_cases():
+    """top_k and lags_step with NaN / +-inf inside the accumulated vector, made by the reference."""
+    z = load_npz("nonfinite_cases.npz")
+    topk = [(z[f"tx{i}"], int(z[f"tk{i}"]), z[f"tidx{i}"], z[f"tval{i}"]) for i in range(int(z["n_topk"]))]
+    steps = [dict(dims=[int(d) for d in z[f"dims{i}"]], counts=[int(c) for c in z[f"counts{i}"]],
+                  alpha=float(z[f"alpha{i}"]), v=z[f"v{i}"], g=z[f"g{i}"], r_in=z[f"r_in{i}"],
+                  r_out=z[f"r_out{i}"], v_out=z[f"v_out{i}"]) for i in range(int(z["n_step"]))]
+    return topk, steps

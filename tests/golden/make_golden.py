@@ -16,6 +16,7 @@ Fixtures:
   perf_cases.json        select_ratios / comm_time / schedules     R: perf.py:59-260
   wire_cases.json        encode_chunk / fusion_flush               R: sparsify.py:209-310
   delta_cases.npz        topk_aggregation_ratio (delta^(l))        R: analysis.py:24-56
+  nonfinite_cases.npz    top_k / lags_step with NaN and +-inf      R: sparsify.py:84-90, training.py:250-254
 """
 
 from __future__ import annotations
@@ -306,6 +307,76 @@ def make_delta():
     out["n"] = np.array(n)
     np.savez_compressed(os.path.join(HERE, "delta_cases.npz"), **out)
     return n
+
+
+def make_nonfinite():
+    """NaN / +-inf inside the accumulated vector (gradients stay finite, R: training.py:174).
+
+    top_k ranks NaN after every number (stable argsort of -|x|) and then drops it with `mag > 0`;
+    +-inf is the largest magnitude.  In lags_step a NaN reaches acc through the residual, and an
+    overflowing r + alpha * g makes acc = +-inf, whose residual becomes inf - inf = NaN
+    (R: sparsify.py:84-90, training.py:250-254)."""
+    rng = np.random.default_rng(11)
+    out = {}
+    topk = [
+        (np.array([np.nan, 1.0, 2.0, -3.0]), 2),
+        (np.array([np.nan, np.nan, 1.0]), 3),
+        (np.array([np.inf, -np.inf, 1.0, np.nan]), 2),
+        (np.array([np.inf, -np.inf, 1.0, np.nan]), 4),
+        (np.array([np.nan, 0.0, -0.0, np.nan]), 2),
+        (np.array([np.nan, np.nan, np.nan]), 1),
+    ]
+    for dtype in (np.float64, np.float32):
+        for d, k in ((3000, 30), (12_000, 120), (20_000, 20)):
+            x = _dist(rng, "heavy", d, dtype)
+            x[rng.integers(0, d, size=d // 100)] = np.nan
+            x[rng.integers(0, d, size=3)] = np.inf
+            x[rng.integers(0, d, size=3)] = -np.inf
+            topk.append((x, k))
+    out["n_topk"] = np.array(len(topk))
+    for i, (x, k) in enumerate(topk):
+        ch = top_k(x, k)
+        out[f"tx{i}"] = x
+        out[f"tk{i}"] = np.array(k)
+        out[f"tidx{i}"] = ch.indices
+        out[f"tval{i}"] = ch.values
+    steps = []
+    for dtype, big in ((np.float32, np.float32(3.0e38)), (np.float64, np.float64(1.5e308))):
+        for P in (1, 3):
+            dims = [3000, 40, 1500]
+            n = sum(dims)
+            counts = [30, 4, 150]
+            g = [_dist(rng, "normal", n, dtype) for _ in range(P)]
+            r = [(0.01 * _dist(rng, "normal", n, dtype)).astype(dtype) for _ in range(P)]
+            for p in range(P):
+                r[p][rng.integers(0, n, size=40)] = np.nan      # NaN residual entries
+                hit = rng.integers(0, n, size=6)
+                r[p][hit] = big                                   # r + alpha * g overflows to +inf
+                g[p][hit] = np.abs(g[p][hit]) + dtype(1.0)
+                neg = rng.integers(0, n, size=6)
+                r[p][neg] = -big
+                g[p][neg] = -(np.abs(g[p][neg]) + dtype(1.0))
+            steps.append(dict(dims=dims, P=P, dtype=dtype, alpha=float(big) / 2 if dtype == np.float32 else 1e308,
+                              counts=counts, v=_dist(rng, "normal", n, dtype), g=g, r=r))
+    out["n_step"] = np.array(len(steps))
+    with np.errstate(all="ignore"):
+        for i, c in enumerate(steps):
+            shape = [LayerShape(j + 1, d) for j, d in enumerate(c["dims"])]
+            v = LayeredVector(shape, np.array(c["v"], dtype=c["dtype"]))
+            grads = [LayeredVector(shape, np.array(x, dtype=c["dtype"])) for x in c["g"]]
+            res = [LayeredVector(shape, np.array(x, dtype=c["dtype"]).copy()) for x in c["r"]]
+            counts = {j + 1: k for j, k in enumerate(c["counts"])}
+            new_v = ref_training.lags_step(v, grads, c["alpha"], counts, res)
+            out[f"dims{i}"] = np.array(c["dims"], dtype=np.int64)
+            out[f"counts{i}"] = np.array(c["counts"], dtype=np.int64)
+            out[f"alpha{i}"] = np.array(float(c["alpha"]))
+            out[f"v{i}"] = v.data
+            out[f"g{i}"] = np.stack([x.data for x in grads])
+            out[f"r_in{i}"] = np.stack([np.array(x, dtype=c["dtype"]) for x in c["r"]])
+            out[f"r_out{i}"] = np.stack([x.data for x in res])
+            out[f"v_out{i}"] = new_v.data
+    np.savez_compressed(os.path.join(HERE, "nonfinite_cases.npz"), **out)
+    return len(topk), len(steps)
 
 
 if __name__ == "__main__":

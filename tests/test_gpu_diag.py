@@ -93,9 +93,9 @@ def test_optimizer_logs_delta_single_rank():
         opt.step()
         g = torch.cat([captured[id(p)].reshape(-1) for p in opt.params]).cpu().numpy()
         acc = res + np.float32(0.05) * g
-        res = opt.residual.detach().cpu().numpy().copy()
+        res = opt.residual_vector().cpu().numpy().copy()
         if (t + 1) % 2 == 0:
             step, got = opt.last_delta()
             assert step == t + 1
-            for o, d, k, dv in zip(opt.offsets, opt.dims, opt.ks, got):
+            for o, d, k, dv in zip(opt.ref_offsets, opt.dims, opt.ks, got):
                 assert close(dv, orc.topk_aggregation_ratio([acc[o:o + d]], k))

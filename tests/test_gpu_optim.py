@@ -43,7 +43,7 @@ def test_lagssgd_matches_oracle(L):
         p.register_post_accumulate_grad_hook(grab)
     opt = LagsSGD(model.parameters(), lr=0.05, rho=0.01, bucket_cap_bytes=4096)
     assert len(opt.buckets) > 1
-    v = opt.flat_param.cpu().numpy().copy()
+    v = opt.params_vector().cpu().numpy().copy()
     res = [np.zeros_like(v)]
     for t in range(8):
         x = torch.randn(32, 256, device="cuda")
@@ -52,8 +52,8 @@ def test_lagssgd_matches_oracle(L):
         opt.step()
         g = torch.cat([captured[id(p)].reshape(-1) for p in opt.params]).cpu().numpy()
         v = orc.lags_step(v, [g], 0.05, opt.dims, opt.ks, res)
-        assert opt.flat_param.cpu().numpy().tobytes() == v.tobytes(), t
-        assert opt.residual.cpu().numpy().tobytes() == res[0].tobytes(), t
+        assert opt.params_vector().cpu().numpy().tobytes() == v.tobytes(), t
+        assert opt.residual_vector().cpu().numpy().tobytes() == res[0].tobytes(), t
         if opt.flat_grad is not None:
             assert not torch.any(opt.flat_grad), "compress clears the gradients"
         else:
@@ -114,6 +114,6 @@ def test_grad_modes_bit_identical(L, model_cls):
             torch.nn.functional.cross_entropy(model(x), y).backward()
             opt.step()
         torch.cuda.synchronize()
-        outs[mode] = (opt.flat_param.cpu().numpy().tobytes(), opt.residual.cpu().numpy().tobytes())
+        outs[mode] = (opt.params_vector().cpu().numpy().tobytes(), opt.residual_vector().cpu().numpy().tobytes())
         opt.remove_hooks()
     assert outs["flat"] == outs["tensors"]

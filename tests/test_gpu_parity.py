@@ -9,6 +9,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+from conftest import same_bits_nan  # noqa: E402
 from oracle import lagsgd_oracle as orc  # noqa: E402
 
 
@@ -96,6 +97,27 @@ def test_lags_step_golden(L, step_cases):
         assert _same_bits(out.data, c["v_out"]), dims
         for a, b in zip(res, c["r_out"]):
             assert _same_bits(a.data, b)
+
+
+def test_nonfinite_golden(L, nonfinite_cases):
+    """NaN / +-inf in the accumulated vector, against the reference's own outputs: NaN is never
+    selected, +-inf is the largest magnitude, and a selected +-inf leaves inf - inf = NaN in the
+    residual (R: sparsify.py:84-90, training.py:252).  Every call runs twice so the second takes
+    the predicted-threshold candidate path."""
+    topk, steps = nonfinite_cases
+    for x, k, idx, val in topk:
+        ch = L.top_k(x, k)
+        np.testing.assert_array_equal(ch.indices, idx)
+        assert same_bits_nan(ch.values, val)
+    for c in steps:
+        dims = c["dims"]
+        counts = {i + 1: k for i, k in enumerate(c["counts"])}
+        for _ in range(2):
+            res = [_lv(L, dims, r.copy()) for r in c["r_in"]]
+            out = L.lags_step(_lv(L, dims, c["v"]), [_lv(L, dims, g) for g in c["g"]], c["alpha"], counts, res)
+            assert same_bits_nan(out.data, c["v_out"]), dims
+            for a, b in zip(res, c["r_out"]):
+                assert same_bits_nan(a.data, b)
 
 
 def test_config1_trajectory_bitexact(L, config1):
@@ -265,7 +287,7 @@ def test_fast_path_ties_equal_exact_path(L):
         assert torch.equal(m_f, m_e), f"messages differ at iteration {it}"
         assert torch.equal(r_f.view(torch.int32), r_e.view(torch.int32)), f"residuals differ at {it}"
     s = fast.stats()
-    assert int((s[:, 5] == 3).sum()) >= 1, s  # a cluster layer took the cluster path
+    assert int(((s[:, 5] == 3) | (s[:, 5] == 4)).sum()) >= 1, s  # a cluster layer took the cluster path
     assert int(st.item()) == 0
 
 

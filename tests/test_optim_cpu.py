@@ -62,8 +62,9 @@ class Tiny(torch.nn.Module):
 def consumed_grad(opt):
     """Flat gradient as the optimizer's compress calls saw it (before the fused zero_grad)."""
     g = np.zeros(sum(opt.dims), dtype=np.float32)
+    ref = opt.ref_offsets
     for b in opt.buckets:
-        g[b.offset:b.offset + b.numel] = b.engine.last_g
+        g[ref[b.lo]:ref[b.lo] + b.numel] = b.engine.last_g
     return g
 
 
@@ -72,7 +73,7 @@ def _run_single(steps, rho, cap, mu=0.0):
     model = Tiny()
     opt = LagsSGD(model.parameters(), lr=0.1, rho=rho, momentum=mu, bucket_cap_bytes=cap,
                   engine_factory=stub_factory)
-    v = opt.flat_param.detach().numpy().copy()
+    v = opt.params_vector().detach().numpy().copy()
     dims = opt.dims
     ks = opt.ks
     res = [np.zeros_like(v)]
@@ -85,7 +86,7 @@ def _run_single(steps, rho, cap, mu=0.0):
         g = consumed_grad(opt)
         if mu == 0.0:
             v = orc.lags_step(v, [g], 0.1, dims, ks, res)
-            assert opt.flat_param.numpy().tobytes() == v.tobytes(), t
+            assert opt.params_vector().numpy().tobytes() == v.tobytes(), t
         assert not np.any(opt.flat_grad.numpy()), "compress must clear the gradients"
     return opt
 
@@ -102,7 +103,7 @@ def test_single_rank_matches_oracle_and_hooks_launch_in_order():
 def test_momentum_runs_and_state_dict_resumes():
     opt = _run_single(3, rho=0.5, cap=1 << 20, mu=0.9)
     sd = opt.state_dict()
-    assert sd["lags"]["residual"].shape == opt.residual.shape
+    assert sd["lags"]["residual"].numel() == sum(opt.dims)  # the reference's layout, no padding
     r0 = opt.residual.clone()
     opt.residual.zero_()
     opt.load_state_dict(sd)
@@ -123,7 +124,7 @@ def _worker(rank, world, port, steps, out):
         model = Tiny()
         opt = LagsSGD(model.parameters(), lr=0.05, rho=0.2, bucket_cap_bytes=96, engine_factory=stub_factory,
                       delta_every=2)
-        v = opt.flat_param.detach().numpy().copy()
+        v = opt.params_vector().detach().numpy().copy()
         res = [np.zeros_like(v) for _ in range(world)]
         for t in range(steps):
             x = torch.randn(4, 12, generator=torch.Generator().manual_seed(10 * t + rank))
@@ -135,17 +136,17 @@ def _worker(rank, world, port, steps, out):
             dist.all_gather(gathered, g)
             accs = [res[p] + 0.05 * gathered[p].numpy() for p in range(world)]  # before lags_step mutates res
             v = orc.lags_step(v, [x.numpy() for x in gathered], 0.05, opt.dims, opt.ks, res)
-            if opt.flat_param.numpy().tobytes() != v.tobytes():
+            if opt.params_vector().numpy().tobytes() != v.tobytes():
                 out.put((rank, f"step {t}: params differ from the oracle"))
                 return
             if (t + 1) % 2 == 0:  # delta^(l) logged on this step (R: training.py:320-337)
                 step, got = opt.last_delta()
                 want = [orc.topk_aggregation_ratio([a[o:o + d] for a in accs], k)
-                        for o, d, k in zip(opt.offsets, opt.dims, opt.ks)]
+                        for o, d, k in zip(opt.ref_offsets, opt.dims, opt.ks)]
                 if step != t + 1 or got != want:
                     out.put((rank, f"step {t}: delta {got} != {want}"))
                     return
-        out.put((rank, opt.flat_param.numpy().tobytes()))
+        out.put((rank, opt.params_vector().numpy().tobytes()))
     finally:
         dist.destroy_process_group()
 

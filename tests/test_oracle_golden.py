@@ -11,7 +11,7 @@ import itertools
 import numpy as np
 import pytest
 
-from conftest import load_json
+from conftest import load_json, same_bits_nan
 from oracle import lagsgd_oracle as orc
 
 
@@ -170,3 +170,20 @@ def test_delta_golden():
             assert got is None
         else:
             assert got is not None and abs(got - want) <= 1e-12 * max(1.0, abs(want)), (i, got, want)
+
+
+def test_nonfinite_golden(nonfinite_cases):
+    """NaN never selected (ranked after every number, then dropped by `mag > 0`), +-inf first; an
+    overflowed acc leaves inf - inf = NaN in the residual (R: sparsify.py:84-90, training.py:252)."""
+    topk, steps = nonfinite_cases
+    for x, k, idx, val in topk:
+        got_i, got_v = orc.top_k(x, k)
+        np.testing.assert_array_equal(got_i, idx)
+        assert same_bits_nan(got_v, val)
+    for c in steps:
+        res = [r.copy() for r in c["r_in"]]
+        with np.errstate(all="ignore"):
+            v = orc.lags_step(c["v"], list(c["g"]), c["alpha"], c["dims"], c["counts"], res)
+        assert same_bits_nan(v, c["v_out"])
+        for a, b in zip(res, c["r_out"]):
+            assert same_bits_nan(a, b)

@@ -61,11 +61,11 @@ def test_lagssgd_set_policy_replans_buckets():
     model = torch.nn.Sequential(torch.nn.Linear(32, 64), torch.nn.Tanh(), torch.nn.Linear(64, 4))
     opt = LagsSGD(model.parameters(), lr=0.1, rho=0.5, bucket_cap_bytes=128, engine_factory=stub_factory)
     before = list(opt.ks)
-    r0 = opt.residual.clone()
+    r0 = opt.residual_vector()
     L = len(opt.dims)
     opt.set_policy(CompressionPolicy({i + 1: 10.0 for i in range(L)}, 10.0))
     assert opt.ks == [min(d, max(1, d // 10)) for d in opt.dims] and opt.ks != before
-    assert torch.equal(opt.residual, r0)
+    assert torch.equal(opt.residual_vector(), r0)  # carried over through the re-layout
     covered = sorted(l for b in opt.buckets for l in range(b.lo, b.hi + 1))
     assert covered == list(range(L))
     x = torch.randn(3, 32)

@@ -13,9 +13,8 @@ import paper_1911_08727_b200 as L  # noqa: E402
 from paper_1911_08727_b200 import _native as N  # noqa: E402
 from bench import ks_for, resnet50_dims  # noqa: E402
 
-NAMES = ["entry", "counts loaded", "block sums", "cluster.sync 1", "remote counts", "gather", "cluster.sync 2",
-         "select (rank 0)", "cluster.sync 3", "compaction counts", "cluster.sync 4", "ordered compact",
-         "P=1 update", "final sync"]
+NAMES = ["entry", "counts loaded", "block sums", "cluster wait", "histogram cut", "gather", "push",
+         "cluster.sync", "resolve", "lower-rank counts", "-", "ordered compact", "zero histogram", "end"]
 
 dims = resnet50_dims()
 ks = ks_for(dims)
