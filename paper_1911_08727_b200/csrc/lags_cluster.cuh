@@ -189,7 +189,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                                      const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r,
                                      int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words,
                                      int force_exact, float* vupd, uint32_t* dyn, SelectSmem& cs, ClusterShared& csh,
-                                     ClusterRadix& cr, uint32_t t_launch, uint32_t* hist) {
+                                     ClusterRadix& cr, uint32_t t_launch, uint32_t* hist, bool dry = false) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t t_start = globaltimer_lo();
@@ -208,9 +208,15 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   // wait just before the first remote store (the loads below overlap the barrier)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   LAGS_STAMP(0);
-  if (hl) stage_hist(hl, cs);  // every CTA its own copy, in flight together with the counts
-  // 1. counts: every CTA reads ALL of the layer's task counts (one load per thread for layers
-  // up to SEL_NT tasks) and derives m, the ranks' sums and its own offset -- no exchange
+  // 1. one round trip: the own tasks' candidates (speculative, see spec_load), the histogram (every
+  // CTA its own copy) and ALL of the layer's task counts (one load per thread for layers up to
+  // SEL_NT tasks), from which every CTA derives m, the ranks' sums and its own offset
+  const int nt_own = t_hi - t_lo;
+  const bool spec = T <= SEL_NT;  // counts cached in shared memory, candidates loaded speculatively
+  SpecGather g;
+  if (spec) spec_load(g, t_lo, nt_own, cand_idx, cand_val, cap);
+  HistRegs hr;
+  if (hl) hist_load(hl, hr);  // every CTA its own copy
   int bnd[CLUSTER + 1];
 #pragma unroll
   for (int q = 0; q <= CLUSTER; ++q) bnd[q] = tr.x + static_cast<int>((static_cast<int64_t>(T) * q) / CLUSTER);
@@ -219,11 +225,10 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
 #pragma unroll
   for (int q = 0; q < CLUSTER; ++q) qs[q] = 0u;
   uint32_t over = 0;
-  const bool cache = T <= SEL_NT;  // the counts stay in shared memory for the gather
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
-    if (cache) cs.tcache[t - tr.x] = c;
+    if (spec) cs.tcache[t - tr.x] = c;
     const uint32_t cc = min(c, static_cast<uint32_t>(cap));
 #pragma unroll
     for (int q = 0; q < CLUSTER; ++q) qs[q] += (t >= bnd[q] && t < bnd[q + 1]) ? cc : 0u;
@@ -235,7 +240,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     const uint32_t w = __reduce_add_sync(0xffffffffu, qs[q]);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(&csh.qsum[q], w);
   }
-  const uint32_t over_any = __syncthreads_or(over) ? 1u : 0u;  // (also publishes the staged histogram)
+  const uint32_t over_any = __syncthreads_or(over) ? 1u : 0u;
   LAGS_STAMP(2);
   uint32_t m = 0, pre = 0, m_max = 0;
   uint32_t rpre[CLUSTER + 1];  // prefix of the ranks' candidate counts
@@ -249,7 +254,10 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     rpre[q + 1] = rpre[q] + mq;
   }
   const uint32_t mr = csh.qsum[rank];
-  const bool fits = 2ull * m_max <= static_cast<uint64_t>(smem_words);  // own values + indices
+  // own values + indices (+ the parked weights of the P = 1 update)
+  const bool park = spec && vupd != nullptr;
+  const uint32_t mx4 = (m_max + 3u) & ~3u;  // 16-byte aligned planes (the staged compaction reads vectors)
+  const bool fits = (park ? 3ull : 2ull) * mx4 <= static_cast<uint64_t>(smem_words);
   int why = 0;
   if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
   else if (over_any) why = FB_OVERFLOW;
@@ -285,20 +293,27 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   HistCut hc{~0u, 0u, 0u, 0u};
   bool cut = hl != nullptr && k < m;
   if (cut) {
-    hc = hist_cut(cs, k, k2, m);
+    hc = hist_cut(hr, cs, k, k2, m);
     cut = hc.bin < HIST_BINS - 1u && hc.in_bin <= BIN_LIST_MAX;
   }
   if (threadIdx.x == 0) {
     cs.sm.list_n = 0u;
     cs.sm.gtb = 0u;
+    cs.sm.diff_acc = 0u;
   }
   __syncthreads();
   LAGS_STAMP(4);
   float* sv = reinterpret_cast<float*>(dyn);
-  int32_t* si = reinterpret_cast<int32_t*>(dyn + m_max);
-  gather_candidates(t_lo, t_hi, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
-                    &cs.sm.gtb, cs.hist2, &cs.sm.list_n, vupd ? vupd + L.offset : nullptr,
-                    cache ? cs.tcache : nullptr, tr.x);
+  int32_t* si = reinterpret_cast<int32_t*>(dyn + mx4);
+  float* sw = park ? reinterpret_cast<float*>(dyn + 2 * mx4) : nullptr;  // parked weights
+  if (spec) {
+    spec_place(g, t_lo, nt_own, cs.tcache + (t_lo - tr.x), cand_idx, cand_val, cap, sv, si, sw,
+               vupd ? vupd + L.offset : nullptr, cs, st.thr, base, cut ? hc.bin : ~0u, &cs.sm.gtb, cs.hist2,
+               &cs.sm.list_n);
+  } else {
+    gather_candidates(t_lo, t_hi, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
+                      &cs.sm.gtb, cs.hist2, &cs.sm.list_n, vupd ? vupd + L.offset : nullptr, nullptr, tr.x);
+  }
   __syncthreads();
   LAGS_STAMP(5);
   if (cut) {  // push the own count above the cut and the cut bin's keys into every CTA
@@ -338,44 +353,68 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       gsum += csh.gtb[q];
     }
     if (off[CLUSTER] == hc.in_bin && gsum == hc.above) {  // uniform: the same pushed data everywhere
-      const uint32_t c = off[CLUSTER];
-      uint32_t* list = cs.hist2;  // the cut bin's keys of all ranks, contiguous
-      for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) {
-        int q = 0;
-        while (i >= off[q + 1]) ++q;
-        list[i] = csh.lists[q][i - off[q]];
+      const uint32_t c = off[CLUSTER], r = k - hc.above;
+      uint32_t low_gt, low_eq, gt_in;
+      if (c <= WARP_CUT_MAX) {  // every warp resolves it from the pushed lists, no barrier
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t kk[WARP_CUT_KEYS], oo[WARP_CUT_KEYS];  // list entries lane + 32 j, their owner ranks
+#pragma unroll
+        for (int jj = 0; jj < WARP_CUT_KEYS; ++jj) {
+          const uint32_t i = lane + 32u * jj;
+          uint32_t q = 0, o = 0;
+#pragma unroll
+          for (int p = 1; p < CLUSTER; ++p) {
+            if (i >= off[p]) {
+              q = static_cast<uint32_t>(p);
+              o = off[p];
+            }
+          }
+          kk[jj] = i < c ? csh.lists[q][i - o] : 0u;
+          oo[jj] = q;
+        }
+        const WarpCut wc = warp_resolve(kk, oo, c, r, static_cast<uint32_t>(rank));
+        th.prefix = wc.key;
+        gt_in = wc.gt;
+        low_gt = wc.low_gt;
+        low_eq = wc.low_eq;
+      } else {
+        uint32_t* list = cs.hist2;  // the cut bin's keys of all ranks, contiguous
+        for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) {
+          int q = 0;
+          while (i >= off[q + 1]) ++q;
+          list[i] = csh.lists[q][i - off[q]];
+        }
+        __syncthreads();
+        const SelectThreshold<uint32_t> t2 = resolve_cut(list, c, r, hc.above, cs);
+        th.prefix = t2.prefix;
+        gt_in = t2.n_gt - hc.above;
+        uint32_t lge = 0u;  // the lower ranks' listed keys above / equal to the threshold
+        if (threadIdx.x < c && threadIdx.x < off[rank]) {
+          const uint32_t x = list[threadIdx.x];
+          lge = x > th.prefix ? 1u : (x == th.prefix ? 0x10000u : 0u);
+        }
+        lge = block_sum(lge, cs.sm);
+        low_gt = lge & 0xffffu;
+        low_eq = lge >> 16;
       }
-      __syncthreads();
-      th = resolve_cut(list, c, k - hc.above, hc.above, cs);
-      LAGS_STAMP(8);
-      // carried counts of the lower ranks: their entries above the cut bin plus their listed keys
-      // above / equal to the threshold (c <= BIN_LIST_MAX < SEL_NT: one key per thread)
-      uint32_t lge = 0u;
-      if (threadIdx.x < c && threadIdx.x < off[rank]) {
-        const uint32_t x = list[threadIdx.x];
-        lge = x > th.prefix ? 1u : (x == th.prefix ? 0x10000u : 0u);
-      }
-      lge = block_sum(lge, cs.sm);
+      th.pmask = 0x7fffffffu;
+      th.n_gt = hc.above + gt_in;
+      th.need_eq = r - gt_in;
       for (int q = 0; q < rank; ++q) cg0 += csh.gtb[q];
-      cg0 += lge & 0xffffu;
-      ce0 = lge >> 16;
+      cg0 += low_gt;
+      ce0 = low_eq;
       key2 = (base + hc.bin2) << HIST_SHIFT;  // lower edge of the k2-th candidate's bin
       resolved = true;
+      LAGS_STAMP(8);
       LAGS_STAMP(9);
       LAGS_STAMP(10);
     }
   }
   const bool hard = !resolved;  // uniform
-  uint32_t cut_diag = 0u;  // why the cut did not resolve (diagnostic): 1 no histogram, 2 top bin or
-                           // crowded, 4 counts mismatch; bits 8.. the cut bin's count
-  if (hard) {
-    if (!hl) cut_diag = 1u;
-    else if (!cut) cut_diag = 2u;
-    else cut_diag = 4u;
-    if (hl && k < m) cut_diag |= min(hc.in_bin, 0xffffffu) << 8;
-    if (cut_diag == 4u && threadIdx.x == 0 && rank == 0)
-      cut_diag |= (min(csh.lc[0] + csh.lc[1] + csh.lc[2] + csh.lc[3], 255u) << 16) | (hc.in_bin == 0 ? 0x80u : 0u);
-  }
+  // diagnostic: 0 resolved by the cut, 1 no histogram, 2 top bin or crowded, 4 counts mismatch;
+  // bits 8.. the cut bin's count
+  uint32_t cut_diag = !hard ? 0u : (!hl ? 1u : (!cut ? 2u : 4u));
+  if (hl && k < m) cut_diag |= min(hc.in_bin, 0xffffffu) << 8;
   if (hard) {  // top (open) bin or a crowded one: the distributed radix select over every CTA's keys
     int q0 = 0;
     while (rpre[q0 + 1] == rpre[q0]) ++q0;  // the first rank with candidates (m > 0)
@@ -415,6 +454,10 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       ce0 += o->eq;
     }
   }
+  if (sw) {
+    spec_store_weights(g, nt_own, sw, cs);
+    __syncthreads();
+  }
   const long long c2 = clock64();
   // 3. ordered compaction of the own range with the carried counts of the lower ranks
   float* data = r + L.offset;
@@ -426,7 +469,16 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     *ix = si[i];
   };
   uint32_t end;
-  if (vupd) {  // fused P = 1 update: the weights are loaded before the compaction's scan
+  if (sw || !vupd) {  // staged: vector reads of the planes (weights parked or none)
+    float* vl = vupd ? vupd + L.offset : nullptr;
+    auto emit = [=](uint32_t pos, int32_t ix, float x, float w) {
+      oidx[pos] = ix;
+      oval[pos] = x;
+      data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
+      if (vl) vl[ix] = single_rank_update(w, x);
+    };
+    end = compact_staged(mr, th, sv, si, sw, emit, cs.sm, cg0, ce0);
+  } else {  // fused P = 1 update: the weights are loaded before the compaction's scan
     float* vl = vupd + L.offset;
     auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
       oidx[pos] = static_cast<int32_t>(ix);
@@ -434,17 +486,11 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       vl[ix] = single_rank_update(w, x);
     };
-    end = ordered_compact_pf<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0, [=](int64_t ix) { return vl[ix]; });
-  } else {
-    auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
-      oidx[pos] = static_cast<int32_t>(ix);
-      oval[pos] = x;
-      data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
-    };
-    end = ordered_compact<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0);
+    end = ordered_compact_pf<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0,
+                                              [=](int64_t, int64_t ix) { return vl[ix]; });
   }
   LAGS_STAMP(11);
-  if (hl) zero_hist(hl, rank * (HIST_BINS / CLUSTER), (rank + 1) * (HIST_BINS / CLUSTER));
+  if (hl && !dry) zero_hist(hl, rank * (HIST_BINS / CLUSTER), (rank + 1) * (HIST_BINS / CLUSTER));
   LAGS_STAMP(12);
   const long long c3 = clock64();
   if (rank == CLUSTER - 1 && threadIdx.x == 0) count_out[j] = static_cast<int32_t>(end);
@@ -458,11 +504,11 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     FastState ns = candidate_state(st, next_threshold(st, m, k, k2, th.prefix, key2), m, k, ph);
     ns.cycles = static_cast<uint32_t>(clock64() - t_begin);
     ns.path = hard ? 4u : 3u;
-    ns.cut = cut_diag | (hard && cut ? (min(csh.gtb[0] + csh.gtb[1] + csh.gtb[2] + csh.gtb[3], 0xffu) << 24) : 0u);
+    ns.cut = cut_diag;
     ns.t_start = t_start;
     ns.t_end = globaltimer_lo();
     ns.t_launch = t_launch;
-    state[j] = ns;
+    if (!dry) state[j] = ns;
   }
   // the distributed select reads other CTAs' shared memory up to its last barrier: no CTA leaves
   // before every CTA is past it (the cut path reads only its own after the gather barrier)
@@ -483,7 +529,7 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval,
     float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, SelectCounters sc,
     float* vupd, uint32_t* hist) {
-  extern __shared__ uint32_t dyn[];
+  extern __shared__ __align__(16) uint32_t dyn[];
   __shared__ SelectSmem cs;
   __shared__ ClusterShared csh;
   __shared__ ClusterRadix cr;
@@ -496,6 +542,16 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
   griddep_wait();  // K1 has completed and its writes are visible (programmatic dependent launch)
   LAGS_STAMP(15);
   if (static_cast<int>(blockIdx.x) < cl_ctas) {
+#ifdef LAGS_DBG_TWICE  // diagnostic: the layer twice, the first run without side effects on state / histogram
+    {
+      unsigned long long t0 = clock64();
+      cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val,
+                           cap, gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh,
+                           cr, t_launch, hist, true);
+      cluster_sync_exec();
+      if (blockIdx.x < CLUSTER && threadIdx.x == 0) lags_dbg_stamps[blockIdx.x][0][16] = clock64() - t0;
+    }
+#endif
     cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap,
                          gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh, cr,
                          t_launch, hist);

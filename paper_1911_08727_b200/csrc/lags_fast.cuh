@@ -496,11 +496,17 @@ struct HistCut {
   uint32_t bin2;                // rank k2 (the next prediction): its bin
 };
 
-// Stage the layer's histogram into cs.sm.hist (16-byte loads; the caller synchronises).
-__device__ __forceinline__ void stage_hist(const uint32_t* hl, SelectSmem& cs) {
-  const uint4* src = reinterpret_cast<const uint4*>(hl);
-  uint4* dst = reinterpret_cast<uint4*>(cs.sm.hist);
-  for (int i = threadIdx.x; i < HIST_BINS / 4; i += SEL_NT) dst[i] = __ldcg(src + i);
+// The layer's histogram in registers: thread t holds the 8 consecutive bins of chunk
+// SEL_NT - 1 - t (two 16-byte loads), so the block scan over threads runs from the top bin down.
+constexpr int HIST_PER_THREAD = HIST_BINS / SEL_NT;
+static_assert(HIST_PER_THREAD == 8, "two uint4 of bins per thread");
+struct HistRegs {
+  uint4 lo, hi;  // bins c*8 + 0..3, c*8 + 4..7 of chunk c = SEL_NT - 1 - threadIdx.x
+};
+__device__ __forceinline__ void hist_load(const uint32_t* hl, HistRegs& h) {
+  const uint4* src = reinterpret_cast<const uint4*>(hl) + 2 * (SEL_NT - 1 - static_cast<int>(threadIdx.x));
+  h.lo = __ldcg(src);
+  h.hi = __ldcg(src + 1);
 }
 
 // Clear bins [lo, hi) of a layer histogram for the next call's K1 (16-byte stores).
@@ -509,11 +515,88 @@ __device__ __forceinline__ void zero_hist(uint32_t* hl, int lo, int hi) {
   for (int i = lo / 4 + threadIdx.x; i < hi / 4; i += SEL_NT) dst[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
-// All threads; the staged histogram must be visible (after a barrier).
-__device__ __forceinline__ HistCut hist_cut(SelectSmem& cs, uint32_t k, uint32_t k2, uint32_t m) {
-  uint32_t bin[2], above[2], in_bin[2];
-  find_bin2<Key<float>::RB>(cs.sm, cs.sm.hist, min(k, m), min(k2, m), bin, above, in_bin);
-  return HistCut{bin[0], above[0], in_bin[0], bin[1]};
+// The bins of ranks k and k2 (<= m) from the register histogram: one block scan, no staging.
+// All threads.
+__device__ __forceinline__ HistCut hist_cut(const HistRegs& h, SelectSmem& cs, uint32_t k, uint32_t k2, uint32_t m) {
+  // descending: bin 7 of the chunk first
+  const uint32_t hv[8] = {h.hi.w, h.hi.z, h.hi.y, h.hi.x, h.lo.w, h.lo.z, h.lo.y, h.lo.x};
+  uint32_t s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += hv[q];
+  uint32_t tot;
+  const uint32_t ex = block_exclusive_scan<SEL_NT>(s, cs.sm.warp_tot, &tot);
+  const uint32_t top = (SEL_NT - threadIdx.x) * 8u - 1u;  // the chunk's highest bin
+  const uint32_t rr[2] = {min(k, m), min(k2, m)};
+#pragma unroll
+  for (int w = 0; w < 2; ++w) {
+    const uint32_t r = rr[w];
+    if (ex < r && r <= ex + s) {
+      uint32_t c = ex;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (r <= c + hv[q]) {
+          cs.sm.count2[w] = hv[q];
+          cs.sm.above2[w] = c;
+          cs.sm.found2[w] = top - q;
+          break;
+        }
+        c += hv[q];
+      }
+    }
+  }
+  __syncthreads();
+  const HistCut hc{cs.sm.found2[0], cs.sm.above2[0], cs.sm.count2[0], cs.sm.found2[1]};
+  __syncthreads();
+  return hc;
+}
+
+// Warp-level resolution of the cut (every warp computes it redundantly: no block barrier).  The
+// cut bin's c <= WARP_CUT_MAX keys, lane i holding keys i + 32 j (kk[j]) of owner ranks oo[j]
+// (cluster rank; 0 single CTA): the r-th largest is the threshold T; returns {T, gt = keys > T,
+// low_gt / low_eq = keys > / == T owned by ranks below `rank`}.
+struct WarpCut {
+  uint32_t key, gt, low_gt, low_eq;
+};
+constexpr int WARP_CUT_KEYS = 2;  // keys per lane (4: local-memory arrays, slower than the block path)
+constexpr uint32_t WARP_CUT_MAX = 32u * WARP_CUT_KEYS;
+__device__ __forceinline__ WarpCut warp_resolve(const uint32_t (&kk)[WARP_CUT_KEYS],
+                                                const uint32_t (&oo)[WARP_CUT_KEYS], uint32_t c, uint32_t r,
+                                                uint32_t rank) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t gt[WARP_CUT_KEYS], eq[WARP_CUT_KEYS];
+#pragma unroll
+  for (int j = 0; j < WARP_CUT_KEYS; ++j) gt[j] = eq[j] = 0u;
+#pragma unroll
+  for (int jq = 0; jq < WARP_CUT_KEYS; ++jq) {  // source slot jq: keys 32 jq .. 32 jq + 31
+    const uint32_t n = c > 32u * jq ? min(c - 32u * jq, 32u) : 0u;
+    for (uint32_t q = 0; q < n; ++q) {
+      const uint32_t x = __shfl_sync(0xffffffffu, kk[jq], q);
+#pragma unroll
+      for (int j = 0; j < WARP_CUT_KEYS; ++j) {
+        gt[j] += x > kk[j] ? 1u : 0u;
+        eq[j] += x == kk[j] ? 1u : 0u;
+      }
+    }
+  }
+  WarpCut wc{0u, 0u, 0u, 0u};
+  bool found = false;
+#pragma unroll
+  for (int j = 0; j < WARP_CUT_KEYS; ++j) {  // equal keys give equal answers: any hit
+    const unsigned hit = __ballot_sync(0xffffffffu, lane + 32u * j < c && gt[j] < r && r <= gt[j] + eq[j]);
+    if (!found && hit) {
+      const int src = __ffs(hit) - 1;
+      wc.key = __shfl_sync(0xffffffffu, kk[j], src);
+      wc.gt = __shfl_sync(0xffffffffu, gt[j], src);
+      found = true;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < WARP_CUT_KEYS; ++j) {
+    const bool low = lane + 32u * j < c && oo[j] < rank;
+    wc.low_gt += __popc(__ballot_sync(0xffffffffu, low && kk[j] > wc.key));
+    wc.low_eq += __popc(__ballot_sync(0xffffffffu, low && kk[j] == wc.key));
+  }
+  return wc;
 }
 
 // The exact threshold from the keys of the cut bin (list[0..c), any order): the r-th largest of
@@ -555,7 +638,7 @@ __device__ __forceinline__ SelectThreshold<uint32_t> resolve_cut(const uint32_t*
 // counts already in shared memory, tc[t - t_base] for every task of the range.  Returns the
 // number gathered.  All threads.
 #ifndef LAGS_GATHER_TASKS
-#define LAGS_GATHER_TASKS 6
+#define LAGS_GATHER_TASKS 5
 #endif
 constexpr int GATHER_TASKS = LAGS_GATHER_TASKS;
 
@@ -630,6 +713,159 @@ __device__ uint32_t gather_candidates(int t_lo, int t_hi, const int32_t* __restr
   return carry;
 }
 
+// Speculative candidate gather: counts, histogram and candidates in ONE round trip.  Before the
+// counts are known, warp w loads entry `lane` of its tasks t_lo + w + NW * u (u < GATHER_TASKS),
+// i.e. each task's first 32 candidates (usually all of them; reading past a short list stays
+// inside its cap slots).  After the counts' scan, spec_place puts them at their positions,
+// classifies them against the histogram cut and issues the loads of the possibly selected
+// entries' weights (P = 1 update) into registers; spec_store_weights parks those in shared
+// memory once the threshold is resolved, so the compaction never waits on HBM.  Leftovers (tasks
+// beyond NW * GATHER_TASKS, lists longer than 32) are gathered synchronously.  nt <= SEL_NT.
+struct SpecGather {
+  float xv[GATHER_TASKS];
+  int32_t xi[GATHER_TASKS];
+  float wv[GATHER_TASKS];
+};
+
+__device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const int32_t* __restrict__ cand_idx,
+                                          const float* __restrict__ cand_val, int cap) {
+  constexpr int NW = SEL_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int u = 0; u < GATHER_TASKS; ++u) {
+    const int tt = warp + NW * u;
+    g.wv[u] = 0.0f;
+    if (tt < nt) {
+      const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + lane;
+      g.xv[u] = __ldcg(cand_val + src);
+      g.xi[u] = __ldcg(cand_idx + src);
+    }
+  }
+}
+
+// All threads.  tc[0..nt): the range's task counts (shared).  sw (nullable, with vl): the
+// weights' staging; vl: the layer's weights (P = 1 update).  Classification as gather_candidates.
+__device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* tc, const int32_t* __restrict__ cand_idx,
+                               const float* __restrict__ cand_val, int cap, float* sv, int32_t* si, float* sw,
+                               const float* vl, SelectSmem& cs, uint32_t key0, uint32_t base, uint32_t cut_bin,
+                               uint32_t* gtb, uint32_t* list, uint32_t* list_n) {
+  constexpr int NW = SEL_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t c = threadIdx.x < nt ? min(tc[threadIdx.x], static_cast<uint32_t>(cap)) : 0u;
+  uint32_t tot;
+  const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
+  cs.tpos[threadIdx.x] = pos;
+  cs.tcnt[threadIdx.x] = c;
+  __syncthreads();
+  uint32_t my_gt = 0, dx = 0;
+  // returns whether the entry may be selected (its weight is wanted)
+  auto take = [&](float x, int32_t ix, uint32_t e) -> bool {
+    const uint32_t key = Key<float>::of(x);
+    sv[e] = x;
+    si[e] = ix;
+    dx |= key ^ key0;
+    const uint32_t b = hist_bin(key, base);
+    if (cut_bin != ~0u) {
+      if (b < cut_bin) return false;
+      if (b > cut_bin) {
+        ++my_gt;
+      } else {
+        const uint32_t at = atomicAdd(list_n, 1u);
+        if (at < BIN_LIST_MAX) list[at] = key;
+      }
+    }
+    return true;
+  };
+#pragma unroll
+  for (int u = 0; u < GATHER_TASKS; ++u) {
+    const int tt = warp + NW * u;
+    if (tt < nt && static_cast<uint32_t>(lane) < cs.tcnt[tt]) {
+      if (take(g.xv[u], g.xi[u], cs.tpos[tt] + lane) && vl) g.wv[u] = vl[g.xi[u]];  // in flight until parked
+    }
+  }
+#pragma unroll 1
+  for (int tt = warp; tt < nt; tt += NW) {  // leftovers: synchronous
+    const uint32_t cc = cs.tcnt[tt];
+    const int64_t row = static_cast<int64_t>(t_lo + tt) * cap;
+    for (uint32_t e = (tt < NW * GATHER_TASKS ? 32u : 0u) + lane; e < cc; e += 32u) {
+      const float x = __ldcg(cand_val + row + e);
+      const int32_t ix = __ldcg(cand_idx + row + e);
+      if (take(x, ix, cs.tpos[tt] + e) && sw) sw[cs.tpos[tt] + e] = vl[ix];
+    }
+  }
+  dx = __reduce_or_sync(0xffffffffu, dx);
+  if (lane == 0 && dx) atomicOr(&cs.sm.diff_acc, dx);
+  my_gt = __reduce_add_sync(0xffffffffu, my_gt);
+  if (gtb && lane == 0 && my_gt) atomicAdd(gtb, my_gt);
+  return tot;
+}
+
+// Park the speculatively loaded weights at their entries' positions (cs.tpos / tcnt of the
+// spec_place scan still hold).  The caller synchronises before reading sw.
+__device__ __forceinline__ void spec_store_weights(const SpecGather& g, int nt, float* sw, const SelectSmem& cs) {
+  constexpr int NW = SEL_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int u = 0; u < GATHER_TASKS; ++u) {
+    const int tt = warp + NW * u;
+    if (tt < nt && static_cast<uint32_t>(lane) < cs.tcnt[tt]) sw[cs.tpos[tt] + lane] = g.wv[u];
+  }
+}
+
+// Ordered compaction of candidates staged in shared memory (sv / si / sw: 16-byte aligned planes
+// in index order; sw nullable), 4 entries per thread read as one 16-byte vector per plane.  The
+// rule and the result are ordered_compact_pf's: (key & pmask) > prefix, plus the first need_eq
+// equal ones in index order; carry_gt / carry_eq count the lower ranks' entries.
+// emit(pos, ix, x, w).  Returns the selected count (all threads).
+template <typename Emit>
+__device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& th, const float* sv, const int32_t* si,
+                                   const float* sw, Emit emit, RadixSmem<Key<float>::RB>& sm, uint32_t carry_gt,
+                                   uint32_t carry_eq) {
+  static_assert(SEL_VEC == 4, "one 16-byte vector per plane and thread");
+  for (uint32_t base = 0; base < m; base += SEL_NT * 4u) {
+    const uint32_t i0 = base + threadIdx.x * 4u;
+    float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i0 < m) x4 = *reinterpret_cast<const float4*>(sv + i0);
+    const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+    uint32_t gtm = 0, eqm = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const uint32_t key = i0 + v < m ? Key<float>::of(xs[v]) : 0u;
+      const uint32_t hk = key & th.pmask;
+      if (key != 0u) {
+        if (hk > th.prefix) gtm |= 1u << v;
+        else if (hk == th.prefix) eqm |= 1u << v;
+      }
+    }
+    int4 ix4 = make_int4(0, 0, 0, 0);
+    float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gtm | eqm) {
+      ix4 = *reinterpret_cast<const int4*>(si + i0);
+      if (sw) w4 = *reinterpret_cast<const float4*>(sw + i0);
+    }
+    const int32_t ixs[4] = {ix4.x, ix4.y, ix4.z, ix4.w};
+    const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
+    const uint32_t packed = (static_cast<uint32_t>(__popc(eqm)) << 16) | static_cast<uint32_t>(__popc(gtm));
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<SEL_NT>(packed, sm.warp_tot, &tot);
+    uint32_t gt_before = carry_gt + (ex & 0xffffu);
+    uint32_t eq_before = carry_eq + (ex >> 16);
+    if (gtm | eqm) {
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
+        if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), ixs[v], xs[v], ws[v]);
+        gt_before += g;
+        eq_before += e;
+      }
+    }
+    carry_gt += tot & 0xffffu;
+    carry_eq += tot >> 16;
+    __syncthreads();  // warp_tot reuse by the next scan
+  }
+  return carry_gt + min(carry_eq, th.need_eq);
+}
+
 // Candidate path of one layer inside one CTA.  Returns 0 on success, or why the candidate set
 // cannot be proven to hold the top-k (FB_TOO_FEW / FB_OVERFLOW); the caller then runs a dense
 // exact path in the same CTA.  Candidates are gathered once into shared memory (value + index,
@@ -671,18 +907,24 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
                                 float* vupd, const uint32_t* hl) {
   RadixSmem<Key<float>::RB>& sm = cs.sm;
   const uint32_t k = static_cast<uint32_t>(L.k);
-  uint32_t local = 0, over = 0;
+  const int T = tr.y - tr.x;
+  const bool spec = T <= SEL_NT;  // counts cached in shared memory, candidates loaded speculatively
+  float* vl = vupd ? vupd + L.offset : nullptr;
   LAGS_CSTAMP(0);
-  if (hl) stage_hist(hl, cs);  // in flight together with the counts
-  const bool cache = tr.y - tr.x <= SEL_NT;  // the counts stay in shared memory for the gather
+  // 1. one round trip: the candidates (speculative), the histogram and the task counts
+  SpecGather g;
+  if (spec) spec_load(g, tr.x, T, cand_idx, cand_val, cap);
+  HistRegs hr;
+  if (hl) hist_load(hl, hr);
+  uint32_t local = 0, over = 0;
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
     local += min(c, static_cast<uint32_t>(cap));
-    if (cache) cs.tcache[t - tr.x] = c;
+    if (spec) cs.tcache[t - tr.x] = c;
   }
   LAGS_CSTAMP(1);
-  const uint32_t m = block_sum(local, sm);  // (its barriers also publish the staged histogram)
+  const uint32_t m = block_sum(local, sm);
   if (__syncthreads_or(over)) return FB_OVERFLOW;
   LAGS_CSTAMP(2);
   if (m < k && st.thr > 1u) return FB_TOO_FEW;
@@ -691,38 +933,75 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
   uint32_t pred = st.thr;
   const uint32_t k2 = pred_rank(st, k);
   uint32_t phases = 0;  // diagnostic: gather / select / compact cycles (units of 64, 11 bits each)
+  uint32_t cut_diag = 0u;  // diagnostic (FastState.cut): 0 resolved by the cut, 2 not; bits 8.. the bin's count
   if (m > 0) {
     const long long c0 = clock64();
-    const bool in_smem = 2u * m <= static_cast<uint32_t>(smem_words);
+    const uint32_t m4 = (m + 3u) & ~3u;  // 16-byte aligned planes (the staged compaction reads vectors)
+    const bool in_smem = (vl && spec ? 3u : 2u) * m4 <= static_cast<uint32_t>(smem_words);
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
     float* sv = in_smem ? reinterpret_cast<float*>(dyn) : gval + gbase;
-    int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + m : gidx + gbase;
+    int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + m4 : gidx + gbase;
+    float* sw = in_smem && vl && spec ? reinterpret_cast<float*>(dyn) + 2 * m4 : nullptr;  // parked weights
     const uint32_t base = st.thr >> HIST_SHIFT;
     // the histogram cut (uniform): usable when the k-th candidate is in a closed bin with few keys
     HistCut hc{~0u, 0u, 0u, 0u};
     bool cut = hl != nullptr && k < m;
     if (cut) {
-      hc = hist_cut(cs, k, k2, m);
+      hc = hist_cut(hr, cs, k, k2, m);
       cut = hc.bin < HIST_BINS - 1u && hc.in_bin <= BIN_LIST_MAX;
     }
     if (threadIdx.x == 0) {
       sm.list_n = 0u;
       sm.gtb = 0u;  // entries above the cut bin, counted by the gather
+      sm.diff_acc = 0u;
     }
     __syncthreads();
     uint32_t* list = cs.hist2;
-    gather_candidates(tr.x, tr.y, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
-                      &sm.gtb, list, &sm.list_n, vupd ? vupd + L.offset : nullptr, cache ? cs.tcache : nullptr, tr.x);
+    if (spec) {
+      spec_place(g, tr.x, T, cs.tcache, cand_idx, cand_val, cap, sv, si, sw, sw ? vl : nullptr, cs, st.thr, base,
+                 cut ? hc.bin : ~0u, &sm.gtb, list, &sm.list_n);
+      if (!sw && vl) {  // weights not parked: prefetch the possibly selected ones for the compaction
+        for (uint32_t i = threadIdx.x; i < m; i += SEL_NT) {
+          const uint32_t key = Key<float>::of(sv[i]);
+          if (!cut || hist_bin(key, base) >= hc.bin) asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + si[i]));
+        }
+      }
+    } else {
+      gather_candidates(tr.x, tr.y, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
+                        &sm.gtb, list, &sm.list_n, vl, nullptr, tr.x);
+    }
     __syncthreads();  // the gather's counts (gtb, list_n) are complete: one uniform decision below
     const long long c1 = clock64();
     LAGS_CSTAMP(3);
     SelectThreshold<uint32_t> th;
     uint32_t key2 = 0u;
     if (cut && sm.list_n == hc.in_bin && sm.gtb == hc.above) {
-      th = resolve_cut(list, hc.in_bin, k - hc.above, hc.above, cs);
+      const uint32_t c = hc.in_bin, r = k - hc.above;
+      if (c <= WARP_CUT_MAX) {  // every warp resolves it from the list, no barrier
+        const uint32_t lane = threadIdx.x & 31;
+        uint32_t kk[WARP_CUT_KEYS], oo[WARP_CUT_KEYS];
+#pragma unroll
+        for (int jj = 0; jj < WARP_CUT_KEYS; ++jj) {
+          kk[jj] = lane + 32u * jj < c ? list[lane + 32u * jj] : 0u;
+          oo[jj] = 0u;
+        }
+        const WarpCut wc = warp_resolve(kk, oo, c, r, 0u);
+        th.prefix = wc.key;
+        th.pmask = 0x7fffffffu;
+        th.n_gt = hc.above + wc.gt;
+        th.need_eq = r - wc.gt;
+      } else {
+        th = resolve_cut(list, c, r, hc.above, cs);
+      }
       key2 = (base + hc.bin2) << HIST_SHIFT;  // lower edge of the k2-th candidate's bin
     } else {
       candidate_radix(sv, m, k, k2, sm.diff_acc, st.thr, cs, &th, &key2);
+      cut_diag = 2u;
+    }
+    if (hl && k < m) cut_diag |= min(hc.in_bin, 0xffffffu) << 8;
+    if (sw) {
+      spec_store_weights(g, T, sw, cs);
+      __syncthreads();
     }
     const long long c2 = clock64();
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
@@ -732,9 +1011,16 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     };
     int32_t* oidx = idx_out + L.slot;
     float* oval = val_out + L.slot;
-    float* vl = vupd ? vupd + L.offset : nullptr;
     LAGS_CSTAMP(4);
-    if (vl) {  // fused P = 1 update: the weights are loaded before the compaction's scan
+    if (in_smem && (sw || !vl)) {  // staged: vector reads of the planes (weights parked or none)
+      auto emit = [=](uint32_t pos, int32_t ix, float x, float w) {
+        oidx[pos] = ix;
+        oval[pos] = x;
+        data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
+        if (vl) vl[ix] = single_rank_update(w, x);
+      };
+      cnt = compact_staged(m, th, sv, si, sw, emit, sm, 0u, 0u);
+    } else if (vl) {  // fused P = 1 update: the weights are loaded before the compaction's scan
       auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
         oidx[pos] = static_cast<int32_t>(ix);
         oval[pos] = x;
@@ -742,7 +1028,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
         vl[ix] = single_rank_update(w, x);
       };
       cnt = ordered_compact_pf<uint32_t, float>(m, th, load, emit, sm, 0u, 0u,
-                                                [=](int64_t ix) { return vl[ix]; });
+                                                [=](int64_t, int64_t ix) { return vl[ix]; });
     } else {
       auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x) {
         oidx[pos] = static_cast<int32_t>(ix);
@@ -762,7 +1048,9 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     pred = next_threshold(st, m, k, k2, th.prefix, key2);
   }
   if (threadIdx.x == 0) {
-    state[j] = candidate_state(st, pred, m, k, phases);
+    FastState ns = candidate_state(st, pred, m, k, phases);
+    ns.cut = cut_diag;
+    state[j] = ns;
     count_out[j] = static_cast<int32_t>(cnt);
   }
   __syncthreads();
@@ -885,6 +1173,10 @@ __device__ LAGS_COLD void small_fallback_select(int j, const lags_layer_t& L, Fa
 #define LAGS_WARP_TOPK 8
 #endif
 constexpr int WARP_TOPK = LAGS_WARP_TOPK;
+#ifndef LAGS_WARP_MAX_DIM
+#define LAGS_WARP_MAX_DIM 2048
+#endif
+constexpr int WARP_MAX_DIM = LAGS_WARP_MAX_DIM;  // larger tiny layers: a whole CTA (persistent role)
 
 __device__ void warp_topk_layer(int j, const lags_layer_t& L, FastState* state, float* r, int32_t* idx_out,
                                 float* val_out, int32_t* count_out, float* vupd, uint32_t t_launch) {

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <string>
@@ -428,12 +429,13 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
 
 // Selection groups of an fp32 bucket: 0 = one CTA per layer (select_kernel's persistent role),
 // 1 = the largest layers, one thread-block cluster per layer (select_kernel's cluster role),
-// 2 = tiny layers with k <= WARP_TOPK, one warp per layer (select_kernel's warp role).
+// 2 = tiny layers (d <= WARP_MAX_DIM) with k <= WARP_TOPK, one warp per layer (select_kernel's warp
+// role; a warp's two passes over a 4096-element layer took longer than a whole CTA's dense path).
 std::vector<int> plan_groups(const int64_t* dims, const int32_t* ks, int L) {
   std::vector<int> gid(L, 0);
   for (int j = 0; j < L; ++j) {
     if (dims[j] > SMALL_LAYER && ks[j] >= CLUSTER_MIN_K) gid[j] = 1;
-    else if (dims[j] <= TINY_LAYER && ks[j] <= WARP_TOPK) gid[j] = 2;
+    else if (dims[j] <= WARP_MAX_DIM && ks[j] <= WARP_TOPK) gid[j] = 2;
   }
   return gid;
 }
@@ -662,33 +664,29 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     float* vu = static_cast<float*>(v_update);
     const int fe = exact ? 1 : 0;
     const bool zg = (flags & LAGS_COMPRESS_ZERO_GRAD) != 0;
-    // K1 over one group's task range (candidate lists indexed by global task id)
-    auto k1 = [&](const lags_bucket::Group& G, cudaStream_t st) -> cudaError_t {
-      if (G.ntasks == 0) return cudaSuccess;
-      const int blocks = (G.ntasks + K1_WARPS - 1) / K1_WARPS;
-      const int64_t cb = static_cast<int64_t>(G.task_base) * b->cap;
-      if (zg)
-        return launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
-                          G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
-                          b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work, b->hist);
-      return launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, st, b->tasks + G.task_base,
-                        G.ntasks, b->layers, b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx + cb,
-                        b->cand_val + cb, b->cand_cnt + G.task_base, status, b->sel_ctr.work, b->hist);
-    };
+    // K1 over every task (candidate lists indexed by global task id)
+    const lags_bucket::Group& G0 = b->grp[0];
+    const lags_bucket::Group& G1 = b->grp[1];
+    const lags_bucket::Group& G2 = b->grp[2];
+    const int ntasks = G0.ntasks + G1.ntasks + G2.ntasks;
+    const int blocks = (ntasks + K1_WARPS - 1) / K1_WARPS;
     cudaError_t e = cudaSuccess;
-    lags_bucket::Group all = b->grp[0];  // K1 streams every task (group 0's then group 1's)
-    all.task_base = 0;
-    all.ntasks = b->grp[0].ntasks + b->grp[1].ntasks + b->grp[2].ntasks;
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
-    if (e == cudaSuccess) e = k1(all, s);
+    if (e == cudaSuccess) {
+      if (zg)
+        e = launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
+                       b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status,
+                       b->sel_ctr.work, b->hist);
+      else
+        e = launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
+                       b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status,
+                       b->sel_ctr.work, b->hist);
+    }
     if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
     if (e == cudaSuccess) {
       // the selection: one launch (PDL behind K1).  Group 1 (the largest layers): one 4-CTA
       // cluster each; group 2 (tiny layers): one warp each; group 0: persistent CTAs, one wave
       // on the SMs the others leave free.
-      const lags_bucket::Group& G0 = b->grp[0];
-      const lags_bucket::Group& G1 = b->grp[1];
-      const lags_bucket::Group& G2 = b->grp[2];
       const int ncl = G1.nlayers;
       const int cl = ncl > 0 ? CLUSTER : 1;
       const int tiny_ctas = (G2.nlayers + SEL_NT / 32 - 1) / (SEL_NT / 32);

@@ -247,10 +247,10 @@ __device__ SelectThreshold<K> radix_select(KeyAt key_at, int64_t m, uint32_t k, 
 // to output position pos.  Returns the selected count (all threads).
 // carry_gt0 / carry_eq0: counts of gt / eq entries before entry 0 (multi-CTA compaction).
 // Without a prefetch functor the emit is emit(pos, i, index, val).  ordered_compact_pf takes
-// pf(index) -> W, called for every entry at or above the threshold BEFORE the block scan (so its
+// pf(i, index) -> W, called for every entry at or above the threshold BEFORE the block scan (so its
 // loads are in flight across the scan's barriers), and calls emit(pos, i, index, val, w).
 struct NoPrefetch {
-  __device__ __forceinline__ float operator()(int64_t) const { return 0.0f; }
+  __device__ __forceinline__ float operator()(int64_t, int64_t) const { return 0.0f; }
 };
 
 template <typename K, typename T, typename Load, typename Emit, int RB, typename Pf = NoPrefetch>
@@ -276,9 +276,9 @@ __device__ uint32_t ordered_compact_pf(int64_t m, const SelectThreshold<K>& th, 
         else if (hi == th.prefix) eqm |= 1u << v;
       }
     }
-    decltype(pf(0)) w[SEL_VEC];
+    decltype(pf(0, 0)) w[SEL_VEC];
 #pragma unroll
-    for (int v = 0; v < SEL_VEC; ++v) w[v] = ((gtm | eqm) >> v) & 1u ? pf(ix[v]) : decltype(pf(0))(0);
+    for (int v = 0; v < SEL_VEC; ++v) w[v] = ((gtm | eqm) >> v) & 1u ? pf(i0 + v, ix[v]) : decltype(pf(0, 0))(0);
     const uint32_t packed = (static_cast<uint32_t>(__popc(eqm)) << 16) | static_cast<uint32_t>(__popc(gtm));
     uint32_t tot;
     const uint32_t ex = block_exclusive_scan<SEL_NT>(packed, sm.warp_tot, &tot);

@@ -57,9 +57,8 @@ print(f"  {'griddep wait':18s}", " ".join(f"{x:7.0f}" for x in w))
 g0 = gt[:, :, 15].min(axis=1, keepdims=True)
 print("globaltimer ns after the first rank's wait: entry / end per rank (median):")
 print("  entry", np.median(gt[:, :, 0] - g0, axis=0), " end", np.median(gt[:, :, 13] - g0, axis=0))
-if np.any(cyc[:, 0, 17]):
-    print("rank 0 select, first / second (warm) run, cycles:", np.median(cyc[:, 0, 16] - cyc[:, 0, 6]),
-          np.median(cyc[:, 0, 17] - cyc[:, 0, 16]))
+if np.any(cyc[:, 0, 16]):
+    print("LAGS_DBG_TWICE: cycles of the first (dry) run per rank:", np.median(cyc[:, :, 16], axis=0))
 # the candidate-path layer LAGS_DBG_J (one CTA)
 cs_ = []
 for t in range(30):

@@ -57,9 +57,8 @@ def main():
             ph = lambda w: (int(w) & 2047, (int(w) >> 11) & 2047, (int(w) >> 22) & 2047)  # noqa: E731
             print("   candidate-path phases x64 cycles (gather, select, compact):",
                   [ph(s[j, 7]) for j in slow], flush=True)
-            print("   cut diagnostic (code, in_bin / list, gtb):",
-                  [(int(s[j, 11]) & 0xff, (int(s[j, 11]) >> 8) & 0xff, (int(s[j, 11]) >> 16) & 0xff,
-                    int(s[j, 11]) >> 24) for j in slow], flush=True)
+            print("   histogram cut (code 0 = resolved, cut bin's count):",
+                  [(int(s[j, 11]) & 0xff, int(s[j, 11]) >> 8) for j in slow], flush=True)
 
 
 if __name__ == "__main__":
