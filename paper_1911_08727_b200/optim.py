@@ -279,18 +279,21 @@ class LagsSGD(torch.optim.Optimizer):
         self.ks = selection_counts(self.dims, self.ratios)
         self._build_buckets()
 
-    def adapt(self, network, ratio_cap: float = 1000.0, ratio_grid=None) -> CompressionPolicy:
+    ADAPT_GRID = (25, 50, 100, 250, 500, 1000)
+
+    def adapt(self, network, ratio_cap: float = 1000.0, ratio_grid=None, workers: int | None = None) -> CompressionPolicy:
         """Adaptive rho_l (R: perf.py:231-260) from this rank's device timings of the last step
         (enable_layer_timing + enable_timing before it): each layer gets the smallest grid ratio
-        whose exchange + compress hides behind the next layer's backprop.  Rank 0's choice is
+        whose exchange + compress hides behind the next layer's backprop.  ``workers`` prices the
+        exchange for that many workers (default: the process group's size).  Rank 0's choice is
         broadcast so every rank plans identical buckets and messages."""
         from . import perf
 
         # default grid keeps rho <= 4 %: the reference's selector prices sparsification as a
         # per-layer constant, while on the device selecting near-dense layers costs much more
-        grid = (25, 50, 100, 250, 500, 1000) if ratio_grid is None else ratio_grid
+        grid = self.ADAPT_GRID if ratio_grid is None else ratio_grid
         pol = perf.select_ratios(self.dims, self.layer_backward_times(), self.layer_spar_times(), network,
-                                 self.world, ratio_cap, grid)
+                                 self.world if workers is None else int(workers), ratio_cap, grid)
         ratios = torch.tensor([pol.ratio_for(i + 1) for i in range(len(self.params))], dtype=torch.float64,
                               device=self.device)
         if self.world > 1:

@@ -27,6 +27,7 @@ from .errors import DivergenceError, StructureError
 from .layered import layout_of
 
 SCHEDULE_KINDS = ("constant", "inv-sqrt-T", "diminishing")
+MAX_WORKERS = 32  # workers one decode combines (lags_bucket_create: max_world <= 32)
 
 
 @dataclass(frozen=True)
@@ -214,6 +215,19 @@ def _host_copy(dst: np.ndarray, src: np.ndarray, plan: list) -> list:
     return joins
 
 
+def _all_gather(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    """out = every rank's inp in rank order.  NCCL gathers the device tensors directly; other
+    backends (gloo: e.g. several worker processes sharing one GPU) go through host copies."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+        return
+    host = torch.empty(out.shape, dtype=out.dtype)
+    dist.all_gather_into_tensor(host, inp.cpu(), group=group)
+    out.copy_(host, non_blocking=False)
+
+
 def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v, group=None):
     """The drop-in step with its host transfers overlapped, chunk by chunk of layers.
 
@@ -274,7 +288,7 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v, gr
                                             pre[p:p + 1].data_ptr(), s_cmp.cuda_stream), "lags_check_finite")
         if world > 1:  # every worker's flags, in rank order (R: training.py:174-175 names the first)
             pre_all = torch.empty(world, dtype=torch.int32, device=dev)
-            dist.all_gather_into_tensor(pre_all, pre, group=group)
+            _all_gather(pre_all, pre, group)
             pre = pre_all
         pre_h = torch.empty(world * P, dtype=torch.int32, pin_memory=True)
         pre_h.copy_(pre, non_blocking=True)
@@ -315,7 +329,7 @@ def _pipelined_step(v, grads, residuals, alpha, dims, ks, mode, t, promote_v, gr
         for c, (bucket, msgs, e0, e1, _) in enumerate(staged):
             if world > 1:  # every worker's message for this chunk, rank order
                 allm = bucket.new_messages(world)
-                dist.all_gather_into_tensor(allm, msgs, group=group)
+                _all_gather(allm, msgs, group)
                 msgs = allm
             join_copy[c]()  # this chunk of the output holds v: update its selected entries in place
             bucket.decode(msgs, world * P, out[e0:e1], stream=s_cmp)
@@ -362,7 +376,8 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
               group=None, _promote_v: bool = False):
     """Per-layer selection with error feedback on the B200; R: training.py:227-255.
 
-    ``group`` (a torch.distributed NCCL process group): run as one worker of a multi-process job --
+    ``group`` (a torch.distributed process group; NCCL, or gloo for workers sharing a GPU): run as
+    one worker of a multi-process job --
     ``grads``/``residuals`` hold this rank's own single gradient and residual, ``v`` the replica;
     the workers are the ranks in group order, and every rank returns the parameters the
     single-process step over all of their gradients would return (same bits).
@@ -373,6 +388,13 @@ def lags_step(v, grads: Sequence, alpha, counts: dict, residuals: Sequence, t: i
     P = len(grads)
     if P < 1 or len(residuals) != P:
         raise ValueError("need one residual per worker and at least one worker")
+    workers = P
+    if group is not None:
+        import torch.distributed as dist
+
+        workers = P * dist.get_world_size(group)
+    if workers > MAX_WORKERS:  # the decode's per-element rank bitmask is 32 bits
+        raise ValueError(f"at most {MAX_WORKERS} workers per step, got {workers}")
     dtype = v.data.dtype
     mode = mode_for(dtype, alpha)
     # R: training.py:171-175 -- worker by worker: layout, then finiteness.

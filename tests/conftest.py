@@ -13,6 +13,18 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs on the GPU box via gpurun)")
+    config.addinivalue_line("markers", "gpu2: needs two B200s (gpurun --gpus 2; selected only by -m gpu2)")
+
+
+def pytest_collection_modifyitems(config, items):
+    """Two-GPU tests run only when asked for (-m gpu2): on one GPU they could only skip."""
+    if "gpu2" in (config.getoption("markexpr") or ""):
+        return
+    keep = [it for it in items if it.get_closest_marker("gpu2") is None]
+    dropped = [it for it in items if it.get_closest_marker("gpu2") is not None]
+    if dropped:
+        config.hook.pytest_deselected(items=dropped)
+        items[:] = keep
 
 
 def load_npz(name):
