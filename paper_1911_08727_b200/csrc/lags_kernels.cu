@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "lags_common.cuh"
 #include "lags_internal.h"
 #include "lags_cluster.cuh"
@@ -158,6 +160,77 @@ __global__ void __launch_bounds__(DEC_NT) decode_update_kernel(const lags_layer_
   }
   v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
   mask[i] = 0u;
+}
+
+// The whole decode of P > 1 messages in ONE cooperative launch: phase A scatters every rank's
+// pairs into its plane and marks the rank bitmask; a grid-wide barrier; phase B lets the lowest
+// rank holding index i sum the planes in rank order (fp64) and apply v - total / P
+// (R: training.py:248,253-254) -- each thread keeps its ITEMS (element, rank) pairs in registers
+// across the barrier, so phase B starts from the mask without re-reading the messages.  With
+// momentum (mu > 0) phase B is a dense pass over the bucket: m = mu m + total / P, v -= m.
+template <typename TV, typename TVal, int ITEMS>
+__global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t* __restrict__ layers,
+                                                              const int2* __restrict__ tiles, int ntiles, MsgView msg,
+                                                              int P, TVal* planes, int64_t n, uint32_t* mask, TV* v,
+                                                              TV* mom, double mu) {
+  griddep_wait();
+  const int nitems = P * ntiles;
+  int64_t ii[ITEMS];
+  int pp[ITEMS];
+#pragma unroll
+  for (int u = 0; u < ITEMS; ++u) {
+    const int c = static_cast<int>(blockIdx.x) + u * static_cast<int>(gridDim.x);
+    ii[u] = -1;
+    pp[u] = 0;
+    if (c < nitems) {
+      const int p = c % P;
+      const int2 tc = tiles[c / P];
+      const lags_layer_t L = layers[tc.x];
+      const int e = tc.y * DEC_NT + static_cast<int>(threadIdx.x);
+      if (e < msg.count(p, tc.x)) {
+        const int64_t s = L.slot + e;
+        const int64_t i = L.offset + msg.idx(p, s);
+        planes[static_cast<int64_t>(p) * n + i] = msg.val<TVal>(p, s);
+        atomicOr(mask + i, 1u << p);
+        ii[u] = i;
+        pp[u] = p;
+      }
+    }
+  }
+  cooperative_groups::this_grid().sync();  // every rank's pairs are in the planes and the mask
+  if (mu == 0.0) {
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int64_t i = ii[u];
+      if (i < 0) continue;
+      const uint32_t bits = mask[i];
+      if (bits == 0 || (__ffs(bits) - 1) != pp[u]) continue;  // only the lowest holding rank applies
+      const double vi = static_cast<double>(v[i]);
+      double total = 0.0;
+      for (uint32_t b = bits; b; b &= b - 1) {
+        const int q = __ffs(b) - 1;
+        total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
+      }
+      v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
+      mask[i] = 0u;
+    }
+    return;
+  }
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t bits = mask[i];
+    double total = 0.0;
+    if (bits) {
+      for (uint32_t b = bits; b; b &= b - 1) {
+        const int q = __ffs(b) - 1;
+        total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
+      }
+      mask[i] = 0u;
+    }
+    const double mnew = __dadd_rn(__dmul_rn(mu, static_cast<double>(mom[i])), __ddiv_rn(total, static_cast<double>(P)));
+    mom[i] = static_cast<TV>(mnew);
+    v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), mnew));
+  }
 }
 
 template <typename TV, typename TVal>
@@ -727,11 +800,74 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
 }  // extern "C"
 
 namespace {
+// Cooperative launch of decode_fused_kernel<TV, TVal, ITEMS> (grid <= co-resident CTAs), with
+// programmatic dependent launch when the driver takes both attributes.
+template <typename TV, typename TVal, int ITEMS>
+cudaError_t launch_fused_decode(lags_bucket_t* b, const MsgView& mv, int32_t P, int grid, void* v, void* momentum,
+                                double mu, cudaStream_t s) {
+  auto kern = decode_fused_kernel<TV, TVal, ITEMS>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(DEC_NT);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const lags_layer_t* layers = b->layers;
+  const int2* tiles = b->tiles_dec;
+  const int ntiles = b->dec_tiles;
+  TVal* planes = reinterpret_cast<TVal*>(b->planes);
+  const int64_t n = b->n_total;
+  uint32_t* mask = b->mask;
+  TV* vv = static_cast<TV*>(v);
+  TV* mm = static_cast<TV*>(momentum);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv,
+                                     mm, mu);
+  if (e != cudaSuccess) {  // without PDL
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv, mm, mu);
+  }
+  return e;
+}
+
+// Largest cooperative grid of decode_fused_kernel (co-resident CTAs on the device).
+template <typename TV, typename TVal>
+int fused_decode_grid() {
+  static int grid = 0;
+  if (grid == 0) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, decode_fused_kernel<TV, TVal, 1>, DEC_NT, 0);
+    int per8 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per8, decode_fused_kernel<TV, TVal, 8>, DEC_NT, 0);
+    grid = std::max(1, std::min(per, per8)) * num_sms();
+  }
+  return grid;
+}
+
 template <typename TV, typename TVal>
 int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* momentum, double mu, cudaStream_t s) {
   const int64_t n = b->n_total, S = b->total_k;
   const int gwork = stream_grid(S * P, 256, 8);
   TVal* planes = reinterpret_cast<TVal*>(b->planes);
+  if (P > 1 || mu != 0.0) {  // one cooperative launch: scatter, grid barrier, update
+    const int cap = fused_decode_grid<TV, TVal>();
+    const int64_t nitems = static_cast<int64_t>(P) * b->dec_tiles;
+    const int items = static_cast<int>((nitems + cap - 1) / cap);
+    const int grid = static_cast<int>(std::min<int64_t>(nitems, cap));
+    cudaError_t e = cudaErrorNotSupported;
+    if (items <= 1) e = launch_fused_decode<TV, TVal, 1>(b, mv, P, grid, v, momentum, mu, s);
+    else if (items <= 2) e = launch_fused_decode<TV, TVal, 2>(b, mv, P, grid, v, momentum, mu, s);
+    else if (items <= 4) e = launch_fused_decode<TV, TVal, 4>(b, mv, P, grid, v, momentum, mu, s);
+    else if (items <= 8) e = launch_fused_decode<TV, TVal, 8>(b, mv, P, grid, v, momentum, mu, s);
+    if (e == cudaSuccess) return cuda_check("decode(fused)", 1);
+    if (items <= 8) return fail(LAGS_ERR_CUDA, std::string("fused decode launch: ") + cudaGetErrorString(e));
+    // more than 8 pairs per thread of a co-resident grid: the two-kernel decode below
+  }
   if (mu != 0.0) {
     decode_scatter_kernel<TVal><<<P * b->dec_tiles, DEC_NT, 0, s>>>(b->layers, b->tiles_dec, mv, P, planes, n, b->mask);
     decode_momentum_kernel<TV, TVal><<<stream_grid(n, 256, 8), 256, 0, s>>>(

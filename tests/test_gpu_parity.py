@@ -507,3 +507,46 @@ def test_survey_config_full_size_vs_oracle(L, config):
                 want_r[off[j] + w_idx] = 0.0
             assert _same_bits(r_new, want_r), (config, it)
     assert int(st.item()) == 0
+
+
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_multi_rank_momentum_decode_exact(L, P):
+    """Decode of P > 1 messages with heavy-ball momentum (one cooperative launch: scatter, grid
+    barrier, dense update).  The reference has no momentum (R: SPEC.md:366), so its definition is
+    this library's: total = fp64 rank-ordered sum of the sent values (R: training.py:248,253),
+    m = fl32(mu * m + total / P), v = fl32(v - m) with fp64 intermediates -- emulated exactly in
+    numpy over 6 chained steps (bit equality, not a tolerance)."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [300_000, 7, 5_000, 70_001]
+    ks = [300, 1, 50, 70]
+    n = sum(dims)
+    b = L.Bucket(dims, ks, N.F32, max_world=P)
+    gen = torch.Generator(device="cuda").manual_seed(17 + P)
+    rs = [torch.zeros(n, device="cuda") for _ in range(P)]
+    v = torch.randn(n, device="cuda", generator=gen)
+    m = torch.zeros(n, device="cuda")
+    v_h = v.cpu().numpy().copy()
+    m_h = m.cpu().numpy().copy()
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    off = np.concatenate([[0], np.cumsum(dims)])
+    mu = 0.9
+    for t in range(6):
+        msgs = b.new_messages(P)
+        for p in range(P):
+            b.compress(torch.randn(n, device="cuda", generator=gen), rs[p],
+                       0.1, msgs[p * b.msg_bytes:(p + 1) * b.msg_bytes], st)
+        b.decode(msgs, P, v, momentum=m, mu=mu)
+        total = np.zeros(n)
+        for p in range(P):  # rank order, fp64 adds (entries a rank did not send add nothing)
+            sent = np.zeros(n)
+            for j, (ii, vv) in enumerate(b.unpack(msgs[p * b.msg_bytes:(p + 1) * b.msg_bytes])):
+                sent[off[j] + ii] = vv
+            total = total + sent
+        mnew = np.float64(mu) * m_h.astype(np.float64) + total / np.float64(P)
+        m_h = mnew.astype(np.float32)
+        v_h = (v_h.astype(np.float64) - mnew).astype(np.float32)
+        torch.cuda.synchronize()
+        assert m.cpu().numpy().tobytes() == m_h.tobytes(), t
+        assert v.cpu().numpy().tobytes() == v_h.tobytes(), t
+    assert int(st.item()) == 0
