@@ -490,6 +490,9 @@ def run_ours(args, dims, ks, world, rank, local):
         train = measure_train(args, world, rank, local, dev)
     if not args.no_e2e:  # all ranks: at N > 1 each rank is one worker of the drop-in (NCCL group)
         e2e = measure_e2e(args, dims, ks, L, dev, world, rank, union)
+    decode = None
+    if world == 1:  # the P-rank decode alone (emulated messages), N = 1 only
+        decode = measure_decode(dims, ks, dev, P=8)
     if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
         threads = os.cpu_count() or 1
         s, reps = cpu_oracle_step_rate(dims, ks, 1, threads, budget=args.cpu_budget)
@@ -519,6 +522,7 @@ def run_ours(args, dims, ks, world, rank, local):
                             + (")" if world == 1 else " and receive parity; peer-memory exchange)")) if graphs is not None
             else "eager (ctypes -> cudaLaunchKernelEx with programmatic dependent launch)",
             "resnet50_train": train,
+            "decode_P8": decode,
             "exchange": exchange,
             "selection": {"layers": len(dims),
                           "dense_fallbacks_in_timed_region": int(stats[:, 1].sum() - stats0[:, 1].sum()),
@@ -528,6 +532,55 @@ def run_ours(args, dims, ks, world, rank, local):
         print(json.dumps(out), flush=True)
     if peer is not None:
         peer.close()  # collective
+
+
+def measure_decode(dims, ks, dev, P=8, reps=50):
+    """The rank-ordered decode of P ranks' messages on one GPU (the step after the exchange at
+    N = P): one cooperative launch.  mu = 0 (reference parity: only touched weights) is reported as
+    latency; mu > 0 (heavy-ball momentum, a dense pass) as GB/s against 16 d + 8 pairs bytes
+    (read + write of v and m, the received pairs) and the copy peak."""
+    import torch
+
+    import paper_1911_08727_b200 as L
+    from paper_1911_08727_b200 import _native as N
+
+    n = sum(dims)
+    b = L.Bucket(dims, ks, N.F32, max_world=P)
+    gen = torch.Generator(device=dev).manual_seed(3)
+    msgs = b.new_messages(P)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    r = torch.zeros(n, device=dev)
+    for p in range(P):
+        r.zero_()
+        for _ in range(3):
+            b.compress(torch.randn(n, device=dev, generator=gen), r, 0.1, msgs[p * b.msg_bytes:(p + 1) * b.msg_bytes], st)
+    del r
+    v = torch.randn(n, device=dev, generator=gen)
+    m = torch.zeros(n, device=dev)
+    pairs = sum(int(b.counts_view(msgs[p * b.msg_bytes:(p + 1) * b.msg_bytes]).sum()) for p in range(P))
+    out = {"P": P, "pairs": pairs, "launches_per_decode": 1}
+    for mu in (0.0, 0.9):
+        for _ in range(10):
+            b.decode(msgs, P, v, momentum=m if mu else None, mu=mu)
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            b.decode(msgs, P, v, momentum=m if mu else None, mu=mu)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        us = e0.elapsed_time(e1) / reps * 1e3
+        if mu == 0.0:
+            out["mu0_us"] = round(us, 2)
+        else:
+            byt = 16 * n + 8 * pairs
+            peak, _ = read_peaks()
+            out["momentum_us"] = round(us, 2)
+            out["momentum_GBs"] = round(byt / (us * 1e-6) / 1e9, 1)
+            out["momentum_frac"] = round(byt / (us * 1e-6) / 1e9 / peak, 4)
+            out["momentum_algorithmic_bytes"] = int(byt)
+    assert int(st.item()) == 0
+    return out
 
 
 TRAIN_WINDOWS = 5

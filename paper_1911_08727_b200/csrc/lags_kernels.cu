@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstdlib>
 #include <cstring>
@@ -162,17 +163,50 @@ __global__ void __launch_bounds__(DEC_NT) decode_update_kernel(const lags_layer_
   mask[i] = 0u;
 }
 
+// Rank-ordered fp64 sum of the planes holding element i (bits = its rank mask): the loads of a
+// batch of 8 ranks are issued together (predicated), then added in rank order (R: training.py:248,253).
+template <typename TVal>
+__device__ __forceinline__ double plane_sum(const TVal* planes, int64_t n, int64_t i, uint32_t bits, int P) {
+  double total = 0.0;
+  for (int q0 = 0; q0 < P; q0 += 8) {
+    TVal x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      x[u] = (bits >> (q0 + u)) & 1u ? planes[static_cast<int64_t>(q0 + u) * n + i] : TVal(0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if ((bits >> (q0 + u)) & 1u) total = __dadd_rn(total, static_cast<double>(x[u]));
+  }
+  return total;
+}
+
+// Momentum update of one element: m = fl(mu m + upd), v = fl(v - m) with fp64 intermediates, upd =
+// total / P (+0.0 for an element no rank sent: 0 / P without the division).
+template <typename TV>
+__device__ __forceinline__ void momentum_update(TV& v, TV& m, double upd, double mu) {
+#ifdef LAGS_MOM_F32_PROBE  // diagnostic only (different rounding): is the fp64 arithmetic the bound?
+  const float mf = __fadd_rn(__fmul_rn(static_cast<float>(mu), static_cast<float>(m)), static_cast<float>(upd));
+  m = static_cast<TV>(mf);
+  v = static_cast<TV>(__fsub_rn(static_cast<float>(v), mf));
+  return;
+#endif
+  const double mnew = __dadd_rn(__dmul_rn(mu, static_cast<double>(m)), upd);
+  m = static_cast<TV>(mnew);
+  v = static_cast<TV>(__dsub_rn(static_cast<double>(v), mnew));
+}
+
 // The whole decode of P > 1 messages in ONE cooperative launch: phase A scatters every rank's
 // pairs into its plane and marks the rank bitmask; a grid-wide barrier; phase B lets the lowest
 // rank holding index i sum the planes in rank order (fp64) and apply v - total / P
 // (R: training.py:248,253-254) -- each thread keeps its ITEMS (element, rank) pairs in registers
 // across the barrier, so phase B starts from the mask without re-reading the messages.  With
-// momentum (mu > 0) phase B is a dense pass over the bucket: m = mu m + total / P, v -= m.
-template <typename TV, typename TVal, int ITEMS>
+// momentum (mu > 0) phase B is a dense pass over the bucket (16-byte vectors when v and m are
+// aligned): m = mu m + total / P, v -= m.
+template <typename TV, typename TVal, int ITEMS, bool MOM>
 __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t* __restrict__ layers,
                                                               const int2* __restrict__ tiles, int ntiles, MsgView msg,
                                                               int P, TVal* planes, int64_t n, uint32_t* mask, TV* v,
-                                                              TV* mom, double mu) {
+                                                              TV* mom, double mu, uint32_t* touched) {
   griddep_wait();
   const int nitems = P * ntiles;
   int64_t ii[ITEMS];
@@ -192,13 +226,14 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t
         const int64_t i = L.offset + msg.idx(p, s);
         planes[static_cast<int64_t>(p) * n + i] = msg.val<TVal>(p, s);
         atomicOr(mask + i, 1u << p);
+        if (MOM) atomicOr(touched + (i >> 5), 1u << (i & 31));  // the dense pass skips the mask
         ii[u] = i;
         pp[u] = p;
       }
     }
   }
   cooperative_groups::this_grid().sync();  // every rank's pairs are in the planes and the mask
-  if (mu == 0.0) {
+  if (!MOM) {
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
       const int64_t i = ii[u];
@@ -206,30 +241,60 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t
       const uint32_t bits = mask[i];
       if (bits == 0 || (__ffs(bits) - 1) != pp[u]) continue;  // only the lowest holding rank applies
       const double vi = static_cast<double>(v[i]);
-      double total = 0.0;
-      for (uint32_t b = bits; b; b &= b - 1) {
-        const int q = __ffs(b) - 1;
-        total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
-      }
+      const double total = plane_sum(planes, n, i, bits, P);
       v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
       mask[i] = 0u;
     }
     return;
   }
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t bits = mask[i];
-    double total = 0.0;
-    if (bits) {
-      for (uint32_t b = bits; b; b &= b - 1) {
-        const int q = __ffs(b) - 1;
-        total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
+  // dense momentum pass, one 16-byte vector of v and m per thread and iteration: the touched
+  // bitmap (1 bit per element, 8 threads share a word through L1) replaces the per-element rank
+  // mask, which only the touched elements read, so the pass moves 16 B per element (v and m read
+  // and written); each thread clears its own bits of the bitmap (atomicAnd, touched groups only)
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  constexpr int VW = 16 / sizeof(TV);  // elements per 16-byte vector
+  using VT = typename std::conditional<sizeof(TV) == 4, float4, double2>::type;
+  const bool vec = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(mom)) & 15u) == 0;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / VW;
+    VT* v4 = reinterpret_cast<VT*>(v);
+    VT* m4 = reinterpret_cast<VT*>(mom);
+    for (int64_t q = tid; q < nv; q += nthreads) {
+      const int64_t i0 = q * VW;
+      const uint32_t sh = static_cast<uint32_t>(i0 & 31);
+      const uint32_t grp = (__ldg(touched + (i0 >> 5)) >> sh) & ((1u << VW) - 1u);
+      VT vv = __ldcs(v4 + q), mm = __ldcs(m4 + q);
+      TV* ve = reinterpret_cast<TV*>(&vv);
+      TV* me = reinterpret_cast<TV*>(&mm);
+#pragma unroll
+      for (int u = 0; u < VW; ++u) {
+        double upd = 0.0;
+        if ((grp >> u) & 1u) {
+          const uint32_t bits = mask[i0 + u];
+          upd = __ddiv_rn(plane_sum(planes, n, i0 + u, bits, P), static_cast<double>(P));
+          mask[i0 + u] = 0u;
+        }
+        momentum_update(ve[u], me[u], upd, mu);
       }
-      mask[i] = 0u;
+      __stcs(v4 + q, vv);
+      __stcs(m4 + q, mm);
+      if (grp) atomicAnd(touched + (i0 >> 5), ~(((1u << VW) - 1u) << sh));
     }
-    const double mnew = __dadd_rn(__dmul_rn(mu, static_cast<double>(mom[i])), __ddiv_rn(total, static_cast<double>(P)));
-    mom[i] = static_cast<TV>(mnew);
-    v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), mnew));
+    done = nv * VW;
+  }
+  for (int64_t i = done + tid; i < n; i += nthreads) {  // unaligned buffers / the tail
+    const uint32_t bits = mask[i];
+    const double upd = bits ? __ddiv_rn(plane_sum(planes, n, i, bits, P), static_cast<double>(P)) : 0.0;
+    if (bits) {
+      mask[i] = 0u;
+      atomicAnd(touched + (i >> 5), ~(1u << (i & 31)));
+    }
+    TV vi = v[i], mi = mom[i];
+    momentum_update(vi, mi, upd, mu);
+    mom[i] = mi;
+    v[i] = vi;
   }
 }
 
@@ -363,6 +428,7 @@ struct lags_bucket {
   int dec_tiles = 0;
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
   uint32_t* hist = nullptr;       // fp32: per-layer candidate-key histograms (K1 -> select_kernel)
+  uint32_t* touched = nullptr;    // decode with momentum: one bit per element sent by any rank
   // selection groups of an fp32 bucket (plan_groups): 0 persistent role, 1 cluster role, 2 warp
   // role; each group's tasks and `order` entries are contiguous
   struct Group {
@@ -444,7 +510,7 @@ struct Plan {
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
          o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
-         o_hist = 0, bytes = 0;
+         o_hist = 0, o_touched = 0, bytes = 0;
   int32_t ntiles = 0;
 };
 
@@ -496,6 +562,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   const bool f32 = dtype == LAGS_F32;
   p->o_ctr = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (SelectCounters)
   p->o_hist = take(f32 ? sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(L) : 0);
+  p->o_touched = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total / 32 + 1));
   p->bytes = o;
   return LAGS_OK;
 }
@@ -605,6 +672,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->dec_tiles = p.ntiles;
   b->sel_ctr.work = reinterpret_cast<uint32_t*>(base + p.o_ctr);
   b->hist = dtype == LAGS_F32 ? reinterpret_cast<uint32_t*>(base + p.o_hist) : nullptr;
+  b->touched = reinterpret_cast<uint32_t*>(base + p.o_touched);
   b->off_cnt = 0;
   b->off_idx = static_cast<int64_t>(align_up(4 * static_cast<size_t>(nlayers), 16));
   b->off_val = static_cast<int64_t>(align_up(b->off_idx + 4 * static_cast<size_t>(p.total_k), 16));
@@ -669,6 +737,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
+      cudaMemsetAsync(b->touched, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total / 32 + 1), s) == cudaSuccess &&
       (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
       (dtype != LAGS_F32 ||
        cudaMemsetAsync(b->hist, 0, sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(nlayers), s) == cudaSuccess) &&
@@ -802,10 +871,10 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
 namespace {
 // Cooperative launch of decode_fused_kernel<TV, TVal, ITEMS> (grid <= co-resident CTAs), with
 // programmatic dependent launch when the driver takes both attributes.
-template <typename TV, typename TVal, int ITEMS>
+template <typename TV, typename TVal, int ITEMS, bool MOM>
 cudaError_t launch_fused_decode(lags_bucket_t* b, const MsgView& mv, int32_t P, int grid, void* v, void* momentum,
                                 double mu, cudaStream_t s) {
-  auto kern = decode_fused_kernel<TV, TVal, ITEMS>;
+  auto kern = decode_fused_kernel<TV, TVal, ITEMS, MOM>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(DEC_NT);
@@ -825,28 +894,45 @@ cudaError_t launch_fused_decode(lags_bucket_t* b, const MsgView& mv, int32_t P, 
   uint32_t* mask = b->mask;
   TV* vv = static_cast<TV*>(v);
   TV* mm = static_cast<TV*>(momentum);
+  uint32_t* touched = b->touched;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv,
-                                     mm, mu);
+                                     mm, mu, touched);
   if (e != cudaSuccess) {  // without PDL
     cudaGetLastError();
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv, mm, mu);
+    e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv, mm, mu,
+                           touched);
   }
   return e;
 }
 
 // Largest cooperative grid of decode_fused_kernel (co-resident CTAs on the device).
-template <typename TV, typename TVal>
+template <typename TV, typename TVal, bool MOM>
 int fused_decode_grid() {
   static int grid = 0;
   if (grid == 0) {
     int per = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, decode_fused_kernel<TV, TVal, 1>, DEC_NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, decode_fused_kernel<TV, TVal, 1, MOM>, DEC_NT, 0);
     int per8 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per8, decode_fused_kernel<TV, TVal, 8>, DEC_NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per8, decode_fused_kernel<TV, TVal, 8, MOM>, DEC_NT, 0);
     grid = std::max(1, std::min(per, per8)) * num_sms();
   }
   return grid;
+}
+
+template <typename TV, typename TVal, bool MOM>
+cudaError_t fused_decode(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* momentum, double mu,
+                         cudaStream_t s) {
+  const int cap = fused_decode_grid<TV, TVal, MOM>();
+  const int64_t nitems = static_cast<int64_t>(P) * b->dec_tiles;
+  const int items = static_cast<int>((nitems + cap - 1) / cap);
+  // momentum: the dense pass wants every co-resident CTA; otherwise one CTA per work item
+  const int grid = MOM ? cap : static_cast<int>(std::min<int64_t>(nitems, cap));
+  if (items <= 1) return launch_fused_decode<TV, TVal, 1, MOM>(b, mv, P, grid, v, momentum, mu, s);
+  if (items <= 2) return launch_fused_decode<TV, TVal, 2, MOM>(b, mv, P, grid, v, momentum, mu, s);
+  if (items <= 4) return launch_fused_decode<TV, TVal, 4, MOM>(b, mv, P, grid, v, momentum, mu, s);
+  if (items <= 8) return launch_fused_decode<TV, TVal, 8, MOM>(b, mv, P, grid, v, momentum, mu, s);
+  return cudaErrorNotSupported;  // more than 8 pairs per thread of a co-resident grid
 }
 
 template <typename TV, typename TVal>
@@ -855,17 +941,11 @@ int decode_impl(lags_bucket_t* b, const MsgView& mv, int32_t P, void* v, void* m
   const int gwork = stream_grid(S * P, 256, 8);
   TVal* planes = reinterpret_cast<TVal*>(b->planes);
   if (P > 1 || mu != 0.0) {  // one cooperative launch: scatter, grid barrier, update
-    const int cap = fused_decode_grid<TV, TVal>();
-    const int64_t nitems = static_cast<int64_t>(P) * b->dec_tiles;
-    const int items = static_cast<int>((nitems + cap - 1) / cap);
-    const int grid = static_cast<int>(std::min<int64_t>(nitems, cap));
-    cudaError_t e = cudaErrorNotSupported;
-    if (items <= 1) e = launch_fused_decode<TV, TVal, 1>(b, mv, P, grid, v, momentum, mu, s);
-    else if (items <= 2) e = launch_fused_decode<TV, TVal, 2>(b, mv, P, grid, v, momentum, mu, s);
-    else if (items <= 4) e = launch_fused_decode<TV, TVal, 4>(b, mv, P, grid, v, momentum, mu, s);
-    else if (items <= 8) e = launch_fused_decode<TV, TVal, 8>(b, mv, P, grid, v, momentum, mu, s);
+    const cudaError_t e = mu != 0.0 ? fused_decode<TV, TVal, true>(b, mv, P, v, momentum, mu, s)
+                                    : fused_decode<TV, TVal, false>(b, mv, P, v, momentum, mu, s);
     if (e == cudaSuccess) return cuda_check("decode(fused)", 1);
-    if (items <= 8) return fail(LAGS_ERR_CUDA, std::string("fused decode launch: ") + cudaGetErrorString(e));
+    if (e != cudaErrorNotSupported)
+      return fail(LAGS_ERR_CUDA, std::string("fused decode launch: ") + cudaGetErrorString(e));
     // more than 8 pairs per thread of a co-resident grid: the two-kernel decode below
   }
   if (mu != 0.0) {
