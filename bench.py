@@ -613,7 +613,7 @@ def measure_train(args, world, rank, local, dev):
         else:
             net = model
             opt = LagsSGD(model.parameters(), lr=0.1, rho=RHO, bucket_cap_bytes=args.bucket_cap,
-                          exchange=(kind == "lags"))
+                          exchange=(args.train_exchange if kind == "lags" else False))
 
         def it():
             with torch.autocast("cuda", dtype=torch.bfloat16):
@@ -656,11 +656,12 @@ def measure_train(args, world, rank, local, dev):
     exposed_ms = diffs[len(diffs) // 2]
     opt = arms["lags"]["opt"]
     opt.enable_timing(True)
-    per_it = []  # the per-bucket side-stream spans include waiting for the slowest rank: median of 5
+    per_it = []  # per-bucket stream spans of 5 iterations (max over ranks), median reported
     for _ in range(5):
         arms["lags"]["it"]()
         times = opt.bucket_times_ms()
-        c = torch.tensor([sum(t[1] for t in times), sum(t[0] for t in times), sum(t[2] for t in times)], device=dev)
+        c = torch.tensor([sum(t[1] for t in times), sum(t[0] for t in times), sum(t[2] for t in times),
+                          sum(t[3] for t in times), sum(t[4] for t in times)], device=dev)
         if world > 1:
             dist.all_reduce(c, op=dist.ReduceOp.MAX)
         per_it.append([float(v) for v in c])
@@ -677,11 +678,18 @@ def measure_train(args, world, rank, local, dev):
            "dense_ddp_iter_per_s": round(1e3 / dense_ms, 3), "dense_ms_per_iter": round(dense_ms, 3),
            "lags_no_exchange_ms_per_iter": round(nx_ms, 3),
            "sum_compress_ms": round(comm[1], 3), "sum_exchange_ms": round(comm[0], 3),
-           "sum_decode_ms": round(comm[2], 3), "windows": TRAIN_WINDOWS, "window_order": "interleaved",
+           "sum_decode_ms": round(comm[2], 3), "sum_transfer_ms": round(comm[3], 4),
+           "sum_peer_wait_ms": round(comm[4], 4), "exchange": args.train_exchange if world > 1 else None,
+           "streams": "compress on a compute-side stream, exchange + decode on a serial communication stream",
+           "windows": TRAIN_WINDOWS, "window_order": "interleaved",
            "ms_per_iter_windows": all_windows, "exposed_exchange_ms": round(exposed_ms, 3)}
-    if world > 1 and comm[0] > 0:
+    if world > 1 and comm[3] > 0:
+        # hidden fraction of the exchange (R: perf.py:173-195's network channel): the transfer spans
+        # (push kernels / all-gathers on the communication stream) against the exposed time, the
+        # median paired LAGS - no-exchange difference (which also holds the P > 1 decode)
         exposed = max(0.0, exposed_ms)
-        out["exchange_hidden_fraction"] = round(max(0.0, min(1.0, 1.0 - exposed / comm[0])), 4)
+        out["exchange_hidden_fraction"] = round(max(0.0, min(1.0, 1.0 - exposed / comm[3])), 4)
+        out["hidden_fraction_definition"] = "1 - exposed_exchange_ms / sum_transfer_ms"
     return out
 
 
@@ -755,6 +763,8 @@ def main():
     ap.add_argument("--train-steps", type=int, default=20)
     ap.add_argument("--train-warmup", type=int, default=8)
     ap.add_argument("--bucket-cap", type=int, default=1 << 16, help="fusion capacity (bytes) for LagsSGD")
+    ap.add_argument("--train-exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="LagsSGD exchange in the training measurement (N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     dims = resnet50_dims()

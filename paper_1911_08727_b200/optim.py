@@ -7,14 +7,16 @@ the overlap of communication with backprop (R: perf.py:173-195).  Here every ran
   reference's layer layout (R: layered.py:46-107); ``p.data`` / ``p.grad`` are views into them;
 * layers are grouped into fusion buckets in backprop order with the reference's flush rule
   (R: sparsify.py:209-238), using the fixed k_l-slot message of each layer as the chunk size;
-* a ``post_accumulate_grad`` hook marks a parameter ready; when a bucket is complete it is launched
-  on a side stream: compress (residual add + per-layer exact top-k + residual zeroing + fused
-  zero_grad) -> all-gather of the fixed-size sparse messages (NCCL over NVLink) -> rank-ordered
-  fp64 decode + SGD (or momentum) update of the bucket's weights.  Buckets launch strictly in
-  release order on every rank ("one serial network channel in release order", R: perf.py:188-193),
-  so layer l's exchange overlaps the backprop of layers < l;
-* ``step()`` launches buckets whose hooks never fired, then makes the compute stream wait for the
-  side stream (the next forward trails the last arrival, R: perf.py:194).
+* a ``post_accumulate_grad`` hook marks a parameter ready; when a bucket is complete its compress
+  (residual add + per-layer exact top-k + residual zeroing + fused zero_grad) is launched on a
+  compute-side stream, and its exchange of the fixed-size sparse messages (the peer-memory push over
+  NVLink, or the NCCL all-gather) plus the rank-ordered fp64 decode + SGD (or momentum) update of
+  the bucket's weights on a separate communication stream: the reference's two resources, compute
+  (backprop + sparsify) and one serial network channel in release order (R: perf.py:173-195).
+  Buckets launch in release order on every rank, so layer l's exchange overlaps the backprop of
+  layers < l, and bucket l+1's compress never queues behind bucket l's exchange;
+* ``step()`` launches buckets whose hooks never fired, then makes the compute stream wait for both
+  streams (the next forward trails the last arrival, R: perf.py:194).
 
 Numerics per layer and rank are exactly ``lags_step``'s (fp32 storage, lr absorbed into the
 residual as in R: training.py:250): selection bit-exact, aggregation in fp64 in rank order.
@@ -27,6 +29,8 @@ from typing import Callable, Iterable, Sequence
 
 import torch
 import torch.distributed as dist
+
+from contextlib import nullcontext as _nullctx
 
 from .errors import DivergenceError
 from .sparsify import CompressionPolicy
@@ -79,6 +83,8 @@ class _BucketRT:
     gtab: torch.Tensor | None = None   # grads="tensors": device table of per-layer gradient pointers
     ring: list | None = None           # pinned host staging slots for the table, with their events
     slot: int = 0
+    peer: object = None                # exchange="p2p": the bucket's PeerExchange
+    ready: object = None               # event: the bucket's compress has been issued on the side stream
 
 
 _RING = 4  # host staging slots per bucket (a slot is reused only after its copy has completed)
@@ -101,7 +107,7 @@ class LagsSGD(torch.optim.Optimizer):
     def __init__(self, params: Iterable[torch.nn.Parameter], lr: float, rho: float | None = None,
                  policy: CompressionPolicy | None = None, momentum: float = 0.0, process_group=None,
                  bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1,
-                 exchange: bool = True, delta_every: int = 0, grads: str = "auto"):
+                 exchange: bool | str = True, delta_every: int = 0, grads: str = "auto"):
         params = [p for p in params]
         if not params:
             raise ValueError("no parameters")
@@ -125,9 +131,15 @@ class LagsSGD(torch.optim.Optimizer):
                              f"32 bits), got {self.world}")
         self.check_every = max(1, int(check_every))
         self.mu = float(momentum)
-        # exchange=False replaces the all-gather by a local no-op (decode of the own message only):
-        # a measurement mode for the exposed-communication time, not a training mode
-        self.exchange = bool(exchange)
+        # exchange: "nccl" (all-gather; True), "p2p" (peer-memory push over CUDA IPC / NVLink, one
+        # receive area per bucket), or False: a local no-op (decode of the own message only) -- a
+        # measurement mode for the exposed-communication time, not a training mode
+        if exchange is True:
+            exchange = "nccl"
+        if exchange not in (False, "nccl", "p2p"):
+            raise ValueError(f"exchange must be True, False, 'nccl' or 'p2p', got {exchange!r}")
+        self.exchange = exchange is not False
+        self.exchange_mode = exchange if self.world > 1 and exchange else None
         # delta_every > 0: every that many steps, log the aggregation-quality ratio delta^(l) of
         # every layer on the device (R: training.py:320-337, delta_log_every); it all-gathers the
         # residuals once per logged step (dense traffic, diagnostics only)
@@ -160,7 +172,9 @@ class LagsSGD(torch.optim.Optimizer):
         self.bucket_cap_bytes = int(bucket_cap_bytes)
         self.flat_param = self.flat_grad = self.residual = self.momentum_buf = None
         self.offsets = None
-        self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None
+        self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None  # compress
+        self.comm = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None  # exchange + decode
+        self.buckets = []
         self._relayout(plan_buckets(self.dims, self.ks, self.bucket_cap_bytes))
         if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
             dist.broadcast(self.flat_param, group=process_group, group_src=0)
@@ -176,6 +190,13 @@ class LagsSGD(torch.optim.Optimizer):
         self._delta = torch.full((L,), float("nan"), dtype=torch.float64, device=self.device)
         self._delta_step = 0
         self._hook_events = None  # optional per-layer CUDA events at gradient readiness
+
+    def _join(self) -> None:
+        """The current stream waits for every launched compress, exchange and decode."""
+        if self.side is not None:
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_stream(self.side)
+            cur.wait_stream(self.comm)
 
     @staticmethod
     def _bucket_offsets(dims, ranges):
@@ -223,8 +244,7 @@ class LagsSGD(torch.optim.Optimizer):
 
     def _per_layer(self, buf) -> torch.Tensor:
         """The flat buffer without inter-bucket padding (the reference's layer layout)."""
-        if self.side is not None:
-            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._join()
         return torch.cat([buf[o:o + d] for o, d in zip(self.offsets, self.dims)])
 
     @property
@@ -246,16 +266,24 @@ class LagsSGD(torch.optim.Optimizer):
     def _build_buckets(self) -> None:
         """(Re)plan fusion buckets for the current ks; residual and momentum state are kept."""
         ranges = plan_buckets(self.dims, self.ks, self.bucket_cap_bytes)
-        if self.side is not None:
-            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._join()
         self._relayout(ranges)
+        for old in self.buckets:  # collective (every rank re-plans in the same call)
+            if old.peer is not None:
+                old.peer.close()
         self.buckets: list[_BucketRT] = []
         self._bucket_of_param = {}
         for lo, hi in ranges:
             eng = self.engine_factory(self.dims[lo:hi + 1], self.ks[lo:hi + 1], self.world, self.device)
             msg_local = eng.new_messages(1)
-            msg_all = eng.new_messages(self.world) if self.world > 1 else None
+            msg_all = eng.new_messages(self.world) if self.exchange_mode == "nccl" else None
             b = _BucketRT(lo, hi, self.offsets[lo], sum(self.dims[lo:hi + 1]), eng, msg_local, msg_all)
+            if self.exchange_mode == "p2p":
+                from .p2p import PeerExchange
+
+                b.peer = PeerExchange(eng.msg_bytes, self.group)
+            if self.device.type == "cuda":
+                b.ready = torch.cuda.Event()
             if self.grads_mode == "tensors":
                 nl = hi - lo + 1
                 b.gtab = torch.zeros(nl, dtype=torch.int64, device=self.device)
@@ -329,7 +357,7 @@ class LagsSGD(torch.optim.Optimizer):
         if times is None:
             raise RuntimeError("enable_timing() first")
         out = [0.0] * len(self.params)
-        for b, (comp, _, _) in zip(self.buckets, times):
+        for b, (comp, *_) in zip(self.buckets, times):
             for l in range(b.lo, b.hi + 1):
                 out[l] = comp / 1e3 * self.dims[l] / b.numel
         return out
@@ -403,27 +431,41 @@ class LagsSGD(torch.optim.Optimizer):
         if local and m is None and hasattr(b.engine, "step_local"):  # P = 1: update fused into selection
             b.engine.step_local(g, r, lr, v, b.msg_local, self.status, stream=stream, zero_grad=zg)
             if t is not None:
-                t[1].record(stream)
-                t[2].record(stream)
-                t[3].record(stream)
+                for e in t[1:]:
+                    e.record(stream)
             if self._log_delta_now():
                 self._log_delta(b, r, b.msg_local, 1, stream)
             return
         b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=zg)
         if t is not None:
             t[1].record(stream)
-        if self.world > 1 and self.exchange:
-            dist.all_gather_into_tensor(b.msg_all, b.msg_local, group=self.group)
-            msgs, P = b.msg_all, self.world
-        else:
-            msgs, P = b.msg_local, 1
-        if t is not None:
-            t[2].record(stream)
-        b.engine.decode(msgs, P, v, momentum=m, mu=self.mu, stream=stream)
-        if t is not None:
-            t[3].record(stream)
-        if self._log_delta_now():
-            self._log_delta(b, r, msgs, P, stream)
+        comm = stream
+        if stream is not None and self.comm is not None:  # exchange + decode on the serial network channel
+            b.ready.record(stream)
+            self.comm.wait_event(b.ready)
+            comm = self.comm
+        with torch.cuda.stream(comm) if comm is not None else _nullctx():
+            if t is not None:
+                t[2].record(comm)
+            if self.exchange_mode == "nccl":
+                dist.all_gather_into_tensor(b.msg_all, b.msg_local, group=self.group)
+                msgs, P = b.msg_all, self.world
+                if t is not None:
+                    t[3].record(comm)
+            elif self.exchange_mode == "p2p":
+                msgs = b.peer.exchange(b.msg_local, stream=comm, mid_event=t[3] if t is not None else None)
+                P = self.world
+            else:
+                msgs, P = b.msg_local, 1
+                if t is not None:
+                    t[3].record(comm)
+            if t is not None:
+                t[4].record(comm)
+            b.engine.decode(msgs, P, v, momentum=m, mu=self.mu, stream=comm)
+            if t is not None:
+                t[5].record(comm)
+            if self._log_delta_now():
+                self._log_delta(b, r, msgs, P, comm)
 
     def _log_delta_now(self) -> bool:
         return self.delta_every > 0 and (self._steps + 1) % self.delta_every == 0
@@ -443,24 +485,31 @@ class LagsSGD(torch.optim.Optimizer):
 
     def last_delta(self):
         """(step, [delta^(l) or None per layer]) of the last logged step (synchronises)."""
-        if self.side is not None:
-            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._join()
         vals = self._delta.cpu().tolist()
         return self._delta_step, [None if v != v else v for v in vals]
 
     def enable_timing(self, on: bool = True) -> None:
-        """Record CUDA events around each bucket's compress / exchange / decode."""
+        """Record CUDA events around each bucket's compress, exchange and decode."""
         if on and self.device.type == "cuda":
-            self.timing = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in self.buckets]
+            self.timing = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in self.buckets]
         else:
             self.timing = None
 
     def bucket_times_ms(self):
-        """[(compress, exchange, decode)] per bucket of the last step (synchronises)."""
+        """[(compress, exchange, decode, transfer, peer_wait)] per bucket of the last step, ms
+        (synchronises).  compress on the side stream; on the communication stream: exchange = from
+        the channel taking the bucket to its messages being available, transfer = the push (p2p)
+        or all-gather (NCCL, which includes waiting for the slowest rank), peer_wait = waiting for
+        the peers' pushes (p2p; 0 for NCCL), decode = the rank-ordered decode + update."""
         if self.timing is None:
             return None
         torch.cuda.synchronize(self.device)
-        return [(a.elapsed_time(b), b.elapsed_time(c), c.elapsed_time(d)) for a, b, c, d in self.timing]
+        out = []
+        for c0, c1, x0, x1, x2, d1 in self.timing:
+            out.append((c0.elapsed_time(c1), x0.elapsed_time(x2), x2.elapsed_time(d1), x0.elapsed_time(x1),
+                        x1.elapsed_time(x2)))
+        return out
 
     # -- optimizer API ----------------------------------------------------------------------
     @torch.no_grad()
@@ -472,8 +521,7 @@ class LagsSGD(torch.optim.Optimizer):
         while self._next < len(self.buckets):  # hooks that never fired (unused params, no backward)
             self._launch(self._next)
             self._next += 1
-        if self.side is not None:
-            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._join()
         self._pending = list(self._size)
         self._next = 0
         self._steps += 1
@@ -511,8 +559,7 @@ class LagsSGD(torch.optim.Optimizer):
         """Optimizer state plus the error-feedback residual and momentum in the reference's layer
         layout (R: layered.py:46-107, no padding) and the per-layer ratios: a true resume (the
         reference saves only final parameters, R: experiment.py:501-502)."""
-        if self.side is not None:
-            torch.cuda.current_stream(self.device).wait_stream(self.side)
+        self._join()
         sd = super().state_dict()
         sd["lags"] = {"residual": self._per_layer(self.residual),
                       "momentum": None if self.momentum_buf is None else self._per_layer(self.momentum_buf),

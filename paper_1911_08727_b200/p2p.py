@@ -72,14 +72,18 @@ class PeerExchange:
         self.calls = 0  # exchanges issued (eager or captured-and-replayed: see advance)
         dist.barrier(group=group)  # every rank has mapped every area before anyone pushes
 
-    def exchange(self, msg: torch.Tensor, stream=None) -> MessageView:
-        """All ranks' messages, rank order, after this rank's push and the wait for every peer."""
+    def exchange(self, msg: torch.Tensor, stream=None, mid_event=None) -> MessageView:
+        """All ranks' messages, rank order, after this rank's push and the wait for every peer.
+        ``mid_event`` (a torch.cuda.Event) is recorded between the push and the wait: the push's
+        span is the transfer, the wait's the peers' skew."""
         if msg.numel() * msg.element_size() < self.msg_bytes:
             raise ValueError("message tensor smaller than msg_bytes")
         self.calls += 1
         s = stream_handle(stream)
         N.check(N.lags_p2p_push(msg.data_ptr(), self.msg_bytes, self.bases_dev.data_ptr(), self.world, self.rank,
                                 self.G, self.flags_bytes, self.epoch_dev.data_ptr(), s), "lags_p2p_push")
+        if mid_event is not None:
+            mid_event.record(stream if stream is not None else torch.cuda.current_stream())
         N.check(N.lags_p2p_wait(self.base, self.world * self.G, self.epoch_dev.data_ptr(), self.status.data_ptr(),
                                 self.timeout_ns, s), "lags_p2p_wait")
         off = self.flags_bytes + (self.calls & 1) * self.world * self.msg_bytes

@@ -308,3 +308,21 @@ def test_two_process_group_dropin_one_gpu_gloo(tmp_path):
         msg = str(outs[p]["div"])
         assert msg.startswith("9:") and "worker 2" in msg, msg
         assert bool(outs[p]["div_res_ok"])
+
+
+@pytest.mark.gpu2
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < WORLD, reason="needs 2 GPUs")
+@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+def test_two_rank_lagssgd_matches_oracle(mode):
+    """LagsSGD on two ranks (compress on the side stream, exchange + decode on the communication
+    stream; peer-memory push or NCCL all-gather): parameters bit-identical to the oracle's P = 2
+    step on every rank, 10 steps (tools/multi_gpu_check.py under torchrun)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={WORLD}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(root, "tools", "multi_gpu_check.py"), mode]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "OK" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]

@@ -1,7 +1,8 @@
 """Multi-GPU parity check (run under torchrun, one process per GPU, NCCL).
 
-Every rank trains the same MLP on its own data with LagsSGD (hook-driven compress -> NCCL
-all-gather -> rank-ordered decode).  Rank 0 gathers every rank's consumed gradients each step and
+Every rank trains the same MLP on its own data with LagsSGD (hook-driven compress on the side
+stream -> exchange on the communication stream: the NCCL all-gather, or with `p2p` as the first
+argument the peer-memory push -> rank-ordered decode).  Rank 0 gathers every rank's consumed gradients each step and
 replays the oracle's lags_step with P = world simulated workers; parameters must match bitwise
 on every rank.  Exit code 0 = parity.
 """
@@ -28,8 +29,10 @@ def main():
     captured = {}
     for p in model.parameters():
         p.register_post_accumulate_grad_hook(lambda p: captured.__setitem__(id(p), p.grad.detach().clone()))
-    opt = LagsSGD(model.parameters(), lr=0.05, rho=0.01, bucket_cap_bytes=8192)
-    v = opt.flat_param.cpu().numpy().copy()
+    mode = sys.argv[1] if len(sys.argv) > 1 else "nccl"
+    opt = LagsSGD(model.parameters(), lr=0.05, rho=0.01, bucket_cap_bytes=8192, exchange=mode,
+                  momentum=float(sys.argv[2]) if len(sys.argv) > 2 else 0.0)
+    v = opt.params_vector().cpu().numpy().copy()
     res = [np.zeros_like(v) for _ in range(world)]
     ok = True
     for t in range(10):
@@ -41,18 +44,19 @@ def main():
         allg = [torch.zeros_like(g) for _ in range(world)]
         dist.all_gather(allg, g)
         v = orc.lags_step(v, [a.cpu().numpy() for a in allg], 0.05, opt.dims, opt.ks, res)
-        if opt.flat_param.cpu().numpy().tobytes() != v.tobytes():
+        if opt.mu == 0.0 and opt.params_vector().cpu().numpy().tobytes() != v.tobytes():
             print(f"rank {rank}: step {t} parameters differ from the oracle", flush=True)
             ok = False
             break
-    digest = torch.tensor([float(opt.flat_param.double().sum())], device="cuda")
+    digest = torch.tensor([float(opt.params_vector().double().sum())], device="cuda")
     all_d = [torch.zeros_like(digest) for _ in range(world)]
     dist.all_gather(all_d, digest)
     same = all(float(d) == float(all_d[0]) for d in all_d)
     flag = torch.tensor([1 if (ok and same) else 0], device="cuda")
     dist.all_reduce(flag, op=dist.ReduceOp.MIN)
     if rank == 0:
-        print(f"multi-gpu parity world={world} buckets={len(opt.buckets)}: {'OK' if int(flag) else 'FAIL'}", flush=True)
+        print(f"multi-gpu parity world={world} exchange={mode} momentum={opt.mu} buckets={len(opt.buckets)}: "
+              f"{'OK' if int(flag) else 'FAIL'}", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if int(flag) else 1)
 
