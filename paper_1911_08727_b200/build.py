@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "liblagsb200.so")
 SOURCES = ["lags_kernels.cu", "lags_wire.cu", "lags_p2p.cu"]
-HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh", "lags_cluster.cuh", "lags_internal.h"]
+HEADERS = ["lags_common.cuh", "lags_select.cuh", "lags_fast.cuh", "lags_cluster.cuh", "lags_f64.cuh", "lags_internal.h"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",

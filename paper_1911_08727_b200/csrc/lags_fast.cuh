@@ -599,32 +599,28 @@ __device__ __forceinline__ WarpCut warp_resolve(const uint32_t (&kk)[WARP_CUT_KE
   return wc;
 }
 
-// The exact threshold from the keys of the cut bin (list[0..c), any order): the r-th largest of
-// them (1 <= r <= c) is T; the selection is every key > T (n_gt = above + those in the list) plus
-// the first need_eq entries equal to T in index order (R: sparsify.py:85-88, lowest index wins).
-// All threads; ends with a barrier.  Uses cs.sm.list_key / list_gt.
+// The exact threshold from the keys of the cut bin (list[0..c), any order; they share every bit
+// above HIST_SHIFT): the r-th largest of them (1 <= r <= c) is T; the selection is every key > T
+// (n_gt = above + those in the list) plus the first need_eq entries equal to T in index order
+// (R: sparsify.py:85-88, lowest index wins).  A second-level histogram over the keys' low
+// HIST_SHIFT bits (in cs.sm.hist, free after the register histogram cut) and one find_bin: O(c)
+// work over the block instead of the O(c^2) rank counting of a plain list.  All threads; ends with
+// a barrier.
+static_assert((1 << HIST_SHIFT) <= RadixSmem<Key<float>::RB>::NB, "the low bits fit the radix histogram");
 __device__ __forceinline__ SelectThreshold<uint32_t> resolve_cut(const uint32_t* list, uint32_t c, uint32_t r,
                                                                  uint32_t above, SelectSmem& cs) {
-  for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) {
-    const uint32_t mine = list[i];
-    uint32_t gt = 0, eq = 0;
-    for (uint32_t q = 0; q < c; ++q) {
-      const uint32_t x = list[q];
-      gt += x > mine ? 1u : 0u;
-      eq += x == mine ? 1u : 0u;
-    }
-    if (gt < r && r <= gt + eq) {  // equal keys write equal values
-      cs.sm.list_key = mine;
-      cs.sm.list_gt = gt;
-    }
-  }
+  constexpr uint32_t LOW = (1u << HIST_SHIFT) - 1u;
+  for (int b = threadIdx.x; b < RadixSmem<Key<float>::RB>::NB; b += SEL_NT) cs.sm.hist[b] = 0u;
   __syncthreads();
+  for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) atomicAdd(&cs.sm.hist[list[i] & LOW], 1u);
+  __syncthreads();
+  uint32_t bin, gt, in_bin;
+  find_bin<Key<float>::RB>(cs.sm, r, &bin, &gt, &in_bin);
   SelectThreshold<uint32_t> th;
-  th.prefix = cs.sm.list_key;
+  th.prefix = (list[0] & ~LOW) | bin;
   th.pmask = 0x7fffffffu;
-  th.n_gt = above + cs.sm.list_gt;
-  th.need_eq = r - cs.sm.list_gt;
-  __syncthreads();  // list_key / list_gt are read before any reuse
+  th.n_gt = above + gt;
+  th.need_eq = r - gt;
   return th;
 }
 

@@ -22,6 +22,7 @@
 #include "lags_common.cuh"
 #include "lags_internal.h"
 #include "lags_cluster.cuh"
+#include "lags_f64.cuh"
 #include "lags_fast.cuh"
 #include "lags_select.cuh"
 
@@ -417,7 +418,10 @@ struct lags_bucket {
   int32_t* slot_layer = nullptr;
   int32_t* cand_cnt = nullptr;
   int32_t* cand_idx = nullptr;
-  float* cand_val = nullptr;
+  float* cand_val = nullptr;   // LAGS_F32 candidate values (cand_val64 for LAGS_F64)
+  double* cand_val64 = nullptr;
+  double* gval64 = nullptr;
+  State64* state64 = nullptr;   // LAGS_F64 selection state
   int32_t* gidx = nullptr;
   float* gval = nullptr;
   double* acc64 = nullptr;
@@ -510,7 +514,7 @@ struct Plan {
   int32_t ntasks = 0, cap = 0;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
          o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
-         o_hist = 0, o_touched = 0, bytes = 0;
+         o_hist = 0, o_touched = 0, o_state64 = 0, bytes = 0;
   int32_t ntiles = 0;
 };
 
@@ -535,7 +539,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   const double want = 16.0 * PRED_FACTOR * max_per_task;
   int cap = 256;
   while (cap < want && cap < TASK_ELEMS) cap <<= 1;
-  p->cap = dtype == LAGS_F32 ? cap : 0;
+  p->cap = dtype == LAGS_F32_ACC64 ? 0 : cap;  // candidate lists: the fp32 and fp64 fast paths
   size_t o = 0;
   auto take = [&](size_t bytes) {
     const size_t at = o;
@@ -550,9 +554,10 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_slot = take(sizeof(int32_t) * static_cast<size_t>(p->total_k));
   p->o_ccnt = take(sizeof(int32_t) * nt);
   p->o_cidx = take(sizeof(int32_t) * nt * cp);
-  p->o_cval = take(sizeof(float) * nt * cp);
+  p->o_cval = take(val_size(dtype) * nt * cp);
   p->o_gidx = take(sizeof(int32_t) * nt * cp);
-  p->o_gval = take(sizeof(float) * nt * cp);
+  p->o_gval = take(val_size(dtype) * nt * cp);
+  p->o_state64 = take(dtype == LAGS_F64 ? sizeof(State64) * L : 0);
   p->o_acc = take(dtype == LAGS_F32_ACC64 ? sizeof(double) * static_cast<size_t>(p->n_total) : 0);
   p->o_mask = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total));
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
@@ -663,6 +668,9 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->cand_val = reinterpret_cast<float*>(base + p.o_cval);
   b->gidx = reinterpret_cast<int32_t*>(base + p.o_gidx);
   b->gval = reinterpret_cast<float*>(base + p.o_gval);
+  b->cand_val64 = reinterpret_cast<double*>(base + p.o_cval);
+  b->gval64 = reinterpret_cast<double*>(base + p.o_gval);
+  b->state64 = dtype == LAGS_F64 ? reinterpret_cast<State64*>(base + p.o_state64) : nullptr;
   b->acc64 = reinterpret_cast<double*>(base + p.o_acc);
   b->mask = reinterpret_cast<uint32_t*>(base + p.o_mask);
   b->planes = base + p.o_planes;
@@ -736,6 +744,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       cudaMemcpyAsync(b->tiles_dec, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, s) ==
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
+      (dtype != LAGS_F64 || cudaMemsetAsync(b->state64, 0, sizeof(State64) * nlayers, s) == cudaSuccess) &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
       cudaMemsetAsync(b->touched, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total / 32 + 1), s) == cudaSuccess &&
       (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
@@ -761,6 +770,25 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     for (int j = 0; j < nlayers; ++j)
       words = std::max<int64_t>(words, dims[j] <= SMALL_LAYER ? dims[j] : (15 * static_cast<int64_t>(ks[j])) / 2);
     b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), select_smem_words_max()));
+  }
+  if (dtype == LAGS_F64) {
+    static int words64 = 0;  // the device's opt-in shared memory minus select64_kernel's static part
+    if (words64 == 0) {
+      int dev = 0, optin = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, select64_kernel);
+      words64 = std::max(4096, static_cast<int>((static_cast<size_t>(optin) - fa.sharedSizeBytes - 1024) / 4) / 1024 * 1024);
+      if (cudaFuncSetAttribute(select64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, words64 * 4) != cudaSuccess) {
+        delete b;
+        return cuda_check("select64 kernel attributes", 0);
+      }
+    }
+    // candidate staging: value (2 words) + index per candidate, ~2.5 k of them at the adaptive margin
+    int64_t words = 4096;
+    for (int j = 0; j < nlayers; ++j) words = std::max<int64_t>(words, 3 * ((5 * static_cast<int64_t>(ks[j])) / 2) + 2);
+    b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), words64));
   }
   *out = b;
   return LAGS_OK;
@@ -846,13 +874,24 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     return cuda_check("lags_bucket_compress(f32)", launches);
   }
   if (v_update) return fail(LAGS_ERR_INVALID_ARG, "fused single-rank update needs an LAGS_F32 bucket");
-  if (b->dtype == LAGS_F64) {
-    accum_kernel<double, double><<<stream_grid(n, 256, 8), 256, 0, s>>>(
-        static_cast<const double*>(g), static_cast<double*>(r), static_cast<double*>(r), alpha, n, status);
-    select_dense_kernel<double><<<b->nlayers, SEL_NT, 0, s>>>(b->layers, lags_layer_t{}, static_cast<double*>(r), idx,
-                                                              reinterpret_cast<double*>(m + b->off_val), cnt, 1);
-    if ((flags & LAGS_COMPRESS_ZERO_GRAD) && cudaMemsetAsync(const_cast<void*>(g), 0, sizeof(double) * n, s) != cudaSuccess)
-      return cuda_check("zero grad", 2);
+  if (b->dtype == LAGS_F64) {  // K1 (candidates above the predicted threshold) + one CTA per layer
+    const int ntasks = b->ntasks;
+    const int blocks = (ntasks + K1_WARPS - 1) / K1_WARPS;
+    double* rr = static_cast<double*>(r);
+    double* gg = static_cast<double*>(g);
+    cudaError_t e;
+    if (flags & LAGS_COMPRESS_ZERO_GRAD)
+      e = launch_pdl(accum_emit64_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
+                     b->state64, gg, rr, alpha, b->cap, b->cand_idx, b->cand_val64, b->cand_cnt, status);
+    else
+      e = launch_pdl(accum_emit64_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
+                     b->state64, gg, rr, alpha, b->cap, b->cand_idx, b->cand_val64, b->cand_cnt, status);
+    if (e == cudaSuccess)
+      e = launch_pdl(select64_kernel, dim3(b->nlayers), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s,
+                     b->layers, b->layer_tasks, b->state64, b->cand_cnt, b->cand_idx, b->cand_val64, b->cap, b->gidx,
+                     b->gval64, rr, idx, reinterpret_cast<double*>(m + b->off_val), cnt, b->smem_keys,
+                     (flags & LAGS_COMPRESS_EXACT) ? 1 : 0);
+    if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress(f64) launch: ") + cudaGetErrorString(e));
     return cuda_check("lags_bucket_compress(f64)", 2);
   }
   // LAGS_F32_ACC64: fp64 acc in the bucket memory, fp32 residual rewritten after selection

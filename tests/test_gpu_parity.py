@@ -550,3 +550,54 @@ def test_multi_rank_momentum_decode_exact(L, P):
         assert m.cpu().numpy().tobytes() == m_h.tobytes(), t
         assert v.cpu().numpy().tobytes() == v_h.tobytes(), t
     assert int(st.item()) == 0
+
+
+def test_f64_fast_path_equals_exact_path_and_oracle(L):
+    """The fp64 fast path (K1 on 64-bit keys with candidate lists + one CTA per layer) against the
+    dense exact path and the oracle, bit for bit: steady state, a threshold collapse (too few
+    candidates), a task-list overflow, an all-zero layer, tie-heavy integer data."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [20000, 64, 300000, 5000, 589824, 70001, 1000]
+    ks = [max(1, d // 1000) for d in dims]
+    fast = L.Bucket(dims, ks, N.F64)
+    exact = L.Bucket(dims, ks, N.F64)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(13)
+    r_f = torch.zeros(n, device="cuda", dtype=torch.float64)
+    r_e = torch.zeros(n, device="cuda", dtype=torch.float64)
+    r_h = np.zeros(n)
+    m_f, m_e = fast.new_messages(1), exact.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    off = np.concatenate([[0], np.cumsum(dims)])
+    for it in range(20):
+        if it >= 16:  # integer-valued: many ties
+            g = torch.randint(-6, 7, (n,), device="cuda", generator=gen).double()
+        else:
+            g = torch.randn(n, device="cuda", generator=gen, dtype=torch.float64)
+        if it in (7, 8):
+            g *= 1e-3
+        if it == 11:
+            g[off[2]:off[2] + 8192] *= 1e4
+        if it == 13:
+            g[off[4]:off[5]] = 0.0
+            r_f[off[4]:off[5]] = 0.0
+            r_e[off[4]:off[5]] = 0.0
+            r_h[off[4]:off[5]] = 0.0
+        alpha = 1.0 if it >= 16 else 0.05
+        fast.compress(g, r_f, alpha, m_f, st)
+        exact.compress(g, r_e, alpha, m_e, st, exact=True)
+        assert torch.equal(m_f, m_e), f"messages differ at iteration {it}"
+        assert torch.equal(r_f.view(torch.int64), r_e.view(torch.int64)), f"residuals differ at {it}"
+        gh = g.cpu().numpy()
+        acc = r_h + alpha * gh
+        for j, (ii, vv) in enumerate(fast.unpack(m_f)):
+            wi, wv = orc.top_k(acc[off[j]:off[j + 1]], ks[j])
+            np.testing.assert_array_equal(ii, wi)
+            assert _same_bits(vv, wv), (it, j)
+        acc_sent = acc.copy()
+        for j, (ii, vv) in enumerate(fast.unpack(m_f)):
+            acc_sent[off[j] + ii] = acc[off[j] + ii] - vv
+        r_h = acc_sent
+        assert r_f.cpu().numpy().tobytes() == r_h.tobytes(), it
+    assert int(st.item()) == 0

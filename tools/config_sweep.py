@@ -23,14 +23,15 @@ def peak_gbs():
         return None
 
 
-def run(name, dims, rho, steps=100):
+def run(name, dims, rho, steps=100, f64=False):
     ks = [min(d, max(1, int(d // (1.0 / rho)))) for d in dims]
     n = sum(dims)
-    b = L.Bucket(dims, ks, N.F32)
+    b = L.Bucket(dims, ks, N.F64 if f64 else N.F32)
+    dt = torch.float64 if f64 else torch.float32
     gen = torch.Generator(device="cuda").manual_seed(5)
-    gs = [torch.randn(n, device="cuda", generator=gen) for _ in range(3)]
-    r = torch.zeros(n, device="cuda")
-    v = torch.randn(n, device="cuda", generator=gen)
+    gs = [torch.randn(n, device="cuda", generator=gen, dtype=dt) for _ in range(3)]
+    r = torch.zeros(n, device="cuda", dtype=dt)
+    v = torch.randn(n, device="cuda", generator=gen, dtype=dt)
     msg = b.new_messages(1)
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
     for t in range(60):
@@ -58,14 +59,18 @@ def run(name, dims, rho, steps=100):
     paths = {}
     for p in s1[:, 5]:
         paths[int(p)] = paths.get(int(p), 0) + 1
-    gbs = (12 * n + 8 * sum(ks)) / (ms * 1e-3) / 1e9
+    # algorithmic bytes: compress 12 d + 8 n_sel (fp32) / 24 d + 12 n_sel (fp64); the fp64 step also
+    # runs the P = 1 decode (8 B read + 8 B write per touched weight + the 12 B pair)
+    gbs = ((24 * n + 12 * sum(ks) + 28 * sum(ks)) if f64 else (12 * n + 8 * sum(ks))) / (ms * 1e-3) / 1e9
     pk = peak_gbs()
     assert int(st.item()) == 0
-    return {"config": name, "rho": rho, "layers": len(dims), "elements": n, "max_layer": max(dims),
+    return {"config": name, "dtype": "f64" if f64 else "f32", "rho": rho, "layers": len(dims), "elements": n,
+            "max_layer": max(dims),
             "sum_k": sum(ks), "us_per_step": round(ms * 1e3, 1), "GBs": round(gbs, 1),
             "frac_of_copy_peak": round(gbs / pk, 3) if pk else None,
             "dense_fallbacks_in_timed_steps": int((s1[:, 1] - s0[:, 1]).sum()),
-            "paths": {{0: "small/tiny", 1: "candidate", 2: "dense", 3: "cluster"}[k]: v for k, v in sorted(paths.items())}}
+            "paths": ({{0: "small/tiny", 1: "candidate", 2: "dense", 3: "cluster", 4: "cluster (radix)"}[k]: v
+                       for k, v in sorted(paths.items())} if not f64 else None)}
 
 
 def main():
@@ -76,8 +81,14 @@ def main():
         ("resnet50 (config 4)", [p.numel() for p in resnet50().parameters()], 0.01),
         ("lstm-ptb (config 5)", [p.numel() for p in LSTMPTB().parameters()], 0.001),
     ]
+    only = sys.argv[1:]
     for name, dims, rho in configs:
-        print(json.dumps(run(name, dims, rho)))
+        if not only or "f32" in only:
+            print(json.dumps(run(name, dims, rho)), flush=True)
+    if not only or "f64" in only:  # the reference's default dtype (R: layered.py:88-90)
+        print(json.dumps(run("mlp 64-16-4 (config 1)", [1040, 68], 0.01, f64=True)), flush=True)
+        print(json.dumps(run("resnet50 (config 4)", [p.numel() for p in resnet50().parameters()], 0.001, f64=True)),
+              flush=True)
 
 
 if __name__ == "__main__":
