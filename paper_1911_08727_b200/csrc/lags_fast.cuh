@@ -36,16 +36,20 @@ constexpr int TINY_LAYER = 4096;   // layers up to this size always take it (che
 #ifndef LAGS_K1_MINB
 #define LAGS_K1_MINB 1
 #endif
-// K1's residual traffic (read + write of r, 8 B/element) streams through L2 with evict-first
-// priority like the gradient: normal-priority lines (the candidate lists and histograms K1 writes,
-// the weights, the selection kernel's own code) then stay in L2 for the selection that follows.
-#ifndef LAGS_R_NORMAL
-#define LAGS_R_LOAD(p) __ldcs(p)
-#define LAGS_R_STORE(p, v) __stcs((p), (v))
-#else
-#define LAGS_R_LOAD(p) (*(p))
-#define LAGS_R_STORE(p, v) (*(p) = (v))
-#endif
+// K1's residual traffic (read + write of r, 8 B/element): for a residual much larger than L2 it
+// streams through with evict-first priority like the gradient, so normal-priority lines (the
+// candidate lists and histograms K1 writes, the weights, the selection kernel's own code) stay in
+// L2 for the selection that follows (ResNet-50: 75.4 -> 71.4 us per step); a residual that fits in
+// L2 keeps normal priority and is re-read from L2 by the next step (VGG-16: 53.7 -> 49.5 us).
+template <bool RSTREAM>
+__device__ __forceinline__ float4 r_load(const float4* p) {
+  return RSTREAM ? __ldcs(p) : *p;
+}
+template <bool RSTREAM>
+__device__ __forceinline__ void r_store(float4* p, float4 v) {
+  if (RSTREAM) __stcs(p, v);
+  else *p = v;
+}
 constexpr int K1_WARPS = LAGS_K1_WARPS;  // warps per K1 CTA
 constexpr int K1_MINB = LAGS_K1_MINB;    // K1 CTAs per SM the register allocation must allow
 constexpr int K1_UNROLL = LAGS_K1_UNROLL;        // float4 loads in flight per lane per operand (K1)
@@ -169,7 +173,7 @@ __device__ __forceinline__ void emit_candidates(uint32_t bits, float4 vals, int6
 // vectors when both share an alignment, scalar otherwise.
 // ZERO_G: also clear the gradient after reading it (the optimizer's zero_grad fused into the pass;
 // +4 B/element of writes instead of a separate memset pass).
-template <bool ZERO_G, int UNROLL>
+template <bool ZERO_G, bool RSTREAM, int UNROLL>
 __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, const lags_layer_t* __restrict__ layers,
                                             const FastState* state, float* __restrict__ gt, float* __restrict__ rt,
                                             float alpha, int cap, int32_t* __restrict__ cand_idx,
@@ -215,7 +219,7 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
       const int q = q0 + u * 32 + lane;
       if (q < n4) {
         gv[u] = __ldcs(g4 + q);
-        rv[u] = LAGS_R_LOAD(r4 + q);
+        rv[u] = r_load<RSTREAM>(r4 + q);
       }
     }
     if (ZERO_G) {
@@ -236,7 +240,7 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
         a.y = accum(rv[u].y, gv[u].y, alpha);
         a.z = accum(rv[u].z, gv[u].z, alpha);
         a.w = accum(rv[u].w, gv[u].w, alpha);
-        LAGS_R_STORE(r4 + q, a);
+        r_store<RSTREAM>(r4 + q, a);
         bits = (Key<float>::of(a.x) >= thr ? 1u : 0u) | (Key<float>::of(a.y) >= thr ? 2u : 0u) |
                (Key<float>::of(a.z) >= thr ? 4u : 0u) | (Key<float>::of(a.w) >= thr ? 8u : 0u);
       }
@@ -250,7 +254,7 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
 }
 
 // K1: one warp per task.  gtab (nullable): per-layer gradient pointers replacing the flat g.
-template <bool ZERO_G>
+template <bool ZERO_G, bool RSTREAM>
 __global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
     const FastState* __restrict__ state, float* __restrict__ g, float* const* __restrict__ gtab,
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
   if (wid >= ntasks) return;
   const Task T = tasks[wid];
   float* gt = gtab ? gtab[T.layer] + (T.start - layers[T.layer].offset) : g + T.start;
-  stream_task<ZERO_G, K1_UNROLL>(T, wid, lane, layers, state, gt, r + T.start, alpha, cap, cand_idx, cand_val,
+  stream_task<ZERO_G, RSTREAM, K1_UNROLL>(T, wid, lane, layers, state, gt, r + T.start, alpha, cap, cand_idx, cand_val,
                                  cand_cnt, status, hist);
 }
 
@@ -557,7 +561,7 @@ __device__ __forceinline__ HistCut hist_cut(const HistRegs& h, SelectSmem& cs, u
 struct WarpCut {
   uint32_t key, gt, low_gt, low_eq;
 };
-constexpr int WARP_CUT_KEYS = 2;  // keys per lane (4: local-memory arrays, slower than the block path)
+constexpr int WARP_CUT_KEYS = 1;  // keys per lane: beyond 32 keys the histogram resolve is faster
 constexpr uint32_t WARP_CUT_MAX = 32u * WARP_CUT_KEYS;
 __device__ __forceinline__ WarpCut warp_resolve(const uint32_t (&kk)[WARP_CUT_KEYS],
                                                 const uint32_t (&oo)[WARP_CUT_KEYS], uint32_t c, uint32_t r,

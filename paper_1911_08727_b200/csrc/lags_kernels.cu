@@ -433,6 +433,7 @@ struct lags_bucket {
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
   uint32_t* hist = nullptr;       // fp32: per-layer candidate-key histograms (K1 -> select_kernel)
   uint32_t* touched = nullptr;    // decode with momentum: one bit per element sent by any rank
+  bool r_stream = true;           // K1 streams r with evict-first priority (r larger than half the L2)
   // selection groups of an fp32 bucket (plan_groups): 0 persistent role, 1 cluster role, 2 warp
   // role; each group's tasks and `order` entries are contiguous
   struct Group {
@@ -756,6 +757,10 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     return cuda_check("lags_bucket_create upload", 0);
   }
   if (dtype == LAGS_F32) {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    b->r_stream = static_cast<int64_t>(p.n_total) * 4 > static_cast<int64_t>(l2 > 0 ? l2 : (126 << 20)) / 2;
     const int smem = select_smem_words_max() * static_cast<int>(sizeof(uint32_t));
     if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
         cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess) {
@@ -843,14 +848,11 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     cudaError_t e = cudaSuccess;
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
     if (e == cudaSuccess) {
-      if (zg)
-        e = launch_pdl(accum_emit_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
-                       b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status,
-                       b->sel_ctr.work, b->hist);
-      else
-        e = launch_pdl(accum_emit_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
-                       b->state, gg, b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status,
-                       b->sel_ctr.work, b->hist);
+      auto kern = zg ? (b->r_stream ? accum_emit_kernel<true, true> : accum_emit_kernel<true, false>)
+                     : (b->r_stream ? accum_emit_kernel<false, true> : accum_emit_kernel<false, false>);
+      e = launch_pdl(kern, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers, b->state, gg,
+                     b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status, b->sel_ctr.work,
+                     b->hist);
     }
     if (e == cudaSuccess && b->probe_after) e = cudaEventRecord(b->probe_after, s);
     if (e == cudaSuccess) {

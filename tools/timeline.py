@@ -94,10 +94,11 @@ def main():
     end = [rel(s[j, 9]) - base for j in range(len(dims))]
     launch = [x - base for x in launch]
     rows = sorted(range(len(dims)), key=lambda j: -(end[j] - start[j]))
-    print("--- selection CTAs (us from the first CTA launch): launch, start, end, kcycles, path, dim, k, m")
+    print("--- selection CTAs (us from the first CTA launch): launch, start, end, kcycles, path, dim, k, m, "
+          "cut bin count")
     for j in rows[:8]:
         print(f"  {launch[j]:7.2f} {start[j]:7.2f} {end[j]:7.2f} {s[j, 4] // 1000:4d} {s[j, 5]} {dims[j]:8d}"
-              f" {ks[j]:5d} {s[j, 2]:6d}")
+              f" {ks[j]:5d} {s[j, 2]:6d} {int(s[j, 11]) >> 8:5d}")
     print("  latest-ending:", [(dims[j], round(end[j], 2)) for j in sorted(range(len(dims)), key=lambda j: -end[j])[:6]])
     print("  latest-launched:", [(dims[j], round(launch[j], 2))
                                  for j in sorted(range(len(dims)), key=lambda j: -launch[j])[:6]])
