@@ -512,7 +512,7 @@ int select_smem_words_max() {
 // Device memory layout shared by lags_bucket_device_bytes and lags_bucket_create.
 struct Plan {
   int64_t n_total = 0, total_k = 0;
-  int32_t ntasks = 0, cap = 0;
+  int32_t ntasks = 0, cap = 0, task_elems = TASK_ELEMS;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
          o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
          o_hist = 0, o_touched = 0, o_state64 = 0, bytes = 0;
@@ -523,6 +523,13 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   if (!valid_dtype(dtype)) return fail(LAGS_ERR_INVALID_ARG, "unknown dtype");
   if (!dims || !ks || L <= 0) return fail(LAGS_ERR_INVALID_ARG, "empty bucket");
   if (max_world < 1 || max_world > 32) return fail(LAGS_ERR_INVALID_ARG, "max_world must be in 1..32");
+  // task size: TASK_ELEMS, smaller for small buckets so that K1 still has about a warp per SM
+  // slot (ResNet-20's 0.27 M elements in 8192-element tasks were 34 warps: 20 us of latency)
+  int64_t n_all = 0;
+  for (int j = 0; j < L; ++j) n_all += std::max<int64_t>(dims[j], 0);
+  int task = TASK_ELEMS;
+  while (task > MIN_TASK_ELEMS && n_all / task < static_cast<int64_t>(num_sms()) * K1_WARPS) task >>= 1;
+  p->task_elems = task;
   double max_per_task = 0.0;  // expected selected entries in one task of a layer
   for (int j = 0; j < L; ++j) {
     if (dims[j] < 1) return fail(LAGS_ERR_STRUCTURE, "layer " + std::to_string(j + 1) + ": dim must be positive");
@@ -531,15 +538,15 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
       return fail(LAGS_ERR_K_OUT_OF_RANGE, "k=" + std::to_string(ks[j]) + " outside 1.." + std::to_string(dims[j]));
     p->n_total += dims[j];
     p->total_k += ks[j];
-    p->ntasks += static_cast<int32_t>((dims[j] + TASK_ELEMS - 1) / TASK_ELEMS);
+    p->ntasks += static_cast<int32_t>((dims[j] + task - 1) / task);
     p->ntiles += (ks[j] + DEC_NT - 1) / DEC_NT;
-    max_per_task = std::max(max_per_task, static_cast<double>(ks[j]) * std::min<int64_t>(dims[j], TASK_ELEMS) / dims[j]);
+    max_per_task = std::max(max_per_task, static_cast<double>(ks[j]) * std::min<int64_t>(dims[j], task) / dims[j]);
   }
   // per-task candidate capacity: 16x the expected PRED_FACTOR * (selected per task), power of two
   // in [256, TASK]
   const double want = 16.0 * PRED_FACTOR * max_per_task;
   int cap = 256;
-  while (cap < want && cap < TASK_ELEMS) cap <<= 1;
+  while (cap < want && cap < task) cap <<= 1;
   p->cap = dtype == LAGS_F32_ACC64 ? 0 : cap;  // candidate lists: the fp32 and fp64 fast paths
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -708,8 +715,8 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     for (int j = 0; j < nlayers; ++j) {
       if (gid[j] != g) continue;
       ltasks[j].x = static_cast<int>(tasks.size());
-      for (int64_t s = 0; s < dims[j]; s += TASK_ELEMS)
-        tasks.push_back(Task{offs[j] + s, static_cast<int32_t>(std::min<int64_t>(TASK_ELEMS, dims[j] - s)), j});
+      for (int64_t s = 0; s < dims[j]; s += p.task_elems)
+        tasks.push_back(Task{offs[j] + s, static_cast<int32_t>(std::min<int64_t>(p.task_elems, dims[j] - s)), j});
       ltasks[j].y = static_cast<int>(tasks.size());
     }
     b->grp[g].ntasks = static_cast<int>(tasks.size()) - b->grp[g].task_base;

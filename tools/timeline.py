@@ -37,7 +37,7 @@ def show(title, ks, last=12):
 
 
 def main():
-    # optional workload: resnet50 (default) | resnet50:RHO | lstm | vgg16
+    # optional workload: resnet50 (default) | resnet50:RHO | lstm | vgg16 | resnet20
     arg = sys.argv[1] if len(sys.argv) > 1 else "resnet50"
     name, _, rho = arg.partition(":")
     rho = float(rho) if rho else 0.001
@@ -47,6 +47,9 @@ def main():
     elif name == "vgg16":
         from paper_1911_08727_b200.workloads import vgg16_cifar
         dims = [p.numel() for p in vgg16_cifar().parameters()]
+    elif name == "resnet20":
+        from paper_1911_08727_b200.workloads import resnet20
+        dims = [p.numel() for p in resnet20().parameters()]
     else:
         dims = resnet50_dims()
     ks = ks_for(dims, rho)
