@@ -32,9 +32,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 RHO = 0.001
-# DRAM bytes of one K1 launch from the committed ncu --set full capture (profiles/r1e_ncu_full_raw.csv:
-# dram__bytes_read.sum 204.637440 MB + dram__bytes_write.sum 50.829568 MB; ncu flushes caches per replay)
-K1_DRAM_TRAFFIC = 255_467_008
+# Steady-state DRAM traffic of K1, measured by ncu WITHOUT cache flushes (--cache-control none, the
+# dram__bytes metrics only, consecutive launches of tools/prof_step.py): tools/k1_traffic.sh writes
+# profiles/<round>_k1_traffic.csv; the bench reports the median per launch of the newest file.
+TRAFFIC_GLOB = "profiles/*_k1_traffic.csv"
 METRIC ="LAGS sparsify/decode GB/s (ResNet-50 layer shapes, rho=0.001); iter/s of the hot-path step"
 UNIT = "GB/s"
 
@@ -57,6 +58,88 @@ def algorithmic_bytes(n, counts_per_rank, union, world):
     compress = world * (12 * n + 8 * sel)
     decode = world * (8 * world * sel + 8 * union)
     return compress, decode
+
+
+def read_k1_traffic():
+    """(median DRAM bytes per K1 launch, source file) from the newest committed ncu traffic capture."""
+    import csv
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, TRAFFIC_GLOB)), key=os.path.getmtime)
+    if not files:
+        return None, None
+    per = {}
+    with open(files[-1]) as fh:
+        rows = [r for r in csv.reader(fh)]
+    hdr = next((i for i, r in enumerate(rows) if "Metric Name" in r), None)
+    if hdr is None:
+        return None, None
+    h = rows[hdr]
+    ik, iid, im, iv, iu = (h.index("Kernel Name"), h.index("ID"), h.index("Metric Name"), h.index("Metric Value"),
+                           h.index("Metric Unit"))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    for r in rows[hdr + 1:]:
+        if len(r) <= iu or "accum_emit" not in r[ik] or not r[im].startswith("dram__bytes_"):
+            continue
+        per.setdefault(r[iid], 0.0)
+        per[r[iid]] += float(r[iv].replace(",", "")) * scale.get(r[iu], 1.0)
+    if not per:
+        return None, None
+    vals = sorted(per.values())
+    return int(vals[len(vals) // 2]), os.path.relpath(files[-1], ROOT) + f" (median of {len(vals)} K1 launches)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def one_core_baseline(dims, ks, budget=8.0):
+    """the reference algorithm (numpy oracle port, stable argsort as the
+    reference) pinned to ONE core (sched_setaffinity + 1 BLAS / OpenMP thread) in a subprocess, on
+    a bounded sample: the largest layers of the ResNet-50 shapes adding up to about 1/8 of the
+    elements, repeated for about `budget` seconds; reported as full-model-equivalent GB/s."""
+    code = f"""
+import os, sys, time, json
+import numpy as np
+os.sched_setaffinity(0, {{sorted(os.sched_getaffinity(0))[0]}})
+sys.path.insert(0, {ROOT!r})
+from oracle import lagsgd_oracle as orc
+dims, ks = {list(dims)!r}, {list(ks)!r}
+order = sorted(range(len(dims)), key=lambda j: -dims[j])
+pick, tot = [], 0
+for j in order:
+    if tot >= sum(dims) / 8: break
+    pick.append(j); tot += dims[j]
+pick.sort()
+sd, sk = [dims[j] for j in pick], [ks[j] for j in pick]
+n = sum(sd)
+rng = np.random.default_rng(0)
+v = rng.standard_normal(n).astype(np.float32)
+g = [rng.standard_normal(n).astype(np.float32)]
+r = [np.zeros(n, np.float32)]
+orc.lags_step(v, g, 0.1, sd, sk, r, ranking="argsort")
+t, reps = 0.0, 0
+while reps == 0 or t < {budget}:
+    t0 = time.perf_counter(); orc.lags_step(v, g, 0.1, sd, sk, r, ranking="argsort"); t += time.perf_counter() - t0; reps += 1
+print(json.dumps({{"n": n, "sel": sum(sk), "s_per_step": t / reps, "reps": reps, "layers": len(pick)}}))
+"""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # pragma: no cover - reported, not fatal
+        return {"error": str(exc)[:200]}
+    cb, dbb = algorithmic_bytes(d["n"], [d["sel"]], d["sel"], 1)
+    return {"value": round((cb + dbb) / d["s_per_step"] / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{d['layers']} largest ResNet-50 layers ({d['n']} elements, 1/8 of the model), {d['reps']} "
+                      f"lags_steps, {d['s_per_step']:.3f} s each, pinned to one core",
+            "nproc": os.cpu_count(), "cpu_model": cpu_model()}
 
 
 def read_peaks():
@@ -166,11 +249,11 @@ def cpu_oracle_step_rate(dims, ks, world, threads, budget=10.0, seed=0):
     v = rng.standard_normal(n).astype(np.float32)
     grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
     res = [(0.01 * rng.standard_normal(n)).astype(np.float32) for _ in range(world)]
-    orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)  # warm-up (page faults, pools)
+    orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads, ranking="argsort")  # warm-up (page faults, pools)
     total, reps = 0.0, 0
     while reps == 0 or total < budget:
         t0 = time.perf_counter()
-        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)
+        v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads, ranking="argsort")
         total += time.perf_counter() - t0
         reps += 1
     return total / reps, reps
@@ -189,7 +272,7 @@ def run_reference(args, dims, ks, world, rank):
     grads = [rng.standard_normal(n).astype(np.float32) for _ in range(world)]
     res = [np.zeros(n, np.float32) for _ in range(world)]
     t0 = time.perf_counter()
-    v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads)  # one full step sizes the sample
+    v = orc.lags_step(v, grads, 0.1, dims, ks, res, threads=threads, ranking="argsort")  # one full step sizes the sample
     t_full = time.perf_counter() - t0
     # bound the whole run to ~budget seconds: each step processes one group of layers (groups of
     # roughly equal element count cycle over the whole model)
@@ -214,12 +297,12 @@ def run_reference(args, dims, ks, world, rank):
         samples.append((gd, gk, cat(v), [cat(g) for g in grads], [cat(r) for r in res]))
     for i in range(args.warmup):
         gd, gk, vv, gg, rr = samples[i % len(samples)]
-        orc.lags_step(vv, gg, 0.1, gd, gk, rr, threads=threads)
+        orc.lags_step(vv, gg, 0.1, gd, gk, rr, threads=threads, ranking="argsort")
     t, done_bytes = 0.0, 0
     for i in range(args.steps):
         gd, gk, vv, gg, rr = samples[(args.warmup + i) % len(samples)]
         t0 = time.perf_counter()
-        orc.lags_step(vv, gg, 0.1, gd, gk, rr, threads=threads)
+        orc.lags_step(vv, gg, 0.1, gd, gk, rr, threads=threads, ranking="argsort")
         t += time.perf_counter() - t0
         comp, dec = algorithmic_bytes(sum(gd), gk, sum(gk) * world, world)
         done_bytes += comp + dec
@@ -235,8 +318,9 @@ def run_reference(args, dims, ks, world, rank):
         "cpu_baseline": {"value": round(val, 4), "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"each step = 1 of {len(groups)} layer groups of the ResNet-50-shaped lags_step "
                                    f"(P={world} simulated workers; full step measured {t_full:.2f} s), numpy oracle "
-                                   f"port of R: training.py:227-255, layers over {threads} threads; ms_per_step and "
-                                   f"iter_per_s are full-model equivalents"},
+                                   f"port of R: training.py:227-255 with the reference's stable argsort ranking, "
+                                   f"layers over {threads} threads; ms_per_step and iter_per_s are full-model "
+                                   f"equivalents", "nproc": os.cpu_count(), "cpu_model": cpu_model()},
         "e2e": {"value": round(val, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -478,6 +562,7 @@ def run_ours(args, dims, ks, world, rank, local):
                                        "alg_GBs": round(palg, 2), "bus_GBs": round(palg * (world - 1) / world, 2)}
             assert int(peer.status.item()) == 0, "peer exchange timed out"
     peak, peak_src = read_peaks()
+    k1_traffic, traffic_src = read_k1_traffic()
     comp_bytes_rank = 12 * n + 8 * sel_local
     achieved = comp_bytes_rank / (comp_ms / 1e3) / 1e9
 
@@ -499,7 +584,9 @@ def run_ours(args, dims, ks, world, rank, local):
         cb, dbb = algorithmic_bytes(n, ks, sum(ks), 1)
         cpu = {"value": round((cb + dbb) / s / 1e9, 4), "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{reps} full ResNet-50-shaped lags_steps, P=1 ({reps * s:.1f} s, mean {s:.3f} s/step; "
-                         f"numpy oracle of R: training.py:227-255)"}
+                         f"numpy oracle of R: training.py:227-255, stable argsort ranking as the reference, layers "
+                         f"over {threads} threads)", "nproc": os.cpu_count(), "cpu_model": cpu_model(),
+               "one_core": one_core_baseline(dims, ks)}
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -510,8 +597,9 @@ def run_ours(args, dims, ks, world, rank, local):
             "roofline": {"kernel": "K1 accum_emit_kernel (dominant: acc = r + a*g, r <- acc, candidate emission)",
                          "bound": "hbm", "achieved": round(12 * n / (k1_ms / 1e3) / 1e9, 2), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",
-                         "frac": round(12 * n / (k1_ms / 1e3) / 1e9 / peak, 4), "traffic": K1_DRAM_TRAFFIC,
-                         "traffic_source": "profiles/r1e_ncu_full_raw.csv dram__bytes_read.sum + dram__bytes_write.sum",
+                         "frac": round(12 * n / (k1_ms / 1e3) / 1e9 / peak, 4), "traffic": k1_traffic,
+                         "traffic_source": (f"{traffic_src}: dram__bytes_read.sum + dram__bytes_write.sum, ncu "
+                                            f"--cache-control none (steady state)") if traffic_src else None,
                          "algorithmic_bytes_per_launch": int(12 * n), "ms_per_launch": round(k1_ms, 4),
                          "compress": {"what": "K1 + K2 select/compact (+fused P=1 update at N=1)",
                                       "achieved": round(achieved, 2), "frac": round(achieved / peak, 4),

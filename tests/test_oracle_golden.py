@@ -19,10 +19,11 @@ def _bits(a):
     return np.ascontiguousarray(a).view(np.uint8)
 
 
-def test_topk_golden(topk_cases):
+@pytest.mark.parametrize("ranking", orc.RANKINGS)
+def test_topk_golden(topk_cases, ranking):
     assert len(topk_cases) > 100
     for x, k, idx, val in topk_cases:
-        got_i, got_v = orc.top_k(x, k)
+        got_i, got_v = orc.top_k(x, k, ranking)
         assert got_i.dtype == np.int64
         np.testing.assert_array_equal(got_i, idx)
         assert got_v.dtype == val.dtype
@@ -61,10 +62,11 @@ def test_topk_brute_force():
         assert ours == best
 
 
-def test_lags_step_golden(step_cases):
+@pytest.mark.parametrize("ranking", orc.RANKINGS)
+def test_lags_step_golden(step_cases, ranking):
     for c in step_cases:
         res = [r.copy() for r in c["r_in"]]
-        out = orc.lags_step(c["v"], list(c["g"]), c["alpha"], c["dims"], c["counts"], res)
+        out = orc.lags_step(c["v"], list(c["g"]), c["alpha"], c["dims"], c["counts"], res, ranking=ranking)
         assert out.dtype == c["v_out"].dtype
         assert _bits(out).tobytes() == _bits(c["v_out"]).tobytes()
         for a, b in zip(res, c["r_out"]):
