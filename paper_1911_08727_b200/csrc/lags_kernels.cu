@@ -125,6 +125,17 @@ __global__ void __launch_bounds__(256) decode_single_kernel(const lags_layer_t* 
 // dependent-load chain is tile -> (layer, count) -> pair -> planes (the latency-bound part).
 constexpr int DEC_NT = 256;
 
+// A decode tile with everything its threads need to address their pairs: the layer's first flat
+// element and id, the tile's first message slot and entry, and how many of its DEC_NT slots lie in
+// the layer (so the pair loads can be issued before the layer's count is known).
+struct DecTile {
+  int64_t offset;  // the layer's first flat element
+  int32_t slot;    // message slot of the tile's first entry (layer slot + e0)
+  int32_t layer;
+  int32_t e0;      // the tile's first entry within the layer
+  int32_t len;     // entries of the tile within the layer's k slots
+};
+
 template <typename TVal>
 __global__ void __launch_bounds__(DEC_NT) decode_scatter_kernel(const lags_layer_t* __restrict__ layers,
                                                                 const int2* __restrict__ tiles, MsgView msg, int P,
@@ -204,8 +215,7 @@ __device__ __forceinline__ void momentum_update(TV& v, TV& m, double upd, double
 // momentum (mu > 0) phase B is a dense pass over the bucket (16-byte vectors when v and m are
 // aligned): m = mu m + total / P, v -= m.
 template <typename TV, typename TVal, int ITEMS, bool MOM>
-__global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t* __restrict__ layers,
-                                                              const int2* __restrict__ tiles, int ntiles, MsgView msg,
+__global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const DecTile* __restrict__ tiles, int ntiles, MsgView msg,
                                                               int P, TVal* planes, int64_t n, uint32_t* mask, TV* v,
                                                               TV* mom, double mu, uint32_t* touched) {
   griddep_wait();
@@ -219,13 +229,19 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t
     pp[u] = 0;
     if (c < nitems) {
       const int p = c % P;
-      const int2 tc = tiles[c / P];
-      const lags_layer_t L = layers[tc.x];
-      const int e = tc.y * DEC_NT + static_cast<int>(threadIdx.x);
-      if (e < msg.count(p, tc.x)) {
-        const int64_t s = L.slot + e;
-        const int64_t i = L.offset + msg.idx(p, s);
-        planes[static_cast<int64_t>(p) * n + i] = msg.val<TVal>(p, s);
+      const DecTile tl = tiles[c / P];
+      const int e = static_cast<int>(threadIdx.x);
+      // the pair and the layer's count in one round trip (the slot is inside the layer's k slots)
+      int32_t cnt = 0, ix = 0;
+      TVal x = TVal(0);
+      if (e < tl.len) {
+        cnt = msg.count(p, tl.layer);
+        ix = msg.idx(p, tl.slot + e);
+        x = msg.val<TVal>(p, tl.slot + e);
+      }
+      if (e < tl.len && tl.e0 + e < cnt) {
+        const int64_t i = tl.offset + ix;
+        planes[static_cast<int64_t>(p) * n + i] = x;
         atomicOr(mask + i, 1u << p);
         if (MOM) atomicOr(touched + (i >> 5), 1u << (i & 31));  // the dense pass skips the mask
         ii[u] = i;
@@ -240,8 +256,9 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const lags_layer_t
       const int64_t i = ii[u];
       if (i < 0) continue;
       const uint32_t bits = mask[i];
+      const TV vold = v[i];  // in flight with the mask
       if (bits == 0 || (__ffs(bits) - 1) != pp[u]) continue;  // only the lowest holding rank applies
-      const double vi = static_cast<double>(v[i]);
+      const double vi = static_cast<double>(vold);
       const double total = plane_sum(planes, n, i, bits, P);
       v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
       mask[i] = 0u;
@@ -429,6 +446,7 @@ struct lags_bucket {
   char* planes = nullptr;
   int32_t* order = nullptr;  // layers by decreasing selection work, group by group (persistent-role schedule)
   int2* tiles_dec = nullptr;  // decode tiles: (layer, chunk of DEC_NT slots)
+  DecTile* dtiles = nullptr;  // the same tiles with their layer offset / slot (fused decode)
   int dec_tiles = 0;
   double* delta_part = nullptr;  // [2 * ntasks] lags_bucket_delta partial sums
   uint32_t* hist = nullptr;       // fp32: per-layer candidate-key histograms (K1 -> select_kernel)
@@ -515,7 +533,7 @@ struct Plan {
   int32_t ntasks = 0, cap = 0, task_elems = TASK_ELEMS;
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
          o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
-         o_hist = 0, o_touched = 0, o_state64 = 0, bytes = 0;
+         o_hist = 0, o_touched = 0, o_state64 = 0, o_dtiles = 0, bytes = 0;
   int32_t ntiles = 0;
 };
 
@@ -576,6 +594,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_ctr = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (SelectCounters)
   p->o_hist = take(f32 ? sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(L) : 0);
   p->o_touched = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total / 32 + 1));
+  p->o_dtiles = take(sizeof(DecTile) * static_cast<size_t>(p->ntiles));
   p->bytes = o;
   return LAGS_OK;
 }
@@ -685,6 +704,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->order = reinterpret_cast<int32_t*>(base + p.o_order);
   b->delta_part = reinterpret_cast<double*>(base + p.o_delta);
   b->tiles_dec = reinterpret_cast<int2*>(base + p.o_tiles);
+  b->dtiles = reinterpret_cast<DecTile*>(base + p.o_dtiles);
   b->dec_tiles = p.ntiles;
   b->sel_ctr.work = reinterpret_cast<uint32_t*>(base + p.o_ctr);
   b->hist = dtype == LAGS_F32 ? reinterpret_cast<uint32_t*>(base + p.o_hist) : nullptr;
@@ -736,8 +756,13 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     b->grp[g].nlayers = static_cast<int>(og.size());
   }
   std::vector<int2> tiles;  // decode tiles
+  std::vector<DecTile> dtiles;
   for (int j = 0; j < nlayers; ++j)
-    for (int c = 0; c * DEC_NT < ks[j]; ++c) tiles.push_back(make_int2(j, c));
+    for (int c = 0; c * DEC_NT < ks[j]; ++c) {
+      tiles.push_back(make_int2(j, c));
+      dtiles.push_back(DecTile{offs[j], static_cast<int32_t>(layers[j].slot + c * DEC_NT), j, c * DEC_NT,
+                               std::min(DEC_NT, ks[j] - c * DEC_NT)});
+    }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const bool ok =
       cudaMemcpyAsync(b->layers, layers.data(), sizeof(lags_layer_t) * nlayers, cudaMemcpyHostToDevice, s) ==
@@ -748,6 +773,8 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       cudaMemcpyAsync(b->slot_layer, slot_layer.data(), sizeof(int32_t) * slot_layer.size(), cudaMemcpyHostToDevice,
                       s) == cudaSuccess &&
       cudaMemcpyAsync(b->order, order.data(), sizeof(int32_t) * nlayers, cudaMemcpyHostToDevice, s) ==
+          cudaSuccess &&
+      cudaMemcpyAsync(b->dtiles, dtiles.data(), sizeof(DecTile) * dtiles.size(), cudaMemcpyHostToDevice, s) ==
           cudaSuccess &&
       cudaMemcpyAsync(b->tiles_dec, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, s) ==
           cudaSuccess &&
@@ -934,8 +961,7 @@ cudaError_t launch_fused_decode(lags_bucket_t* b, const MsgView& mv, int32_t P, 
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  const lags_layer_t* layers = b->layers;
-  const int2* tiles = b->tiles_dec;
+  const DecTile* tiles = b->dtiles;
   const int ntiles = b->dec_tiles;
   TVal* planes = reinterpret_cast<TVal*>(b->planes);
   const int64_t n = b->n_total;
@@ -943,13 +969,12 @@ cudaError_t launch_fused_decode(lags_bucket_t* b, const MsgView& mv, int32_t P, 
   TV* vv = static_cast<TV*>(v);
   TV* mm = static_cast<TV*>(momentum);
   uint32_t* touched = b->touched;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv,
-                                     mm, mu, touched);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv, mm, mu,
+                                     touched);
   if (e != cudaSuccess) {  // without PDL
     cudaGetLastError();
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, layers, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv, mm, mu,
-                           touched);
+    e = cudaLaunchKernelEx(&cfg, kern, tiles, ntiles, mv, static_cast<int>(P), planes, n, mask, vv, mm, mu, touched);
   }
   return e;
 }

@@ -43,7 +43,8 @@ def main():
     torch.backends.cudnn.benchmark = True
     torch.manual_seed(0)
     model = vgg16_cifar().to(dev)
-    opt = LagsSGD(model.parameters(), lr=0.05, rho=0.001, bucket_cap_bytes=1 << 14)
+    opt = LagsSGD(model.parameters(), lr=0.05, rho=0.001, bucket_cap_bytes=1 << 14,
+                  exchange=os.environ.get("LAGS_EXCHANGE", "p2p"))
     x, y = synthetic_images(32, 32, 10, dev, seed=rank)
 
     def it():
@@ -56,6 +57,7 @@ def main():
     opt.enable_layer_timing(True)
     opt.enable_timing(True)
     it()
+    bt, st = opt.layer_backward_times(), opt.layer_spar_times()
     sizes, secs = perf.measure_allgather(device=dev)
     net = perf.fit_network(sizes, secs, world)
     pol = opt.adapt(net, ratio_cap=1000.0)
@@ -70,7 +72,9 @@ def main():
                           "ms_per_iter_adaptive": after, "network_fit": {"latency_s": net.latency,
                                                                           "inv_bandwidth_s_per_B": net.inv_bandwidth},
                           "ratios": ratios, "k_total": sum(opt.ks), "dims_total": sum(opt.dims),
-                          "buckets": len(opt.buckets)}), flush=True)
+                          "buckets": len(opt.buckets), "exchange": opt.exchange_mode,
+                          "measured_backward_ms": [round(x * 1e3, 4) for x in bt],
+                          "measured_compress_ms": [round(x * 1e3, 4) for x in st]}), flush=True)
     dist.destroy_process_group()
 
 
