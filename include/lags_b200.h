@@ -140,6 +140,18 @@ int lags_bucket_reconstruct(const lags_bucket_t* bucket, const void* msgs, int64
 int lags_bucket_delta(const lags_bucket_t* bucket, const void* acc, const void* r, int64_t plane_stride, int32_t P,
                       double* out, lags_stream_t stream);
 
+/* Residual-identity monitor -- the dense shadow sequence of R: training.py:197-200 and the
+ * identity check of R: training.py:356-369 (Eq. 10: v - x equals the mean error-feedback residual).
+ * lags_bucket_shadow_step: x = x - (alpha * g_sum) / P in fp64 (x: float64[n_total]; g_sum: the
+ * sum of the P workers' gradients in the bucket's storage dtype).
+ * lags_bucket_identity: out[j] = ||mean residual of layer j||^2 (j < nlayers), out[nlayers] =
+ * ||v - x||^2, out[nlayers + 1] = max_i |(v - x)_i - r_sum_i / P| (out: device double[nlayers + 2];
+ * v and r_sum in the storage dtype). */
+int lags_bucket_shadow_step(const lags_bucket_t* bucket, const void* g_sum, double* x, double alpha, int32_t P,
+                            lags_stream_t stream);
+int lags_bucket_identity(const lags_bucket_t* bucket, const void* v, const double* x, const void* r_sum, int32_t P,
+                         double* out, lags_stream_t stream);
+
 /* ---- single-vector operators ---------------------------------------------------------------- */
 
 /* Finiteness of x[0:n) (R: training.py:174); ORs LAGS_STATUS_NONFINITE into *status. */

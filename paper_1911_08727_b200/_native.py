@@ -59,6 +59,8 @@ lags_bucket_set_probe_events = _fn("lags_bucket_set_probe_events", C.c_int, _vp,
 lags_bucket_set_grad_table = _fn("lags_bucket_set_grad_table", C.c_int, _vp, _vp)
 lags_bucket_reconstruct = _fn("lags_bucket_reconstruct", C.c_int, _vp, _vp, _i64, _i32, _vp, _vp, _i64, _vp)
 lags_bucket_delta = _fn("lags_bucket_delta", C.c_int, _vp, _vp, _vp, _i64, _i32, _vp, _vp)
+lags_bucket_shadow_step = _fn("lags_bucket_shadow_step", C.c_int, _vp, _vp, _vp, _dbl, _i32, _vp)
+lags_bucket_identity = _fn("lags_bucket_identity", C.c_int, _vp, _vp, _vp, _vp, _i32, _vp, _vp)
 lags_check_finite = _fn("lags_check_finite", C.c_int, _i32, _vp, _i64, _vp, _vp)
 lags_top_k_workspace_bytes = _fn("lags_top_k_workspace_bytes", _sz, _i32, _i64)
 lags_top_k = _fn("lags_top_k", C.c_int, _i32, _vp, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp)
@@ -84,7 +86,8 @@ EXPORTS = [
     "lags_abi_version", "lags_last_error", "lags_kernel_launches", "lags_bucket_device_bytes",
     "lags_bucket_create", "lags_bucket_destroy", "lags_bucket_message_layout", "lags_bucket_compress",
     "lags_bucket_decode_update", "lags_bucket_stats", "lags_bucket_step_local", "lags_bucket_set_probe_events", "lags_bucket_set_grad_table",
-    "lags_check_finite", "lags_bucket_reconstruct", "lags_bucket_delta",
+    "lags_check_finite", "lags_bucket_reconstruct", "lags_bucket_delta", "lags_bucket_shadow_step",
+    "lags_bucket_identity",
     "lags_top_k_workspace_bytes",
     "lags_top_k", "lags_decompress", "lags_wire_encode", "lags_wire_decode",
     "lags_ipc_malloc", "lags_ipc_open", "lags_ipc_close", "lags_ipc_free", "lags_p2p_push", "lags_p2p_wait",

@@ -398,6 +398,76 @@ __global__ void delta_final_kernel(const lags_layer_t* __restrict__ layers, cons
   out[j] = denom == 0.0 ? __longlong_as_double(0x7ff8000000000000ll) : __ddiv_rn(num, denom);
 }
 
+// ------------------------------------------------------------------------------------------
+// residual-identity monitor (R: training.py:356-369 with the dense shadow sequence of
+// R: training.py:197-200): x -= (alpha * sum_p g_p) / P every step, and on logged steps per layer
+// ||mean residual||, plus ||v - x|| and max |(v - x) - mean residual| (Eq. 10: the gap between
+// the sparsified and the dense sequence is exactly the mean error-feedback residual).
+// ------------------------------------------------------------------------------------------
+template <typename TV>
+__global__ void __launch_bounds__(256) shadow_step_kernel(const TV* __restrict__ gsum, double* x, double alpha, int P,
+                                                          int64_t n) {
+  griddep_wait();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+    x[i] = __dsub_rn(x[i], __ddiv_rn(__dmul_rn(alpha, static_cast<double>(gsum[i])), static_cast<double>(P)));
+}
+
+template <typename TV>
+__global__ void __launch_bounds__(256) identity_partial_kernel(const Task* __restrict__ tasks, int ntasks,
+                                                               const TV* __restrict__ v, const double* __restrict__ x,
+                                                               const TV* __restrict__ rsum, int P, double* part) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5);
+  griddep_wait();
+  if (w >= ntasks) return;
+  const Task tk = tasks[w];
+  double gsq = 0.0, msq = 0.0, dmax = 0.0;
+  for (int64_t i = tk.start + lane; i < tk.start + tk.len; i += 32) {
+    const double gap = __dsub_rn(static_cast<double>(v[i]), x[i]);
+    const double mres = __ddiv_rn(static_cast<double>(rsum[i]), static_cast<double>(P));
+    gsq = __fma_rn(gap, gap, gsq);
+    msq = __fma_rn(mres, mres, msq);
+    dmax = fmax(dmax, fabs(__dsub_rn(gap, mres)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gsq = __dadd_rn(gsq, __shfl_down_sync(0xffffffffu, gsq, o));
+    msq = __dadd_rn(msq, __shfl_down_sync(0xffffffffu, msq, o));
+    dmax = fmax(dmax, __shfl_down_sync(0xffffffffu, dmax, o));
+  }
+  if (lane == 0) {
+    part[3 * w] = gsq;
+    part[3 * w + 1] = msq;
+    part[3 * w + 2] = dmax;
+  }
+}
+
+// out[j] = sum of mean-residual squares of layer j; out[L] = sum of gap squares; out[L+1] = max
+// deviation (one CTA, deterministic task order).
+__global__ void identity_final_kernel(const int2* __restrict__ layer_tasks, int nlayers,
+                                      const double* __restrict__ part, double* out) {
+  griddep_wait();
+  for (int j = threadIdx.x; j < nlayers; j += blockDim.x) {
+    const int2 tr = layer_tasks[j];
+    double msq = 0.0;
+    for (int t = tr.x; t < tr.y; ++t) msq = __dadd_rn(msq, part[3 * t + 1]);
+    out[j] = msq;
+  }
+  if (threadIdx.x == 0) {
+    double gsq = 0.0, dmax = 0.0;
+    for (int j = 0; j < nlayers; ++j) {
+      const int2 tr = layer_tasks[j];
+      for (int t = tr.x; t < tr.y; ++t) {
+        gsq = __dadd_rn(gsq, part[3 * t]);
+        dmax = fmax(dmax, part[3 * t + 2]);
+      }
+    }
+    out[nlayers] = gsq;
+    out[nlayers + 1] = dmax;
+  }
+}
+
 // acc_p[L.offset + idx] = val for every sent pair of message p (acc_p pre-filled with r_p).
 template <typename T>
 __global__ void __launch_bounds__(256) reconstruct_kernel(const lags_layer_t* __restrict__ layers,
@@ -588,7 +658,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_mask = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total));
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
   p->o_order = take(sizeof(int32_t) * L);
-  p->o_delta = take(2 * sizeof(double) * nt);
+  p->o_delta = take(3 * sizeof(double) * nt);  // delta (2 per task) / identity monitor (3 per task)
   p->o_tiles = take(sizeof(int2) * static_cast<size_t>(p->ntiles));
   const bool f32 = dtype == LAGS_F32;
   p->o_ctr = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (SelectCounters)
@@ -1144,6 +1214,35 @@ int lags_bucket_delta(const lags_bucket_t* b, const void* acc, const void* r, in
   delta_final_kernel<<<(b->nlayers + 127) / 128, 128, 0, s>>>(b->layers, b->layer_tasks, b->nlayers, b->delta_part,
                                                               out);
   return cuda_check("delta kernels", 2);
+}
+
+int lags_bucket_shadow_step(const lags_bucket_t* b, const void* g_sum, double* x, double alpha, int32_t P,
+                            lags_stream_t stream) {
+  if (!b || !g_sum || !x) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_shadow_step: null pointer");
+  if (P < 1) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_shadow_step: P must be >= 1");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = stream_grid(b->n_total, 256, 8);
+  if (b->dtype == LAGS_F64)
+    shadow_step_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(g_sum), x, alpha, P, b->n_total);
+  else
+    shadow_step_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(g_sum), x, alpha, P, b->n_total);
+  return cuda_check("shadow_step_kernel");
+}
+
+int lags_bucket_identity(const lags_bucket_t* b, const void* v, const double* x, const void* r_sum, int32_t P,
+                         double* out, lags_stream_t stream) {
+  if (!b || !v || !x || !r_sum || !out) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_identity: null pointer");
+  if (P < 1) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_identity: P must be >= 1");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int blocks = (b->ntasks + 7) / 8;
+  if (b->dtype == LAGS_F64)
+    identity_partial_kernel<double><<<blocks, 256, 0, s>>>(b->tasks, b->ntasks, static_cast<const double*>(v), x,
+                                                           static_cast<const double*>(r_sum), P, b->delta_part);
+  else
+    identity_partial_kernel<float><<<blocks, 256, 0, s>>>(b->tasks, b->ntasks, static_cast<const float*>(v), x,
+                                                          static_cast<const float*>(r_sum), P, b->delta_part);
+  identity_final_kernel<<<1, 256, 0, s>>>(b->layer_tasks, b->nlayers, b->delta_part, out);
+  return cuda_check("identity kernels", 2);
 }
 
 int lags_check_finite(int32_t dtype, const void* x, int64_t n, uint32_t* status, lags_stream_t stream) {

@@ -184,6 +184,24 @@ class Bucket:
                                     stream_handle(stream)), "lags_bucket_delta")
         return out
 
+    # -- residual-identity monitor (R: training.py:197-200, 356-369) -----------------------------
+    def shadow_step(self, g_sum: torch.Tensor, x: torch.Tensor, alpha: float, P: int, stream=None) -> None:
+        """Dense shadow sequence: x -= (alpha * g_sum) / P in float64 (g_sum: the workers' summed
+        gradient in the storage dtype)."""
+        if x.dtype != torch.float64 or x.numel() < self.n_total or g_sum.dtype != storage_dtype(self.mode):
+            raise TypeError("shadow_step: x float64 and g_sum in the bucket's storage dtype")
+        N.check(N.lags_bucket_shadow_step(self._h, g_sum.data_ptr(), x.data_ptr(), float(alpha), int(P),
+                                          stream_handle(stream)), "lags_bucket_shadow_step")
+
+    def identity(self, v: torch.Tensor, x: torch.Tensor, r_sum: torch.Tensor, P: int, out: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+        """[||mean residual of layer j||^2 per layer, ||v - x||^2, max |(v - x) - r_sum / P|] (float64
+        device tensor of nlayers + 2)."""
+        out = torch.empty(self.nlayers + 2, dtype=torch.float64, device=self.device) if out is None else out
+        N.check(N.lags_bucket_identity(self._h, v.data_ptr(), x.data_ptr(), r_sum.data_ptr(), int(P), out.data_ptr(),
+                                       stream_handle(stream)), "lags_bucket_identity")
+        return out
+
     # -- sparse wire format (R: sparsify.py:260-310) -------------------------------------------
     def _wire_tables(self, layer_ids):
         if getattr(self, "_wire", None) is None or self._wire[0] != tuple(layer_ids):

@@ -107,7 +107,7 @@ class LagsSGD(torch.optim.Optimizer):
     def __init__(self, params: Iterable[torch.nn.Parameter], lr: float, rho: float | None = None,
                  policy: CompressionPolicy | None = None, momentum: float = 0.0, process_group=None,
                  bucket_cap_bytes: int = 1 << 20, engine_factory: Callable | None = None, check_every: int = 1,
-                 exchange: bool | str = True, delta_every: int = 0, grads: str = "auto"):
+                 exchange: bool | str = True, delta_every: int = 0, grads: str = "auto", monitor_every: int = 0):
         params = [p for p in params]
         if not params:
             raise ValueError("no parameters")
@@ -144,6 +144,13 @@ class LagsSGD(torch.optim.Optimizer):
         # every layer on the device (R: training.py:320-337, delta_log_every); it all-gathers the
         # residuals once per logged step (dense traffic, diagnostics only)
         self.delta_every = int(delta_every)
+        # monitor_every > 0: the residual-identity monitor of R: training.py:356-369 -- a dense fp64
+        # shadow sequence x advanced every step with the workers' mean gradient (R: training.py:197-200;
+        # a dense all-reduce of each bucket's gradient at N > 1: a diagnostic mode), and every that
+        # many steps ||v - x||, max |(v - x) - mean residual| and the per-layer mean-residual norms
+        self.monitor_every = int(monitor_every)
+        self.shadow = None
+        self._identity = None
         if engine_factory is None:
             from . import _native as N
             from .engine import Bucket
@@ -178,6 +185,8 @@ class LagsSGD(torch.optim.Optimizer):
         self._relayout(plan_buckets(self.dims, self.ks, self.bucket_cap_bytes))
         if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
             dist.broadcast(self.flat_param, group=process_group, group_src=0)
+        if self.monitor_every > 0:
+            self.shadow = self.flat_param.double()  # x_0 = v_0 (R: training.py:278)
         self._build_buckets()
         self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._status_host = torch.zeros(1, dtype=torch.int32, pin_memory=self.device.type == "cuda")
@@ -219,7 +228,7 @@ class LagsSGD(torch.optim.Optimizer):
         old = self.offsets
 
         def moved(buf, fill_params=False):
-            new = torch.zeros(n, dtype=torch.float32, device=self.device)
+            new = torch.zeros(n, dtype=buf.dtype if buf is not None else torch.float32, device=self.device)
             for l, d in enumerate(self.dims):
                 dst = new[offsets[l]:offsets[l] + d]
                 if buf is not None:
@@ -233,6 +242,8 @@ class LagsSGD(torch.optim.Optimizer):
         self.residual = moved(self.residual)
         self.momentum_buf = moved(self.momentum_buf) if self.mu else None
         self.flat_grad = moved(self.flat_grad) if flat_mode else None
+        if getattr(self, "shadow", None) is not None:
+            self.shadow = moved(self.shadow)
         self.offsets = offsets
         for l, (p, d) in enumerate(zip(self.params, self.dims)):
             off = offsets[l]
@@ -394,12 +405,51 @@ class LagsSGD(torch.optim.Optimizer):
         with torch.cuda.stream(self.side):
             if self.grads_mode == "tensors":
                 held = self._stage_grad_table(b)
+                if self.shadow is not None:
+                    self._shadow_step(b, torch.cat([gt.reshape(-1) for _, gt in held]), lr)
                 self._run_bucket(i, b, None, r, v, m, lr, self.side)
                 for p, gt in held:  # released to autograd: the next backward hands over a fresh tensor
                     gt.record_stream(self.side)
                     p.grad = None
             else:
-                self._run_bucket(i, b, self.flat_grad[b.offset:b.offset + b.numel], r, v, m, lr, self.side)
+                g = self.flat_grad[b.offset:b.offset + b.numel]
+                if self.shadow is not None:
+                    self._shadow_step(b, g, lr)
+                self._run_bucket(i, b, g, r, v, m, lr, self.side)
+
+    def _shadow_step(self, b, g, lr) -> None:
+        """x -= lr * (sum of the workers' gradients) / P for the bucket (before the compress clears g)."""
+        gsum = g.clone()
+        if self.world > 1:
+            dist.all_reduce(gsum, group=self.group)
+        b.engine.shadow_step(gsum, self.shadow[b.offset:b.offset + b.numel], lr, self.world, stream=self.side)
+
+    def _log_identity(self) -> None:
+        """The residual identity of every bucket after this step (R: training.py:356-369)."""
+        outs = []
+        for b in self.buckets:
+            r = self.residual[b.offset:b.offset + b.numel]
+            if self.world > 1:
+                r = r.clone()
+                dist.all_reduce(r, group=self.group)
+            outs.append(b.engine.identity(self.flat_param[b.offset:b.offset + b.numel],
+                                          self.shadow[b.offset:b.offset + b.numel], r, self.world))
+        self._identity = (self._steps, outs)
+
+    def last_identity(self):
+        """(step, {"v_x_gap", "resid_dev", "residual_norms"}) of the last logged step, as the
+        reference's IterationRecord fields (R: training.py:356-369); synchronises."""
+        if self._identity is None:
+            return None
+        step, outs = self._identity
+        norms, gsq, dev = [0.0] * len(self.params), 0.0, 0.0
+        for b, o in zip(self.buckets, outs):  # buckets are in release order (layer L first)
+            h = o.cpu().tolist()
+            nl = b.hi - b.lo + 1
+            norms[b.lo:b.hi + 1] = [x ** 0.5 for x in h[:nl]]
+            gsq += h[nl]
+            dev = max(dev, h[nl + 1])
+        return step, {"v_x_gap": gsq ** 0.5, "resid_dev": dev, "residual_norms": norms}
 
     def _stage_grad_table(self, b):
         """Point the bucket's device table at its parameters' autograd gradient tensors (a pinned
@@ -525,6 +575,8 @@ class LagsSGD(torch.optim.Optimizer):
         self._pending = list(self._size)
         self._next = 0
         self._steps += 1
+        if self.shadow is not None and self._steps % self.monitor_every == 0:
+            self._log_identity()
         self._poll_status()
         return loss
 

@@ -20,10 +20,10 @@ from paper_1911_08727_b200 import _native as N  # noqa: E402
 RTOL = 1e-12
 
 
-def close(got, want):
+def close(got, want, rel=None, abs_=0.0):
     if want is None or (isinstance(want, float) and math.isnan(want)):
         return got is None
-    return got is not None and abs(got - want) <= RTOL * max(1e-300, abs(want))
+    return got is not None and abs(got - want) <= max((RTOL if rel is None else rel) * max(1e-300, abs(want)), abs_)
 
 
 def test_topk_aggregation_ratio_golden():
@@ -99,3 +99,43 @@ def test_optimizer_logs_delta_single_rank():
             assert step == t + 1
             for o, d, k, dv in zip(opt.ref_offsets, opt.dims, opt.ks, got):
                 assert close(dv, orc.topk_aggregation_ratio([acc[o:o + d]], k))
+
+
+def test_lagssgd_residual_identity_monitor():
+    """The residual-identity monitor (R: training.py:356-369): a dense fp64 shadow sequence x
+    advanced with every step's gradient (R: training.py:197-200) and, on logged steps, ||v - x||,
+    max |(v - x) - mean residual| and the per-layer mean-residual norms -- against the same
+    quantities computed in numpy from the oracle's parameter and residual trajectory (the
+    optimizer's own trajectory is bit-exact to it, test_gpu_optim.py).  Eq. 10 holds: the deviation
+    is rounding-sized next to the residual."""
+    from paper_1911_08727_b200.optim import LagsSGD
+
+    torch.manual_seed(7)
+    model = torch.nn.Sequential(torch.nn.Linear(64, 128), torch.nn.Tanh(), torch.nn.Linear(128, 10)).cuda()
+    captured = {}
+    for p in model.parameters():
+        p.register_post_accumulate_grad_hook(lambda p: captured.__setitem__(id(p), p.grad.detach().clone()))
+    opt = LagsSGD(model.parameters(), lr=0.05, rho=0.05, monitor_every=2, bucket_cap_bytes=512)
+    assert len(opt.buckets) > 1
+    v = opt.params_vector().cpu().numpy().copy()
+    x = v.astype(np.float64)
+    res = [np.zeros_like(v)]
+    off = np.concatenate([[0], np.cumsum(opt.dims)])
+    for t in range(6):
+        xin = torch.randn(32, 64, device="cuda")
+        y = torch.randint(0, 10, (32,), device="cuda")
+        torch.nn.functional.cross_entropy(model(xin), y).backward()
+        opt.step()
+        g = torch.cat([captured[id(p)].reshape(-1) for p in opt.params]).cpu().numpy()
+        v = orc.lags_step(v, [g], 0.05, opt.dims, opt.ks, res)
+        x = x - (0.05 * g.astype(np.float64)) / 1.0
+        if (t + 1) % 2 == 0:
+            step, got = opt.last_identity()
+            assert step == t + 1
+            gap = v.astype(np.float64) - x
+            mres = res[0].astype(np.float64)
+            assert close(got["v_x_gap"], float(np.sqrt(gap @ gap)), rel=1e-9)
+            assert close(got["resid_dev"], float(np.max(np.abs(gap - mres))), rel=1e-6, abs_=1e-12)
+            want = [float(np.sqrt(mres[a:b] @ mres[a:b])) for a, b in zip(off[:-1], off[1:])]
+            assert all(close(a, b, rel=1e-9) for a, b in zip(got["residual_norms"], want))
+            assert got["resid_dev"] < 1e-5 * max(got["residual_norms"])  # Eq. 10 up to fp32 rounding of v
