@@ -413,6 +413,7 @@ def run_ours(args, dims, ks, world, rank, local):
     # N > 1 with the peer-memory exchange (all launches are this library's, the exchange epoch is
     # device-resident) one per (gradient buffer, receive parity), replayed in capture order.
     graphs = None
+    chain = None
     l_graph = 0
     n_replay = 0
     if not args.no_graph and (world == 1 or (peer is not None and args.graph_mgpu)):
@@ -435,6 +436,17 @@ def run_ours(args, dims, ks, world, rank, local):
             if peer is not None:
                 peer.calls = c0  # captured, not executed: replays advance it
             l_graph = (N.lags_kernel_launches() - lc0) // NGR  # our kernels per captured step
+            if world == 1:  # chains of consecutive steps in one graph: steps link by PDL, no graph-launch gap
+                chain = {}
+                for reps in CHAIN_REPS:
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, stream=cap):
+                        for _ in range(reps):
+                            for i in range(NG):
+                                bucket.step_local(g_bufs[i], r, alpha, v, msg_local, status, stream=cap)
+                    chain[reps * NG] = gr
+                    for _ in range(2):
+                        gr.replay()
             for i in range(2 * NGR):  # graph warm-up replays (steps like any other)
                 graphs[n_replay % NGR].replay()
                 n_replay += 1
@@ -442,6 +454,7 @@ def run_ours(args, dims, ks, world, rank, local):
         except Exception as exc:  # pragma: no cover - report and time eagerly
             print(f"cuda graph capture failed ({exc}); timing eager launches", file=sys.stderr)
             graphs = None
+            chain = None
             if peer is not None:  # a failed capture must not leave the exchange state behind
                 raise
     if world > 1:
@@ -454,12 +467,20 @@ def run_ours(args, dims, ks, world, rank, local):
         dist.barrier()
     wall0 = time.time()
     start.record(stream)
-    for t in range(args.steps):
-        if graphs is not None:
+    t = 0
+    while t < args.steps:
+        fit = [c for c in (chain or {}) if c <= args.steps - t] if n_replay % NG == 0 else []
+        if fit:
+            chain[max(fit)].replay()  # steps t .. t + c - 1 (gradient buffers 0 .. NG - 1, repeated)
+            n_replay += max(fit)
+            t += max(fit)
+        elif graphs is not None:
             graphs[n_replay % len(graphs)].replay()
             n_replay += 1
+            t += 1
         else:
             step(t)
+            t += 1
     stop.record(stream)
     torch.cuda.synchronize(dev)
     wall1 = time.time()
@@ -606,8 +627,11 @@ def run_ours(args, dims, ks, world, rank, local):
                                       "algorithmic_bytes_per_call": int(comp_bytes_rank),
                                       "ms_per_call": round(comp_ms, 4)}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clk,
-            "launch_mode": ("cuda graph replay (one captured step per gradient buffer"
-                            + (")" if world == 1 else " and receive parity; peer-memory exchange)")) if graphs is not None
+            "launch_mode": ("cuda graph replay (N = 1: graphs of 24, 18 and 3 consecutive steps over the three "
+                            "gradient buffers, chained by programmatic dependent launch; single-step graphs for a "
+                            "remainder)" if world == 1 else
+                            "cuda graph replay (one captured step per gradient buffer and receive parity; "
+                            "peer-memory exchange)") if graphs is not None
             else "eager (ctypes -> cudaLaunchKernelEx with programmatic dependent launch)",
             "resnet50_train": train,
             "decode_P8": decode,
@@ -670,6 +694,8 @@ def measure_decode(dims, ks, dev, P=8, reps=50):
     assert int(st.item()) == 0
     return out
 
+
+CHAIN_REPS = (8, 6, 1)  # N = 1 timing: graphs of 24, 18 and 3 consecutive steps, single-step graphs for the rest
 
 TRAIN_WINDOWS = 5
 TRAIN_KINDS = ("lags", "lags_noexchange", "dense")
