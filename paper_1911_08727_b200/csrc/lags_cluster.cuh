@@ -240,6 +240,11 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     const uint32_t w = __reduce_add_sync(0xffffffffu, qs[q]);
     if ((threadIdx.x & 31) == 0 && w) atomicAdd(&csh.qsum[q], w);
   }
+  if (threadIdx.x == 0) {  // the gather's counters (published by the barrier below)
+    cs.sm.list_n = 0u;
+    cs.sm.gtb = 0u;
+    cs.sm.diff_acc = 0u;
+  }
   const uint32_t over_any = __syncthreads_or(over) ? 1u : 0u;
   LAGS_STAMP(2);
   uint32_t m = 0, pre = 0, m_max = 0;
@@ -296,12 +301,6 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     hc = hist_cut(hr, cs, k, k2, m);
     cut = hc.bin < HIST_BINS - 1u && hc.in_bin <= BIN_LIST_MAX;
   }
-  if (threadIdx.x == 0) {
-    cs.sm.list_n = 0u;
-    cs.sm.gtb = 0u;
-    cs.sm.diff_acc = 0u;
-  }
-  __syncthreads();
   LAGS_STAMP(4);
   float* sv = reinterpret_cast<float*>(dyn);
   int32_t* si = reinterpret_cast<int32_t*>(dyn + mx4);
@@ -384,18 +383,21 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
           while (i >= off[q + 1]) ++q;
           list[i] = csh.lists[q][i - off[q]];
         }
+        clear_cut_counters(cs);
         __syncthreads();
         const SelectThreshold<uint32_t> t2 = resolve_cut(list, c, r, hc.above, cs);
         th.prefix = t2.prefix;
         gt_in = t2.n_gt - hc.above;
-        uint32_t lge = 0u;  // the lower ranks' listed keys above / equal to the threshold
+        // the lower ranks' listed keys above / equal to the threshold (the rank prefix of the list)
+        uint32_t* tot = cut_counters(cs) + 2 * BIN_LIST_MAX;
         if (threadIdx.x < c && threadIdx.x < off[rank]) {
           const uint32_t x = list[threadIdx.x];
-          lge = x > th.prefix ? 1u : (x == th.prefix ? 0x10000u : 0u);
+          if (x > th.prefix) atomicAdd(&tot[0], 1u);
+          else if (x == th.prefix) atomicAdd(&tot[1], 1u);
         }
-        lge = block_sum(lge, cs.sm);
-        low_gt = lge & 0xffffu;
-        low_eq = lge >> 16;
+        __syncthreads();
+        low_gt = tot[0];
+        low_eq = tot[1];
       }
       th.pmask = 0x7fffffffu;
       th.n_gt = hc.above + gt_in;

@@ -554,9 +554,9 @@ __device__ __forceinline__ HistCut hist_cut(const HistRegs& h, SelectSmem& cs, u
     }
   }
   __syncthreads();
-  const HistCut hc{cs.sm.found2[0], cs.sm.above2[0], cs.sm.count2[0], cs.sm.found2[1]};
-  __syncthreads();
-  return hc;
+  // (no trailing barrier: found2 / above2 / count2 are written again only by a later layer's cut,
+  // many barriers later)
+  return HistCut{cs.sm.found2[0], cs.sm.above2[0], cs.sm.count2[0], cs.sm.found2[1]};
 }
 
 // Warp-level resolution of the cut (every warp computes it redundantly: no block barrier).  The
@@ -608,28 +608,47 @@ __device__ __forceinline__ WarpCut warp_resolve(const uint32_t (&kk)[WARP_CUT_KE
   return wc;
 }
 
-// The exact threshold from the keys of the cut bin (list[0..c), any order; they share every bit
-// above HIST_SHIFT): the r-th largest of them (1 <= r <= c) is T; the selection is every key > T
-// (n_gt = above + those in the list) plus the first need_eq entries equal to T in index order
-// (R: sparsify.py:85-88, lowest index wins).  A second-level histogram over the keys' low
-// HIST_SHIFT bits (in cs.sm.hist, free after the register histogram cut) and one find_bin: O(c)
-// work over the block instead of the O(c^2) rank counting of a plain list.  All threads; ends with
-// a barrier.
-static_assert((1 << HIST_SHIFT) <= RadixSmem<Key<float>::RB>::NB, "the low bits fit the radix histogram");
+// The exact threshold from the keys of the cut bin (list[0..c), any order, c <= BIN_LIST_MAX): the
+// r-th largest of them (1 <= r <= c) is T; the selection is every key > T (n_gt = above + those in
+// the list) plus the first need_eq entries equal to T in index order (R: sparsify.py:85-88, lowest
+// index wins).  Every key's rank is counted against the list by all threads at once (key i, slice
+// t / c of the others), the partial counts added in shared memory: two barriers.  The counters
+// (cut_counters) must be zero on entry (the callers clear them before an earlier barrier).
+constexpr int CUT_COUNTERS = 2 * BIN_LIST_MAX + 2;  // gt[c], eq[c], and two totals for the callers
+__device__ __forceinline__ uint32_t* cut_counters(SelectSmem& cs) { return cs.sm.hist; }
+__device__ __forceinline__ void clear_cut_counters(SelectSmem& cs) {
+  for (int i = threadIdx.x; i < CUT_COUNTERS; i += SEL_NT) cs.sm.hist[i] = 0u;
+}
 __device__ __forceinline__ SelectThreshold<uint32_t> resolve_cut(const uint32_t* list, uint32_t c, uint32_t r,
                                                                  uint32_t above, SelectSmem& cs) {
-  constexpr uint32_t LOW = (1u << HIST_SHIFT) - 1u;
-  for (int b = threadIdx.x; b < RadixSmem<Key<float>::RB>::NB; b += SEL_NT) cs.sm.hist[b] = 0u;
+  uint32_t* gtc = cut_counters(cs);
+  uint32_t* eqc = gtc + BIN_LIST_MAX;
+  const uint32_t slices = SEL_NT / c, per = (c + slices - 1) / slices;
+  if (threadIdx.x < slices * c) {
+    const uint32_t i = threadIdx.x % c, sl = threadIdx.x / c;
+    const uint32_t mine = list[i];
+    uint32_t gt = 0, eq = 0;
+    for (uint32_t j = sl * per; j < min(c, (sl + 1) * per); ++j) {
+      const uint32_t x = list[j];
+      gt += x > mine ? 1u : 0u;
+      eq += x == mine ? 1u : 0u;
+    }
+    if (gt) atomicAdd(&gtc[i], gt);
+    if (eq) atomicAdd(&eqc[i], eq);
+  }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) atomicAdd(&cs.sm.hist[list[i] & LOW], 1u);
+  for (uint32_t i = threadIdx.x; i < c; i += SEL_NT) {
+    if (gtc[i] < r && r <= gtc[i] + eqc[i]) {  // equal keys write equal values
+      cs.sm.list_key = list[i];
+      cs.sm.list_gt = gtc[i];
+    }
+  }
   __syncthreads();
-  uint32_t bin, gt, in_bin;
-  find_bin<Key<float>::RB>(cs.sm, r, &bin, &gt, &in_bin);
   SelectThreshold<uint32_t> th;
-  th.prefix = (list[0] & ~LOW) | bin;
+  th.prefix = cs.sm.list_key;
   th.pmask = 0x7fffffffu;
-  th.n_gt = above + gt;
-  th.need_eq = r - gt;
+  th.n_gt = above + cs.sm.list_gt;
+  th.need_eq = r - cs.sm.list_gt;
   return th;
 }
 
@@ -929,6 +948,11 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     if (spec) cs.tcache[t - tr.x] = c;
   }
   LAGS_CSTAMP(1);
+  if (threadIdx.x == 0) {  // the gather's counters (published by the barriers below)
+    sm.list_n = 0u;
+    sm.gtb = 0u;  // entries above the cut bin, counted by the gather
+    sm.diff_acc = 0u;
+  }
   const uint32_t m = block_sum(local, sm);
   if (__syncthreads_or(over)) return FB_OVERFLOW;
   LAGS_CSTAMP(2);
@@ -955,12 +979,6 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       hc = hist_cut(hr, cs, k, k2, m);
       cut = hc.bin < HIST_BINS - 1u && hc.in_bin <= BIN_LIST_MAX;
     }
-    if (threadIdx.x == 0) {
-      sm.list_n = 0u;
-      sm.gtb = 0u;  // entries above the cut bin, counted by the gather
-      sm.diff_acc = 0u;
-    }
-    __syncthreads();
     uint32_t* list = cs.hist2;
     if (spec) {
       spec_place(g, tr.x, T, cs.tcache, cand_idx, cand_val, cap, sv, si, sw, sw ? vl : nullptr, cs, st.thr, base,
@@ -975,6 +993,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       gather_candidates(tr.x, tr.y, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
                         &sm.gtb, list, &sm.list_n, vl, nullptr, tr.x);
     }
+    clear_cut_counters(cs);
     __syncthreads();  // the gather's counts (gtb, list_n) are complete: one uniform decision below
     const long long c1 = clock64();
     LAGS_CSTAMP(3);
