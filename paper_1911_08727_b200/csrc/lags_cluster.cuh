@@ -492,7 +492,8 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                                               [=](int64_t, int64_t ix) { return vl[ix]; });
   }
   LAGS_STAMP(11);
-  if (hl && !dry) zero_hist(hl, rank * (HIST_BINS / CLUSTER), (rank + 1) * (HIST_BINS / CLUSTER));
+  // the nonzero bins of the own quarter of the chunks (every CTA read its own register copy)
+  if (hl && !dry && (SEL_NT - 1 - static_cast<int>(threadIdx.x)) / (SEL_NT / CLUSTER) == rank) clear_hist_chunk(hr, hl);
   LAGS_STAMP(12);
   const long long c3 = clock64();
   if (rank == CLUSTER - 1 && threadIdx.x == 0) count_out[j] = static_cast<int32_t>(end);

@@ -518,6 +518,14 @@ __device__ __forceinline__ void hist_load(const uint32_t* hl, HistRegs& h) {
   h.hi = __ldcg(src + 1);
 }
 
+// Clear the nonzero bins of this thread's chunk (its register copy) for the next call's K1: a
+// few hundred bins of the 4096 are in use, so this writes ~50 KB instead of 16 KB per layer x 53.
+__device__ __forceinline__ void clear_hist_chunk(const HistRegs& h, uint32_t* hl) {
+  uint4* dst = reinterpret_cast<uint4*>(hl) + 2 * (SEL_NT - 1 - static_cast<int>(threadIdx.x));
+  if (h.lo.x | h.lo.y | h.lo.z | h.lo.w) dst[0] = make_uint4(0u, 0u, 0u, 0u);
+  if (h.hi.x | h.hi.y | h.hi.z | h.hi.w) dst[1] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 // Clear bins [lo, hi) of a layer histogram for the next call's K1 (16-byte stores).
 __device__ __forceinline__ void zero_hist(uint32_t* hl, int lo, int hi) {
   uint4* dst = reinterpret_cast<uint4*>(hl);
@@ -954,9 +962,15 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     sm.diff_acc = 0u;
   }
   const uint32_t m = block_sum(local, sm);
-  if (__syncthreads_or(over)) return FB_OVERFLOW;
+  if (__syncthreads_or(over)) {
+    if (hl) clear_hist_chunk(hr, const_cast<uint32_t*>(hl));
+    return FB_OVERFLOW;
+  }
   LAGS_CSTAMP(2);
-  if (m < k && st.thr > 1u) return FB_TOO_FEW;
+  if (m < k && st.thr > 1u) {
+    if (hl) clear_hist_chunk(hr, const_cast<uint32_t*>(hl));
+    return FB_TOO_FEW;
+  }
   float* data = r + L.offset;
   uint32_t cnt = 0;
   uint32_t pred = st.thr;
@@ -1071,6 +1085,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
 #endif
     pred = next_threshold(st, m, k, k2, th.prefix, key2);
   }
+  if (hl) clear_hist_chunk(hr, const_cast<uint32_t*>(hl));  // the cut is consumed (every thread read its own)
   if (threadIdx.x == 0) {
     FastState ns = candidate_state(st, pred, m, k, phases);
     ns.cut = cut_diag;
@@ -1361,7 +1376,8 @@ __device__ void select_layer(int j, const lags_layer_t* __restrict__ layers, con
     dense_fallback_select(j, L, st, r, idx_out, val_out, count_out, state, force_exact != 0, why, cs, vupd);
   const uint32_t path = why ? (L.dim <= SMALL_LAYER ? 0u : 2u) : 1u;
   __syncthreads();
-  if (hl) zero_hist(hl, 0, HIST_BINS);  // every path: the staged copy has been consumed
+  // candidate_select clears the histogram it read; a forced exact call never read it
+  if (hl && force_exact) zero_hist(hl, 0, HIST_BINS);
   if (threadIdx.x == 0) {
     state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
     state[j].path = path;
