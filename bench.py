@@ -761,9 +761,16 @@ def measure_train(args, world, rank, local, dev):
     # ranks; the median window is reported, and the exposed exchange is the median of the paired
     # per-round differences lags - no-exchange.
     arms = {k: setup(k) for k in TRAIN_KINDS}
+
+    def fallbacks(opt):  # dense-path selections after a prediction existed, summed over buckets / layers
+        return sum(int(b.engine.stats()[:, 1].sum()) for b in opt.buckets)
+
+    fb0 = fallbacks(arms["lags"]["opt"])
     for _ in range(TRAIN_WINDOWS):
         for k in TRAIN_KINDS:
             all_windows[k].append(window(arms[k]["it"]))
+    fb_windows = fallbacks(arms["lags"]["opt"]) - fb0
+    sel_calls = TRAIN_WINDOWS * args.train_steps * len(arms["lags"]["opt"].params)
     med = {k: sorted(w)[len(w) // 2] for k, w in all_windows.items()}
     lags_ms, nx_ms, dense_ms = med["lags"], med["lags_noexchange"], med["dense"]
     diffs = sorted(a - b for a, b in zip(all_windows["lags"], all_windows["lags_noexchange"]))
@@ -781,6 +788,9 @@ def measure_train(args, world, rank, local, dev):
         per_it.append([float(v) for v in c])
     comm = [sorted(col)[len(col) // 2] for col in zip(*per_it)]
     nb = len(opt.buckets)
+    last = opt.bucket_times_ms()
+    bucket_detail = [{"layers": b.hi - b.lo + 1, "elements": b.numel, "compress_ms": round(t[0], 4),
+                      "exchange_ms": round(t[1], 4), "decode_ms": round(t[2], 4)} for b, t in zip(opt.buckets, last)]
     for k in ("lags", "lags_noexchange"):
         arms[k]["opt"].remove_hooks()
     del arms, opt
@@ -792,11 +802,15 @@ def measure_train(args, world, rank, local, dev):
            "dense_ddp_iter_per_s": round(1e3 / dense_ms, 3), "dense_ms_per_iter": round(dense_ms, 3),
            "lags_no_exchange_ms_per_iter": round(nx_ms, 3),
            "sum_compress_ms": round(comm[1], 3), "sum_exchange_ms": round(comm[0], 3),
-           "sum_decode_ms": round(comm[2], 3), "sum_transfer_ms": round(comm[3], 4),
+           "sum_decode_ms": round(comm[2], 3), "sum_transfer_ms": round(comm[3], 4), "buckets_detail": bucket_detail,
            "sum_peer_wait_ms": round(comm[4], 4), "exchange": args.train_exchange if world > 1 else None,
            "streams": "compress on a compute-side stream, exchange + decode on a serial communication stream",
            "windows": TRAIN_WINDOWS, "window_order": "interleaved",
-           "ms_per_iter_windows": all_windows, "exposed_exchange_ms": round(exposed_ms, 3)}
+           "ms_per_iter_windows": all_windows, "exposed_exchange_ms": round(exposed_ms, 3),
+           "dense_fallbacks": {"count": fb_windows, "layer_selections": sel_calls,
+                               "rate": round(fb_windows / max(1, sel_calls), 6),
+                               "what": "selections that fell back to the dense exact path after a prediction "
+                                       "existed, real ResNet-50 gradients, the timed windows of the LAGS arm"}}
     if world > 1 and comm[3] > 0:
         # hidden fraction of the exchange (R: perf.py:173-195's network channel): the transfer spans
         # (push kernels / all-gathers on the communication stream) against the exposed time, the
