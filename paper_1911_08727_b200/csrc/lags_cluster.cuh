@@ -259,10 +259,9 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     rpre[q + 1] = rpre[q] + mq;
   }
   const uint32_t mr = csh.qsum[rank];
-  // own values + indices (+ the parked weights of the P = 1 update)
-  const bool park = spec && vupd != nullptr;
+  // own values + indices
   const uint32_t mx4 = (m_max + 3u) & ~3u;  // 16-byte aligned planes (the staged compaction reads vectors)
-  const bool fits = (park ? 3ull : 2ull) * mx4 <= static_cast<uint64_t>(smem_words);
+  const bool fits = 2ull * mx4 <= static_cast<uint64_t>(smem_words);
   int why = 0;
   if (force_exact || st.thr == 0u) why = FB_TOO_FEW;
   else if (over_any) why = FB_OVERFLOW;
@@ -304,9 +303,8 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   LAGS_STAMP(4);
   float* sv = reinterpret_cast<float*>(dyn);
   int32_t* si = reinterpret_cast<int32_t*>(dyn + mx4);
-  float* sw = park ? reinterpret_cast<float*>(dyn + 2 * mx4) : nullptr;  // parked weights
   if (spec) {
-    spec_place(g, t_lo, nt_own, cs.tcache + (t_lo - tr.x), cand_idx, cand_val, cap, sv, si, sw,
+    spec_place(g, t_lo, nt_own, cs.tcache + (t_lo - tr.x), cand_idx, cand_val, cap, sv, si,
                vupd ? vupd + L.offset : nullptr, cs, st.thr, base, cut ? hc.bin : ~0u, &cs.sm.gtb, cs.hist2,
                &cs.sm.list_n);
   } else {
@@ -456,22 +454,13 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       ce0 += o->eq;
     }
   }
-  if (sw) {
-    spec_store_weights(g, nt_own, sw, cs);
-    __syncthreads();
-  }
   const long long c2 = clock64();
   // 3. ordered compaction of the own range with the carried counts of the lower ranks
   float* data = r + L.offset;
   int32_t* oidx = idx_out + L.slot;
   float* oval = val_out + L.slot;
-  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
-    *x = sv[i];
-    *key = Key<float>::of(*x);
-    *ix = si[i];
-  };
   uint32_t end;
-  if (sw || !vupd) {  // staged: vector reads of the planes (weights parked or none)
+  {  // staged: vector reads of the planes; the P = 1 weights loaded before each chunk's scan
     float* vl = vupd ? vupd + L.offset : nullptr;
     auto emit = [=](uint32_t pos, int32_t ix, float x, float w) {
       oidx[pos] = ix;
@@ -479,17 +468,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
       data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       if (vl) vl[ix] = single_rank_update(w, x);
     };
-    end = compact_staged(mr, th, sv, si, sw, emit, cs.sm, cg0, ce0);
-  } else {  // fused P = 1 update: the weights are loaded before the compaction's scan
-    float* vl = vupd + L.offset;
-    auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
-      oidx[pos] = static_cast<int32_t>(ix);
-      oval[pos] = x;
-      data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
-      vl[ix] = single_rank_update(w, x);
-    };
-    end = ordered_compact_pf<uint32_t, float>(mr, th, load, emit, cs.sm, cg0, ce0,
-                                              [=](int64_t, int64_t ix) { return vl[ix]; });
+    end = compact_staged(mr, th, sv, si, vl, emit, cs.sm, cg0, ce0);
   }
   LAGS_STAMP(11);
   // the nonzero bins of the own quarter of the chunks (every CTA read its own register copy)

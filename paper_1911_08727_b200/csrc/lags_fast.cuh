@@ -296,6 +296,7 @@ struct SelectSmem {
   uint32_t tpos[SEL_NT];     // candidate gather: per-task output position / count
   uint32_t tcnt[SEL_NT];
   uint32_t tcache[SEL_NT];   // the layer's task counts from the counting pass (layers of <= SEL_NT tasks)
+  uint32_t rpos[SEL_NT];     // speculative gather: positions of the tasks' remainders
 };
 
 // P = 1 update fused into the selection epilogue (no exchange, no separate decode): exactly the
@@ -672,6 +673,10 @@ __device__ __forceinline__ SelectThreshold<uint32_t> resolve_cut(const uint32_t*
 #ifndef LAGS_GATHER_TASKS
 #define LAGS_GATHER_TASKS 5
 #endif
+#ifndef LAGS_GATHER_ILP
+#define LAGS_GATHER_ILP 4
+#endif
+constexpr int GATHER_ILP = LAGS_GATHER_ILP;  // leftover candidate loads in flight per thread
 constexpr int GATHER_TASKS = LAGS_GATHER_TASKS;
 
 __device__ uint32_t gather_candidates(int t_lo, int t_hi, const int32_t* __restrict__ cand_cnt,
@@ -749,14 +754,12 @@ __device__ uint32_t gather_candidates(int t_lo, int t_hi, const int32_t* __restr
 // counts are known, warp w loads entry `lane` of its tasks t_lo + w + NW * u (u < GATHER_TASKS),
 // i.e. each task's first 32 candidates (usually all of them; reading past a short list stays
 // inside its cap slots).  After the counts' scan, spec_place puts them at their positions,
-// classifies them against the histogram cut and issues the loads of the possibly selected
-// entries' weights (P = 1 update) into registers; spec_store_weights parks those in shared
-// memory once the threshold is resolved, so the compaction never waits on HBM.  Leftovers (tasks
-// beyond NW * GATHER_TASKS, lists longer than 32) are gathered synchronously.  nt <= SEL_NT.
+// classifies them against the histogram cut and prefetches the possibly selected entries' weights
+// (P = 1 update) into L2 for the compaction.  Leftovers (tasks beyond NW * GATHER_TASKS, lists
+// longer than 32) follow with one thread per entry.  nt <= SEL_NT.
 struct SpecGather {
   float xv[GATHER_TASKS];
   int32_t xi[GATHER_TASKS];
-  float wv[GATHER_TASKS];
 };
 
 __device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const int32_t* __restrict__ cand_idx,
@@ -766,7 +769,6 @@ __device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const
 #pragma unroll
   for (int u = 0; u < GATHER_TASKS; ++u) {
     const int tt = warp + NW * u;
-    g.wv[u] = 0.0f;
     if (tt < nt) {
       const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + lane;
       g.xv[u] = __ldcg(cand_val + src);
@@ -775,10 +777,10 @@ __device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const
   }
 }
 
-// All threads.  tc[0..nt): the range's task counts (shared).  sw (nullable, with vl): the
-// weights' staging; vl: the layer's weights (P = 1 update).  Classification as gather_candidates.
+// All threads.  tc[0..nt): the range's task counts (shared).  vl (nullable): the layer's weights
+// (P = 1 update), prefetched for the possibly selected.  Classification as gather_candidates.
 __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* tc, const int32_t* __restrict__ cand_idx,
-                               const float* __restrict__ cand_val, int cap, float* sv, int32_t* si, float* sw,
+                               const float* __restrict__ cand_val, int cap, float* sv, int32_t* si,
                                const float* vl, SelectSmem& cs, uint32_t key0, uint32_t base, uint32_t cut_bin,
                                uint32_t* gtb, uint32_t* list, uint32_t* list_n) {
   constexpr int NW = SEL_NT / 32;
@@ -812,17 +814,47 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
   for (int u = 0; u < GATHER_TASKS; ++u) {
     const int tt = warp + NW * u;
     if (tt < nt && static_cast<uint32_t>(lane) < cs.tcnt[tt]) {
-      if (take(g.xv[u], g.xi[u], cs.tpos[tt] + lane) && vl) g.wv[u] = vl[g.xi[u]];  // in flight until parked
+      if (take(g.xv[u], g.xi[u], cs.tpos[tt] + lane) && vl)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + g.xi[u]));  // P = 1 weight
     }
   }
-#pragma unroll 1
-  for (int tt = warp; tt < nt; tt += NW) {  // leftovers: synchronous
-    const uint32_t cc = cs.tcnt[tt];
-    const int64_t row = static_cast<int64_t>(t_lo + tt) * cap;
-    for (uint32_t e = (tt < NW * GATHER_TASKS ? 32u : 0u) + lane; e < cc; e += 32u) {
-      const float x = __ldcg(cand_val + row + e);
-      const int32_t ix = __ldcg(cand_idx + row + e);
-      if (take(x, ix, cs.tpos[tt] + e) && sw) sw[cs.tpos[tt] + e] = vl[ix];
+  // leftovers (tasks beyond NW * GATHER_TASKS, entries past a task's first 32): one thread per
+  // entry over a scan of the remainders, GATHER_ILP loads in flight per thread (large k: a
+  // 2.4 M-element layer at rho = 0.01 has ~160 candidates per task)
+  const uint32_t skip = static_cast<int>(threadIdx.x) < NW * GATHER_TASKS ? 32u : 0u;
+  const uint32_t rem = c > skip ? c - skip : 0u;
+  uint32_t rtot;
+  const uint32_t rp = block_exclusive_scan<SEL_NT>(rem, cs.sm.warp_tot, &rtot);
+  if (rtot) {
+    cs.rpos[threadIdx.x] = rp;
+    __syncthreads();
+    for (uint32_t e0 = 0; e0 < rtot; e0 += SEL_NT * GATHER_ILP) {
+      int tk[GATHER_ILP];
+      uint32_t off[GATHER_ILP];
+      float x[GATHER_ILP];
+      int32_t ix[GATHER_ILP];
+#pragma unroll
+      for (int u = 0; u < GATHER_ILP; ++u) {
+        const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
+        tk[u] = -1;
+        if (e < rtot) {
+          int lo = 0, hi = nt - 1;  // last task whose remainder starts at or before e
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cs.rpos[mid] <= e) lo = mid;
+            else hi = mid - 1;
+          }
+          tk[u] = lo;
+          off[u] = (lo < NW * GATHER_TASKS ? 32u : 0u) + (e - cs.rpos[lo]);
+          const int64_t src = static_cast<int64_t>(t_lo + lo) * cap + off[u];
+          x[u] = __ldcg(cand_val + src);
+          ix[u] = __ldcg(cand_idx + src);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < GATHER_ILP; ++u)
+        if (tk[u] >= 0 && take(x[u], ix[u], cs.tpos[tk[u]] + off[u]) && vl)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + ix[u]));  // P = 1 weight
     }
   }
   dx = __reduce_or_sync(0xffffffffu, dx);
@@ -832,36 +864,27 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
   return tot;
 }
 
-// Park the speculatively loaded weights at their entries' positions (cs.tpos / tcnt of the
-// spec_place scan still hold).  The caller synchronises before reading sw.
-__device__ __forceinline__ void spec_store_weights(const SpecGather& g, int nt, float* sw, const SelectSmem& cs) {
-  constexpr int NW = SEL_NT / 32;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// compact_staged with V entries per thread (see below).
+template <int V, typename Emit>
+__device__ uint32_t compact_staged_v(uint32_t m, const SelectThreshold<uint32_t>& th, const float* sv,
+                                     const int32_t* si, const float* vl, Emit emit, RadixSmem<Key<float>::RB>& sm,
+                                     uint32_t carry_gt, uint32_t carry_eq) {
+  static_assert(V % 4 == 0, "whole 16-byte vectors per plane and thread");
+  for (uint32_t base = 0; base < m; base += SEL_NT * V) {
+    const uint32_t i0 = base + threadIdx.x * V;
+    float xs[V];
 #pragma unroll
-  for (int u = 0; u < GATHER_TASKS; ++u) {
-    const int tt = warp + NW * u;
-    if (tt < nt && static_cast<uint32_t>(lane) < cs.tcnt[tt]) sw[cs.tpos[tt] + lane] = g.wv[u];
-  }
-}
-
-// Ordered compaction of candidates staged in shared memory (sv / si / sw: 16-byte aligned planes
-// in index order; sw nullable), 4 entries per thread read as one 16-byte vector per plane.  The
-// rule and the result are ordered_compact_pf's: (key & pmask) > prefix, plus the first need_eq
-// equal ones in index order; carry_gt / carry_eq count the lower ranks' entries.
-// emit(pos, ix, x, w).  Returns the selected count (all threads).
-template <typename Emit>
-__device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& th, const float* sv, const int32_t* si,
-                                   const float* sw, Emit emit, RadixSmem<Key<float>::RB>& sm, uint32_t carry_gt,
-                                   uint32_t carry_eq) {
-  static_assert(SEL_VEC == 4, "one 16-byte vector per plane and thread");
-  for (uint32_t base = 0; base < m; base += SEL_NT * 4u) {
-    const uint32_t i0 = base + threadIdx.x * 4u;
-    float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i0 < m) x4 = *reinterpret_cast<const float4*>(sv + i0);
-    const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+    for (int q = 0; q < V / 4; ++q) {
+      float4 x4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i0 + 4 * q < m) x4 = *reinterpret_cast<const float4*>(sv + i0 + 4 * q);
+      xs[4 * q] = x4.x;
+      xs[4 * q + 1] = x4.y;
+      xs[4 * q + 2] = x4.z;
+      xs[4 * q + 3] = x4.w;
+    }
     uint32_t gtm = 0, eqm = 0;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
+    for (int v = 0; v < V; ++v) {
       const uint32_t key = i0 + v < m ? Key<float>::of(xs[v]) : 0u;
       const uint32_t hk = key & th.pmask;
       if (key != 0u) {
@@ -869,14 +892,21 @@ __device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& 
         else if (hk == th.prefix) eqm |= 1u << v;
       }
     }
-    int4 ix4 = make_int4(0, 0, 0, 0);
-    float4 w4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gtm | eqm) {
-      ix4 = *reinterpret_cast<const int4*>(si + i0);
-      if (sw) w4 = *reinterpret_cast<const float4*>(sw + i0);
+    int32_t ixs[V];
+    float ws[V];
+#pragma unroll
+    for (int q = 0; q < V / 4; ++q) {
+      int4 ix4 = make_int4(0, 0, 0, 0);
+      if (((gtm | eqm) >> (4 * q)) & 0xfu) ix4 = *reinterpret_cast<const int4*>(si + i0 + 4 * q);
+      ixs[4 * q] = ix4.x;
+      ixs[4 * q + 1] = ix4.y;
+      ixs[4 * q + 2] = ix4.z;
+      ixs[4 * q + 3] = ix4.w;
     }
-    const int32_t ixs[4] = {ix4.x, ix4.y, ix4.z, ix4.w};
-    const float ws[4] = {w4.x, w4.y, w4.z, w4.w};
+    // the weights of the entries at or above the threshold (P = 1 update; L2-prefetched by the
+    // gather), in flight across the block scan
+#pragma unroll
+    for (int v = 0; v < V; ++v) ws[v] = vl && (((gtm | eqm) >> v) & 1u) ? vl[ixs[v]] : 0.0f;
     const uint32_t packed = (static_cast<uint32_t>(__popc(eqm)) << 16) | static_cast<uint32_t>(__popc(gtm));
     uint32_t tot;
     const uint32_t ex = block_exclusive_scan<SEL_NT>(packed, sm.warp_tot, &tot);
@@ -884,7 +914,7 @@ __device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& 
     uint32_t eq_before = carry_eq + (ex >> 16);
     if (gtm | eqm) {
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
+      for (int v = 0; v < V; ++v) {
         const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
         if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), ixs[v], xs[v], ws[v]);
         gt_before += g;
@@ -896,6 +926,19 @@ __device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& 
     __syncthreads();  // warp_tot reuse by the next scan
   }
   return carry_gt + min(carry_eq, th.need_eq);
+}
+
+// Ordered compaction of candidates staged in shared memory (sv / si: 16-byte aligned planes in
+// index order), 4 (8 for large sets: half the block scans) entries per thread read as 16-byte
+// vectors per plane; vl (nullable): the layer's weights for the fused P = 1 update.  The rule and the result are ordered_compact_pf's: (key & pmask) >
+// prefix, plus the first need_eq equal ones in index order; carry_gt / carry_eq count the lower
+// ranks' entries.  emit(pos, ix, x, w).  Returns the selected count (all threads).
+template <typename Emit>
+__device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& th, const float* sv, const int32_t* si,
+                                   const float* vl, Emit emit, RadixSmem<Key<float>::RB>& sm, uint32_t carry_gt,
+                                   uint32_t carry_eq) {
+  if (m > 2u * SEL_NT * 4u) return compact_staged_v<8>(m, th, sv, si, vl, emit, sm, carry_gt, carry_eq);
+  return compact_staged_v<4>(m, th, sv, si, vl, emit, sm, carry_gt, carry_eq);
 }
 
 // Candidate path of one layer inside one CTA.  Returns 0 on success, or why the candidate set
@@ -980,11 +1023,10 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
   if (m > 0) {
     const long long c0 = clock64();
     const uint32_t m4 = (m + 3u) & ~3u;  // 16-byte aligned planes (the staged compaction reads vectors)
-    const bool in_smem = (vl && spec ? 3u : 2u) * m4 <= static_cast<uint32_t>(smem_words);
+    const bool in_smem = 2u * m4 <= static_cast<uint32_t>(smem_words);
     const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
     float* sv = in_smem ? reinterpret_cast<float*>(dyn) : gval + gbase;
     int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + m4 : gidx + gbase;
-    float* sw = in_smem && vl && spec ? reinterpret_cast<float*>(dyn) + 2 * m4 : nullptr;  // parked weights
     const uint32_t base = st.thr >> HIST_SHIFT;
     // the histogram cut (uniform): usable when the k-th candidate is in a closed bin with few keys
     HistCut hc{~0u, 0u, 0u, 0u};
@@ -995,14 +1037,8 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     }
     uint32_t* list = cs.hist2;
     if (spec) {
-      spec_place(g, tr.x, T, cs.tcache, cand_idx, cand_val, cap, sv, si, sw, sw ? vl : nullptr, cs, st.thr, base,
-                 cut ? hc.bin : ~0u, &sm.gtb, list, &sm.list_n);
-      if (!sw && vl) {  // weights not parked: prefetch the possibly selected ones for the compaction
-        for (uint32_t i = threadIdx.x; i < m; i += SEL_NT) {
-          const uint32_t key = Key<float>::of(sv[i]);
-          if (!cut || hist_bin(key, base) >= hc.bin) asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + si[i]));
-        }
-      }
+      spec_place(g, tr.x, T, cs.tcache, cand_idx, cand_val, cap, sv, si, vl, cs, st.thr, base, cut ? hc.bin : ~0u,
+                 &sm.gtb, list, &sm.list_n);
     } else {
       gather_candidates(tr.x, tr.y, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
                         &sm.gtb, list, &sm.list_n, vl, nullptr, tr.x);
@@ -1037,10 +1073,6 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
       cut_diag = 2u;
     }
     if (hl && k < m) cut_diag |= min(hc.in_bin, 0xffffffu) << 8;
-    if (sw) {
-      spec_store_weights(g, T, sw, cs);
-      __syncthreads();
-    }
     const long long c2 = clock64();
     auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
       *x = sv[i];
@@ -1050,14 +1082,14 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     int32_t* oidx = idx_out + L.slot;
     float* oval = val_out + L.slot;
     LAGS_CSTAMP(4);
-    if (in_smem && (sw || !vl)) {  // staged: vector reads of the planes (weights parked or none)
+    if (in_smem) {  // staged: vector reads of the planes
       auto emit = [=](uint32_t pos, int32_t ix, float x, float w) {
         oidx[pos] = ix;
         oval[pos] = x;
         data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
         if (vl) vl[ix] = single_rank_update(w, x);
       };
-      cnt = compact_staged(m, th, sv, si, sw, emit, sm, 0u, 0u);
+      cnt = compact_staged(m, th, sv, si, vl, emit, sm, 0u, 0u);
     } else if (vl) {  // fused P = 1 update: the weights are loaded before the compaction's scan
       auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
         oidx[pos] = static_cast<int32_t>(ix);
