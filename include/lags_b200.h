@@ -122,7 +122,9 @@ int lags_bucket_set_grad_table(lags_bucket_t* bucket, const void* table);
 
 /* Diagnostics: per layer {threshold key, fallbacks, last candidate count, calls, last select
  * cycles, last path (0 small dense, 1 candidates, 2 dense after a failed prediction), phase
- * cycles, select start / end / CTA launch (%globaltimer ns, low 32 bits), 0} (synchronous). */
+ * cycles, select start / end / CTA launch (%globaltimer ns, low 32 bits), 0} (synchronous).
+ * LAGS_F64 / LAGS_F32_ACC64 buckets: {threshold key >> 32, fallbacks, last candidate count, calls,
+ * 0, last path (0 small layer, 1 candidates, 2 dense), 0...}. */
 #define LAGS_STATS_WORDS 12
 int lags_bucket_stats(const lags_bucket_t* bucket, uint32_t* out /* [nlayers * 12] */, lags_stream_t stream);
 

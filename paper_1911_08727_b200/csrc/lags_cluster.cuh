@@ -462,13 +462,11 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   uint32_t end;
   {  // staged: vector reads of the planes; the P = 1 weights loaded before each chunk's scan
     float* vl = vupd ? vupd + L.offset : nullptr;
-    auto emit = [=](uint32_t pos, int32_t ix, float x, float w) {
-      oidx[pos] = ix;
-      oval[pos] = x;
+    auto emit = [=](int32_t ix, float x, float w) {
       data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       if (vl) vl[ix] = single_rank_update(w, x);
     };
-    end = compact_staged(mr, th, sv, si, vl, emit, cs.sm, cg0, ce0);
+    end = compact_staged(mr, th, sv, si, vl, emit, cs, cg0, ce0, oidx, oval);
   }
   LAGS_STAMP(11);
   // the nonzero bins of the own quarter of the chunks (every CTA read its own register copy)

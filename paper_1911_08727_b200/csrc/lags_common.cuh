@@ -46,6 +46,14 @@ template <> struct Key<double> {
 __device__ __forceinline__ float sent_residual(float x) { return __fsub_rn(x, x); }
 __device__ __forceinline__ double sent_residual(double x) { return __dsub_rn(x, x); }
 
+// total / P, the workers' mean of the decode (R: training.py:253-254).  A power-of-two P divides
+// by multiplying with 2^-log2(P): both are the correctly rounded value of total * 2^-e (subnormal
+// results included), so the bits match the IEEE division, which the other worker counts take.
+__device__ __forceinline__ double div_workers(double total, int P) {
+  if ((P & (P - 1)) == 0) return __dmul_rn(total, __longlong_as_double(static_cast<long long>(992 + __clz(P)) << 52));
+  return __ddiv_rn(total, static_cast<double>(P));
+}
+
 // acc = r + alpha * g rounded twice (numpy evaluates `alpha * g` then `+`; no FMA).
 __device__ __forceinline__ float accum(float r, float g, float a) { return __fadd_rn(r, __fmul_rn(a, g)); }
 __device__ __forceinline__ double accum(double r, double g, double a) { return __dadd_rn(r, __dmul_rn(a, g)); }

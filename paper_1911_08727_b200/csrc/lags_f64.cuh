@@ -6,7 +6,10 @@
 //    and appends every entry with key(acc) >= the layer's predicted threshold to the task's
 //    candidate list in ascending index order (warp ballot, no atomics).  Algorithmic traffic:
 //    24 B/element (+8 with the fused zero_grad).
-// select64_kernel: one CTA per layer.  When the candidate set provably holds the top-k (no task
+//    LAGS_F32_ACC64 (fp32 storage, numpy-float64 alpha, R: training.py:250 under NEP 50) runs the
+//    same kernel on float g / r: acc in fp64 into the bucket's acc64 (the selection's dense
+//    fallback reads it) and fl32(acc) back into r -- 20 B/element.
+// select64_kernel: one CTA per layer (r32: LAGS_F32_ACC64's fp32 residual, r = acc64 then).  When the candidate set provably holds the top-k (no task
 //    overflow, count >= k): gather into shared memory, radix select on the 64-bit keys starting
 //    below the candidates' common prefix, ordered compaction (ascending indices, residual
 //    acc - acc at the selected entries), and the next threshold from the same passes.  Otherwise
@@ -23,7 +26,7 @@ struct State64 {
   uint32_t fallbacks;      // dense-path executions after a prediction existed (diagnostic)
   uint32_t calls;
   uint32_t last_cands;     // candidates at the last call (0 = dense path)
-  uint32_t path;           // 0 dense, 1 candidates
+  uint32_t path;           // 0 small layer (always dense), 1 candidates, 2 dense (first call / fallback)
   uint32_t pad;
 };
 
@@ -32,11 +35,14 @@ struct State64 {
 #endif
 constexpr int K1_64_UNROLL = LAGS_K1_64_UNROLL;  // doubles in flight per lane per operand
 
-template <bool ZERO_G>
+// TS: the storage type of g and r (double; float for LAGS_F32_ACC64, which also writes the fp64 acc
+// into acc64).
+template <bool ZERO_G, typename TS>
 __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit64_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
-    const State64* __restrict__ state, double* __restrict__ g, double* __restrict__ r, double alpha, int cap,
-    int32_t* __restrict__ cand_idx, double* __restrict__ cand_val, int32_t* __restrict__ cand_cnt, uint32_t* status) {
+    const State64* __restrict__ state, TS* __restrict__ g, TS* __restrict__ r, double* __restrict__ acc64,
+    double alpha, int cap, int32_t* __restrict__ cand_idx, double* __restrict__ cand_val,
+    int32_t* __restrict__ cand_cnt, uint32_t* status) {
   const int lane = threadIdx.x & 31;
   const int wid = blockIdx.x * K1_WARPS + (threadIdx.x >> 5);
   griddep_wait();  // the previous kernel on the stream has completed
@@ -46,8 +52,8 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit64_kernel(
   const int64_t local0 = T.start - layers[T.layer].offset;
   const unsigned long long thr0 = state[T.layer].thr;
   const unsigned long long thr = thr0 ? thr0 : ~0ull;
-  double* gt = g + T.start;
-  double* rt = r + T.start;
+  TS* gt = g + T.start;
+  TS* rt = r + T.start;
   int32_t* cidx = cand_idx + static_cast<int64_t>(wid) * cap;
   double* cval = cand_val + static_cast<int64_t>(wid) * cap;
   const uint32_t below = (1u << lane) - 1u;
@@ -55,7 +61,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit64_kernel(
   bool bad = false;
   const int n = T.len;
   for (int q0 = 0; q0 < n; q0 += 32 * K1_64_UNROLL) {
-    double gv[K1_64_UNROLL], rv[K1_64_UNROLL];
+    TS gv[K1_64_UNROLL], rv[K1_64_UNROLL];
 #pragma unroll
     for (int u = 0; u < K1_64_UNROLL; ++u) {
       const int i = q0 + u * 32 + lane;
@@ -70,10 +76,11 @@ __global__ void __launch_bounds__(K1_WARPS * 32) accum_emit64_kernel(
       bool c = false;
       double a = 0.0;
       if (i < n) {
-        if (ZERO_G) __stcs(gt + i, 0.0);
+        if (ZERO_G) __stcs(gt + i, TS(0));
         bad |= nonfinite(gv[u]);
-        a = accum(rv[u], gv[u], alpha);
-        __stcs(rt + i, a);
+        a = accum(static_cast<double>(rv[u]), static_cast<double>(gv[u]), alpha);
+        __stcs(rt + i, static_cast<TS>(a));
+        if (sizeof(TS) == 4) __stcs(acc64 + T.start + i, a);
         c = Key<double>::of(a) >= thr;
       }
       const uint32_t bal = __ballot_sync(0xffffffffu, c);
@@ -100,20 +107,90 @@ __device__ __forceinline__ unsigned long long lower_threshold64(unsigned long lo
   return next >= thr ? (thr > 1ull ? thr - 1ull : 1ull) : (next ? next : 1ull);
 }
 
+// Ordered compaction of candidates staged in sv (doubles) / si (indices, 16-byte aligned; both
+// in index order, readable 3 entries past m): 4 entries per thread per block scan, read as
+// 16-byte vectors.  The rule is ordered_compact's: (key & pmask) > prefix, plus the first need_eq
+// equal ones in index order.  emit(pos, ix, x).  Returns the selected count (all threads).
+template <typename Emit>
+__device__ uint32_t compact64_staged(uint32_t m, const SelectThreshold<unsigned long long>& th, const double* sv,
+                                     const int32_t* si, Emit emit, RadixSmem<Key<double>::RB>& sm) {
+  constexpr int V = 4;
+  uint32_t carry_gt = 0, carry_eq = 0;
+  for (uint32_t base = 0; base < m; base += SEL_NT * V) {
+    const uint32_t i0 = base + threadIdx.x * V;
+    double xs[V];
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) {
+      double2 x2 = make_double2(0.0, 0.0);
+      if (i0 + 2 * q < m) x2 = *reinterpret_cast<const double2*>(sv + i0 + 2 * q);
+      xs[2 * q] = x2.x;
+      xs[2 * q + 1] = x2.y;
+    }
+    uint32_t gtm = 0, eqm = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const unsigned long long key = i0 + v < m ? Key<double>::of(xs[v]) : 0ull;
+      const unsigned long long hk = key & th.pmask;
+      if (key != 0ull) {
+        if (hk > th.prefix) gtm |= 1u << v;
+        else if (hk == th.prefix) eqm |= 1u << v;
+      }
+    }
+    int4 ix4 = make_int4(0, 0, 0, 0);
+    if (gtm | eqm) ix4 = *reinterpret_cast<const int4*>(si + i0);
+    const int32_t ixs[V] = {ix4.x, ix4.y, ix4.z, ix4.w};
+    const uint32_t packed = (static_cast<uint32_t>(__popc(eqm)) << 16) | static_cast<uint32_t>(__popc(gtm));
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<SEL_NT>(packed, sm.warp_tot, &tot);
+    uint32_t gt_before = carry_gt + (ex & 0xffffu);
+    uint32_t eq_before = carry_eq + (ex >> 16);
+    if (gtm | eqm) {
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
+        if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), ixs[v], xs[v]);
+        gt_before += g;
+        eq_before += e;
+      }
+    }
+    carry_gt += tot & 0xffffu;
+    carry_eq += tot >> 16;
+    __syncthreads();  // warp_tot reuse by the next scan
+  }
+  return carry_gt + min(carry_eq, th.need_eq);
+}
+
+#ifdef LAGS_DBG_STAMPS
+// Diagnostic builds only: per layer (j < 1024) clock64 after the wait / counts / gather / radix /
+// compaction / end, and %globaltimer at the wait and the end.
+__device__ unsigned long long lags_dbg_s64[1024][8];
+#define LAGS_S64(i, v)                                            \
+  do {                                                            \
+    if (j < 1024 && threadIdx.x == 0) lags_dbg_s64[j][i] = (v);   \
+  } while (0)
+#else
+#define LAGS_S64(i, v) \
+  do {                 \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __restrict__ layers,
                                                           const int2* __restrict__ layer_tasks, State64* state,
                                                           const int32_t* __restrict__ cand_cnt,
                                                           const int32_t* __restrict__ cand_idx,
                                                           const double* __restrict__ cand_val, int cap, int32_t* gidx,
                                                           double* gval, double* r, int32_t* idx_out, double* val_out,
-                                                          int32_t* count_out, int smem_words, int force_exact) {
+                                                          int32_t* count_out, int smem_words, int force_exact,
+                                                          float* r32) {
   using K = unsigned long long;
   constexpr int RB = Key<double>::RB;
   extern __shared__ __align__(16) uint32_t dyn[];
   __shared__ RadixSmem<RB> sm;
-  __shared__ uint32_t tpos[SEL_NT];
+  __shared__ uint32_t tpos[SEL_NT], tcnt[SEL_NT];
   griddep_wait();  // K1 has completed and its writes are visible
   const int j = blockIdx.x;
+  LAGS_S64(0, clock64());
+  LAGS_S64(6, globaltimer_lo());
   const lags_layer_t L = layers[j];
   const int2 tr = layer_tasks[j];
   const State64 st = state[j];
@@ -129,8 +206,12 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
     local += min(c, static_cast<uint32_t>(cap));
   }
   const uint32_t m = block_sum(local, sm);
+  LAGS_S64(1, clock64());
   const bool overflow = __syncthreads_or(over) != 0;
-  const bool cand = !force_exact && st.thr != 0ull && !overflow && !(m < k && st.thr > 1ull);
+  // layers of <= TINY_LAYER entries always take the dense path (no prediction: K1 emits nothing);
+  // a k = 1 prediction over a few hundred entries missed every other step
+  const bool tiny = L.dim <= TINY_LAYER;
+  const bool cand = !tiny && !force_exact && st.thr != 0ull && !overflow && !(m < k && st.thr > 1ull);
   State64 ns = st;
   ns.calls += 1;
   uint32_t cnt = 0;
@@ -138,12 +219,17 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
     const uint32_t k2 = max(k + 1u, static_cast<uint32_t>(fminf(pf * static_cast<float>(k), 4.0e9f)));
     K key2 = st.thr;
     if (m > 0) {
-      const bool in_smem = 3ull * m + 2ull <= static_cast<uint64_t>(smem_words);
+      // staging: doubles, then the indices at a 16-byte boundary (+4 words of vector over-read)
+      const uint32_t si_off = (2u * m + 3u) & ~3u;
+      const bool in_smem = static_cast<uint64_t>(si_off) + m + 4ull <= static_cast<uint64_t>(smem_words);
       const int64_t gbase = static_cast<int64_t>(tr.x) * cap;
       double* sv = in_smem ? reinterpret_cast<double*>(dyn) : gval + gbase;
-      int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + 2 * m : gidx + gbase;
-      // gather: positions by a block scan over the task counts, one thread per entry (the owning
-      // task by binary search), index order kept
+      int32_t* si = in_smem ? reinterpret_cast<int32_t*>(dyn) + si_off : gidx + gbase;
+      // gather: positions by a block scan over the task counts; one warp per task, lane = entry
+      // (a task holds ~17 candidates of a 2.4 M-element layer at the margin), GATHER_TASKS tasks'
+      // loads in flight per warp, entries past the first 32 in a loop; index order kept
+      constexpr int NW = SEL_NT / 32;
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       uint32_t carry = 0;
       for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
         const int nt = min(SEL_NT, tr.y - t0);
@@ -151,35 +237,54 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
                                                   static_cast<uint32_t>(cap))
                                             : 0u;
         uint32_t tot;
-        tpos[threadIdx.x] = block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
+        tpos[threadIdx.x] = carry + block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
+        tcnt[threadIdx.x] = c;
         __syncthreads();
-        for (uint32_t e = threadIdx.x; e < tot; e += SEL_NT) {
-          int lo = 0, hi = nt - 1;
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (tpos[mid] <= e) lo = mid;
-            else hi = mid - 1;
+        for (int tb = warp; tb < nt; tb += NW * GATHER_TASKS) {
+          uint32_t cc[GATHER_TASKS], pp[GATHER_TASKS];
+          double xv[GATHER_TASKS];
+          int32_t xi[GATHER_TASKS];
+#pragma unroll
+          for (int u = 0; u < GATHER_TASKS; ++u) {
+            const int tt = tb + u * NW;
+            cc[u] = tt < nt ? tcnt[tt] : 0u;
+            pp[u] = tt < nt ? tpos[tt] : 0u;
+            if (static_cast<uint32_t>(lane) < cc[u]) {
+              const int64_t src = static_cast<int64_t>(t0 + tt) * cap + lane;
+              xv[u] = __ldcg(cand_val + src);
+              xi[u] = __ldcg(cand_idx + src);
+            }
           }
-          const int64_t src = static_cast<int64_t>(t0 + lo) * cap + (e - tpos[lo]);
-          sv[carry + e] = __ldcg(cand_val + src);
-          si[carry + e] = __ldcg(cand_idx + src);
+#pragma unroll
+          for (int u = 0; u < GATHER_TASKS; ++u)
+            if (static_cast<uint32_t>(lane) < cc[u]) {
+              sv[pp[u] + lane] = xv[u];
+              si[pp[u] + lane] = xi[u];
+            }
+#pragma unroll 1
+          for (int u = 0; u < GATHER_TASKS; ++u) {  // lists longer than a warp
+            const int64_t row = static_cast<int64_t>(t0 + tb + u * NW) * cap;
+            for (uint32_t e = 32u + lane; e < cc[u]; e += 32u) {
+              sv[pp[u] + e] = __ldcg(cand_val + row + e);
+              si[pp[u] + e] = __ldcg(cand_idx + row + e);
+            }
+          }
         }
         carry += tot;
-        __syncthreads();
+        __syncthreads();  // tpos / tcnt reuse; the staged candidates are visible
       }
+      LAGS_S64(2, clock64());
       auto key_at = [=](int64_t i) { return Key<double>::of(sv[i]); };
       const SelectThreshold<K> th = radix_select<K, Key<double>::BITS, RB>(key_at, m, k, sm, min(k2, m), &key2, true);
-      auto load = [=](int64_t i, K* key, double* x, int64_t* ix) {
-        *x = sv[i];
-        *key = Key<double>::of(*x);
-        *ix = si[i];
-      };
-      auto emit = [=](uint32_t pos, int64_t, int64_t ix, double x) {
+      LAGS_S64(3, clock64());
+      auto emit = [=](uint32_t pos, int32_t ix, double x) {
         oidx[pos] = static_cast<int32_t>(ix);
         oval[pos] = x;
-        data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
+        if (r32) r32[L.offset + ix] = static_cast<float>(sent_residual(x));  // fl32(acc - acc)
+        else data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       };
-      cnt = ordered_compact<K, double>(m, th, load, emit, sm);
+      cnt = compact64_staged(m, th, sv, si, emit, sm);
+      LAGS_S64(4, clock64());
     }
     ns.thr = m >= k2 ? max(key2, 1ull) : lower_threshold64(st.thr, m, k2);
     ns.last_cands = m;
@@ -196,16 +301,23 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
     const uint32_t k2 = static_cast<uint32_t>(pk < L.dim ? (pk > k ? pk : k + 1) : L.dim);
     K key2 = 0ull;
     cnt = exact_topk_dense<double, double>(data, L.dim, k, oidx, oval, true, sm, k2, &key2);
-    ns.thr = max(key2, 1ull);
+    if (r32) {  // the fp32 residual of the selected entries (the compaction's writes are visible)
+      __syncthreads();
+      for (uint32_t q = threadIdx.x; q < cnt; q += SEL_NT)
+        r32[L.offset + oidx[q]] = static_cast<float>(sent_residual(oval[q]));
+    }
+    ns.thr = tiny ? 0ull : max(key2, 1ull);
     ns.fallbacks += predicted ? 1u : 0u;
     ns.last_cands = 0;
     ns.pf256 = pf_encode(pf_next);
-    ns.path = 0u;
+    ns.path = tiny ? 0u : 2u;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     count_out[j] = static_cast<int32_t>(cnt);
     state[j] = ns;
+    LAGS_S64(5, clock64());
+    LAGS_S64(7, globaltimer_lo());
   }
 }
 

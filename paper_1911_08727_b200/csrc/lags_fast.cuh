@@ -299,12 +299,12 @@ struct SelectSmem {
   uint32_t rpos[SEL_NT];     // speculative gather: positions of the tasks' remainders
 };
 
-// P = 1 update fused into the selection epilogue (no exchange, no separate decode): exactly the
-// decode of R: training.py:248,253-254 with one worker, v = fl32(fl64(v) - (0.0 + x) / 1).
-__device__ __forceinline__ float single_rank_update(float v, float x) {
-  const double total = __dadd_rn(0.0, static_cast<double>(x));
-  return static_cast<float>(__dsub_rn(static_cast<double>(v), __ddiv_rn(total, 1.0)));
-}
+// P = 1 update fused into the selection epilogue (no exchange, no separate decode): the decode of
+// R: training.py:248,253-254 with one worker, v = fl32(fl64(v) - (0.0 + x) / 1).  Computed in fp32:
+// the division by 1 is exact, 0.0 + x only maps -0 to +0, and rounding the exact difference of two
+// floats to double (53 >= 2*24 + 2 bits) then to float gives the directly rounded float difference
+// (innocuous double rounding), so the bits are the same.
+__device__ __forceinline__ float single_rank_update(float v, float x) { return __fsub_rn(v, __fadd_rn(0.0f, x)); }
 
 // Post-pass over a layer's selected (idx, val) just written by the compaction: batches of
 // independent weight loads in flight per thread (the weights are HBM-resident and scattered).
@@ -838,12 +838,12 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
         const uint32_t e = e0 + u * SEL_NT + threadIdx.x;
         tk[u] = -1;
         if (e < rtot) {
-          int lo = 0, hi = nt - 1;  // last task whose remainder starts at or before e
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (cs.rpos[mid] <= e) lo = mid;
-            else hi = mid - 1;
-          }
+          // the last task whose remainder starts at or before e; fixed steps, so the
+          // GATHER_ILP searches interleave
+          int lo = 0;
+#pragma unroll
+          for (int step = SEL_NT / 2; step > 0; step >>= 1)
+            if (lo + step < nt && cs.rpos[lo + step] <= e) lo += step;
           tk[u] = lo;
           off[u] = (lo < NW * GATHER_TASKS ? 32u : 0u) + (e - cs.rpos[lo]);
           const int64_t src = static_cast<int64_t>(t_lo + lo) * cap + off[u];
@@ -867,10 +867,15 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
 // compact_staged with V entries per thread (see below).
 template <int V, typename Emit>
 __device__ uint32_t compact_staged_v(uint32_t m, const SelectThreshold<uint32_t>& th, const float* sv,
-                                     const int32_t* si, const float* vl, Emit emit, RadixSmem<Key<float>::RB>& sm,
-                                     uint32_t carry_gt, uint32_t carry_eq) {
+                                     const int32_t* si, const float* vl, Emit emit, SelectSmem& cs,
+                                     uint32_t carry_gt, uint32_t carry_eq, int32_t* oidx, float* oval) {
   static_assert(V % 4 == 0, "whole 16-byte vectors per plane and thread");
+  static_assert(SEL_NT * V <= F32_BINS, "a chunk's output fits the staging arrays");
+  RadixSmem<Key<float>::RB>& sm = cs.sm;
+  int32_t* st_idx = reinterpret_cast<int32_t*>(sm.hist);  // free here: the threshold is known
+  float* st_val = reinterpret_cast<float*>(cs.hist2);
   for (uint32_t base = 0; base < m; base += SEL_NT * V) {
+    const uint32_t out0 = carry_gt + min(carry_eq, th.need_eq);  // the chunk's first output slot
     const uint32_t i0 = base + threadIdx.x * V;
     float xs[V];
 #pragma unroll
@@ -916,29 +921,43 @@ __device__ uint32_t compact_staged_v(uint32_t m, const SelectThreshold<uint32_t>
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
-        if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), ixs[v], xs[v], ws[v]);
+        if (g || (e && eq_before < th.need_eq)) {
+          const uint32_t q = gt_before + min(eq_before, th.need_eq) - out0;
+          st_idx[q] = ixs[v];
+          st_val[q] = xs[v];
+          emit(ixs[v], xs[v], ws[v]);
+        }
         gt_before += g;
         eq_before += e;
       }
     }
     carry_gt += tot & 0xffffu;
     carry_eq += tot >> 16;
-    __syncthreads();  // warp_tot reuse by the next scan
+    __syncthreads();  // the staged pairs are complete (and warp_tot is free for the next scan)
+    // the chunk's (index, value) pairs leave as coalesced runs (the per-thread emits are scattered)
+    const uint32_t n_out = carry_gt + min(carry_eq, th.need_eq) - out0;
+    for (uint32_t q = threadIdx.x; q < n_out; q += SEL_NT) {
+      oidx[out0 + q] = st_idx[q];
+      oval[out0 + q] = st_val[q];
+    }
   }
+  __syncthreads();  // the staging arrays are read before the callers reuse them
   return carry_gt + min(carry_eq, th.need_eq);
 }
 
 // Ordered compaction of candidates staged in shared memory (sv / si: 16-byte aligned planes in
 // index order), 4 (8 for large sets: half the block scans) entries per thread read as 16-byte
-// vectors per plane; vl (nullable): the layer's weights for the fused P = 1 update.  The rule and the result are ordered_compact_pf's: (key & pmask) >
-// prefix, plus the first need_eq equal ones in index order; carry_gt / carry_eq count the lower
-// ranks' entries.  emit(pos, ix, x, w).  Returns the selected count (all threads).
+// vectors per plane; vl (nullable): the layer's weights for the fused P = 1 update.  The rule and
+// the result are ordered_compact_pf's: (key & pmask) > prefix, plus the first need_eq equal ones
+// in index order; carry_gt / carry_eq count the lower ranks' entries.  The (index, value) pairs
+// leave through shared memory as coalesced runs into oidx / oval; emit(ix, x, w) does the
+// scattered residual / weight writes.  Returns the selected count (all threads).
 template <typename Emit>
 __device__ uint32_t compact_staged(uint32_t m, const SelectThreshold<uint32_t>& th, const float* sv, const int32_t* si,
-                                   const float* vl, Emit emit, RadixSmem<Key<float>::RB>& sm, uint32_t carry_gt,
-                                   uint32_t carry_eq) {
-  if (m > 2u * SEL_NT * 4u) return compact_staged_v<8>(m, th, sv, si, vl, emit, sm, carry_gt, carry_eq);
-  return compact_staged_v<4>(m, th, sv, si, vl, emit, sm, carry_gt, carry_eq);
+                                   const float* vl, Emit emit, SelectSmem& cs, uint32_t carry_gt, uint32_t carry_eq,
+                                   int32_t* oidx, float* oval) {
+  if (m > 2u * SEL_NT * 4u) return compact_staged_v<8>(m, th, sv, si, vl, emit, cs, carry_gt, carry_eq, oidx, oval);
+  return compact_staged_v<4>(m, th, sv, si, vl, emit, cs, carry_gt, carry_eq, oidx, oval);
 }
 
 // Candidate path of one layer inside one CTA.  Returns 0 on success, or why the candidate set
@@ -1083,13 +1102,11 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     float* oval = val_out + L.slot;
     LAGS_CSTAMP(4);
     if (in_smem) {  // staged: vector reads of the planes
-      auto emit = [=](uint32_t pos, int32_t ix, float x, float w) {
-        oidx[pos] = ix;
-        oval[pos] = x;
+      auto emit = [=](int32_t ix, float x, float w) {
         data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
         if (vl) vl[ix] = single_rank_update(w, x);
       };
-      cnt = compact_staged(m, th, sv, si, vl, emit, sm, 0u, 0u);
+      cnt = compact_staged(m, th, sv, si, vl, emit, cs, 0u, 0u, oidx, oval);
     } else if (vl) {  // fused P = 1 update: the weights are loaded before the compaction's scan
       auto emit = [=](uint32_t pos, int64_t, int64_t ix, float x, float w) {
         oidx[pos] = static_cast<int32_t>(ix);

@@ -4,13 +4,14 @@
 //   accum_emit_kernel     (lags_fast.cuh) fp32 accumulate + candidate emission (K1)  R: training.py:250,174
 //   select_kernel         (lags_cluster.cuh) exact top-k from the candidates: 4-CTA clusters
 //                         for the largest layers, persistent per-layer CTAs for the rest   R: sparsify.py:84-90
-//   accum_kernel / select_dense_kernel  exact dense path (fp64, mixed, forced exact)  R: training.py:250-252
+//   accum_emit64_kernel / select64_kernel (lags_f64.cuh) the same two launches for LAGS_F64 and
+//                         LAGS_F32_ACC64 on 64-bit keys                             R: training.py:250-252
+//   select_dense_kernel   exact dense top-k of one vector (the top_k drop-in)      R: sparsify.py:84-90
 //   decode_* kernels    rank-ordered fp64 accumulation + SGD/momentum update          R: training.py:248,253-254
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <type_traits>
-#include <cstdlib>
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
@@ -27,23 +28,6 @@
 #include "lags_select.cuh"
 
 namespace lags {
-
-// ------------------------------------------------------------------------------------------
-// dense accumulate (all dtypes): acc = r + alpha*g (two roundings), finiteness of g
-// ------------------------------------------------------------------------------------------
-template <typename TIn, typename TAcc>
-__global__ void __launch_bounds__(256) accum_kernel(const TIn* __restrict__ g, TIn* r, TAcc* acc_out, TAcc alpha,
-                                                    int64_t n, uint32_t* status) {
-  bool bad = false;
-  griddep_wait();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const TIn gi = g[i];
-    bad |= nonfinite(gi);
-    acc_out[i] = accum(static_cast<TAcc>(r[i]), static_cast<TAcc>(gi), alpha);
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
-}
 
 template <typename T>
 __global__ void __launch_bounds__(256) finite_kernel(const T* __restrict__ x, int64_t n, uint32_t* status) {
@@ -65,15 +49,6 @@ __global__ void __launch_bounds__(SEL_NT) select_dense_kernel(const lags_layer_t
   const uint32_t cnt = exact_topk_dense<T, T>(acc + L.offset, L.dim, static_cast<uint32_t>(L.k),
                                               idx_out + L.slot, val_out + L.slot, zero_selected != 0, sm);
   if (threadIdx.x == 0) count_out[layers ? blockIdx.x : 0] = static_cast<int32_t>(cnt);
-}
-
-// Mixed mode epilogue: r (fp32) <- fl32(acc) where acc (fp64) has +0.0 at the selected slots.
-__global__ void __launch_bounds__(256) store_residual_kernel(const double* __restrict__ acc, float* __restrict__ r,
-                                                             int64_t n) {
-  griddep_wait();
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-    r[i] = static_cast<float>(acc[i]);
 }
 
 template <typename T>
@@ -116,7 +91,7 @@ __global__ void __launch_bounds__(256) decode_single_kernel(const lags_layer_t* 
     if (s - L.slot >= msg.count(0, j)) continue;
     const int64_t i = L.offset + msg.idx(0, s);
     const double total = __dadd_rn(0.0, static_cast<double>(msg.val<TVal>(0, s)));
-    v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), __ddiv_rn(total, 1.0)));
+    v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), total)  /* total / 1 == total */);
   }
 }
 
@@ -171,7 +146,7 @@ __global__ void __launch_bounds__(DEC_NT) decode_update_kernel(const lags_layer_
     const int q = __ffs(b) - 1;
     total = __dadd_rn(total, static_cast<double>(planes[static_cast<int64_t>(q) * n + i]));
   }
-  v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
+  v[i] = static_cast<TV>(__dsub_rn(vi, div_workers(total, P)));
   mask[i] = 0u;
 }
 
@@ -260,7 +235,7 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const DecTile* __r
       if (bits == 0 || (__ffs(bits) - 1) != pp[u]) continue;  // only the lowest holding rank applies
       const double vi = static_cast<double>(vold);
       const double total = plane_sum(planes, n, i, bits, P);
-      v[i] = static_cast<TV>(__dsub_rn(vi, __ddiv_rn(total, static_cast<double>(P))));
+      v[i] = static_cast<TV>(__dsub_rn(vi, div_workers(total, P)));
       mask[i] = 0u;
     }
     return;
@@ -291,7 +266,7 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const DecTile* __r
         double upd = 0.0;
         if ((grp >> u) & 1u) {
           const uint32_t bits = mask[i0 + u];
-          upd = __ddiv_rn(plane_sum(planes, n, i0 + u, bits, P), static_cast<double>(P));
+          upd = div_workers(plane_sum(planes, n, i0 + u, bits, P), P);
           mask[i0 + u] = 0u;
         }
         momentum_update(ve[u], me[u], upd, mu);
@@ -304,7 +279,7 @@ __global__ void __launch_bounds__(DEC_NT) decode_fused_kernel(const DecTile* __r
   }
   for (int64_t i = done + tid; i < n; i += nthreads) {  // unaligned buffers / the tail
     const uint32_t bits = mask[i];
-    const double upd = bits ? __ddiv_rn(plane_sum(planes, n, i, bits, P), static_cast<double>(P)) : 0.0;
+    const double upd = bits ? div_workers(plane_sum(planes, n, i, bits, P), P) : 0.0;
     if (bits) {
       mask[i] = 0u;
       atomicAnd(touched + (i >> 5), ~(1u << (i & 31)));
@@ -332,7 +307,7 @@ __global__ void __launch_bounds__(256) decode_momentum_kernel(const TVal* planes
       mask[i] = 0u;
     }
     const double mnew =
-        __dadd_rn(__dmul_rn(mu, static_cast<double>(mom[i])), __ddiv_rn(total, static_cast<double>(P)));
+        __dadd_rn(__dmul_rn(mu, static_cast<double>(mom[i])), div_workers(total, P));
     mom[i] = static_cast<TV>(mnew);
     v[i] = static_cast<TV>(__dsub_rn(static_cast<double>(v[i]), mnew));
   }
@@ -505,10 +480,10 @@ struct lags_bucket {
   int32_t* slot_layer = nullptr;
   int32_t* cand_cnt = nullptr;
   int32_t* cand_idx = nullptr;
-  float* cand_val = nullptr;   // LAGS_F32 candidate values (cand_val64 for LAGS_F64)
+  float* cand_val = nullptr;   // LAGS_F32 candidate values (cand_val64 for LAGS_F64 / LAGS_F32_ACC64)
   double* cand_val64 = nullptr;
   double* gval64 = nullptr;
-  State64* state64 = nullptr;   // LAGS_F64 selection state
+  State64* state64 = nullptr;   // LAGS_F64 / LAGS_F32_ACC64 selection state
   int32_t* gidx = nullptr;
   float* gval = nullptr;
   double* acc64 = nullptr;
@@ -635,7 +610,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   const double want = 16.0 * PRED_FACTOR * max_per_task;
   int cap = 256;
   while (cap < want && cap < task) cap <<= 1;
-  p->cap = dtype == LAGS_F32_ACC64 ? 0 : cap;  // candidate lists: the fp32 and fp64 fast paths
+  p->cap = cap;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     const size_t at = o;
@@ -653,7 +628,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_cval = take(val_size(dtype) * nt * cp);
   p->o_gidx = take(sizeof(int32_t) * nt * cp);
   p->o_gval = take(val_size(dtype) * nt * cp);
-  p->o_state64 = take(dtype == LAGS_F64 ? sizeof(State64) * L : 0);
+  p->o_state64 = take(dtype != LAGS_F32 ? sizeof(State64) * L : 0);
   p->o_acc = take(dtype == LAGS_F32_ACC64 ? sizeof(double) * static_cast<size_t>(p->n_total) : 0);
   p->o_mask = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total));
   p->o_planes = take(val_size(dtype) * static_cast<size_t>(p->n_total) * static_cast<size_t>(max_world));
@@ -767,7 +742,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
   b->gval = reinterpret_cast<float*>(base + p.o_gval);
   b->cand_val64 = reinterpret_cast<double*>(base + p.o_cval);
   b->gval64 = reinterpret_cast<double*>(base + p.o_gval);
-  b->state64 = dtype == LAGS_F64 ? reinterpret_cast<State64*>(base + p.o_state64) : nullptr;
+  b->state64 = dtype != LAGS_F32 ? reinterpret_cast<State64*>(base + p.o_state64) : nullptr;
   b->acc64 = reinterpret_cast<double*>(base + p.o_acc);
   b->mask = reinterpret_cast<uint32_t*>(base + p.o_mask);
   b->planes = base + p.o_planes;
@@ -849,7 +824,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       cudaMemcpyAsync(b->tiles_dec, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, s) ==
           cudaSuccess &&
       cudaMemsetAsync(b->state, 0, sizeof(FastState) * nlayers, s) == cudaSuccess &&
-      (dtype != LAGS_F64 || cudaMemsetAsync(b->state64, 0, sizeof(State64) * nlayers, s) == cudaSuccess) &&
+      (dtype == LAGS_F32 || cudaMemsetAsync(b->state64, 0, sizeof(State64) * nlayers, s) == cudaSuccess) &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
       cudaMemsetAsync(b->touched, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total / 32 + 1), s) == cudaSuccess &&
       (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
@@ -880,7 +855,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       words = std::max<int64_t>(words, dims[j] <= SMALL_LAYER ? dims[j] : (15 * static_cast<int64_t>(ks[j])) / 2);
     b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), select_smem_words_max()));
   }
-  if (dtype == LAGS_F64) {
+  if (dtype != LAGS_F32) {
     static int words64 = 0;  // the device's opt-in shared memory minus select64_kernel's static part
     if (words64 == 0) {
       int dev = 0, optin = 0;
@@ -896,7 +871,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     }
     // candidate staging: value (2 words) + index per candidate, ~2.5 k of them at the adaptive margin
     int64_t words = 4096;
-    for (int j = 0; j < nlayers; ++j) words = std::max<int64_t>(words, 3 * ((5 * static_cast<int64_t>(ks[j])) / 2) + 2);
+    for (int j = 0; j < nlayers; ++j) words = std::max<int64_t>(words, 3 * ((5 * static_cast<int64_t>(ks[j])) / 2) + 8);
     b->smem_keys = static_cast<int>(std::min<int64_t>(align_up(static_cast<size_t>(words), 1024), words64));
   }
   *out = b;
@@ -933,7 +908,6 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
   char* m = static_cast<char*>(msg);
   int32_t* cnt = reinterpret_cast<int32_t*>(m + b->off_cnt);
   int32_t* idx = reinterpret_cast<int32_t*>(m + b->off_idx);
-  const int64_t n = b->n_total;
   if (b->dtype == LAGS_F32) {
     const bool exact = (flags & LAGS_COMPRESS_EXACT) != 0;
     const float a = static_cast<float>(alpha);  // numpy casts a Python float to float32 (NEP 50)
@@ -980,35 +954,34 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     return cuda_check("lags_bucket_compress(f32)", launches);
   }
   if (v_update) return fail(LAGS_ERR_INVALID_ARG, "fused single-rank update needs an LAGS_F32 bucket");
-  if (b->dtype == LAGS_F64) {  // K1 (candidates above the predicted threshold) + one CTA per layer
-    const int ntasks = b->ntasks;
-    const int blocks = (ntasks + K1_WARPS - 1) / K1_WARPS;
+  // LAGS_F64 / LAGS_F32_ACC64: K1 (candidates above the predicted threshold) + one CTA per layer;
+  // the mixed mode keeps the fp64 acc in the bucket memory and its fp32 residual in r
+  const int ntasks = b->ntasks;
+  const int blocks = (ntasks + K1_WARPS - 1) / K1_WARPS;
+  const bool zg = (flags & LAGS_COMPRESS_ZERO_GRAD) != 0;
+  const bool mixed = b->dtype == LAGS_F32_ACC64;
+  double* acc = mixed ? b->acc64 : static_cast<double*>(r);
+  cudaError_t e;
+  if (mixed) {
+    float* rr = static_cast<float*>(r);
+    float* gg = static_cast<float*>(g);
+    e = launch_pdl(zg ? accum_emit64_kernel<true, float> : accum_emit64_kernel<false, float>, dim3(blocks),
+                   dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers, b->state64, gg, rr, b->acc64, alpha,
+                   b->cap, b->cand_idx, b->cand_val64, b->cand_cnt, status);
+  } else {
     double* rr = static_cast<double*>(r);
     double* gg = static_cast<double*>(g);
-    cudaError_t e;
-    if (flags & LAGS_COMPRESS_ZERO_GRAD)
-      e = launch_pdl(accum_emit64_kernel<true>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
-                     b->state64, gg, rr, alpha, b->cap, b->cand_idx, b->cand_val64, b->cand_cnt, status);
-    else
-      e = launch_pdl(accum_emit64_kernel<false>, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers,
-                     b->state64, gg, rr, alpha, b->cap, b->cand_idx, b->cand_val64, b->cand_cnt, status);
-    if (e == cudaSuccess)
-      e = launch_pdl(select64_kernel, dim3(b->nlayers), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s,
-                     b->layers, b->layer_tasks, b->state64, b->cand_cnt, b->cand_idx, b->cand_val64, b->cap, b->gidx,
-                     b->gval64, rr, idx, reinterpret_cast<double*>(m + b->off_val), cnt, b->smem_keys,
-                     (flags & LAGS_COMPRESS_EXACT) ? 1 : 0);
-    if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress(f64) launch: ") + cudaGetErrorString(e));
-    return cuda_check("lags_bucket_compress(f64)", 2);
+    e = launch_pdl(zg ? accum_emit64_kernel<true, double> : accum_emit64_kernel<false, double>, dim3(blocks),
+                   dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers, b->state64, gg, rr,
+                   static_cast<double*>(nullptr), alpha, b->cap, b->cand_idx, b->cand_val64, b->cand_cnt, status);
   }
-  // LAGS_F32_ACC64: fp64 acc in the bucket memory, fp32 residual rewritten after selection
-  accum_kernel<float, double><<<stream_grid(n, 256, 8), 256, 0, s>>>(
-      static_cast<const float*>(g), static_cast<float*>(r), b->acc64, alpha, n, status);
-  select_dense_kernel<double><<<b->nlayers, SEL_NT, 0, s>>>(b->layers, lags_layer_t{}, b->acc64, idx,
-                                                            reinterpret_cast<double*>(m + b->off_val), cnt, 1);
-  store_residual_kernel<<<stream_grid(n, 256, 8), 256, 0, s>>>(b->acc64, static_cast<float*>(r), n);
-  if ((flags & LAGS_COMPRESS_ZERO_GRAD) && cudaMemsetAsync(const_cast<void*>(g), 0, sizeof(float) * n, s) != cudaSuccess)
-    return cuda_check("zero grad", 3);
-  return cuda_check("lags_bucket_compress(f32/acc64)", 3);
+  if (e == cudaSuccess)
+    e = launch_pdl(select64_kernel, dim3(b->nlayers), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s,
+                   b->layers, b->layer_tasks, b->state64, b->cand_cnt, b->cand_idx, b->cand_val64, b->cap, b->gidx,
+                   b->gval64, acc, idx, reinterpret_cast<double*>(m + b->off_val), cnt, b->smem_keys,
+                   (flags & LAGS_COMPRESS_EXACT) ? 1 : 0, mixed ? static_cast<float*>(r) : static_cast<float*>(nullptr));
+  if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress(f64) launch: ") + cudaGetErrorString(e));
+  return cuda_check(mixed ? "lags_bucket_compress(f32/acc64)" : "lags_bucket_compress(f64)", 2);
 }
 
 }  // extern "C"
@@ -1170,6 +1143,22 @@ int lags_bucket_set_grad_table(lags_bucket_t* b, const void* table) {
 int lags_bucket_stats(const lags_bucket_t* b, uint32_t* out, lags_stream_t stream) {
   if (!b || !out) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_stats: null pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (b->state64) {  // 64-bit-key buckets: {thr high word, fallbacks, last candidates, calls, 0, path, 0...}
+    std::vector<State64> st(b->nlayers);
+    if (cudaMemcpyAsync(st.data(), b->state64, sizeof(State64) * b->nlayers, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return cuda_check("lags_bucket_stats", 0);
+    for (int j = 0; j < b->nlayers; ++j) {
+      uint32_t* o = out + static_cast<size_t>(j) * LAGS_STATS_WORDS;
+      std::fill(o, o + LAGS_STATS_WORDS, 0u);
+      o[0] = static_cast<uint32_t>(st[j].thr >> 32);
+      o[1] = st[j].fallbacks;
+      o[2] = st[j].last_cands;
+      o[3] = st[j].calls;
+      o[5] = st[j].path;
+    }
+    return LAGS_OK;
+  }
   if (cudaMemcpyAsync(out, b->state, sizeof(FastState) * b->nlayers, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
     return cuda_check("lags_bucket_stats", 0);
@@ -1310,6 +1299,9 @@ int lags_decompress(int32_t dtype, const int32_t* idx, const void* val, const in
 // Diagnostic builds only: the phase stamps of the first cluster layer ([rank][clock|globaltimer][16]).
 extern "C" int lags_dbg_stamps_read(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_stamps, sizeof(lags::lags_dbg_stamps)));
+}
+extern "C" int lags_dbg_s64_read(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_s64, sizeof(lags::lags_dbg_s64)));
 }
 extern "C" int lags_dbg_cstamps_read(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_cstamps, sizeof(lags::lags_dbg_cstamps)));

@@ -552,6 +552,52 @@ def test_multi_rank_momentum_decode_exact(L, P):
     assert int(st.item()) == 0
 
 
+def test_mixed_fast_path_equals_exact_path_and_oracle(L):
+    """LAGS_F32_ACC64 (fp32 storage, numpy-float64 alpha: acc and values fp64, residual fp32; R:
+    training.py:250-252 under NEP 50) on the fp64 fast path against its dense exact path and the
+    oracle, bit for bit, through steady state, a threshold collapse and tie-heavy data."""
+    from paper_1911_08727_b200 import _native as N
+
+    dims = [20000, 64, 300000, 5000, 589824, 1000]
+    ks = [max(1, d // 1000) for d in dims]
+    fast = L.Bucket(dims, ks, N.F32_ACC64)
+    exact = L.Bucket(dims, ks, N.F32_ACC64)
+    n = sum(dims)
+    gen = torch.Generator(device="cuda").manual_seed(17)
+    r_f = torch.zeros(n, device="cuda")
+    r_e = torch.zeros(n, device="cuda")
+    r_h = np.zeros(n, dtype=np.float32)
+    m_f, m_e = fast.new_messages(1), exact.new_messages(1)
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    off = np.concatenate([[0], np.cumsum(dims)])
+    paths = set()
+    for it in range(14):
+        if it >= 11:  # integer-valued: many ties
+            g = torch.randint(-6, 7, (n,), device="cuda", generator=gen).float()
+        else:
+            g = torch.randn(n, device="cuda", generator=gen)
+        if it in (6, 7):
+            g *= 1e-3
+        alpha = np.float64(1.0 if it >= 11 else 0.05)
+        fast.compress(g, r_f, alpha, m_f, st)
+        exact.compress(g, r_e, alpha, m_e, st, exact=True)
+        assert torch.equal(m_f, m_e), f"messages differ at iteration {it}"
+        assert torch.equal(r_f.view(torch.int32), r_e.view(torch.int32)), f"residuals differ at {it}"
+        gh = g.cpu().numpy()
+        acc = r_h.astype(np.float64) + alpha * gh.astype(np.float64)
+        acc_sent = acc.copy()
+        for j, (ii, vv) in enumerate(fast.unpack(m_f)):
+            wi, wv = orc.top_k(acc[off[j]:off[j + 1]], ks[j])
+            np.testing.assert_array_equal(ii, wi)
+            assert vv.dtype == np.float64 and _same_bits(vv, wv), (it, j)
+            acc_sent[off[j] + ii] = acc[off[j] + ii] - vv
+        r_h = acc_sent.astype(np.float32)
+        assert r_f.cpu().numpy().tobytes() == r_h.tobytes(), it
+        paths.update(int(x) for x in fast.stats()[:, 5])
+    assert 1 in paths, "the candidate path never ran"
+    assert int(st.item()) == 0
+
+
 def test_f64_fast_path_equals_exact_path_and_oracle(L):
     """The fp64 fast path (K1 on 64-bit keys with candidate lists + one CTA per layer) against the
     dense exact path and the oracle, bit for bit: steady state, a threshold collapse (too few

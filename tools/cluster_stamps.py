@@ -17,7 +17,7 @@ NAMES = ["entry", "counts loaded", "block sums", "cluster wait", "histogram cut"
          "cluster.sync", "resolve", "lower-rank counts", "-", "ordered compact", "zero histogram", "end"]
 
 dims = resnet50_dims()
-ks = ks_for(dims)
+ks = ks_for(dims, float(sys.argv[1]) if len(sys.argv) > 1 else 0.001)
 n = sum(dims)
 b = L.Bucket(dims, ks, N.F32)
 gen = torch.Generator(device="cuda").manual_seed(1)
