@@ -9,12 +9,13 @@
 //    LAGS_F32_ACC64 (fp32 storage, numpy-float64 alpha, R: training.py:250 under NEP 50) runs the
 //    same kernel on float g / r: acc in fp64 into the bucket's acc64 (the selection's dense
 //    fallback reads it) and fl32(acc) back into r -- 20 B/element.
-// select64_kernel: one CTA per layer (r32: LAGS_F32_ACC64's fp32 residual, r = acc64 then).  When the candidate set provably holds the top-k (no task
-//    overflow, count >= k): gather into shared memory, radix select on the 64-bit keys starting
-//    below the candidates' common prefix, ordered compaction (ascending indices, residual
-//    acc - acc at the selected entries), and the next threshold from the same passes.  Otherwise
-//    (first call, failed prediction, forced exact) the dense exact path over r, which also yields
-//    the prediction.  Both return exactly the reference's selection (R: sparsify.py:84-90).
+// select64_kernel: one CTA per layer, the longest first.  When the candidate set provably holds
+//    the top-k (no task overflow, count >= k): gather into shared memory (warp per task), radix
+//    select on the 64-bit keys starting below the candidates' common prefix, ordered compaction
+//    (ascending indices, residual acc - acc at the selected entries; fp32 for LAGS_F32_ACC64),
+//    and the next threshold from the same passes.  Otherwise (first call, failed prediction,
+//    forced exact, layers of <= TINY_LAYER entries) the dense exact path over acc, which also
+//    yields the prediction.  Both return exactly the reference's selection (R: sparsify.py:84-90).
 #pragma once
 #include "lags_fast.cuh"
 
@@ -181,14 +182,14 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
                                                           const double* __restrict__ cand_val, int cap, int32_t* gidx,
                                                           double* gval, double* r, int32_t* idx_out, double* val_out,
                                                           int32_t* count_out, int smem_words, int force_exact,
-                                                          float* r32) {
+                                                          float* r32, const int32_t* __restrict__ order) {
   using K = unsigned long long;
   constexpr int RB = Key<double>::RB;
   extern __shared__ __align__(16) uint32_t dyn[];
   __shared__ RadixSmem<RB> sm;
   __shared__ uint32_t tpos[SEL_NT], tcnt[SEL_NT];
   griddep_wait();  // K1 has completed and its writes are visible
-  const int j = blockIdx.x;
+  const int j = order[blockIdx.x];  // the longest layers first: they must not wait for a second wave
   LAGS_S64(0, clock64());
   LAGS_S64(6, globaltimer_lo());
   const lags_layer_t L = layers[j];

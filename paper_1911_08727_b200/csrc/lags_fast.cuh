@@ -133,13 +133,15 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
 
 // K1's per-layer histogram of its candidate keys -- the selection's first cut without a pass over
 // the candidates: HIST_BINS bins of 2^HIST_SHIFT consecutive keys, counted up from the layer's
-// candidate threshold (8192 bins per octave of |x|, so the 4096 bins span keys up to sqrt(2) times
-// the threshold; larger keys share the top bin).  Error feedback piles the accumulated magnitudes
-// up just below the threshold, so the bins must be fine there (at 1024 per octave the cut bin of a
-// 2.4 M-element layer held 150-220 keys).  HIST_BINS equals the radix histogram size, so the radix
-// find_bin2 resolves ranks on it.
+// candidate threshold (16384 bins per octave of |x|, so the 4096 bins span keys up to 2^(1/4) =
+// 1.19 times the threshold; larger keys share the top bin).  Error feedback piles the accumulated
+// magnitudes up just below the threshold, so the bins must be fine there (at 1024 per octave the
+// cut bin of a 2.4 M-element layer held 150-220 keys; at 8192 a 15 M-element LSTM layer's still
+// held ~400, above BIN_LIST_MAX).  With the adaptive margin (m ~ 2k candidates) the k-th key sits
+// a few percent above the threshold for k >= 16; a cut in the top bin takes the radix select.
+// HIST_BINS equals the radix histogram size, so the radix find_bin2 resolves ranks on it.
 #ifndef LAGS_HIST_SHIFT
-#define LAGS_HIST_SHIFT 10
+#define LAGS_HIST_SHIFT 9
 #endif
 constexpr int HIST_SHIFT = LAGS_HIST_SHIFT;
 constexpr int HIST_BINS = F32_BINS;
@@ -292,7 +294,7 @@ __device__ LAGS_SUM_ATTR uint32_t block_sum(uint32_t v, RadixSmem<RB>& sm) {
 
 struct SelectSmem {
   RadixSmem<Key<float>::RB> sm;
-  uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
+  alignas(16) uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
   uint32_t tpos[SEL_NT];     // candidate gather: per-task output position / count
   uint32_t tcnt[SEL_NT];
   uint32_t tcache[SEL_NT];   // the layer's task counts from the counting pass (layers of <= SEL_NT tasks)

@@ -979,7 +979,8 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     e = launch_pdl(select64_kernel, dim3(b->nlayers), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s,
                    b->layers, b->layer_tasks, b->state64, b->cand_cnt, b->cand_idx, b->cand_val64, b->cap, b->gidx,
                    b->gval64, acc, idx, reinterpret_cast<double*>(m + b->off_val), cnt, b->smem_keys,
-                   (flags & LAGS_COMPRESS_EXACT) ? 1 : 0, mixed ? static_cast<float*>(r) : static_cast<float*>(nullptr));
+                   (flags & LAGS_COMPRESS_EXACT) ? 1 : 0, mixed ? static_cast<float*>(r) : static_cast<float*>(nullptr),
+                   static_cast<const int32_t*>(b->order));
   if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress(f64) launch: ") + cudaGetErrorString(e));
   return cuda_check(mixed ? "lags_bucket_compress(f32/acc64)" : "lags_bucket_compress(f64)", 2);
 }

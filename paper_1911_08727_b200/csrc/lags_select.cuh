@@ -50,33 +50,50 @@ struct RadixSmem {
   uint32_t dbg;                               // -DLAGS_DBG_SELECT: radix_select_dual's shape
 };
 
+// Thread t's PER contiguous bins in descending order, h[q] = H[NB - 1 - t * PER - q], read as
+// 16-byte vectors (H 16-byte aligned): a scalar read at a stride of PER words was a PER-way bank
+// conflict per load.
+template <int NB, int PER>
+__device__ __forceinline__ void load_bins_desc(const uint32_t* H, int t, uint32_t (&h)[PER]) {
+  static_assert(PER % 4 == 0, "whole 16-byte vectors per thread");
+  const uint4* v = reinterpret_cast<const uint4*>(H + NB - PER * (t + 1));
+#pragma unroll
+  for (int c = 0; c < PER / 4; ++c) {
+    const uint4 x = v[c];
+    h[PER - 1 - 4 * c] = x.x;
+    h[PER - 2 - 4 * c] = x.y;
+    h[PER - 3 - 4 * c] = x.z;
+    h[PER - 4 - 4 * c] = x.w;
+  }
+}
+
 // Bin holding the rank-th largest (1-based) of the histogram (descending scan).  All threads.
-// `hist` (shared, NB bins) defaults to sm.hist.
+// `hist` (shared, NB bins, 16-byte aligned) defaults to sm.hist.
 template <int RB>
 __device__ LAGS_FINDBIN_ATTR void find_bin(RadixSmem<RB>& sm, uint32_t rank, uint32_t* bin, uint32_t* above,
                                          uint32_t* in_bin, const uint32_t* hist = nullptr) {
   constexpr int NB = RadixSmem<RB>::NB;
-  constexpr int PER = NB / SEL_NT;  // 2 (fp32) or 8 (fp64) bins per thread
+  constexpr int PER = NB / SEL_NT;  // 8 (fp32) or 16 (fp64) bins per thread at 512 threads
   const uint32_t* H = hist ? hist : sm.hist;
   const int t = threadIdx.x;
+  uint32_t h[PER];
+  load_bins_desc<NB, PER>(H, t, h);
   uint32_t s = 0;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) s += H[NB - 1 - t * PER - q];
+  for (int q = 0; q < PER; ++q) s += h[q];
   uint32_t tot;
   const uint32_t ex = block_exclusive_scan<SEL_NT>(s, sm.warp_tot, &tot);
   if (ex < rank && rank <= ex + s) {
     uint32_t c = ex;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-      const int b = NB - 1 - t * PER - q;
-      const uint32_t h = H[b];
-      if (rank <= c + h) {
-        sm.bin_count = h;
+      if (rank <= c + h[q]) {
+        sm.bin_count = h[q];
         sm.above = c;
-        sm.found = b;
+        sm.found = NB - 1 - t * PER - q;
         break;
       }
-      c += h;
+      c += h[q];
     }
   }
   __syncthreads();
@@ -95,12 +112,10 @@ __device__ LAGS_FINDBIN_ATTR void find_bin2(RadixSmem<RB>& sm, const uint32_t* H
   constexpr int PER = NB / SEL_NT;
   const int t = threadIdx.x;
   uint32_t h[PER];
+  load_bins_desc<NB, PER>(H, t, h);
   uint32_t s = 0;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    h[q] = H[NB - 1 - t * PER - q];
-    s += h[q];
-  }
+  for (int q = 0; q < PER; ++q) s += h[q];
   uint32_t tot;
   const uint32_t ex = block_exclusive_scan<SEL_NT>(s, sm.warp_tot, &tot);
 #pragma unroll
