@@ -90,9 +90,11 @@ int lags_bucket_message_layout(const lags_bucket_t* bucket, int64_t* off_counts,
 int lags_bucket_compress(lags_bucket_t* bucket, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, lags_stream_t stream);
 
-/* Single-rank step (P = 1, no exchange): lags_bucket_compress plus the update v = v - total / 1
- * fused into the selection epilogue (no separate decode pass).  The message is still written.
- * Equivalent to lags_bucket_compress followed by lags_bucket_decode_update(..., P = 1, ...). */
+/* Single-rank step (P = 1, no exchange): lags_bucket_compress plus the update v = v - total / 1,
+ * fused into the selection epilogue for LAGS_F32 buckets of up to 49152 selected entries (no
+ * separate decode pass); larger selections and the fp64 / mixed modes run the ordinary decode
+ * after the compress.  The message is still written.  Equivalent to lags_bucket_compress followed
+ * by lags_bucket_decode_update(..., P = 1, ...). */
 int lags_bucket_step_local(lags_bucket_t* bucket, void* g, void* r, double alpha, void* v, void* msg,
                            uint32_t* status, uint32_t flags, lags_stream_t stream);
 

@@ -318,13 +318,15 @@ def test_fast_path_decode_multi_rank_equals_oracle(L):
             assert _same_bits(rs[p].cpu().numpy(), r_h[p])
 
 
-def test_step_local_equals_compress_plus_decode(L):
-    """P = 1 fused update (lags_bucket_step_local) == compress + decode, over the dense first
-    call, the candidate path and a forced misprediction."""
+@pytest.mark.parametrize("dims,ks", [
+    ([300000, 64, 1000003, 16000, 70001, 9], [300, 64, 1000, 16, 70, 1]),  # fused update; 1000003 -> cluster
+    ([2000000, 300000, 5000], [40000, 12000, 50]),  # > 49152 selected: step_local runs the separate decode
+])
+def test_step_local_equals_compress_plus_decode(L, dims, ks):
+    """P = 1 step (lags_bucket_step_local) == compress + decode, over the dense first call, the
+    candidate path and a forced misprediction."""
     from paper_1911_08727_b200 import _native as N
 
-    dims = [300000, 64, 1000003, 16000, 70001, 9]  # 1000003 / k=1000 -> thread-block-cluster path
-    ks = [300, 64, 1000, 16, 70, 1]
     a, b = L.Bucket(dims, ks, N.F32), L.Bucket(dims, ks, N.F32)
     n = sum(dims)
     gen = torch.Generator(device="cuda").manual_seed(21)
