@@ -904,7 +904,8 @@ __device__ uint32_t compact_staged_v(uint32_t m, const SelectThreshold<uint32_t>
 #pragma unroll
     for (int q = 0; q < V / 4; ++q) {
       int4 ix4 = make_int4(0, 0, 0, 0);
-      if (((gtm | eqm) >> (4 * q)) & 0xfu) ix4 = *reinterpret_cast<const int4*>(si + i0 + 4 * q);
+      if (!si) ix4 = make_int4(i0 + 4 * q, i0 + 4 * q + 1, i0 + 4 * q + 2, i0 + 4 * q + 3);  // a whole layer
+      else if (((gtm | eqm) >> (4 * q)) & 0xfu) ix4 = *reinterpret_cast<const int4*>(si + i0 + 4 * q);
       ixs[4 * q] = ix4.x;
       ixs[4 * q + 1] = ix4.y;
       ixs[4 * q + 2] = ix4.z;
@@ -948,7 +949,8 @@ __device__ uint32_t compact_staged_v(uint32_t m, const SelectThreshold<uint32_t>
 }
 
 // Ordered compaction of candidates staged in shared memory (sv / si: 16-byte aligned planes in
-// index order), 4 (8 for large sets: half the block scans) entries per thread read as 16-byte
+// index order; si == nullptr: sv is a whole layer, the index is the position), 4 (8 for large
+// sets: half the block scans) entries per thread read as 16-byte
 // vectors per plane; vl (nullable): the layer's weights for the fused P = 1 update.  The rule and
 // the result are ordered_compact_pf's: (key & pmask) > prefix, plus the first need_eq equal ones
 // in index order; carry_gt / carry_eq count the lower ranks' entries.  The (index, value) pairs
@@ -1194,6 +1196,63 @@ __device__ LAGS_COLD void dense_fallback_select(int j, const lags_layer_t& L, Fa
   }
 }
 
+// Exact threshold of the k largest keys of a tiny layer staged in shared memory (d <= TINY_LAYER,
+// small k, no prediction wanted): rounds of a block-wide (largest key below the bound, its count)
+// from registers -- one barrier per round, at most k rounds, ~640 cycles each -- instead of three
+// 4096-bin radix passes (a 4096-element layer's radix select took ~9.5 k cycles).  Ties are left to the
+// compaction (the first need_eq equal keys in index order).  All threads.
+constexpr uint32_t SMALL_K_ROUNDS = 16;  // k up to this takes the rounds
+__device__ SelectThreshold<uint32_t> small_k_threshold(const float* sv, uint32_t d, uint32_t k, SelectSmem& cs) {
+  constexpr int NW = SEL_NT / 32, PT = (TINY_LAYER + SEL_NT - 1) / SEL_NT;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t keys[PT];
+#pragma unroll
+  for (int q = 0; q < PT; ++q) {
+    const uint32_t i = threadIdx.x + q * SEL_NT;
+    keys[q] = i < d ? Key<float>::of(sv[i]) : 0u;
+  }
+  uint32_t* red = cs.sm.hist;  // (max, count) per warp, double-buffered by round parity
+  SelectThreshold<uint32_t> th;
+  th.pmask = 0x7fffffffu;
+  uint32_t bound = 0xffffffffu, taken = 0;
+  for (uint32_t round = 0;; ++round) {
+    uint32_t open[PT], mx = 0u, c = 0u;
+#pragma unroll
+    for (int q = 0; q < PT; ++q) {
+      open[q] = keys[q] < bound ? keys[q] : 0u;
+      mx = max(mx, open[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < PT; ++q) c += open[q] == mx ? 1u : 0u;
+    const uint32_t wmx = __reduce_max_sync(0xffffffffu, mx);
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, mx == wmx ? c : 0u);
+    uint32_t* buf = red + (round & 1u) * 2 * NW;
+    if (lane == 0) {
+      buf[warp] = wmx;
+      buf[NW + warp] = wc;
+    }
+    __syncthreads();
+    // the warps' pairs, one per lane
+    const uint32_t v = lane < NW ? buf[lane] : 0u, n = lane < NW ? buf[NW + lane] : 0u;
+    const uint32_t bmx = __reduce_max_sync(0xffffffffu, v);
+    const uint32_t bc = __reduce_add_sync(0xffffffffu, v == bmx ? n : 0u);
+    if (bmx == 0u) {  // fewer than k nonzero keys: every nonzero one (zeros never selected)
+      th.prefix = 0u;
+      th.n_gt = taken;
+      th.need_eq = 0u;
+      return th;
+    }
+    if (taken + bc >= k) {
+      th.prefix = bmx;
+      th.n_gt = taken;
+      th.need_eq = k - taken;
+      return th;
+    }
+    taken += bc;
+    bound = bmx;
+  }
+}
+
 // Dense exact path of a small layer (d <= SMALL_LAYER): staged once in shared memory, so the
 // radix passes and the compaction read shared memory; the same dual-rank select predicts the
 // next candidate threshold (small layers then take the candidate path like the big ones).
@@ -1203,6 +1262,7 @@ __device__ LAGS_COLD void small_fallback_select(int j, const lags_layer_t& L, Fa
   float* data = r + L.offset;
   const int64_t d = L.dim;
   const uint32_t k = static_cast<uint32_t>(L.k);
+  const long long c0 = clock64();
   if ((reinterpret_cast<uintptr_t>(data) & 15u) == 0u) {
     const float4* d4 = reinterpret_cast<const float4*>(data);
     float4* s4 = reinterpret_cast<float4*>(sv);
@@ -1223,21 +1283,23 @@ __device__ LAGS_COLD void small_fallback_select(int j, const lags_layer_t& L, Fa
   auto key_at = [=](int64_t i) { return Key<float>::of(sv[i]); };
   SelectThreshold<uint32_t> th;
   uint32_t key2;
-  radix_select_dual(key_at, d, k, k2, cs, &th, &key2, true);
-  auto load = [=](int64_t i, uint32_t* key, float* x, int64_t* ix) {
-    *x = sv[i];
-    *key = Key<float>::of(*x);
-    *ix = i;
-  };
+  const long long c1 = clock64();
+  if (!predict && d <= TINY_LAYER && k <= SMALL_K_ROUNDS) {
+    th = small_k_threshold(sv, static_cast<uint32_t>(d), k, cs);
+    key2 = 0u;  // no prediction: the layer stays on this path
+  } else {
+    radix_select_dual(key_at, d, k, k2, cs, &th, &key2, true);
+  }
+  const long long c2 = clock64();
   int32_t* oidx = idx_out + L.slot;
   float* oval = val_out + L.slot;
-  auto emit = [=](uint32_t pos, int64_t i, int64_t, float x) {
-    oidx[pos] = static_cast<int32_t>(i);
-    oval[pos] = x;
+  float* vl = vupd ? vupd + L.offset : nullptr;
+  auto emit = [=](int32_t i, float x, float w) {
     data[i] = sent_residual(x);  // acc - acc (R: training.py:252)
+    if (vl) vl[i] = single_rank_update(w, x);
   };
-  const uint32_t cnt = ordered_compact<uint32_t, float>(d, th, load, emit, cs.sm);
-  if (vupd) apply_single_rank_updates(vupd + L.offset, oidx, oval, cnt);
+  // staged compaction over the whole layer (positions are the indices), weights loaded per chunk
+  const uint32_t cnt = compact_staged(static_cast<uint32_t>(d), th, sv, nullptr, vl, emit, cs, 0u, 0u, oidx, oval);
   if (threadIdx.x == 0) {
     count_out[j] = static_cast<int32_t>(cnt);
     FastState ns = st;
@@ -1246,6 +1308,8 @@ __device__ LAGS_COLD void small_fallback_select(int j, const lags_layer_t& L, Fa
     ns.last_cands = 0;
     ns.calls += 1;
     ns.pf256 = pf_encode(pf_next);
+    auto q64 = [](long long c) { return static_cast<uint32_t>(min(c >> 6, 2047ll)); };
+    ns.reserved = q64(c1 - c0) | (q64(c2 - c1) << 11) | (q64(clock64() - c2) << 22);  // load, select, compact
     state[j] = ns;
   }
 }

@@ -388,14 +388,16 @@ def test_slgs_step_golden(L):
 
 
 def test_tiny_layer_warp_path_vs_oracle(L):
-    """Tiny layers (d <= 4096, k <= 8) take one warp each (register top-k) -- checked against the
+    """Tiny layers (d <= 2048, k <= 8) take one warp each (register top-k), larger tiny ones a CTA
+    (rounds of a block max for k <= 16, else radix) -- checked against the
     oracle's top_k on every call: odd sizes (unaligned layer offsets), k from 1 to 8, ties across
     lanes, all-equal layers, zeros, signed zeros, subnormals, a layer with fewer nonzeros than k."""
     from paper_1911_08727_b200 import _native as N
 
     rng = np.random.default_rng(17)
-    dims = [1, 3, 7, 64, 65, 127, 256, 511, 1000, 1023, 2048, 4095, 4096, 33, 97, 600]
-    ks = [1, 1, 3, 8, 5, 2, 4, 8, 1, 7, 2, 8, 4, 8, 6, 3]
+    # the last four: 2048 < d <= 4096 take a whole CTA (k <= 16: rounds of a block max, else radix)
+    dims = [1, 3, 7, 64, 65, 127, 256, 511, 1000, 1023, 2048, 4095, 4096, 33, 97, 600, 3000, 2500, 4096, 3333]
+    ks = [1, 1, 3, 8, 5, 2, 4, 8, 1, 7, 2, 8, 4, 8, 6, 3, 16, 12, 17, 1]
     b = L.Bucket(dims, ks, N.F32)
     n = sum(dims)
     off = np.concatenate([[0], np.cumsum(dims)]).astype(np.int64)
@@ -413,6 +415,9 @@ def test_tiny_layer_warp_path_vs_oracle(L):
             g[off[7]:off[8]] = 0.0
             g[off[12]:off[13]] = np.where(rng.random(dims[12]) < 0.5, -0.0, 0.0)
             g[off[12] + 5] = 2.0  # fewer nonzeros than k there
+            g[off[16]:off[17]] = 0.75  # all-equal again, k = 16 (one round takes every tie)
+            g[off[17]:off[18]] = 0.0
+            g[off[17] + 7] = np.nan if it == 2 else np.inf  # non-finite entries
         if it % 4 == 3:
             g[off[10]:off[11]] = (rng.integers(-40, 41, size=dims[10]) * np.finfo(np.float32).smallest_subnormal)
         acc = (r + np.float32(alpha) * g).astype(np.float32)
@@ -423,9 +428,11 @@ def test_tiny_layer_warp_path_vs_oracle(L):
             np.testing.assert_array_equal(got[j][0], idx, err_msg=f"iteration {it} layer {j}")
             assert _same_bits(got[j][1], val), (it, j)
         r = acc.copy()
-        for j in range(len(dims)):
-            r[off[j] + got[j][0]] = 0.0
-        assert _same_bits(r_d.cpu().numpy(), r), it
+        with np.errstate(invalid="ignore"):
+            for j in range(len(dims)):
+                sel = off[j] + got[j][0]
+                r[sel] = acc[sel] - acc[sel]  # +0.0, NaN for a selected inf (R: training.py:252)
+        assert same_bits_nan(r_d.cpu().numpy(), r), it  # NaN payloads are platform-defined
     s = b.stats()
     assert all(int(s[j, 5]) == 0 for j in range(len(dims)))  # every layer on the warp / dense-small path
 
