@@ -111,13 +111,20 @@ __device__ __forceinline__ unsigned long long lower_threshold64(unsigned long lo
 // Ordered compaction of candidates staged in sv (doubles) / si (indices, 16-byte aligned; both
 // in index order, readable 3 entries past m): 4 entries per thread per block scan, read as
 // 16-byte vectors.  The rule is ordered_compact's: (key & pmask) > prefix, plus the first need_eq
-// equal ones in index order.  emit(pos, ix, x).  Returns the selected count (all threads).
+// equal ones in index order.  The (index, value) pairs leave through shared memory as coalesced
+// runs into oidx / oval; emit(ix, x) does the scattered residual write.  Returns the selected
+// count (all threads).
 template <typename Emit>
 __device__ uint32_t compact64_staged(uint32_t m, const SelectThreshold<unsigned long long>& th, const double* sv,
-                                     const int32_t* si, Emit emit, RadixSmem<Key<double>::RB>& sm) {
+                                     const int32_t* si, Emit emit, RadixSmem<Key<double>::RB>& sm, int32_t* oidx,
+                                     double* oval) {
   constexpr int V = 4;
+  static_assert(3 * SEL_NT * V <= RadixSmem<Key<double>::RB>::NB, "a chunk's output fits the staging arrays");
+  int32_t* st_idx = reinterpret_cast<int32_t*>(sm.hist);  // free here: the threshold is known
+  double* st_val = reinterpret_cast<double*>(sm.hist + SEL_NT * V);
   uint32_t carry_gt = 0, carry_eq = 0;
   for (uint32_t base = 0; base < m; base += SEL_NT * V) {
+    const uint32_t out0 = carry_gt + min(carry_eq, th.need_eq);  // the chunk's first output slot
     const uint32_t i0 = base + threadIdx.x * V;
     double xs[V];
 #pragma unroll
@@ -149,15 +156,26 @@ __device__ uint32_t compact64_staged(uint32_t m, const SelectThreshold<unsigned 
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const bool g = (gtm >> v) & 1u, e = (eqm >> v) & 1u;
-        if (g || (e && eq_before < th.need_eq)) emit(gt_before + min(eq_before, th.need_eq), ixs[v], xs[v]);
+        if (g || (e && eq_before < th.need_eq)) {
+          const uint32_t q = gt_before + min(eq_before, th.need_eq) - out0;
+          st_idx[q] = ixs[v];
+          st_val[q] = xs[v];
+          emit(ixs[v], xs[v]);
+        }
         gt_before += g;
         eq_before += e;
       }
     }
     carry_gt += tot & 0xffffu;
     carry_eq += tot >> 16;
-    __syncthreads();  // warp_tot reuse by the next scan
+    __syncthreads();  // the staged pairs are complete (and warp_tot is free for the next scan)
+    const uint32_t n_out = carry_gt + min(carry_eq, th.need_eq) - out0;
+    for (uint32_t q = threadIdx.x; q < n_out; q += SEL_NT) {
+      oidx[out0 + q] = st_idx[q];
+      oval[out0 + q] = st_val[q];
+    }
   }
+  __syncthreads();  // the staging arrays are read before any reuse
   return carry_gt + min(carry_eq, th.need_eq);
 }
 
@@ -200,11 +218,28 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
   int32_t* oidx = idx_out + L.slot;
   double* oval = val_out + L.slot;
   const float pf = st.pf256 ? st.pf256 / 256.0f : static_cast<float>(PRED_FACTOR);
-  uint32_t local = 0, over = 0;
+  constexpr int NW = SEL_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // speculative: entry `lane` of the warp's first GATHER_TASKS tasks, in flight with the counts
+  // (reading past a short list stays inside its cap slots)
+  double pre_v[GATHER_TASKS];
+  int32_t pre_i[GATHER_TASKS];
+  const bool spec = st.thr != 0ull && L.dim > TINY_LAYER && !force_exact;
+#pragma unroll
+  for (int u = 0; u < GATHER_TASKS; ++u) {
+    const int tt = warp + u * NW;
+    if (spec && tt < min(SEL_NT, tr.y - tr.x)) {
+      const int64_t src = static_cast<int64_t>(tr.x + tt) * cap + lane;
+      pre_v[u] = __ldcg(cand_val + src);
+      pre_i[u] = __ldcg(cand_idx + src);
+    }
+  }
+  uint32_t local = 0, over = 0, c_first = 0;  // c_first: this thread's task count in the first chunk
   for (int t = tr.x + threadIdx.x; t < tr.y; t += SEL_NT) {
     const uint32_t c = static_cast<uint32_t>(__ldcg(cand_cnt + t));
     over |= c > static_cast<uint32_t>(cap) ? 1u : 0u;
     local += min(c, static_cast<uint32_t>(cap));
+    if (t == tr.x + static_cast<int>(threadIdx.x)) c_first = min(c, static_cast<uint32_t>(cap));
   }
   const uint32_t m = block_sum(local, sm);
   LAGS_S64(1, clock64());
@@ -229,14 +264,13 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
       // gather: positions by a block scan over the task counts; one warp per task, lane = entry
       // (a task holds ~17 candidates of a 2.4 M-element layer at the margin), GATHER_TASKS tasks'
       // loads in flight per warp, entries past the first 32 in a loop; index order kept
-      constexpr int NW = SEL_NT / 32;
-      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       uint32_t carry = 0;
       for (int t0 = tr.x; t0 < tr.y; t0 += SEL_NT) {
         const int nt = min(SEL_NT, tr.y - t0);
-        const uint32_t c = threadIdx.x < nt ? min(static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)),
-                                                  static_cast<uint32_t>(cap))
-                                            : 0u;
+        const uint32_t c = threadIdx.x >= nt ? 0u
+                           : t0 == tr.x  ? c_first
+                                         : min(static_cast<uint32_t>(__ldcg(cand_cnt + t0 + threadIdx.x)),
+                                               static_cast<uint32_t>(cap));
         uint32_t tot;
         tpos[threadIdx.x] = carry + block_exclusive_scan<SEL_NT>(c, sm.warp_tot, &tot);
         tcnt[threadIdx.x] = c;
@@ -245,15 +279,21 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
           uint32_t cc[GATHER_TASKS], pp[GATHER_TASKS];
           double xv[GATHER_TASKS];
           int32_t xi[GATHER_TASKS];
+          const bool first = t0 == tr.x && tb == warp;  // the speculative loads
 #pragma unroll
           for (int u = 0; u < GATHER_TASKS; ++u) {
             const int tt = tb + u * NW;
             cc[u] = tt < nt ? tcnt[tt] : 0u;
             pp[u] = tt < nt ? tpos[tt] : 0u;
             if (static_cast<uint32_t>(lane) < cc[u]) {
-              const int64_t src = static_cast<int64_t>(t0 + tt) * cap + lane;
-              xv[u] = __ldcg(cand_val + src);
-              xi[u] = __ldcg(cand_idx + src);
+              if (first) {
+                xv[u] = pre_v[u];
+                xi[u] = pre_i[u];
+              } else {
+                const int64_t src = static_cast<int64_t>(t0 + tt) * cap + lane;
+                xv[u] = __ldcg(cand_val + src);
+                xi[u] = __ldcg(cand_idx + src);
+              }
             }
           }
 #pragma unroll
@@ -278,13 +318,11 @@ __global__ void __launch_bounds__(SEL_NT) select64_kernel(const lags_layer_t* __
       auto key_at = [=](int64_t i) { return Key<double>::of(sv[i]); };
       const SelectThreshold<K> th = radix_select<K, Key<double>::BITS, RB>(key_at, m, k, sm, min(k2, m), &key2, true);
       LAGS_S64(3, clock64());
-      auto emit = [=](uint32_t pos, int32_t ix, double x) {
-        oidx[pos] = static_cast<int32_t>(ix);
-        oval[pos] = x;
+      auto emit = [=](int32_t ix, double x) {
         if (r32) r32[L.offset + ix] = static_cast<float>(sent_residual(x));  // fl32(acc - acc)
         else data[ix] = sent_residual(x);  // acc - acc (R: training.py:252)
       };
-      cnt = compact64_staged(m, th, sv, si, emit, sm);
+      cnt = compact64_staged(m, th, sv, si, emit, sm, oidx, oval);
       LAGS_S64(4, clock64());
     }
     ns.thr = m >= k2 ? max(key2, 1ull) : lower_threshold64(st.thr, m, k2);
