@@ -261,7 +261,10 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
 }
 
 // K1: one warp per task.  gtab (nullable): per-layer gradient pointers replacing the flat g.
-template <bool ZERO_G, bool RSTREAM>
+// UNROLL: float4 loads in flight per lane and operand -- K1_UNROLL (80 registers, 24 warps per SM)
+// or 2 * K1_UNROLL (116 registers, 16 warps per SM); the bucket picks the one whose resident-warp
+// waves are fuller (lags_bucket_create).
+template <bool ZERO_G, bool RSTREAM, int UNROLL = K1_UNROLL>
 __global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
     const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
     const FastState* __restrict__ state, float* __restrict__ g, float* const* __restrict__ gtab,
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MINB) accum_emit_kernel(
   if (wid >= ntasks) return;
   const Task T = tasks[wid];
   float* gt = gtab ? gtab[T.layer] + (T.start - layers[T.layer].offset) : g + T.start;
-  stream_task<ZERO_G, RSTREAM, K1_UNROLL>(T, wid, lane, layers, state, gt, r + T.start, alpha, cap, cand_idx, cand_val,
+  stream_task<ZERO_G, RSTREAM, UNROLL>(T, wid, lane, layers, state, gt, r + T.start, alpha, cap, cand_idx, cand_val,
                                  cand_cnt, status, hist);
 }
 

@@ -497,6 +497,7 @@ struct lags_bucket {
   uint32_t* hist = nullptr;       // fp32: per-layer candidate-key histograms (K1 -> select_kernel)
   uint32_t* touched = nullptr;    // decode with momentum: one bit per element sent by any rank
   bool r_stream = true;           // K1 streams r with evict-first priority (r larger than half the L2)
+  bool k1_wide = false;           // K1 with 2 * K1_UNROLL loads in flight (fuller waves for this bucket)
   // selection groups of an fp32 bucket (plan_groups): 0 persistent role, 1 cluster role, 2 warp
   // role; each group's tasks and `order` entries are contiguous
   struct Group {
@@ -840,6 +841,22 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     b->r_stream = static_cast<int64_t>(p.n_total) * 4 > static_cast<int64_t>(l2 > 0 ? l2 : (126 << 20)) / 2;
+    // K1 runs one warp per task in waves of the resident warps; a partial last wave streams at a
+    // fraction of the bandwidth.  Take the wider unroll when its waves are fuller (measured:
+    // ResNet-50's 3120 tasks fit one 80-register wave, 68.8 vs 79.1 us; VGG-16's 1800 tasks and
+    // LSTM's 8060 fill the 116-register waves better, 48.9 -> 45.7 and 187.8 -> 182.9 us).
+    {
+      int occ_n = 0, occ_w = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_n, accum_emit_kernel<false, true>, K1_WARPS * 32, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_w, accum_emit_kernel<false, true, 2 * K1_UNROLL>,
+                                                    K1_WARPS * 32, 0);
+      auto fill = [&](int occ) {
+        const int64_t slots = static_cast<int64_t>(std::max(occ, 1)) * K1_WARPS * num_sms();
+        const int64_t waves = (p.ntasks + slots - 1) / slots;
+        return static_cast<double>(p.ntasks) / static_cast<double>(waves * slots);
+      };
+      b->k1_wide = occ_w > 0 && fill(occ_w) > fill(occ_n) + 0.05;
+    }
     const int smem = select_smem_words_max() * static_cast<int>(sizeof(uint32_t));
     if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
         cudaFuncSetAttribute(select_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess) {
@@ -926,8 +943,13 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     cudaError_t e = cudaSuccess;
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
     if (e == cudaSuccess) {
-      auto kern = zg ? (b->r_stream ? accum_emit_kernel<true, true> : accum_emit_kernel<true, false>)
-                     : (b->r_stream ? accum_emit_kernel<false, true> : accum_emit_kernel<false, false>);
+      auto kern = b->k1_wide
+                      ? (zg ? (b->r_stream ? accum_emit_kernel<true, true, 2 * K1_UNROLL>
+                                           : accum_emit_kernel<true, false, 2 * K1_UNROLL>)
+                            : (b->r_stream ? accum_emit_kernel<false, true, 2 * K1_UNROLL>
+                                           : accum_emit_kernel<false, false, 2 * K1_UNROLL>))
+                      : (zg ? (b->r_stream ? accum_emit_kernel<true, true> : accum_emit_kernel<true, false>)
+                            : (b->r_stream ? accum_emit_kernel<false, true> : accum_emit_kernel<false, false>));
       e = launch_pdl(kern, dim3(blocks), dim3(K1_WARPS * 32), 0, s, b->tasks, ntasks, b->layers, b->state, gg,
                      b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status, b->sel_ctr.work,
                      b->hist);
