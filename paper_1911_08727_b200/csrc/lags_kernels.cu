@@ -535,6 +535,23 @@ int cuda_check(const char* where, int launches = 1) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+int num_sms();
+// Resident warps of K1 (the narrow unroll) over the whole device: one wave of tasks.
+int64_t k1_resident_warps() {
+  static int64_t w = 0;
+  if (w == 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, accum_emit_kernel<false, true>, K1_WARPS * 32, 0) !=
+            cudaSuccess ||
+        occ <= 0) {
+      cudaGetLastError();
+      occ = 3;  // 80 registers, 8-warp CTAs
+    }
+    w = static_cast<int64_t>(occ) * K1_WARPS * num_sms();
+  }
+  return w;
+}
+
 int num_sms() {
   static int sms = 0;
   if (sms == 0) {
@@ -593,6 +610,21 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   for (int j = 0; j < L; ++j) n_all += std::max<int64_t>(dims[j], 0);
   int task = TASK_ELEMS;
   while (task > MIN_TASK_ELEMS && n_all / task < static_cast<int64_t>(num_sms()) * K1_WARPS) task >>= 1;
+#ifndef LAGS_NO_WAVE_FIT
+  // a bucket that fits one wave of resident K1 warps: the smallest task (multiple of 256 elements)
+  // that still fits, so every warp streams about the same bytes and the wave is full (ResNet-50:
+  // 3120 tasks of 8192 for 3552 warp slots -> 7168-element tasks)
+  if (task == TASK_ELEMS) {
+    auto ntasks_for = [&](int t) {
+      int64_t c = 0;
+      for (int j = 0; j < L; ++j) c += (std::max<int64_t>(dims[j], 1) + t - 1) / t;
+      return c;
+    };
+    const int64_t slots = k1_resident_warps();
+    if (ntasks_for(task) <= slots)
+      while (task - 256 >= MIN_TASK_ELEMS && ntasks_for(task - 256) <= slots) task -= 256;
+  }
+#endif
   p->task_elems = task;
   double max_per_task = 0.0;  // expected selected entries in one task of a layer
   for (int j = 0; j < L; ++j) {
