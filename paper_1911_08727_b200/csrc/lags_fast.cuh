@@ -260,6 +260,154 @@ __device__ __forceinline__ void stream_task(const Task& T, int tid, int lane, co
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
 }
 
+// K1, CTA form (large buckets): one CTA of K1C_NT threads per task of K1C_TASK elements, every
+// thread's loads issued at once (no loop), so the hardware schedules thousands of short CTAs and
+// the kernel ends within one CTA's lifetime of the last byte (a warp looping over a long task
+// left a tail: 55 vs 47 us for the same 12 B/element in torch's elementwise kernel).  Thread t
+// owns the float4 groups f = q * K1C_NT + t (q < 4): each load instruction of a warp reads 512
+// contiguous bytes.  The task's candidates keep ascending index order = (q, t) order: one block
+// scan of the four per-group counts packed into 16-bit fields.
+constexpr int K1C_NT = 256;
+constexpr int K1C_GROUPS = 4;
+constexpr int K1C_TASK = K1C_NT * K1C_GROUPS * 4;  // 4096 elements
+
+// Exclusive block scan of a packed 64-bit value (fields never carry: <= 4 * K1C_NT per field).
+__device__ __forceinline__ unsigned long long k1c_scan(unsigned long long v, unsigned long long* wsum,
+                                                       unsigned long long* total) {
+  constexpr int NW = K1C_NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long w = lane < NW ? wsum[lane] : 0ull;
+    unsigned long long wi = w;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < NW) wsum[lane] = wi - w;
+    if (lane == NW - 1) wsum[NW] = wi;
+  }
+  __syncthreads();
+  *total = wsum[NW];
+  return wsum[warp] + x - v;
+}
+
+template <bool ZERO_G, bool RSTREAM>
+__global__ void __launch_bounds__(K1C_NT) accum_emit_cta_kernel(
+    const Task* __restrict__ tasks, int ntasks, const lags_layer_t* __restrict__ layers,
+    const FastState* __restrict__ state, float* __restrict__ g, float* const* __restrict__ gtab,
+    float* __restrict__ r, float alpha, int cap, int32_t* __restrict__ cand_idx, float* __restrict__ cand_val,
+    int32_t* __restrict__ cand_cnt, uint32_t* status, uint32_t* work, uint32_t* hist) {
+  __shared__ unsigned long long wsum[K1C_NT / 32 + 1];
+  griddep_wait();  // the previous kernel on the stream (last call's select / decode) has completed
+#ifndef LAGS_NO_EARLY_TRIGGER
+  griddep_launch_dependents();
+#endif
+  const int tid = blockIdx.x;
+  const int t = threadIdx.x;
+  if (tid == 0 && t == 0) *work = 0u;  // the previous call's selection kernel has completed
+  const Task T = tasks[tid];
+  const lags_layer_t Lr = layers[T.layer];
+  const int64_t local0 = T.start - Lr.offset;
+  float* gt = gtab ? gtab[T.layer] + local0 : g + T.start;
+  float* rt = r + T.start;
+  const uint32_t thr0 = state[T.layer].thr;
+  const uint32_t thr = thr0 ? thr0 : 0xffffffffu;
+  uint32_t* hl = hist ? hist + static_cast<int64_t>(T.layer) * HIST_BINS : nullptr;
+  const uint32_t hbase = thr0 >> HIST_SHIFT;
+  const int n = T.len;
+  const bool vec = ((reinterpret_cast<uintptr_t>(rt) | reinterpret_cast<uintptr_t>(gt)) & 15u) == 0;
+  float4 gv[K1C_GROUPS], rv[K1C_GROUPS];
+#pragma unroll
+  for (int q = 0; q < K1C_GROUPS; ++q) {
+    const int e = 4 * (q * K1C_NT + t);
+    gv[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    rv[q] = gv[q];
+    if (vec && e + 3 < n) {
+      gv[q] = __ldcs(reinterpret_cast<const float4*>(gt + e));
+      rv[q] = r_load<RSTREAM>(reinterpret_cast<const float4*>(rt + e));
+    } else if (e < n) {  // unaligned task or the layer's last partial group
+      float* gp = &gv[q].x;
+      float* rp = &rv[q].x;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (e + c < n) {
+          gp[c] = gt[e + c];
+          rp[c] = rt[e + c];
+        }
+    }
+  }
+  bool bad = false;
+  uint32_t masks = 0;  // 4 bits per group
+  unsigned long long packed = 0ull;
+  float4 av[K1C_GROUPS];
+#pragma unroll
+  for (int q = 0; q < K1C_GROUPS; ++q) {
+    const int e = 4 * (q * K1C_NT + t);
+    float4 a;
+    a.x = accum(rv[q].x, gv[q].x, alpha);
+    a.y = accum(rv[q].y, gv[q].y, alpha);
+    a.z = accum(rv[q].z, gv[q].z, alpha);
+    a.w = accum(rv[q].w, gv[q].w, alpha);
+    av[q] = a;
+    if (vec && e + 3 < n) {
+      bad |= nonfinite(gv[q].x) | nonfinite(gv[q].y) | nonfinite(gv[q].z) | nonfinite(gv[q].w);
+      if (ZERO_G) __stcs(reinterpret_cast<float4*>(gt + e), make_float4(0.f, 0.f, 0.f, 0.f));
+      r_store<RSTREAM>(reinterpret_cast<float4*>(rt + e), a);
+      const uint32_t m = (Key<float>::of(a.x) >= thr ? 1u : 0u) | (Key<float>::of(a.y) >= thr ? 2u : 0u) |
+                         (Key<float>::of(a.z) >= thr ? 4u : 0u) | (Key<float>::of(a.w) >= thr ? 8u : 0u);
+      masks |= m << (4 * q);
+      packed |= static_cast<unsigned long long>(__popc(m)) << (16 * q);
+    } else if (e < n) {
+      const float* ap = &a.x;
+      const float* gp = &gv[q].x;
+      uint32_t m = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (e + c < n) {
+          bad |= nonfinite(gp[c]);
+          if (ZERO_G) gt[e + c] = 0.0f;
+          rt[e + c] = ap[c];
+          m |= (Key<float>::of(ap[c]) >= thr ? 1u : 0u) << c;
+        }
+      masks |= m << (4 * q);
+      packed |= static_cast<unsigned long long>(__popc(m)) << (16 * q);
+    }
+  }
+  unsigned long long tot;
+  const unsigned long long ex = k1c_scan(packed, wsum, &tot);
+  int32_t* cidx = cand_idx + static_cast<int64_t>(tid) * cap;
+  float* cval = cand_val + static_cast<int64_t>(tid) * cap;
+  uint32_t before = 0;  // candidates of the lower groups (all threads)
+#pragma unroll
+  for (int q = 0; q < K1C_GROUPS; ++q) {
+    uint32_t pos = before + static_cast<uint32_t>((ex >> (16 * q)) & 0xffffu);
+    uint32_t m = (masks >> (4 * q)) & 0xfu;
+    while (m) {
+      const int c = __ffs(m) - 1;
+      const float x = c == 0 ? av[q].x : c == 1 ? av[q].y : c == 2 ? av[q].z : av[q].w;
+      if (pos < static_cast<uint32_t>(cap)) {
+        cidx[pos] = static_cast<int32_t>(local0 + 4 * (q * K1C_NT + t) + c);
+        cval[pos] = x;
+      }
+      if (hl) atomicAdd(hl + hist_bin(Key<float>::of(x), hbase), 1u);
+      ++pos;
+      m &= m - 1;
+    }
+    before += static_cast<uint32_t>((tot >> (16 * q)) & 0xffffu);
+  }
+  if (t == 0) cand_cnt[tid] = static_cast<int32_t>(before);
+  if (__syncthreads_or(bad) && t == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
+}
+
 // K1: one warp per task.  gtab (nullable): per-layer gradient pointers replacing the flat g.
 // UNROLL: float4 loads in flight per lane and operand -- K1_UNROLL (80 registers, 24 warps per SM)
 // or 2 * K1_UNROLL (116 registers, 16 warps per SM); the bucket picks the one whose resident-warp

@@ -498,6 +498,7 @@ struct lags_bucket {
   uint32_t* touched = nullptr;    // decode with momentum: one bit per element sent by any rank
   bool r_stream = true;           // K1 streams r with evict-first priority (r larger than half the L2)
   bool k1_wide = false;           // K1 with 2 * K1_UNROLL loads in flight (fuller waves for this bucket)
+  bool k1_cta = false;            // K1 in its CTA form (Plan::k1_cta)
   // selection groups of an fp32 bucket (plan_groups): 0 persistent role, 1 cluster role, 2 warp
   // role; each group's tasks and `order` entries are contiguous
   struct Group {
@@ -594,6 +595,7 @@ int select_smem_words_max() {
 struct Plan {
   int64_t n_total = 0, total_k = 0;
   int32_t ntasks = 0, cap = 0, task_elems = TASK_ELEMS;
+  bool k1_cta = false;  // K1 in its CTA form (accum_emit_cta_kernel, K1C_TASK-element tasks)
   size_t o_layers = 0, o_ltasks = 0, o_state = 0, o_tasks = 0, o_slot = 0, o_ccnt = 0, o_cidx = 0, o_cval = 0,
          o_gidx = 0, o_gval = 0, o_acc = 0, o_mask = 0, o_planes = 0, o_order = 0, o_ctr = 0, o_delta = 0, o_tiles = 0,
          o_hist = 0, o_touched = 0, o_state64 = 0, o_dtiles = 0, bytes = 0;
@@ -610,11 +612,18 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   for (int j = 0; j < L; ++j) n_all += std::max<int64_t>(dims[j], 0);
   int task = TASK_ELEMS;
   while (task > MIN_TASK_ELEMS && n_all / task < static_cast<int64_t>(num_sms()) * K1_WARPS) task >>= 1;
+#ifndef LAGS_NO_K1_CTA
+  // large fp32 buckets: K1's CTA form, one short CTA per K1C_TASK-element task
+  if (dtype == LAGS_F32 && task == TASK_ELEMS) {
+    task = K1C_TASK;
+    p->k1_cta = true;
+  }
+#endif
 #ifndef LAGS_NO_WAVE_FIT
   // a bucket that fits one wave of resident K1 warps: the smallest task (multiple of 256 elements)
   // that still fits, so every warp streams about the same bytes and the wave is full (ResNet-50:
   // 3120 tasks of 8192 for 3552 warp slots -> 7168-element tasks)
-  if (task == TASK_ELEMS) {
+  if (task == TASK_ELEMS && !p->k1_cta) {
     auto ntasks_for = [&](int t) {
       int64_t c = 0;
       for (int j = 0; j < L; ++j) c += (std::max<int64_t>(dims[j], 1) + t - 1) / t;
@@ -872,7 +881,12 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
     int dev = 0, l2 = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+#ifdef LAGS_NO_RSTREAM
+    b->r_stream = false;
+#else
     b->r_stream = static_cast<int64_t>(p.n_total) * 4 > static_cast<int64_t>(l2 > 0 ? l2 : (126 << 20)) / 2;
+#endif
+    b->k1_cta = p.k1_cta;
     // K1 runs one warp per task in waves of the resident warps; a partial last wave streams at a
     // fraction of the bandwidth.  Take the wider unroll when its waves are fuller (measured:
     // ResNet-50's 3120 tasks fit one 80-register wave, 68.8 vs 79.1 us; VGG-16's 1800 tasks and
@@ -974,7 +988,13 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
     const int blocks = (ntasks + K1_WARPS - 1) / K1_WARPS;
     cudaError_t e = cudaSuccess;
     if (b->probe_before) e = cudaEventRecord(b->probe_before, s);
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && b->k1_cta) {
+      auto kern = zg ? (b->r_stream ? accum_emit_cta_kernel<true, true> : accum_emit_cta_kernel<true, false>)
+                     : (b->r_stream ? accum_emit_cta_kernel<false, true> : accum_emit_cta_kernel<false, false>);
+      e = launch_pdl(kern, dim3(ntasks), dim3(K1C_NT), 0, s, b->tasks, ntasks, b->layers, b->state, gg,
+                     b->grad_table, rr, a, b->cap, b->cand_idx, b->cand_val, b->cand_cnt, status, b->sel_ctr.work,
+                     b->hist);
+    } else if (e == cudaSuccess) {
       auto kern = b->k1_wide
                       ? (zg ? (b->r_stream ? accum_emit_kernel<true, true, 2 * K1_UNROLL>
                                            : accum_emit_kernel<true, false, 2 * K1_UNROLL>)
