@@ -179,8 +179,10 @@ class LagsSGD(torch.optim.Optimizer):
         self.bucket_cap_bytes = int(bucket_cap_bytes)
         self.flat_param = self.flat_grad = self.residual = self.momentum_buf = None
         self.offsets = None
-        self.side = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None  # compress
-        self.comm = torch.cuda.Stream(self.device) if self.device.type == "cuda" else None  # exchange + decode
+        # high priority: a released bucket's compress (many short K1 CTAs) is scheduled ahead of the
+        # remaining backprop kernels instead of interleaving with them for milliseconds
+        self.side = (torch.cuda.Stream(self.device, priority=-1) if self.device.type == "cuda" else None)  # compress
+        self.comm = (torch.cuda.Stream(self.device, priority=-1) if self.device.type == "cuda" else None)  # exchange + decode
         self.buckets = []
         self._relayout(plan_buckets(self.dims, self.ks, self.bucket_cap_bytes))
         if self.world > 1:  # identical starting point on every rank (no DDP: it would double-communicate)
