@@ -65,7 +65,7 @@ def read_k1_traffic():
     import csv
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, TRAFFIC_GLOB)), key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(ROOT, TRAFFIC_GLOB)))  # round-tagged names sort in capture order
     if not files:
         return None, None
     per = {}
@@ -615,7 +615,7 @@ def run_ours(args, dims, ks, world, rank, local):
             "iter_per_s": round(args.steps / (ms / 1e3), 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (torch.randn gradients, seed 1234+rank)",
             "config": config_dict(dims, ks, world),
-            "roofline": {"kernel": "K1 accum_emit_kernel (dominant: acc = r + a*g, r <- acc, candidate emission)",
+            "roofline": {"kernel": "K1 accum_emit_cta_kernel (dominant: acc = r + a*g, r <- acc, candidate emission)",
                          "bound": "hbm", "achieved": round(12 * n / (k1_ms / 1e3) / 1e9, 2), "peak": peak,
                          "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(12 * n / (k1_ms / 1e3) / 1e9 / peak, 4), "traffic": k1_traffic,
