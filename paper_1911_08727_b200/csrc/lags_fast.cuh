@@ -314,15 +314,16 @@ __global__ void __launch_bounds__(K1C_NT) accum_emit_cta_kernel(
   const int tid = blockIdx.x;
   const int t = threadIdx.x;
   if (tid == 0 && t == 0) *work = 0u;  // the previous call's selection kernel has completed
+  // the task descriptor is the only load the streaming loads depend on (flat g): the layer
+  // offset and the threshold are read while they are in flight
   const Task T = tasks[tid];
-  const lags_layer_t Lr = layers[T.layer];
-  const int64_t local0 = T.start - Lr.offset;
-  float* gt = gtab ? gtab[T.layer] + local0 : g + T.start;
   float* rt = r + T.start;
-  const uint32_t thr0 = state[T.layer].thr;
-  const uint32_t thr = thr0 ? thr0 : 0xffffffffu;
-  uint32_t* hl = hist ? hist + static_cast<int64_t>(T.layer) * HIST_BINS : nullptr;
-  const uint32_t hbase = thr0 >> HIST_SHIFT;
+  int64_t local0 = 0;
+  float* gt = g + T.start;
+  if (gtab) {
+    local0 = T.start - layers[T.layer].offset;
+    gt = gtab[T.layer] + local0;
+  }
   const int n = T.len;
   const bool vec = ((reinterpret_cast<uintptr_t>(rt) | reinterpret_cast<uintptr_t>(gt)) & 15u) == 0;
   float4 gv[K1C_GROUPS], rv[K1C_GROUPS];
@@ -345,6 +346,11 @@ __global__ void __launch_bounds__(K1C_NT) accum_emit_cta_kernel(
         }
     }
   }
+  if (!gtab) local0 = T.start - layers[T.layer].offset;
+  const uint32_t thr0 = state[T.layer].thr;
+  const uint32_t thr = thr0 ? thr0 : 0xffffffffu;
+  uint32_t* hl = hist ? hist + static_cast<int64_t>(T.layer) * HIST_BINS : nullptr;
+  const uint32_t hbase = thr0 >> HIST_SHIFT;
   bool bad = false;
   uint32_t masks = 0;  // 4 bits per group
   unsigned long long packed = 0ull;
