@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(K1C_NT) accum_emit_cta_kernel(
     before += static_cast<uint32_t>((tot >> (16 * q)) & 0xffffu);
   }
   if (t == 0) cand_cnt[tid] = static_cast<int32_t>(before);
-  if (__syncthreads_or(bad) && t == 0) atomicOr(status, LAGS_STATUS_NONFINITE);
+  if (__any_sync(0xffffffffu, bad) && (t & 31) == 0) atomicOr(status, LAGS_STATUS_NONFINITE);  // no barrier
 }
 
 // K1: one warp per task.  gtab (nullable): per-layer gradient pointers replacing the flat g.
