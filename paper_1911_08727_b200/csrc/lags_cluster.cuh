@@ -212,7 +212,9 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   // CTA its own copy) and ALL of the layer's task counts (one load per thread for layers up to
   // SEL_NT tasks), from which every CTA derives m, the ranks' sums and its own offset
   const int nt_own = t_hi - t_lo;
-  const bool spec = T <= SEL_NT;  // counts cached in shared memory, candidates loaded speculatively
+  // counts cached in shared memory, candidates loaded speculatively (a 2.36 M-element layer has
+  // 576 tasks of K1's CTA form)
+  const bool spec = T <= 2 * SEL_NT && nt_own <= SEL_NT;
   SpecGather g;
   if (spec) spec_load(g, t_lo, nt_own, cand_idx, cand_val, cap);
   HistRegs hr;

@@ -454,7 +454,8 @@ struct SelectSmem {
   alignas(16) uint32_t hist2[F32_BINS];  // second histogram (prediction rank) of the cooperative dense path
   uint32_t tpos[SEL_NT];     // candidate gather: per-task output position / count
   uint32_t tcnt[SEL_NT];
-  uint32_t tcache[SEL_NT];   // the layer's task counts from the counting pass (layers of <= SEL_NT tasks)
+  uint32_t tcache[2 * SEL_NT];  // the layer's task counts from the counting pass (speculative gathers:
+                                // <= SEL_NT tasks per CTA, <= 2 * SEL_NT per cluster layer)
   uint32_t rpos[SEL_NT];     // speculative gather: positions of the tasks' remainders
 };
 
@@ -916,6 +917,27 @@ __device__ uint32_t gather_candidates(int t_lo, int t_hi, const int32_t* __restr
 // classifies them against the histogram cut and prefetches the possibly selected entries' weights
 // (P = 1 update) into L2 for the compaction.  Leftovers (tasks beyond NW * GATHER_TASKS, lists
 // longer than 32) follow with one thread per entry.  nt <= SEL_NT.
+#ifndef LAGS_SPEC_LANES
+#define LAGS_SPEC_LANES 16
+#endif
+#ifndef LAGS_NO_WPREFETCH
+#define LAGS_NO_WPREFETCH 0
+#endif
+// lanes per task in the speculative loads (SPEC_TPW tasks per warp load instruction): a
+// 4096-element task of K1's CTA form holds ~8 candidates at the margin
+constexpr int SPEC_LANES = LAGS_SPEC_LANES;
+constexpr int SPEC_TPW = 32 / SPEC_LANES;
+#ifdef LAGS_DBG_STAMPS
+__device__ unsigned long long lags_dbg_sp[8];  // spec_place phases of block 0 (diagnostic builds)
+#define LAGS_SPSTAMP(i)                                                          \
+  do {                                                                           \
+    if (blockIdx.x == 0 && threadIdx.x == 0) lags_dbg_sp[i] = clock64();         \
+  } while (0)
+#else
+#define LAGS_SPSTAMP(i) \
+  do {                  \
+  } while (0)
+#endif
 struct SpecGather {
   float xv[GATHER_TASKS];
   int32_t xi[GATHER_TASKS];
@@ -927,11 +949,17 @@ __device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int u = 0; u < GATHER_TASKS; ++u) {
-    const int tt = warp + NW * u;
+    const int tt = (warp + NW * u) * SPEC_TPW + lane / SPEC_LANES;
     if (tt < nt) {
-      const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + lane;
+      const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + lane % SPEC_LANES;
+#ifdef LAGS_SPEC_ASM
+      // issued here (volatile): the compiler may not sink them to their first use
+      asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(g.xv[u]) : "l"(cand_val + src));
+      asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(g.xi[u]) : "l"(cand_idx + src));
+#else
       g.xv[u] = __ldcg(cand_val + src);
       g.xi[u] = __ldcg(cand_idx + src);
+#endif
     }
   }
 }
@@ -944,12 +972,14 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
                                uint32_t* gtb, uint32_t* list, uint32_t* list_n) {
   constexpr int NW = SEL_NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  LAGS_SPSTAMP(0);
   const uint32_t c = threadIdx.x < nt ? min(tc[threadIdx.x], static_cast<uint32_t>(cap)) : 0u;
   uint32_t tot;
   const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
   cs.tpos[threadIdx.x] = pos;
   cs.tcnt[threadIdx.x] = c;
   __syncthreads();
+  LAGS_SPSTAMP(1);
   uint32_t my_gt = 0, dx = 0;
   // returns whether the entry may be selected (its weight is wanted)
   auto take = [&](float x, int32_t ix, uint32_t e) -> bool {
@@ -971,19 +1001,38 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
   };
 #pragma unroll
   for (int u = 0; u < GATHER_TASKS; ++u) {
-    const int tt = warp + NW * u;
-    if (tt < nt && static_cast<uint32_t>(lane) < cs.tcnt[tt]) {
-      if (take(g.xv[u], g.xi[u], cs.tpos[tt] + lane) && vl)
+    const int tt = (warp + NW * u) * SPEC_TPW + lane / SPEC_LANES;
+    const uint32_t en = static_cast<uint32_t>(lane % SPEC_LANES);
+    if (tt < nt && en < cs.tcnt[tt]) {
+      if (take(g.xv[u], g.xi[u], cs.tpos[tt] + en) && vl && !LAGS_NO_WPREFETCH)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + g.xi[u]));  // P = 1 weight
+    }
+  }
+  LAGS_SPSTAMP(2);
+  // a covered task a little longer than SPEC_LANES: its lanes take the rest directly (one more
+  // load each), so a few such tasks do not cost a block-wide leftover pass
+#pragma unroll 1
+  for (int u = 0; u < GATHER_TASKS; ++u) {
+    const int tt = (warp + NW * u) * SPEC_TPW + lane / SPEC_LANES;
+    const uint32_t en = static_cast<uint32_t>(lane % SPEC_LANES) + SPEC_LANES;
+    if (tt < nt && cs.tcnt[tt] > SPEC_LANES && cs.tcnt[tt] <= 2 * SPEC_LANES && en < cs.tcnt[tt]) {
+      const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + en;
+      const int32_t ix = __ldcg(cand_idx + src);
+      if (take(__ldcg(cand_val + src), ix, cs.tpos[tt] + en) && vl)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + ix));  // P = 1 weight
     }
   }
   // leftovers (tasks beyond NW * GATHER_TASKS, entries past a task's first 32): one thread per
   // entry over a scan of the remainders, GATHER_ILP loads in flight per thread (large k: a
   // 2.4 M-element layer at rho = 0.01 has ~160 candidates per task)
-  const uint32_t skip = static_cast<int>(threadIdx.x) < NW * GATHER_TASKS ? 32u : 0u;
+  LAGS_SPSTAMP(3);
+  constexpr int COVERED = NW * GATHER_TASKS * SPEC_TPW;  // tasks whose first SPEC_LANES entries are placed
+  const bool covered = static_cast<int>(threadIdx.x) < COVERED;
+  const uint32_t skip = !covered ? 0u : (c <= 2u * SPEC_LANES ? c : static_cast<uint32_t>(SPEC_LANES));
   const uint32_t rem = c > skip ? c - skip : 0u;
-  uint32_t rtot;
-  const uint32_t rp = block_exclusive_scan<SEL_NT>(rem, cs.sm.warp_tot, &rtot);
+  uint32_t rtot = 0;
+  uint32_t rp = 0;
+  if (__syncthreads_or(rem != 0u)) rp = block_exclusive_scan<SEL_NT>(rem, cs.sm.warp_tot, &rtot);
   if (rtot) {
     cs.rpos[threadIdx.x] = rp;
     __syncthreads();
@@ -1004,7 +1053,7 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
           for (int step = SEL_NT / 2; step > 0; step >>= 1)
             if (lo + step < nt && cs.rpos[lo + step] <= e) lo += step;
           tk[u] = lo;
-          off[u] = (lo < NW * GATHER_TASKS ? 32u : 0u) + (e - cs.rpos[lo]);
+          off[u] = (lo < COVERED ? static_cast<uint32_t>(SPEC_LANES) : 0u) + (e - cs.rpos[lo]);
           const int64_t src = static_cast<int64_t>(t_lo + lo) * cap + off[u];
           x[u] = __ldcg(cand_val + src);
           ix[u] = __ldcg(cand_idx + src);
@@ -1016,6 +1065,7 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
           asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + ix[u]));  // P = 1 weight
     }
   }
+  LAGS_SPSTAMP(4);
   dx = __reduce_or_sync(0xffffffffu, dx);
   if (lane == 0 && dx) atomicOr(&cs.sm.diff_acc, dx);
   my_gt = __reduce_add_sync(0xffffffffu, my_gt);

@@ -1384,6 +1384,9 @@ extern "C" int lags_dbg_stamps_read(unsigned long long* host) {
 extern "C" int lags_dbg_s64_read(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_s64, sizeof(lags::lags_dbg_s64)));
 }
+extern "C" int lags_dbg_sp_read(unsigned long long* host) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_sp, sizeof(lags::lags_dbg_sp)));
+}
 extern "C" int lags_dbg_cstamps_read(unsigned long long* host) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, lags::lags_dbg_cstamps, sizeof(lags::lags_dbg_cstamps)));
 }

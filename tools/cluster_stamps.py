@@ -46,6 +46,16 @@ for t in range(60):
 a = np.stack(acc)  # steps, rank, kind, stamp
 cyc = a[:, :, 0, :]
 gt = a[:, :, 1, :]
+if True:
+    sp = []
+    for t in range(20):
+        graphs[t % 3].replay()
+        torch.cuda.synchronize()
+        b5 = (C.c_ulonglong * 8)()
+        N.lib.lags_dbg_sp_read(b5)
+        sp.append(np.frombuffer(b5, dtype=np.uint64).astype(np.int64))
+    sp = np.median(np.diff(np.stack(sp)[:, :5], axis=1), axis=0)
+    print("spec_place of rank 0 (cycles): scan", sp[0], "takes", sp[1], "extras", sp[2], "leftovers", sp[3])
 print("median cycles per phase (ranks 0..3):")
 for i in range(1, 14):
     d = np.median(cyc[:, :, i] - cyc[:, :, i - 1], axis=0)
