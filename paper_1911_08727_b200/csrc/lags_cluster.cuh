@@ -308,7 +308,7 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
   if (spec) {
     spec_place(g, t_lo, nt_own, cs.tcache + (t_lo - tr.x), cand_idx, cand_val, cap, sv, si,
                vupd ? vupd + L.offset : nullptr, cs, st.thr, base, cut ? hc.bin : ~0u, &cs.sm.gtb, cs.hist2,
-               &cs.sm.list_n);
+               &cs.sm.list_n, mr);
   } else {
     gather_candidates(t_lo, t_hi, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
                       &cs.sm.gtb, cs.hist2, &cs.sm.list_n, vupd ? vupd + L.offset : nullptr, nullptr, tr.x);

@@ -969,15 +969,34 @@ __device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const
 __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* tc, const int32_t* __restrict__ cand_idx,
                                const float* __restrict__ cand_val, int cap, float* sv, int32_t* si,
                                const float* vl, SelectSmem& cs, uint32_t key0, uint32_t base, uint32_t cut_bin,
-                               uint32_t* gtb, uint32_t* list, uint32_t* list_n) {
+                               uint32_t* gtb, uint32_t* list, uint32_t* list_n, uint32_t m_own) {
   constexpr int NW = SEL_NT / 32;
+  // tasks whose first SPEC_LANES entries are loaded speculatively; a covered task of up to
+  // 2 * SPEC_LANES entries has its rest taken by its own lanes, everything else is a leftover
+  constexpr int COVERED = NW * GATHER_TASKS * SPEC_TPW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   LAGS_SPSTAMP(0);
   const uint32_t c = threadIdx.x < nt ? min(tc[threadIdx.x], static_cast<uint32_t>(cap)) : 0u;
-  uint32_t tot;
-  const uint32_t pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
+  const bool covered = static_cast<int>(threadIdx.x) < COVERED;
+  const uint32_t skip = !covered ? 0u : (c <= 2u * SPEC_LANES ? c : static_cast<uint32_t>(SPEC_LANES));
+  const uint32_t rem = c > skip ? c - skip : 0u;
+  // positions of the tasks and of their leftovers: one scan of both counts packed into 16-bit
+  // halves when the range's total fits (m_own: the caller's sum of the range's counts)
+  uint32_t tot, pos, rtot = 0, rp = 0;
+  if (m_own < 65536u) {
+    uint32_t t2;
+    const uint32_t ex = block_exclusive_scan<SEL_NT>(c | (rem << 16), cs.sm.warp_tot, &t2);
+    pos = ex & 0xffffu;
+    rp = ex >> 16;
+    tot = t2 & 0xffffu;
+    rtot = t2 >> 16;
+  } else {
+    pos = block_exclusive_scan<SEL_NT>(c, cs.sm.warp_tot, &tot);
+    if (__syncthreads_or(rem != 0u)) rp = block_exclusive_scan<SEL_NT>(rem, cs.sm.warp_tot, &rtot);
+  }
   cs.tpos[threadIdx.x] = pos;
   cs.tcnt[threadIdx.x] = c;
+  if (rtot) cs.rpos[threadIdx.x] = rp;
   __syncthreads();
   LAGS_SPSTAMP(1);
   uint32_t my_gt = 0, dx = 0;
@@ -1003,39 +1022,24 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
   for (int u = 0; u < GATHER_TASKS; ++u) {
     const int tt = (warp + NW * u) * SPEC_TPW + lane / SPEC_LANES;
     const uint32_t en = static_cast<uint32_t>(lane % SPEC_LANES);
-    if (tt < nt && en < cs.tcnt[tt]) {
-      if (take(g.xv[u], g.xi[u], cs.tpos[tt] + en) && vl && !LAGS_NO_WPREFETCH)
+    if (tt < nt) {
+      const uint32_t ct = cs.tcnt[tt];
+      if (en < ct && take(g.xv[u], g.xi[u], cs.tpos[tt] + en) && vl && !LAGS_NO_WPREFETCH)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + g.xi[u]));  // P = 1 weight
+      if (ct > SPEC_LANES && ct <= 2 * SPEC_LANES && en + SPEC_LANES < ct) {  // the rest, by the same lanes
+        const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + en + SPEC_LANES;
+        const int32_t ix = __ldcg(cand_idx + src);
+        if (take(__ldcg(cand_val + src), ix, cs.tpos[tt] + en + SPEC_LANES) && vl)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + ix));  // P = 1 weight
+      }
     }
   }
   LAGS_SPSTAMP(2);
-  // a covered task a little longer than SPEC_LANES: its lanes take the rest directly (one more
-  // load each), so a few such tasks do not cost a block-wide leftover pass
-#pragma unroll 1
-  for (int u = 0; u < GATHER_TASKS; ++u) {
-    const int tt = (warp + NW * u) * SPEC_TPW + lane / SPEC_LANES;
-    const uint32_t en = static_cast<uint32_t>(lane % SPEC_LANES) + SPEC_LANES;
-    if (tt < nt && cs.tcnt[tt] > SPEC_LANES && cs.tcnt[tt] <= 2 * SPEC_LANES && en < cs.tcnt[tt]) {
-      const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + en;
-      const int32_t ix = __ldcg(cand_idx + src);
-      if (take(__ldcg(cand_val + src), ix, cs.tpos[tt] + en) && vl)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + ix));  // P = 1 weight
-    }
-  }
-  // leftovers (tasks beyond NW * GATHER_TASKS, entries past a task's first 32): one thread per
-  // entry over a scan of the remainders, GATHER_ILP loads in flight per thread (large k: a
-  // 2.4 M-element layer at rho = 0.01 has ~160 candidates per task)
+  // leftovers (tasks beyond the covered ones, lists longer than 2 * SPEC_LANES): one thread per
+  // entry over the scan of the remainders, GATHER_ILP loads in flight per thread (large k: a
+  // 2.4 M-element layer at rho = 0.01 has ~80 candidates per task)
   LAGS_SPSTAMP(3);
-  constexpr int COVERED = NW * GATHER_TASKS * SPEC_TPW;  // tasks whose first SPEC_LANES entries are placed
-  const bool covered = static_cast<int>(threadIdx.x) < COVERED;
-  const uint32_t skip = !covered ? 0u : (c <= 2u * SPEC_LANES ? c : static_cast<uint32_t>(SPEC_LANES));
-  const uint32_t rem = c > skip ? c - skip : 0u;
-  uint32_t rtot = 0;
-  uint32_t rp = 0;
-  if (__syncthreads_or(rem != 0u)) rp = block_exclusive_scan<SEL_NT>(rem, cs.sm.warp_tot, &rtot);
   if (rtot) {
-    cs.rpos[threadIdx.x] = rp;
-    __syncthreads();
     for (uint32_t e0 = 0; e0 < rtot; e0 += SEL_NT * GATHER_ILP) {
       int tk[GATHER_ILP];
       uint32_t off[GATHER_ILP];
@@ -1268,7 +1272,7 @@ __device__ int candidate_select(int j, const lags_layer_t& L, int2 tr, FastState
     uint32_t* list = cs.hist2;
     if (spec) {
       spec_place(g, tr.x, T, cs.tcache, cand_idx, cand_val, cap, sv, si, vl, cs, st.thr, base, cut ? hc.bin : ~0u,
-                 &sm.gtb, list, &sm.list_n);
+                 &sm.gtb, list, &sm.list_n, m);
     } else {
       gather_candidates(tr.x, tr.y, cand_cnt, cand_idx, cand_val, cap, sv, si, cs, st.thr, base, cut ? hc.bin : ~0u,
                         &sm.gtb, list, &sm.list_n, vl, nullptr, tr.x);
