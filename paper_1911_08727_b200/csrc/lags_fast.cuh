@@ -133,15 +133,16 @@ __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
 
 // K1's per-layer histogram of its candidate keys -- the selection's first cut without a pass over
 // the candidates: HIST_BINS bins of 2^HIST_SHIFT consecutive keys, counted up from the layer's
-// candidate threshold (16384 bins per octave of |x|, so the 4096 bins span keys up to 2^(1/4) =
-// 1.19 times the threshold; larger keys share the top bin).  Error feedback piles the accumulated
+// candidate threshold (32768 bins per octave of |x|, so the 4096 bins span keys up to 2^(1/8) =
+// 1.09 times the threshold; larger keys share the top bin).  Error feedback piles the accumulated
 // magnitudes up just below the threshold, so the bins must be fine there (at 1024 per octave the
 // cut bin of a 2.4 M-element layer held 150-220 keys; at 8192 a 15 M-element LSTM layer's still
-// held ~400, above BIN_LIST_MAX).  With the adaptive margin (m ~ 2k candidates) the k-th key sits
-// a few percent above the threshold for k >= 16; a cut in the top bin takes the radix select.
+// held ~400, above BIN_LIST_MAX; at 16384 the 2.4 M-element layers' held 24-35, just above the
+// one-key-per-lane warp resolve).  With the adaptive margin (m ~ 2k candidates) the k-th key sits
+// a few percent above the threshold; a cut in the top bin takes the radix select.
 // HIST_BINS equals the radix histogram size, so the radix find_bin2 resolves ranks on it.
 #ifndef LAGS_HIST_SHIFT
-#define LAGS_HIST_SHIFT 9
+#define LAGS_HIST_SHIFT 8
 #endif
 constexpr int HIST_SHIFT = LAGS_HIST_SHIFT;
 constexpr int HIST_BINS = F32_BINS;
