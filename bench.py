@@ -354,7 +354,7 @@ def run_ours(args, dims, ks, world, rank, local):
     msgs = bucket.new_messages(world) if world > 1 else msg_local
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     peer = None
-    if world > 1 and args.exchange == "p2p":  # peer-memory exchange (CUDA IPC over NVLink / NVSwitch)
+    if world > 1 and args.exchange in ("p2p", "fused"):  # peer-memory exchange (CUDA IPC over NVLink / NVSwitch)
         from paper_1911_08727_b200.p2p import PeerExchange
 
         try:
@@ -379,10 +379,13 @@ def run_ours(args, dims, ks, world, rank, local):
             if timed:
                 ev[t][1].record(stream)
             return
-        bucket.compress(g_bufs[t % NG], r, alpha, msg_local, status, stream=stream)
+        fused = peer is not None and args.exchange == "fused"
+        bucket.compress(g_bufs[t % NG], r, alpha, msg_local, status, stream=stream, peer=peer if fused else None)
         if timed:
             ev[t][1].record(stream)
-        if peer is not None:
+        if fused:  # the selection pushed every finished layer itself: only the wait
+            bucket.decode(peer.wait(stream=stream), world, v, stream=stream)
+        elif peer is not None:
             bucket.decode(peer.exchange(msg_local, stream=stream), world, v, stream=stream)
         else:
             dist.all_gather_into_tensor(msgs, msg_local)
@@ -429,6 +432,9 @@ def run_ours(args, dims, ks, world, rank, local):
                 with torch.cuda.graph(gr, stream=cap):
                     if world == 1:
                         bucket.step_local(g_bufs[i], r, alpha, v, msg_local, status, stream=cap)
+                    elif args.exchange == "fused":
+                        bucket.compress(g_bufs[i % NG], r, alpha, msg_local, status, stream=cap, peer=peer)
+                        bucket.decode(peer.wait(stream=cap), world, v, stream=cap)
                     else:
                         bucket.compress(g_bufs[i % NG], r, alpha, msg_local, status, stream=cap)
                         bucket.decode(peer.exchange(msg_local, stream=cap), world, v, stream=cap)
@@ -560,7 +566,9 @@ def run_ours(args, dims, ks, world, rank, local):
         dist.all_reduce(ex_us, op=dist.ReduceOp.MAX)
         ex_us = float(ex_us)
         alg = world * bucket.msg_bytes / (ex_us * 1e-6) / 1e9
-        exchange = {"in_step": "peer-memory push + flag wait (lags_p2p_push / lags_p2p_wait, CUDA IPC)"
+        exchange = {"in_step": ("selection pushes every finished layer into every peer (lags_bucket_compress_push)"
+                                " + flag wait (lags_p2p_wait, CUDA IPC)" if args.exchange == "fused" else
+                                "peer-memory push + flag wait (lags_p2p_push / lags_p2p_wait, CUDA IPC)")
                                if peer is not None else "NCCL all_gather_into_tensor",
                     "nccl_all_gather": {"bytes_per_rank": int(bucket.msg_bytes), "us": round(ex_us, 2),
                                         "alg_GBs": round(alg, 2), "bus_GBs": round(alg * (world - 1) / world, 2)},
@@ -883,15 +891,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the ResNet-50 training-iteration measurement")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of CUDA graph replay")
-    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
-                    help="N > 1: peer-memory exchange (own kernels over CUDA IPC) or NCCL all-gather")
+    ap.add_argument("--exchange", choices=["p2p", "fused", "nccl"], default="p2p",
+                    help="N > 1: peer-memory exchange (own push kernel over CUDA IPC), the same exchange done "
+                         "by the selection kernel itself (fused), or the NCCL all-gather")
     ap.add_argument("--p2p-ctas", type=int, default=4, help="peer-memory exchange: CTAs per destination rank")
     ap.add_argument("--graph-mgpu", action="store_true",
                     help="N > 1 with the peer-memory exchange: replay CUDA graphs (measured slower than eager)")
     ap.add_argument("--train-steps", type=int, default=20)
     ap.add_argument("--train-warmup", type=int, default=8)
     ap.add_argument("--bucket-cap", type=int, default=1 << 16, help="fusion capacity (bytes) for LagsSGD")
-    ap.add_argument("--train-exchange", choices=["p2p", "nccl"], default="p2p",
+    ap.add_argument("--train-exchange", choices=["p2p", "fused", "nccl"], default="p2p",
                     help="LagsSGD exchange in the training measurement (N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -90,6 +90,21 @@ int lags_bucket_message_layout(const lags_bucket_t* bucket, int64_t* off_counts,
 int lags_bucket_compress(lags_bucket_t* bucket, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, lags_stream_t stream);
 
+/* Compress with the exchange fused into the selection (LAGS_F32 buckets): every finished layer's
+ * count and (index, value) pairs are also stored into slot `rank` of every rank's receive area
+ * (the lags_p2p_push layout and epoch parity, own area included) by the CTA that produced them,
+ * so the NVLink transfer overlaps the rest of the selection; the last CTA publishes the flags.
+ * Follow it with lags_p2p_wait on the receive area, exactly as after lags_p2p_push (which this
+ * replaces).  Replaces R: training.py:245-248 (the all-gather) together with the compress. */
+typedef struct {
+  const void* bases;          /* device uint64[P]: every rank's receive area (lags_ipc_open) */
+  int32_t P, rank, ctas_per_peer;
+  uint64_t flags_bytes;       /* as lags_p2p_push */
+  const void* epoch;          /* device uint32 epoch counter (advanced by lags_p2p_wait) */
+} lags_peer_push_t;
+int lags_bucket_compress_push(lags_bucket_t* bucket, void* g, void* r, double alpha, void* msg, uint32_t* status,
+                              uint32_t flags, const lags_peer_push_t* peer, lags_stream_t stream);
+
 /* Single-rank step (P = 1, no exchange): lags_bucket_compress plus the update v = v - total / 1,
  * fused into the selection epilogue for LAGS_F32 buckets of up to 49152 selected entries (no
  * separate decode pass); larger selections and the fp64 / mixed modes run the ordinary decode

@@ -50,6 +50,16 @@ lags_bucket_create = _fn("lags_bucket_create", C.c_int, _i32, _vp, _vp, _i32, _i
 lags_bucket_destroy = _fn("lags_bucket_destroy", None, _vp)
 lags_bucket_message_layout = _fn("lags_bucket_message_layout", C.c_int, _vp, _i64p, _i64p, _i64p, _i64p)
 lags_bucket_compress = _fn("lags_bucket_compress", C.c_int, _vp, _vp, _vp, _dbl, _vp, _vp, _u32, _vp)
+
+
+class PeerPushDesc(C.Structure):
+    """lags_peer_push_t (include/lags_b200.h)."""
+    _fields_ = [("bases", C.c_void_p), ("P", C.c_int32), ("rank", C.c_int32), ("ctas_per_peer", C.c_int32),
+                ("flags_bytes", C.c_uint64), ("epoch", C.c_void_p)]
+
+
+lags_bucket_compress_push = _fn("lags_bucket_compress_push", C.c_int, _vp, _vp, _vp, _dbl, _vp, _vp, _u32,
+                                C.POINTER(PeerPushDesc), _vp)
 lags_bucket_decode_update = _fn("lags_bucket_decode_update", C.c_int, _vp, _vp, _i64, _i32, _vp, _vp, _dbl, _u32,
                                 _vp)
 DECODE_V64 = 0x1
@@ -85,6 +95,7 @@ WIRE_OK = (1 << 64) - 1
 EXPORTS = [
     "lags_abi_version", "lags_last_error", "lags_kernel_launches", "lags_bucket_device_bytes",
     "lags_bucket_create", "lags_bucket_destroy", "lags_bucket_message_layout", "lags_bucket_compress",
+    "lags_bucket_compress_push",
     "lags_bucket_decode_update", "lags_bucket_stats", "lags_bucket_step_local", "lags_bucket_set_probe_events", "lags_bucket_set_grad_table",
     "lags_check_finite", "lags_bucket_reconstruct", "lags_bucket_delta", "lags_bucket_shadow_step",
     "lags_bucket_identity",

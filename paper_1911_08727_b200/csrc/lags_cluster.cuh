@@ -189,7 +189,8 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                                      const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval, float* r,
                                      int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words,
                                      int force_exact, float* vupd, uint32_t* dyn, SelectSmem& cs, ClusterShared& csh,
-                                     ClusterRadix& cr, uint32_t t_launch, uint32_t* hist, bool dry = false) {
+                                     ClusterRadix& cr, uint32_t t_launch, uint32_t* hist, bool dry = false,
+                                     const PeerPush* pp = nullptr, uint32_t epoch = 0u) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const uint32_t t_start = globaltimer_lo();
@@ -279,6 +280,10 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
                          state, dyn, smem_words, cs, vupd, hl);
       }
       __syncthreads();
+      if (pp) {  // the whole layer: this CTA wrote it
+        const int c = count_out[j];
+        peer_copy(*pp, epoch, idx_out, val_out, L.slot, 0u, static_cast<uint32_t>(c), j, c, threadIdx.x, SEL_NT);
+      }
       if (hl) zero_hist(hl, 0, HIST_BINS);
       if (threadIdx.x == 0) {
         state[j].cycles = static_cast<uint32_t>(clock64() - t_begin);
@@ -470,6 +475,9 @@ __device__ void cluster_select_layer(int j, const lags_layer_t* __restrict__ lay
     };
     end = compact_staged(mr, th, sv, si, vl, emit, cs, cg0, ce0, oidx, oval);
   }
+  if (pp && !dry)  // this CTA's range of the layer's slots (compact_staged ends with a barrier)
+    peer_copy(*pp, epoch, idx_out, val_out, L.slot, cg0 + min(ce0, th.need_eq), end, j,
+              rank == CLUSTER - 1 ? static_cast<int>(end) : -1, threadIdx.x, SEL_NT);
   LAGS_STAMP(11);
   // the nonzero bins of the own quarter of the chunks (every CTA read its own register copy)
   if (hl && !dry && (SEL_NT - 1 - static_cast<int>(threadIdx.x)) / (SEL_NT / CLUSTER) == rank) clear_hist_chunk(hr, hl);
@@ -510,7 +518,7 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
     FastState* state, const int32_t* __restrict__ cand_cnt,
     const int32_t* __restrict__ cand_idx, const float* __restrict__ cand_val, int cap, int32_t* gidx, float* gval,
     float* r, int32_t* idx_out, float* val_out, int32_t* count_out, int smem_words, int force_exact, SelectCounters sc,
-    float* vupd, uint32_t* hist) {
+    float* vupd, uint32_t* hist, PeerPush pp) {
   extern __shared__ __align__(16) uint32_t dyn[];
   __shared__ SelectSmem cs;
   __shared__ ClusterShared csh;
@@ -523,6 +531,8 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
   LAGS_STAMP(14);
   griddep_wait();  // K1 has completed and its writes are visible (programmatic dependent launch)
   LAGS_STAMP(15);
+  const PeerPush* ppp = pp.bases ? &pp : nullptr;
+  const uint32_t epoch = ppp ? *reinterpret_cast<const volatile uint32_t*>(pp.epoch) + 1u : 0u;
   if (static_cast<int>(blockIdx.x) < cl_ctas) {
 #ifdef LAGS_DBG_TWICE  // diagnostic: the layer twice, the first run without side effects on state / histogram
     {
@@ -536,27 +546,38 @@ __global__ void __launch_bounds__(SEL_NT, SEL_MINB) select_kernel(
 #endif
     cluster_select_layer(cl_layers[blockIdx.x / CLUSTER], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap,
                          gidx, gval, r, idx_out, val_out, count_out, smem_words, force_exact, vupd, dyn, cs, csh, cr,
-                         t_launch, hist);
-    return;
-  }
-  // tiny layers: one warp each, in the CTAs right after the clusters (all in the first wave)
-  if (static_cast<int>(blockIdx.x) < cl_ctas + tiny_ctas) {
+                         t_launch, hist, false, ppp, epoch);
+  } else if (static_cast<int>(blockIdx.x) < cl_ctas + tiny_ctas) {
+    // tiny layers: one warp each, in the CTAs right after the clusters (all in the first wave)
     const int t = (static_cast<int>(blockIdx.x) - cl_ctas) * NW + static_cast<int>(threadIdx.x >> 5);
     if (t < n_tiny) {
       const int j = tiny_layers[t];
       warp_topk_layer(j, layers[j], state, r, idx_out, val_out, count_out, vupd, t_launch);
+      if (ppp) {
+        __syncwarp();
+        const int c = count_out[j];
+        peer_copy(pp, epoch, idx_out, val_out, layers[j].slot, 0u, static_cast<uint32_t>(c), j, c,
+                  static_cast<int>(threadIdx.x & 31), 32);
+      }
     }
-    return;
+  } else {
+    const int base = cl_ctas + tiny_ctas;
+    const int grid = static_cast<int>(gridDim.x) - base;
+    for (int pos = static_cast<int>(blockIdx.x) - base; pos < nl;) {
+      if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + grid;
+      const int j = order[pos];
+      select_layer(j, layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out, val_out,
+                   count_out, dyn, smem_words, force_exact, cs, vupd, t_launch, hist);
+      if (ppp) {  // select_layer ends with a barrier after the layer's writes
+        const int c = count_out[j];
+        peer_copy(pp, epoch, idx_out, val_out, layers[j].slot, 0u, static_cast<uint32_t>(c), j, c,
+                  static_cast<int>(threadIdx.x), SEL_NT);
+      }
+      pos = next_pos;
+      __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
+    }
   }
-  const int base = cl_ctas + tiny_ctas;
-  const int grid = static_cast<int>(gridDim.x) - base;
-  for (int pos = static_cast<int>(blockIdx.x) - base; pos < nl;) {
-    if (threadIdx.x == 0) next_pos = static_cast<int>(atomicAdd(sc.work, 1u)) + grid;
-    select_layer(order[pos], layers, layer_tasks, state, cand_cnt, cand_idx, cand_val, cap, gidx, gval, r, idx_out,
-                 val_out, count_out, dyn, smem_words, force_exact, cs, vupd, t_launch, hist);
-    pos = next_pos;
-    __syncthreads();  // every thread has read next_pos before thread 0 overwrites it
-  }
+  if (ppp) peer_publish(pp, epoch);
 }
 
 }  // namespace lags

@@ -122,6 +122,58 @@ struct SelectCounters {
   uint32_t* work;
 };
 
+// Fused push: the selection writes each finished layer's count and (index, value) pairs into slot
+// `rank` of every peer's receive area (csrc/lags_p2p.cu layout, parity of the coming epoch) right
+// after its CTA produced them, so the NVLink transfer overlaps the remaining selection work; the
+// last CTA to finish publishes the flags the peers' lags_p2p_wait acquires.  bases == nullptr: off.
+struct PeerPush {
+  const uint64_t* bases;  // device array: every rank's receive area (own included)
+  int P, rank, G;         // G: flags per source rank (lags_p2p_wait checks P * G flags)
+  uint64_t flags_bytes;
+  int64_t msg_bytes, off_cnt, off_idx, off_val;
+  const uint32_t* epoch;  // device epoch counter (advanced by the wait kernel)
+  uint32_t* done;         // CTAs finished in this launch (reset by the last one)
+};
+
+__device__ __forceinline__ char* peer_slot(const PeerPush& pp, int p, uint32_t epoch) {
+  return reinterpret_cast<char*>(pp.bases[p]) + pp.flags_bytes +
+         static_cast<int64_t>(epoch & 1u) * pp.P * pp.msg_bytes + static_cast<int64_t>(pp.rank) * pp.msg_bytes;
+}
+
+// Threads tid (of nth) copy the layer's slots [lo, hi) (relative to its first slot) and, when
+// cnt >= 0, its count to every peer.  The caller's writes of those slots are visible to it.
+__device__ void peer_copy(const PeerPush& pp, uint32_t epoch, const int32_t* idx_out, const float* val_out, int64_t slot,
+                          uint32_t lo, uint32_t hi, int j, int cnt, int tid, int nth) {
+  for (int p = 0; p < pp.P; ++p) {
+    char* d = peer_slot(pp, p, epoch);
+    int32_t* di = reinterpret_cast<int32_t*>(d + pp.off_idx) + slot;
+    float* dv = reinterpret_cast<float*>(d + pp.off_val) + slot;
+    for (uint32_t i = lo + tid; i < hi; i += nth) {
+      di[i] = idx_out[slot + i];
+      dv[i] = val_out[slot + i];
+    }
+    if (cnt >= 0 && tid == 0) reinterpret_cast<int32_t*>(d + pp.off_cnt)[j] = cnt;
+  }
+}
+
+// Every CTA of the selection, at its end: the last one to finish publishes epoch in its G flags
+// of every peer (system-scope release; each CTA fenced its remote stores before counting itself).
+__device__ void peer_publish(const PeerPush& pp, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    if (atomicAdd(pp.done, 1u) == gridDim.x - 1) {
+      *pp.done = 0u;
+      __threadfence_system();
+      for (int p = 0; p < pp.P; ++p)
+        for (int gq = 0; gq < pp.G; ++gq) {
+          uint32_t* flag = reinterpret_cast<uint32_t*>(pp.bases[p]) + pp.rank * pp.G + gq;
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+        }
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t warp_inclusive_scan(uint32_t x, int lane) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {

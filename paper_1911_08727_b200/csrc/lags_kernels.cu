@@ -678,7 +678,7 @@ int make_plan(int32_t dtype, const int64_t* dims, const int32_t* ks, int32_t L, 
   p->o_delta = take(3 * sizeof(double) * nt);  // delta (2 per task) / identity monitor (3 per task)
   p->o_tiles = take(sizeof(int2) * static_cast<size_t>(p->ntiles));
   const bool f32 = dtype == LAGS_F32;
-  p->o_ctr = take(f32 ? sizeof(uint32_t) : 0);  // selection counter (SelectCounters)
+  p->o_ctr = take(f32 ? 2 * sizeof(uint32_t) : 0);  // selection counter (SelectCounters) + fused-push CTA count
   p->o_hist = take(f32 ? sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(L) : 0);
   p->o_touched = take(sizeof(uint32_t) * static_cast<size_t>(p->n_total / 32 + 1));
   p->o_dtiles = take(sizeof(DecTile) * static_cast<size_t>(p->ntiles));
@@ -869,7 +869,7 @@ int lags_bucket_create(int32_t dtype, const int64_t* dims, const int32_t* ks, in
       (dtype == LAGS_F32 || cudaMemsetAsync(b->state64, 0, sizeof(State64) * nlayers, s) == cudaSuccess) &&
       cudaMemsetAsync(b->mask, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total), s) == cudaSuccess &&
       cudaMemsetAsync(b->touched, 0, sizeof(uint32_t) * static_cast<size_t>(p.n_total / 32 + 1), s) == cudaSuccess &&
-      (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, sizeof(uint32_t), s) == cudaSuccess) &&
+      (dtype != LAGS_F32 || cudaMemsetAsync(b->sel_ctr.work, 0, 2 * sizeof(uint32_t), s) == cudaSuccess) &&
       (dtype != LAGS_F32 ||
        cudaMemsetAsync(b->hist, 0, sizeof(uint32_t) * HIST_BINS * static_cast<size_t>(nlayers), s) == cudaSuccess) &&
       cudaStreamSynchronize(s) == cudaSuccess;
@@ -956,7 +956,7 @@ int lags_bucket_message_layout(const lags_bucket_t* b, int64_t* off_counts, int6
 // compress of one worker; v_update (nullable, LAGS_F32 only) fuses the P = 1 update into the
 // selection epilogue (lags_bucket_step_local).
 static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
-                         uint32_t flags, void* v_update, lags_stream_t stream) {
+                         uint32_t flags, void* v_update, lags_stream_t stream, const lags_peer_push_t* peer = nullptr) {
   const bool table = b && b->grad_table && b->dtype == LAGS_F32;
   if (!b || (!g && !table) || !r || !msg || !status)
     return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress: null pointer");
@@ -1017,14 +1017,29 @@ static int compress_impl(lags_bucket_t* b, void* g, void* r, double alpha, void*
       const int fixed = ncl * CLUSTER + tiny_ctas;
       const int per = std::min(G0.nlayers, std::max(SEL_MINB * num_sms() - fixed, num_sms() / 2));
       const int grid = (fixed + per + cl - 1) / cl * cl;  // a whole number of clusters
+      PeerPush pp{};
+      if (peer) {
+        pp.bases = static_cast<const uint64_t*>(peer->bases);
+        pp.P = peer->P;
+        pp.rank = peer->rank;
+        pp.G = peer->ctas_per_peer;
+        pp.flags_bytes = peer->flags_bytes;
+        pp.msg_bytes = b->msg_bytes;
+        pp.off_cnt = b->off_cnt;
+        pp.off_idx = b->off_idx;
+        pp.off_val = b->off_val;
+        pp.epoch = static_cast<const uint32_t*>(peer->epoch);
+        pp.done = b->sel_ctr.work + 1;
+      }
       e = launch_pdl_cluster(select_kernel, dim3(grid), dim3(SEL_NT), static_cast<size_t>(b->smem_keys) * 4, s, cl,
                              b->layers, b->layer_tasks, b->order + G1.order_base, ncl, b->order + G2.order_base,
                              G2.nlayers, b->order + G0.order_base, G0.nlayers, b->state, b->cand_cnt, b->cand_idx,
                              b->cand_val, b->cap, b->gidx, b->gval, rr, idx, vals, cnt, b->smem_keys, fe, b->sel_ctr, vu,
-                             b->hist);
+                             b->hist, pp);
     }
     const int launches = 2;
     if (e != cudaSuccess) return fail(LAGS_ERR_CUDA, std::string("compress launch: ") + cudaGetErrorString(e));
+
     return cuda_check("lags_bucket_compress(f32)", launches);
   }
   if (v_update) return fail(LAGS_ERR_INVALID_ARG, "fused single-rank update needs an LAGS_F32 bucket");
@@ -1187,6 +1202,16 @@ int lags_bucket_decode_update(lags_bucket_t* b, const void* msgs, int64_t msg_st
 int lags_bucket_compress(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
                          uint32_t flags, lags_stream_t stream) {
   return compress_impl(b, g, r, alpha, msg, status, flags, nullptr, stream);
+}
+
+int lags_bucket_compress_push(lags_bucket_t* b, void* g, void* r, double alpha, void* msg, uint32_t* status,
+                              uint32_t flags, const lags_peer_push_t* peer, lags_stream_t stream) {
+  if (!b || !peer || !peer->bases || !peer->epoch || peer->P < 1 || peer->rank < 0 || peer->rank >= peer->P ||
+      peer->ctas_per_peer < 1 || (peer->flags_bytes & 255) ||
+      peer->flags_bytes < static_cast<uint64_t>(peer->P) * peer->ctas_per_peer * 4u)
+    return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress_push: bad peer description");
+  if (b->dtype != LAGS_F32) return fail(LAGS_ERR_INVALID_ARG, "lags_bucket_compress_push: LAGS_F32 buckets only");
+  return compress_impl(b, g, r, alpha, msg, status, flags, nullptr, stream, peer);
 }
 
 constexpr int64_t FUSE_P1_MAX_K = 49152;  // fused P = 1 update up to this many selected entries

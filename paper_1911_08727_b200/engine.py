@@ -104,11 +104,20 @@ class Bucket:
 
     # -- kernels -----------------------------------------------------------------------------
     def compress(self, g: torch.Tensor, r: torch.Tensor, alpha: float, msg: torch.Tensor,
-                 status: torch.Tensor, stream=None, exact: bool = False, zero_grad: bool = False) -> None:
+                 status: torch.Tensor, stream=None, exact: bool = False, zero_grad: bool = False,
+                 peer=None) -> None:
         """acc = r + alpha*g; per-layer top-k; r <- acc with selected entries +0.0; msg <- pairs.
-        ``zero_grad`` clears g in the same pass (the optimizer's fused zero_grad)."""
+        ``zero_grad`` clears g in the same pass (the optimizer's fused zero_grad).  ``peer`` (a
+        p2p.PeerExchange): the selection also pushes every finished layer into every rank's
+        receive area (fused exchange); follow it with ``peer.wait(stream)``."""
         self._check_buffers(g, r, None, msg)
         flags = (N.COMPRESS_EXACT if exact else 0) | (N.COMPRESS_ZERO_GRAD if zero_grad else 0)
+        if peer is not None:
+            N.check(N.lags_bucket_compress_push(self._h, g.data_ptr() if g is not None else None, r.data_ptr(),
+                                                float(alpha), msg.data_ptr(), status.data_ptr(), flags,
+                                                C.byref(peer.push_desc(self.msg_bytes)), stream_handle(stream)),
+                    "lags_bucket_compress_push")
+            return
         N.check(N.lags_bucket_compress(self._h, g.data_ptr() if g is not None else None, r.data_ptr(), float(alpha),
                                        msg.data_ptr(), status.data_ptr(), flags, stream_handle(stream)),
                 "lags_bucket_compress")

@@ -136,8 +136,10 @@ class LagsSGD(torch.optim.Optimizer):
         # measurement mode for the exposed-communication time, not a training mode
         if exchange is True:
             exchange = "nccl"
-        if exchange not in (False, "nccl", "p2p"):
-            raise ValueError(f"exchange must be True, False, 'nccl' or 'p2p', got {exchange!r}")
+        # "fused": the peer-memory exchange done by the selection itself (every finished layer is
+        # stored into every rank's receive area by the CTA that selected it), then only the wait
+        if exchange not in (False, "nccl", "p2p", "fused"):
+            raise ValueError(f"exchange must be True, False, 'nccl', 'p2p' or 'fused', got {exchange!r}")
         self.exchange = exchange is not False
         self.exchange_mode = exchange if self.world > 1 and exchange else None
         # delta_every > 0: every that many steps, log the aggregation-quality ratio delta^(l) of
@@ -291,7 +293,7 @@ class LagsSGD(torch.optim.Optimizer):
             msg_local = eng.new_messages(1)
             msg_all = eng.new_messages(self.world) if self.exchange_mode == "nccl" else None
             b = _BucketRT(lo, hi, self.offsets[lo], sum(self.dims[lo:hi + 1]), eng, msg_local, msg_all)
-            if self.exchange_mode == "p2p":
+            if self.exchange_mode in ("p2p", "fused"):
                 from .p2p import PeerExchange
 
                 b.peer = PeerExchange(eng.msg_bytes, self.group)
@@ -488,7 +490,9 @@ class LagsSGD(torch.optim.Optimizer):
             if self._log_delta_now():
                 self._log_delta(b, r, b.msg_local, 1, stream)
             return
-        b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=zg)
+        fused = self.exchange_mode == "fused"
+        b.engine.compress(g, r, lr, b.msg_local, self.status, stream=stream, zero_grad=zg,
+                          **({"peer": b.peer} if fused else {}))
         if t is not None:
             t[1].record(stream)
         comm = stream
@@ -507,6 +511,10 @@ class LagsSGD(torch.optim.Optimizer):
             elif self.exchange_mode == "p2p":
                 msgs = b.peer.exchange(b.msg_local, stream=comm, mid_event=t[3] if t is not None else None)
                 P = self.world
+            elif fused:  # the transfer happened inside the compress: only the wait for the peers
+                if t is not None:
+                    t[3].record(comm)
+                msgs, P = b.peer.wait(stream=comm), self.world
             else:
                 msgs, P = b.msg_local, 1
                 if t is not None:

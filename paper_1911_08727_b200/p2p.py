@@ -89,6 +89,26 @@ class PeerExchange:
         off = self.flags_bytes + (self.calls & 1) * self.world * self.msg_bytes
         return MessageView(self.base + off, self.world * self.msg_bytes)
 
+    def push_desc(self, msg_bytes: int) -> "N.PeerPushDesc":
+        """The lags_peer_push_t of this exchange (Bucket.compress(..., peer=self): the selection
+        pushes each finished layer itself; then call wait())."""
+        if msg_bytes != self.msg_bytes:
+            raise ValueError("bucket message size differs from the exchange's")
+        d = getattr(self, "_desc", None)
+        if d is None:
+            d = self._desc = N.PeerPushDesc(self.bases_dev.data_ptr(), self.world, self.rank, self.G,
+                                            self.flags_bytes, self.epoch_dev.data_ptr())
+        return d
+
+    def wait(self, stream=None) -> MessageView:
+        """The second half of exchange() after a fused-push compress: wait for every rank's
+        message of this epoch; returns the receive area (rank order)."""
+        self.calls += 1
+        N.check(N.lags_p2p_wait(self.base, self.world * self.G, self.epoch_dev.data_ptr(), self.status.data_ptr(),
+                                self.timeout_ns, stream_handle(stream)), "lags_p2p_wait")
+        off = self.flags_bytes + (self.calls & 1) * self.world * self.msg_bytes
+        return MessageView(self.base + off, self.world * self.msg_bytes)
+
     def advance(self, n: int) -> None:
         """Account for n executions of captured exchanges (CUDA-graph replays): the receiving
         parity follows the device epoch, i.e. the number of exchanges executed.  Replay captured

@@ -173,8 +173,10 @@ def test_two_rank_peer_memory_exchange_equals_nccl(tmp_path):
     assert outs[0]["v"].tobytes() == outs[1]["v"].tobytes()  # replicas agree
 
 
-def test_peer_memory_protocol_two_ranks_one_process():
-    """The peer-memory exchange kernels (lags_p2p_push / lags_p2p_wait) with two ranks emulated in
+@pytest.mark.parametrize("fused", [False, True])
+def test_peer_memory_protocol_two_ranks_one_process(fused):
+    """The peer-memory exchange kernels (lags_p2p_push / lags_p2p_wait; fused: the selection pushes
+    every finished layer itself, lags_bucket_compress_push) with two ranks emulated in
     ONE process on one GPU: both receive areas are plain device allocations, both pushes are queued
     before either wait on the same stream (no kernel ever spins on another running kernel), and the
     epochs / parities advance as in PeerExchange.  Each emulated rank decodes its own area; both
@@ -216,11 +218,17 @@ def test_peer_memory_protocol_two_ranks_one_process():
     try:
         for t in range(24):
             grads = [rng.standard_normal(n).astype(np.float32) for _ in range(P)]
-            for p in range(P):
-                b.compress(torch.from_numpy(grads[p]).cuda(), r[p], 0.1, msgs[p], st)
             for p in range(P):  # every push first ...
-                N.check(N.lags_p2p_push(msgs[p].data_ptr(), mb, bases.data_ptr(), P, p, G, flags_bytes,
-                                        epochs[p].data_ptr(), s), "lags_p2p_push")
+                if fused:
+                    desc = N.PeerPushDesc(bases.data_ptr(), P, p, G, flags_bytes, epochs[p].data_ptr())
+                    N.check(N.lags_bucket_compress_push(b._h, torch.from_numpy(grads[p]).cuda().data_ptr(),
+                                                        r[p].data_ptr(), 0.1, msgs[p].data_ptr(), st.data_ptr(), 0,
+                                                        C.byref(desc), s), "lags_bucket_compress_push")
+                    torch.cuda.synchronize()  # the gradient tensor above is a temporary
+                else:
+                    b.compress(torch.from_numpy(grads[p]).cuda(), r[p], 0.1, msgs[p], st)
+                    N.check(N.lags_p2p_push(msgs[p].data_ptr(), mb, bases.data_ptr(), P, p, G, flags_bytes,
+                                            epochs[p].data_ptr(), s), "lags_p2p_push")
             for p in range(P):  # ... then every wait: the flags are already published
                 N.check(N.lags_p2p_wait(areas[p], P * G, epochs[p].data_ptr(), status.data_ptr(), int(5e9), s),
                         "lags_p2p_wait")
@@ -312,7 +320,7 @@ def test_two_process_group_dropin_one_gpu_gloo(tmp_path):
 
 @pytest.mark.gpu2
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < WORLD, reason="needs 2 GPUs")
-@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+@pytest.mark.parametrize("mode", ["p2p", "fused", "nccl"])
 def test_two_rank_lagssgd_matches_oracle(mode):
     """LagsSGD on two ranks (compress on the side stream, exchange + decode on the communication
     stream; peer-memory push or NCCL all-gather): parameters bit-identical to the oracle's P = 2
