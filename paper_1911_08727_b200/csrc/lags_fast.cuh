@@ -973,9 +973,6 @@ __device__ uint32_t gather_candidates(int t_lo, int t_hi, const int32_t* __restr
 #ifndef LAGS_SPEC_LANES
 #define LAGS_SPEC_LANES 16
 #endif
-#ifndef LAGS_NO_WPREFETCH
-#define LAGS_NO_WPREFETCH 0
-#endif
 // lanes per task in the speculative loads (SPEC_TPW tasks per warp load instruction): a
 // 4096-element task of K1's CTA form holds ~8 candidates at the margin
 constexpr int SPEC_LANES = LAGS_SPEC_LANES;
@@ -1005,14 +1002,8 @@ __device__ __forceinline__ void spec_load(SpecGather& g, int t_lo, int nt, const
     const int tt = (warp + NW * u) * SPEC_TPW + lane / SPEC_LANES;
     if (tt < nt) {
       const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + lane % SPEC_LANES;
-#ifdef LAGS_SPEC_ASM
-      // issued here (volatile): the compiler may not sink them to their first use
-      asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(g.xv[u]) : "l"(cand_val + src));
-      asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(g.xi[u]) : "l"(cand_idx + src));
-#else
       g.xv[u] = __ldcg(cand_val + src);
       g.xi[u] = __ldcg(cand_idx + src);
-#endif
     }
   }
 }
@@ -1077,7 +1068,7 @@ __device__ uint32_t spec_place(SpecGather& g, int t_lo, int nt, const uint32_t* 
     const uint32_t en = static_cast<uint32_t>(lane % SPEC_LANES);
     if (tt < nt) {
       const uint32_t ct = cs.tcnt[tt];
-      if (en < ct && take(g.xv[u], g.xi[u], cs.tpos[tt] + en) && vl && !LAGS_NO_WPREFETCH)
+      if (en < ct && take(g.xv[u], g.xi[u], cs.tpos[tt] + en) && vl)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(vl + g.xi[u]));  // P = 1 weight
       if (ct > SPEC_LANES && ct <= 2 * SPEC_LANES && en + SPEC_LANES < ct) {  // the rest, by the same lanes
         const int64_t src = static_cast<int64_t>(t_lo + tt) * cap + en + SPEC_LANES;
