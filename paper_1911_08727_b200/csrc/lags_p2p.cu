@@ -32,6 +32,9 @@ __global__ void __launch_bounds__(P2P_NT) p2p_push_kernel(const uint4* __restric
                                                            int G, const uint32_t* epoch_dev) {
   griddep_wait();  // the compress that wrote the message (and the last wait, the epoch) completed
   const uint32_t epoch = *reinterpret_cast<const volatile uint32_t*>(epoch_dev) + 1u;
+  // the wait kernel may start polling now: it reads only the flags (acquire) and the epoch, which
+  // it advances after every flag -- this push's own included, published after the read above
+  griddep_launch_dependents();
   const int p = static_cast<int>(blockIdx.x) / G, gq = static_cast<int>(blockIdx.x) % G;
   char* base = reinterpret_cast<char*>(bases[p]);
   uint4* dst = reinterpret_cast<uint4*>(base + flags_bytes + static_cast<int64_t>(epoch & 1u) * P * msg_bytes +
@@ -139,8 +142,16 @@ int lags_p2p_push(const void* msg, int64_t msg_bytes, const uint64_t* bases, int
 int lags_p2p_wait(const uint32_t* flags, int nflags, uint32_t* epoch, int32_t* status, uint64_t timeout_ns,
                   lags_stream_t stream) {
   if (!flags || !epoch || !status || nflags < 1) return host_fail(LAGS_ERR_INVALID_ARG, "lags_p2p_wait: bad arguments");
-  p2p_wait_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(flags, nflags, epoch, status, timeout_ns);
-  const cudaError_t e = cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // scheduled as the push drains
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, p2p_wait_kernel, flags, nflags, epoch, status, timeout_ns);
   if (e != cudaSuccess) return host_fail(LAGS_ERR_CUDA, std::string("lags_p2p_wait: ") + cudaGetErrorString(e));
   host_count_launches(1);
   return LAGS_OK;
